@@ -1,0 +1,108 @@
+"""Build the sm_100a shared library in-tree.
+
+    python -m paper_2306_09342_b200.build            # incremental
+    python -m paper_2306_09342_b200.build --clean
+
+Every .cu/.cpp under csrc/ is compiled with
+``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` (objects under build/),
+then linked into ``paper_2306_09342_b200/_lib/librevprop_b200.so``. The .so is
+git-ignored but travels to the GPU box with the gpurun snapshot.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OBJ = ROOT / "build" / "obj"
+LIB_DIR = PKG / "_lib"
+LIB = LIB_DIR / "librevprop_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + str(ROOT / "include"),
+          "-I" + str(CSRC)]
+NVFLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+LINK_LIBS = ["-lpthread"]
+
+
+def _sources() -> list[Path]:
+    return sorted(p for p in CSRC.iterdir() if p.suffix in (".cu", ".cpp"))
+
+
+def _headers() -> list[Path]:
+    hs = [p for p in CSRC.iterdir() if p.suffix in (".h", ".cuh", ".hpp")]
+    hs += list((ROOT / "include").glob("*.h"))
+    return hs
+
+
+def _obj_for(src: Path) -> Path:
+    return OBJ / (src.name + ".o")
+
+
+def _stale(src: Path, obj: Path, newest_header: float) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return src.stat().st_mtime > t or newest_header > t
+
+
+def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
+    obj = _obj_for(src)
+    cmd = [NVCC] + NVFLAGS + ["-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":
+        cmd = [NVCC] + ARCH + COMMON + ["-x", "cu", "-c", str(src), "-o", str(obj)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
+    log = r.stdout + r.stderr
+    if verbose:
+        print(log)
+    return obj, log
+
+
+def build(verbose: bool = False, jobs: int | None = None) -> Path:
+    OBJ.mkdir(parents=True, exist_ok=True)
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    srcs = _sources()
+    newest_header = max((h.stat().st_mtime for h in _headers()), default=0.0)
+    todo = [s for s in srcs if _stale(s, _obj_for(s), newest_header)]
+    logs = {}
+    if todo:
+        with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 4)) as ex:
+            for obj, log in ex.map(lambda s: _compile(s, verbose), todo):
+                logs[obj.name] = log
+        (ROOT / "build" / "ptxas.log").write_text(
+            "\n".join(f"== {k}\n{v}" for k, v in sorted(logs.items())))
+    objs = [_obj_for(s) for s in srcs]
+    if todo or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + LINK_LIBS
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--clean", action="store_true")
+    ap.add_argument("-v", "--verbose", action="store_true")
+    a = ap.parse_args(argv)
+    if a.clean:
+        shutil.rmtree(ROOT / "build", ignore_errors=True)
+        if LIB.exists():
+            LIB.unlink()
+    lib = build(verbose=a.verbose)
+    print(lib)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

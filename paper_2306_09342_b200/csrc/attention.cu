@@ -1,0 +1,491 @@
+// Fused multi-head self-attention forward / backward, head_dim 64.
+//
+// Replaces the per-(batch, head, window) loop of ref:proj/core/src/layers.cpp:150-166
+// (gather_block x3, matmul_nt, scale, row_softmax, probs_store, matmul, scatter_block)
+// and of layers.cpp:185-208 (its VJP). The reference caches the full probability tensor
+// [B,H,nW,W,W] (layers.hpp:60); here only the per-row log-sum-exp is kept and P is
+// recomputed in the backward (flash-attention style), and the head split / merge
+// copies (gather/scatter/slice_last/concat_last) disappear: heads are read straight out
+// of the packed qkv buffer [T, 3d] (q | k | v, head i at columns i*64, as
+// layers.cpp:144-146,155) and dq | dk | dv are written straight into d_qkv [T, 3d]
+// (layers.cpp:210 concat_last).
+//
+// Scale is applied after Q.K^T as in layers.cpp:159; windows (layers.cpp:119-122) are
+// handled by treating each window as its own sequence (window == N is full attention).
+//
+// Backward is split into a dK/dV kernel (CTA per key tile, loops over all queries) and
+// a dQ kernel (CTA per query tile, loops over all keys): every output element is owned
+// by exactly one warp, so there are no atomics and the result is bit-reproducible.
+//
+// Tensor-core path: warp-level mma.sync m16n8k16 (bf16 in, fp32 accumulate).
+#include "../../include/revprop_b200.h"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace rp {
+
+constexpr int kHD = 64;          // head dim
+constexpr int kTile = 64;        // query / key rows per CTA tile
+constexpr int kRowBytes = kHD * 2;
+
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return static_cast<uint32_t>(r * kRowBytes + ((c ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Copy `rows` rows of one head (64 bf16) into a swizzled smem tile; rows >= valid are zero.
+__device__ __forceinline__ void load_rows(uint8_t* s, const __nv_bfloat16* g, int64_t ld, int rows,
+                                          int valid) {
+  const uint32_t sb = smem_u32(s);
+  for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) {
+    const int r = i >> 3, c = i & 7;
+    const bool ok = r < valid;
+    const __nv_bfloat16* src = ok ? g + static_cast<int64_t>(r) * ld + c * 8 : g;
+    cp_async16(sb + swz(r, c), src, ok ? 16 : 0);
+  }
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// A fragment (16 rows x 16 k) from a row-major swizzled tile: rows r0.., k-chunk pair kc.
+__device__ __forceinline__ void load_a(uint32_t base, int r0, int kc, uint32_t* a) {
+  const int l = threadIdx.x & 31;
+  ldsm_x4(base + swz(r0 + (l & 15), kc + (l >> 4)), a);
+}
+// B fragments for two n8 tiles (n0..n0+15) x k16 from a tile stored [n][k] (no transpose).
+__device__ __forceinline__ void load_b_nk(uint32_t base, int n0, int kc, uint32_t* b) {
+  const int l = threadIdx.x & 31;
+  ldsm_x4(base + swz(n0 + (l & 7) + ((l >> 4) << 3), kc + ((l >> 3) & 1)), b);
+}
+// B fragments for two n8 tiles (column chunks nc, nc+1) x k16 (rows k0..) from [k][n].
+__device__ __forceinline__ void load_b_kn(uint32_t base, int k0, int nc, uint32_t* b) {
+  const int l = threadIdx.x & 31;
+  ldsm_x4_t(base + swz(k0 + (l & 15), nc + (l >> 4)), b);
+}
+
+// S(16 x 64) = A(16 x 64, regs) . B^T where B tile [64 n][64 k] in smem rows nb..nb+63
+__device__ __forceinline__ void mm_abt(const uint32_t (*a)[4], uint32_t bbase, int nb,
+                                       float (*s)[4]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      uint32_t b[4];
+      load_b_nk(bbase, nb + 16 * np, 2 * ks, b);
+      mma16816(s[2 * np], a[ks], b[0], b[1]);
+      mma16816(s[2 * np + 1], a[ks], b[2], b[3]);
+    }
+  }
+}
+
+// acc(16 x 64) += P(16 x 64 k, C-fragment layout) . B where B tile [64 k][64 n] rows kb..
+__device__ __forceinline__ void mm_pb(const float (*p)[4], uint32_t bbase, int kb,
+                                      float (*acc)[4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t a[4];
+    a[0] = pack_bf16x2(p[2 * ks][0], p[2 * ks][1]);
+    a[1] = pack_bf16x2(p[2 * ks][2], p[2 * ks][3]);
+    a[2] = pack_bf16x2(p[2 * ks + 1][0], p[2 * ks + 1][1]);
+    a[3] = pack_bf16x2(p[2 * ks + 1][2], p[2 * ks + 1][3]);
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      uint32_t b[4];
+      load_b_kn(bbase, kb + 16 * ks, 2 * np, b);
+      mma16816(acc[2 * np], a, b[0], b[1]);
+      mma16816(acc[2 * np + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+struct AttnGeom {
+  int B, N, H;        // sequences, tokens per sequence, heads
+  int64_t ld_qkv;     // row pitch of qkv / d_qkv (3*H*64)
+  int64_t ld_o;       // row pitch of out / d_out (H*64)
+  float scale;        // 1/sqrt(hd)
+  float scale_log2;   // scale * log2(e)
+};
+
+// ------------------------------------------------------------------------ forward
+// grid (ceil(N/64), H, B); block 128 (4 warps x 16 query rows)
+// smem: Q tile [64][64] | K [Npad][64] | V [Npad][64]
+__global__ void __launch_bounds__(128)
+    attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
+                    float* __restrict__ lse, AttnGeom g) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int npad = (g.N + kTile - 1) / kTile * kTile;
+  uint8_t* sQ = sm;
+  uint8_t* sK = sQ + kTile * kRowBytes;
+  uint8_t* sV = sK + npad * kRowBytes;
+  const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
+  load_rows(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0);
+  load_rows(sK, base + g.H * kHD, g.ld_qkv, npad, g.N);
+  load_rows(sV, base + 2 * g.H * kHD, g.ld_qkv, npad, g.N);
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const uint32_t bQ = smem_u32(sQ), bK = smem_u32(sK), bV = smem_u32(sV);
+  uint32_t qa[4][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) load_a(bQ, warp * 16, 2 * ks, qa[ks]);
+
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+
+  for (int kt = 0; kt < npad; kt += kTile) {
+    float s[8][4];
+    mm_abt(qa, bK, kt, s);
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = kt + nt * 8 + 2 * tq + (e & 1);
+        const float v = col < g.N ? s[nt][e] * g.scale_log2 : -INFINITY;
+        s[nt][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float nm = fmaxf(m[r], mx[r]);
+      corr[r] = exp2f(m[r] - nm);
+      m[r] = nm;
+      l[r] *= corr[r];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p = exp2f(s[nt][e] - m[e >> 1]);
+        s[nt][e] = p;
+        l[e >> 1] += p;
+        o[nt][e] *= corr[e >> 1];
+      }
+    }
+    mm_pb(s, bV, kt, o);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+  }
+  const int rowa = q0 + warp * 16 + gq;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = rowa + 8 * r;
+    if (row < g.N) {
+      const float inv = 1.0f / l[r];
+      __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * kHD;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+        *reinterpret_cast<uint32_t*>(orow + nt * 8 + 2 * tq) =
+            pack_bf16x2(o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
+      if (tq == 0)
+        lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = m[r] + log2f(l[r]);
+    }
+  }
+}
+
+// D[b][h][n] = sum_c dO[row][h*64+c] * O[row][h*64+c]   (softmax VJP dot, ops.cpp:219-220)
+__global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out,
+                                    const __nv_bfloat16* __restrict__ dout,
+                                    float* __restrict__ D, AttnGeom g) {
+  const int64_t total = static_cast<int64_t>(g.B) * g.N * g.H;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int h = static_cast<int>(i % g.H);
+    const int64_t row = i / g.H;  // b*N + n
+    const uint4* o = reinterpret_cast<const uint4*>(out + row * g.ld_o + h * kHD);
+    const uint4* d = reinterpret_cast<const uint4*>(dout + row * g.ld_o + h * kHD);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint4 a = o[j], c = d[j];
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 fa = unpack_bf16x2(av[k]), fc = unpack_bf16x2(cv[k]);
+        acc += fa.x * fc.x + fa.y * fc.y;
+      }
+    }
+    const int64_t b = row / g.N, n = row % g.N;
+    D[(b * g.H + h) * g.N + n] = acc;
+  }
+}
+
+// ------------------------------------------------------------------------ dK, dV
+// grid (ceil(N/64), H, B): CTA owns 64 keys; loops over all query tiles.
+// smem: K tile | V tile | Q [Npad] | dO [Npad] | lse [Npad] | D [Npad]
+__global__ void __launch_bounds__(128)
+    attn_bwd_dkdv_kernel(const __nv_bfloat16* __restrict__ qkv,
+                         const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
+                         const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv,
+                         AttnGeom g) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int npad = (g.N + kTile - 1) / kTile * kTile;
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + kTile * kRowBytes;
+  uint8_t* sQ = sV + kTile * kRowBytes;
+  uint8_t* sO = sQ + npad * kRowBytes;
+  float* sL = reinterpret_cast<float*>(sO + npad * kRowBytes);
+  float* sD = sL + npad;
+  const int k0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
+  load_rows(sK, base + static_cast<int64_t>(k0) * g.ld_qkv + g.H * kHD, g.ld_qkv, kTile, g.N - k0);
+  load_rows(sV, base + static_cast<int64_t>(k0) * g.ld_qkv + 2 * g.H * kHD, g.ld_qkv, kTile,
+            g.N - k0);
+  load_rows(sQ, base, g.ld_qkv, npad, g.N);
+  load_rows(sO, dout + static_cast<int64_t>(b) * g.N * g.ld_o + h * kHD, g.ld_o, npad, g.N);
+  const float* lrow = lse + (static_cast<int64_t>(b) * g.H + h) * g.N;
+  const float* drow = Dg + (static_cast<int64_t>(b) * g.H + h) * g.N;
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    sL[i] = i < g.N ? lrow[i] : 0.f;
+    sD[i] = i < g.N ? drow[i] : 0.f;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tq = lane & 3, gq = lane >> 2;
+  const uint32_t bK = smem_u32(sK), bV = smem_u32(sV), bQ = smem_u32(sQ), bO = smem_u32(sO);
+  uint32_t ka[4][4], va[4][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    load_a(bK, warp * 16, 2 * ks, ka[ks]);
+    load_a(bV, warp * 16, 2 * ks, va[ks]);
+  }
+  float dk[8][4], dv[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
+
+  for (int qt = 0; qt < npad; qt += kTile) {
+    float st[8][4], dpt[8][4];
+    mm_abt(ka, bQ, qt, st);   // S^T [16 keys][64 queries]
+    mm_abt(va, bO, qt, dpt);  // dP^T = V . dO^T
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = qt + nt * 8 + 2 * tq + (e & 1);
+        const float p = q < g.N ? exp2f(st[nt][e] * g.scale_log2 - sL[q]) : 0.f;
+        st[nt][e] = p;
+        dpt[nt][e] = p * (dpt[nt][e] - sD[q]) * g.scale;
+      }
+    }
+    mm_pb(st, bO, qt, dv);   // dV += P^T . dO
+    mm_pb(dpt, bQ, qt, dk);  // dK += dS^T . Q
+  }
+  const int rowa = k0 + warp * 16 + gq;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = rowa + 8 * r;
+    if (row < g.N) {
+      __nv_bfloat16* drow_k =
+          dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + g.H * kHD + h * kHD;
+      __nv_bfloat16* drow_v = drow_k + g.H * kHD;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        *reinterpret_cast<uint32_t*>(drow_k + nt * 8 + 2 * tq) =
+            pack_bf16x2(dk[nt][2 * r], dk[nt][2 * r + 1]);
+        *reinterpret_cast<uint32_t*>(drow_v + nt * 8 + 2 * tq) =
+            pack_bf16x2(dv[nt][2 * r], dv[nt][2 * r + 1]);
+      }
+    }
+  }
+  (void)gq;
+}
+
+// ------------------------------------------------------------------------ dQ
+// grid (ceil(N/64), H, B): CTA owns 64 queries; loops over all key tiles.
+// smem: Q tile | dO tile | K [Npad] | V [Npad]
+__global__ void __launch_bounds__(128)
+    attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ qkv,
+                       const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
+                       const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv,
+                       AttnGeom g) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int npad = (g.N + kTile - 1) / kTile * kTile;
+  uint8_t* sQ = sm;
+  uint8_t* sO = sQ + kTile * kRowBytes;
+  uint8_t* sK = sO + kTile * kRowBytes;
+  uint8_t* sV = sK + npad * kRowBytes;
+  const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
+  load_rows(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0);
+  load_rows(sO, dout + (static_cast<int64_t>(b) * g.N + q0) * g.ld_o + h * kHD, g.ld_o, kTile,
+            g.N - q0);
+  load_rows(sK, base + g.H * kHD, g.ld_qkv, npad, g.N);
+  load_rows(sV, base + 2 * g.H * kHD, g.ld_qkv, npad, g.N);
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tq = lane & 3, gq = lane >> 2;
+  const uint32_t bQ = smem_u32(sQ), bO = smem_u32(sO), bK = smem_u32(sK), bV = smem_u32(sV);
+  uint32_t qa[4][4], oa[4][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    load_a(bQ, warp * 16, 2 * ks, qa[ks]);
+    load_a(bO, warp * 16, 2 * ks, oa[ks]);
+  }
+  const int rowa = q0 + warp * 16 + gq;
+  float lr[2], dr[2];
+  const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = rowa + 8 * r;
+    lr[r] = row < g.N ? lse[hb + row] : 0.f;
+    dr[r] = row < g.N ? Dg[hb + row] : 0.f;
+  }
+  float dq[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+
+  for (int kt = 0; kt < npad; kt += kTile) {
+    float s[8][4], dp[8][4];
+    mm_abt(qa, bK, kt, s);
+    mm_abt(oa, bV, kt, dp);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kc = kt + nt * 8 + 2 * tq + (e & 1);
+        const float p = kc < g.N ? exp2f(s[nt][e] * g.scale_log2 - lr[e >> 1]) : 0.f;
+        s[nt][e] = p * (dp[nt][e] - dr[e >> 1]) * g.scale;
+      }
+    }
+    mm_pb(s, bK, kt, dq);  // dQ += dS . K
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = rowa + 8 * r;
+    if (row < g.N) {
+      __nv_bfloat16* drow = dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + h * kHD;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+        *reinterpret_cast<uint32_t*>(drow + nt * 8 + 2 * tq) =
+            pack_bf16x2(dq[nt][2 * r], dq[nt][2 * r + 1]);
+    }
+  }
+}
+
+static AttnGeom make_geom(int64_t B, int64_t N, int64_t H) {
+  AttnGeom g;
+  g.B = static_cast<int>(B);
+  g.N = static_cast<int>(N);
+  g.H = static_cast<int>(H);
+  g.ld_qkv = 3 * H * kHD;
+  g.ld_o = H * kHD;
+  g.scale = 1.0f / sqrtf(static_cast<float>(kHD));
+  g.scale_log2 = g.scale * 1.4426950408889634f;
+  return g;
+}
+
+static int set_smem_attr(const void* fn, int bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+                 cudaSuccess
+             ? RP_OK
+             : RP_ERR_CUDA;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+static int attn_check(int64_t B, int64_t N, int64_t H, int64_t hd) {
+  if (B <= 0 || N <= 0 || H <= 0) return rp_fail(RP_ERR_SHAPE, "attention: empty shape");
+  if (hd != kHD) return rp_fail(RP_ERR_SHAPE, "attention: head_dim must be 64");
+  if (N > 1024) return rp_fail(RP_ERR_SHAPE, "attention: sequence (window) longer than 1024");
+  return RP_OK;
+}
+
+// qkv [B*N, 3*H*64] bf16 -> out [B*N, H*64] bf16, lse [B][H][N] (log2 domain).
+// B here is the number of independent sequences (batch x windows).
+extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64_t H,
+                                int64_t head_dim, uint16_t* out, float* lse,
+                                rp_stream_t stream) {
+  int rc = attn_check(B, N, H, head_dim);
+  if (rc) return rc;
+  const AttnGeom g = make_geom(B, N, H);
+  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
+  const int smem = (kTile + 2 * npad) * kRowBytes;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem))) return rc;
+  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
+            static_cast<unsigned>(B));
+  attn_fwd_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse,
+      g);
+  return rp_check_launch("attention_fwd");
+}
+
+extern "C" int64_t rp_attention_bwd_workspace_floats(int64_t B, int64_t N, int64_t H) {
+  return B * N * H;
+}
+
+// d_out [B*N, H*64] -> d_qkv [B*N, 3*H*64]; workspace: B*N*H floats.
+extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                                const uint16_t* dout, int64_t B, int64_t N, int64_t H,
+                                int64_t head_dim, uint16_t* dqkv, float* workspace,
+                                rp_stream_t stream) {
+  int rc = attn_check(B, N, H, head_dim);
+  if (rc) return rc;
+  const AttnGeom g = make_geom(B, N, H);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t total = B * N * H;
+  int blocks = static_cast<int>((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  attn_bwd_dot_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(out),
+                                             reinterpret_cast<const __nv_bfloat16*>(dout),
+                                             workspace, g);
+  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
+  const int smem_kv = 2 * kTile * kRowBytes + 2 * npad * kRowBytes + 2 * npad * 4;
+  const int smem_q = 2 * kTile * kRowBytes + 2 * npad * kRowBytes;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dkdv_kernel), smem_kv)))
+    return rc;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dq_kernel), smem_q))) return rc;
+  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
+            static_cast<unsigned>(B));
+  attn_bwd_dkdv_kernel<<<grid, 128, smem_kv, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
+      lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  attn_bwd_dq_kernel<<<grid, 128, smem_q, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
+      lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  return rp_check_launch("attention_bwd");
+}

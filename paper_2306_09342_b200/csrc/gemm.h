@@ -1,0 +1,17 @@
+#pragma once
+#include "../../include/revprop_b200.h"
+
+namespace rp {
+// Device-side view of an RpGemmDesc epilogue (plain POD, passed by value to the kernel).
+struct GemmEpi {
+  void* out;
+  int64_t ldo;
+  void* out2;
+  int64_t ldo2;
+  const void* aux;
+  int64_t ldaux;
+  const float* bias;
+  float sign;
+  int64_t split_stride;
+};
+}  // namespace rp

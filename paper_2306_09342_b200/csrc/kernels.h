@@ -1,0 +1,12 @@
+// Host-side helpers shared by the launchers: error reporting that maps onto the
+// reference's exception classes (ref:proj/core/include/revprop/errors.hpp:9-48).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/revprop_b200.h"
+
+// Record `msg` as the thread-local last error and return `code`.
+int rp_fail(int code, const char* msg);
+// cudaGetLastError() -> RP_OK or RP_ERR_CUDA with the CUDA error string.
+int rp_check_launch(const char* what);

@@ -1,0 +1,350 @@
+// LayerNorm forward / backward and deterministic column reductions (HBM-bound kernels).
+//
+// Forward follows ref:proj/core/src/ops.cpp:264-304 (two-pass mean, population variance,
+// inv_std = 1/sqrt(var + eps), y = x_hat*gamma + beta) but keeps (mean, rstd) per row
+// instead of materialising x_hat: x_hat is recomputed from the fp32 residual stream in
+// the backward, which saves a [T,d] write+read per LayerNorm.
+// Backward follows ref:proj/core/src/ops.cpp:306-345
+//   g = dy*gamma; dx = (g - mean(g) - x_hat*mean(g*x_hat)) * inv_std
+//   dgamma = sum_rows dy*x_hat, dbeta = sum_rows dy
+// with the reversible coupling's cotangent add fused in (dx_total = dres + dx,
+// SPEC.md:234) and a bf16 copy of dx_total emitted for the next GEMM.
+// All reductions have a fixed association order that depends only on the problem shape,
+// never on the launch or stream co-residency, so results are bit-reproducible.
+#include "../../include/revprop_b200.h"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace rp {
+
+constexpr int kLnWarps = 8;        // rows per CTA in the forward
+constexpr int kLnBwdRows = 64;     // rows per CTA in the backward (one dgamma/dbeta partial)
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per row; lane l owns float4 columns {l, l+32, ...}.
+template <int V>
+__global__ void __launch_bounds__(kLnWarps * 32)
+    ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                  const float* __restrict__ beta, int64_t rows, int cols, float eps,
+                  __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                  float* __restrict__ rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kLnWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int c4 = cols >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
+  float4 v[V];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < c4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = warp_sum(s) / static_cast<float>(cols);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    if (c < c4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
+  }
+  const float var = warp_sum(q) / static_cast<float>(cols);
+  const float rstd = 1.0f / sqrtf(var + eps);
+  uint2* yr = reinterpret_cast<uint2*>(y + row * cols);
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float4* b4 = reinterpret_cast<const float4*>(beta);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    if (c < c4) {
+      const float4 g = g4[c], b = b4[c];
+      const float o0 = (v[i].x - mean) * rstd * g.x + b.x;
+      const float o1 = (v[i].y - mean) * rstd * g.y + b.y;
+      const float o2 = (v[i].z - mean) * rstd * g.z + b.z;
+      const float o3 = (v[i].w - mean) * rstd * g.w + b.w;
+      yr[c] = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+    }
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// Backward: CTA = 8 warps over kLnBwdRows consecutive rows (warp w: rows w, w+8, ...).
+// dgamma/dbeta: per-lane register accumulation in row order, then warps combined in
+// warp order -> one partial per CTA: part[blk][0][c] = dgamma, part[blk][1][c] = dbeta.
+template <int V>
+__global__ void __launch_bounds__(kLnWarps * 32)
+    ln_bwd_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
+                  const float* __restrict__ rstd_in, const float* __restrict__ gamma,
+                  const __nv_bfloat16* __restrict__ dy, const float* __restrict__ dres,
+                  int64_t rows, int cols, float* __restrict__ dx,
+                  __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part) {
+  extern __shared__ float red[];  // [kLnWarps][2][cols]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c4 = cols >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  float4 ag[V], ab[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    ag[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float inv_n = 1.0f / static_cast<float>(cols);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
+  for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
+    const int64_t row = r0 + rr;
+    if (row >= rows) break;
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
+    const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
+    float4 h[V], d[V];
+    float sg = 0.f, sgh = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + 32 * i;
+      if (c < c4) {
+        const float4 xv = xr[c];
+        const uint2 dv = dyr[c];
+        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+        d[i] = make_float4(d01.x, d01.y, d23.x, d23.y);
+        h[i] = make_float4((xv.x - mean) * rstd, (xv.y - mean) * rstd, (xv.z - mean) * rstd,
+                           (xv.w - mean) * rstd);
+        const float4 g = g4[c];
+        const float gx = d[i].x * g.x, gy = d[i].y * g.y, gz = d[i].z * g.z, gw = d[i].w * g.w;
+        sg += (gx + gy) + (gz + gw);
+        sgh += (gx * h[i].x + gy * h[i].y) + (gz * h[i].z + gw * h[i].w);
+        ag[i].x += d[i].x * h[i].x;
+        ag[i].y += d[i].y * h[i].y;
+        ag[i].z += d[i].z * h[i].z;
+        ag[i].w += d[i].w * h[i].w;
+        ab[i].x += d[i].x;
+        ab[i].y += d[i].y;
+        ab[i].z += d[i].z;
+        ab[i].w += d[i].w;
+      }
+    }
+    const float gm = warp_sum(sg) * inv_n;
+    const float ghm = warp_sum(sgh) * inv_n;
+    float4* dxr = reinterpret_cast<float4*>(dx + row * cols);
+    const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
+    uint2* dxb = dx_bf16 ? reinterpret_cast<uint2*>(dx_bf16 + row * cols) : nullptr;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + 32 * i;
+      if (c < c4) {
+        const float4 g = g4[c];
+        float4 o;
+        o.x = (d[i].x * g.x - gm - h[i].x * ghm) * rstd;
+        o.y = (d[i].y * g.y - gm - h[i].y * ghm) * rstd;
+        o.z = (d[i].z * g.z - gm - h[i].z * ghm) * rstd;
+        o.w = (d[i].w * g.w - gm - h[i].w * ghm) * rstd;
+        if (drr) {
+          const float4 r = drr[c];
+          o.x += r.x;
+          o.y += r.y;
+          o.z += r.z;
+          o.w += r.w;
+        }
+        dxr[c] = o;
+        if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+      }
+    }
+  }
+  // combine warps in fixed order
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    if (c < c4) {
+      reinterpret_cast<float4*>(red + (warp * 2 + 0) * cols)[c] = ag[i];
+      reinterpret_cast<float4*>(red + (warp * 2 + 1) * cols)[c] = ab[i];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
+    const int which = c / cols, col = c % cols;
+    float s = red[which * cols + col];
+    for (int w = 1; w < kLnWarps; ++w) s += red[(w * 2 + which) * cols + col];
+    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = s;
+  }
+}
+
+// Stage 1 of a deterministic column sum over a [rows, cols] matrix (fp32 or bf16):
+// CTA (rb, cb) sums rows [rb*RPB, (rb+1)*RPB) for 4*256 columns, sequentially in row order.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    colsum_partial_kernel(const T* __restrict__ in, int64_t rows, int cols, int rpb,
+                          float* __restrict__ part) {
+  const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
+  if (c >= cols) return;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
+  int64_t r1 = r0 + rpb;
+  if (r1 > rows) r1 = rows;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t r = r0; r < r1; ++r) {
+    float4 v;
+    if constexpr (sizeof(T) == 4) {
+      v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(in) + r * cols + c);
+    } else {
+      const uint2 u = *reinterpret_cast<const uint2*>(
+          reinterpret_cast<const __nv_bfloat16*>(in) + r * cols + c);
+      const float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y);
+      v = make_float4(a.x, a.y, b.x, b.y);
+    }
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  *reinterpret_cast<float4*>(part + static_cast<int64_t>(blockIdx.x) * cols + c) = acc;
+}
+
+// Stage 2: out[c] (+)= sum_p part[p][c] in a fixed order. CTA = 8 warps x 32 columns;
+// warp w owns parts {w, w+8, ...} with 4 interleaved accumulators; combined in order.
+__global__ void __launch_bounds__(256)
+    colsum_final_kernel(const float* __restrict__ part, int64_t nparts, int cols, int64_t ld,
+                        float* __restrict__ out, int accumulate) {
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (c < cols) {
+    int64_t p = warp;
+    for (; p + 24 < nparts; p += 32) {
+      a0 += part[p * ld + c];
+      a1 += part[(p + 8) * ld + c];
+      a2 += part[(p + 16) * ld + c];
+      a3 += part[(p + 24) * ld + c];
+    }
+    for (; p < nparts; p += 8) a0 += part[p * ld + c];
+  }
+  red[warp][lane] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    float s = red[0][lane];
+    for (int w = 1; w < 8; ++w) s += red[w][lane];
+    out[c] = accumulate ? out[c] + s : s;
+  }
+}
+
+template <int V>
+static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_t rows,
+                          int cols, float eps, __nv_bfloat16* y, float* mean, float* rstd,
+                          cudaStream_t s) {
+  const int64_t blocks = (rows + kLnWarps - 1) / kLnWarps;
+  ln_fwd_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, 0, s>>>(x, g, b, rows, cols,
+                                                                           eps, y, mean, rstd);
+}
+
+template <int V>
+static void launch_ln_bwd(const float* x, const float* mean, const float* rstd,
+                          const float* gamma, const __nv_bfloat16* dy, const float* dres,
+                          int64_t rows, int cols, float* dx, __nv_bfloat16* dxb, float* part,
+                          cudaStream_t s) {
+  const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
+  const int smem = kLnWarps * 2 * cols * static_cast<int>(sizeof(float));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(ln_bwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kLnWarps * 2 * 2048 * 4);
+    attr_set = true;
+  }
+  ln_bwd_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, smem, s>>>(
+      x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+int64_t rp_ln_bwd_num_parts(int64_t rows) { return (rows + kLnBwdRows - 1) / kLnBwdRows; }
+
+#define RP_LN_DISPATCH(FN, ...)                      \
+  do {                                               \
+    const int v = (cols / 4 + 31) / 32;              \
+    if (v <= 2)                                      \
+      FN<2>(__VA_ARGS__);                            \
+    else if (v <= 4)                                 \
+      FN<4>(__VA_ARGS__);                            \
+    else if (v <= 6)                                 \
+      FN<6>(__VA_ARGS__);                            \
+    else if (v <= 8)                                 \
+      FN<8>(__VA_ARGS__);                            \
+    else if (v <= 13)                                \
+      FN<13>(__VA_ARGS__);                           \
+    else if (v <= 16)                                \
+      FN<16>(__VA_ARGS__);                           \
+    else                                             \
+      return rp_fail(RP_ERR_SHAPE, "layer_norm: width > 2048 unsupported"); \
+  } while (0)
+
+extern "C" int rp_layer_norm_fwd(const float* x, const float* gamma, const float* beta,
+                                 int64_t rows, int64_t cols, double eps, uint16_t* y,
+                                 float* mean, float* rstd, rp_stream_t stream) {
+  if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm: cols % 4");
+  if (!(eps > 0.0)) return rp_fail(RP_ERR_SHAPE, "layer_norm: eps must be positive");
+  RP_LN_DISPATCH(launch_ln_fwd, x, gamma, beta, rows, static_cast<int>(cols),
+                 static_cast<float>(eps), reinterpret_cast<__nv_bfloat16*>(y), mean, rstd,
+                 static_cast<cudaStream_t>(stream));
+  return rp_check_launch("layer_norm_fwd");
+}
+
+extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float* rstd,
+                                 const float* gamma, const uint16_t* dy, const float* dres,
+                                 int64_t rows, int64_t cols, float* dx, uint16_t* dx_bf16,
+                                 float* dgamma, float* dbeta, float* workspace,
+                                 int accumulate, rp_stream_t stream) {
+  if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma,
+                 reinterpret_cast<const __nv_bfloat16*>(dy), dres, rows, static_cast<int>(cols),
+                 dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16), workspace, s);
+  const int64_t nparts = rp_ln_bwd_num_parts(rows);
+  // workspace holds [nparts][2][cols] (dgamma | dbeta partials)
+  const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
+  if (dgamma)
+    colsum_final_kernel<<<gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(cols), 2 * cols,
+                                           dgamma, accumulate);
+  if (dbeta)
+    colsum_final_kernel<<<gb, 256, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
+                                           2 * cols, dbeta, accumulate);
+  return rp_check_launch("layer_norm_bwd");
+}
+
+extern "C" int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols) {
+  return rp_ln_bwd_num_parts(rows) * 2 * cols;
+}
+
+// column sum of a [rows, cols] matrix: out[c] (+)= sum_r in[r][c]
+// (ref:proj/core/src/layers.cpp:38-52 col_sum, used for the MLP bias grads)
+static const int kColRpb = 128;
+extern "C" int64_t rp_colsum_workspace_floats(int64_t rows, int64_t cols) {
+  return ((rows + kColRpb - 1) / kColRpb) * cols;
+}
+
+extern "C" int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t cols, float* out,
+                         float* workspace, int accumulate, rp_stream_t stream) {
+  if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "col_sum: cols % 4");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nparts = (rows + kColRpb - 1) / kColRpb;
+  dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
+  if (in_is_bf16)
+    colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(in), rows, static_cast<int>(cols), kColRpb, workspace);
+  else
+    colsum_partial_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(in), rows,
+                                                      static_cast<int>(cols), kColRpb,
+                                                      workspace);
+  colsum_final_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(
+      workspace, nparts, static_cast<int>(cols), cols, out, accumulate);
+  return rp_check_launch("col_sum");
+}

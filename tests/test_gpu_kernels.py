@@ -1,0 +1,189 @@
+"""Kernel-level numerics on the B200: each sm_100a kernel against a plain PyTorch fp32
+computation of the same op on the same (bf16-rounded) inputs."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2306_09342_b200 import kernels, _capi
+    _capi.lib()
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return kernels
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
+
+
+def gelu_ref(u):
+    c, a = 0.7978845608028654, 0.044715
+    return 0.5 * u * (1 + torch.tanh(c * (u + a * u ** 3)))
+
+
+def gelu_slope_ref(u):
+    c, a = 0.7978845608028654, 0.044715
+    t = torch.tanh(c * (u + a * u ** 3))
+    return 0.5 * (1 + t) + 0.5 * u * (1 - t * t) * c * (1 + 3 * a * u * u)
+
+
+SHAPES = [(296, 512, 200), (128, 256, 64), (1000, 768, 768), (264, 2304, 136)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("bn", [256, 128])
+def test_gemm_majors_bf16(K, a_mn, b_mn, shape, bn):
+    from paper_2306_09342_b200._capi import RP_EPI_BF16
+    M, N, Kd = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    Bm = torch.randn(Kd, N, device="cuda", generator=g).bfloat16()
+    Ast = A.t().contiguous() if a_mn else A
+    Bst = Bm if b_mn else Bm.t().contiguous()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(Ast, Bst, M, N, Kd, a_mn=a_mn, b_mn=b_mn, epi=RP_EPI_BF16, out=out, bn=bn)
+    ref = A.float() @ Bm.float()
+    assert rel(out, ref) < 1e-2
+
+
+def test_gemm_persistent_grid_independent(K):
+    """Same bits whatever the CTA cap (what PaReprop's SM partitioning relies on)."""
+    from paper_2306_09342_b200._capi import RP_EPI_F32
+    M, N, Kd = 1024, 768, 4096
+    A = torch.randn(Kd, M, device="cuda").bfloat16()
+    Bm = torch.randn(Kd, N, device="cuda").bfloat16()
+    outs = []
+    for cap in (0, 5, 37):
+        o = torch.empty(M, N, device="cuda")
+        ws = torch.empty(4 * M * N, device="cuda")
+        K.gemm(A, Bm, M, N, Kd, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=4, workspace=ws,
+               max_ctas=cap)
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = A.float().t() @ Bm.float()
+    assert rel(outs[0], ref) < 1e-4
+
+
+@pytest.mark.parametrize("splits", [1, 3, 8])
+def test_gemm_wgrad_splitk(K, splits):
+    from paper_2306_09342_b200._capi import RP_EPI_F32
+    T, M, N = 5000, 384, 768
+    X = torch.randn(T, M, device="cuda").bfloat16()
+    dY = torch.randn(T, N, device="cuda").bfloat16()
+    o = torch.empty(M, N, device="cuda")
+    ws = torch.empty(splits * M * N, device="cuda")
+    K.gemm(X, dY, M, N, T, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=splits, workspace=ws)
+    ref = X.float().t() @ dY.float()
+    assert rel(o, ref) < 1e-4
+
+
+def test_gemm_bias_gelu(K):
+    from paper_2306_09342_b200._capi import RP_EPI_BIAS_GELU
+    M, N, Kd = 515, 1024, 192
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    W = (0.1 * torch.randn(Kd, N, device="cuda")).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    a = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU, out=a, out2=u, bias=bias)
+    uref = A.float() @ W.float() + bias
+    assert rel(u, uref) < 1e-2
+    assert rel(a, gelu_ref(uref)) < 1e-2
+
+
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_gemm_residual(K, sign):
+    from paper_2306_09342_b200._capi import RP_EPI_RESID
+    M, N, Kd = 700, 768, 3072
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    W = (0.05 * torch.randn(Kd, N, device="cuda")).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    res = torch.randn(M, N, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=out, aux=res, bias=bias,
+           sign=sign)
+    ref = res + sign * (A.float() @ W.float() + bias)
+    assert rel(out, ref) < 1e-4
+    # in place (out aliases the residual), as the inverse uses it
+    res2 = res.clone()
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=res2, aux=res2, bias=bias,
+           sign=sign)
+    assert torch.equal(res2, out)
+
+
+def test_gemm_gelu_bwd(K):
+    from paper_2306_09342_b200._capi import RP_EPI_GELU_BWD
+    M, N, Kd = 640, 3072, 768
+    dY = torch.randn(M, Kd, device="cuda").bfloat16()
+    W2 = (0.05 * torch.randn(N, Kd, device="cuda")).bfloat16()  # W2 is [h, d] = [N][K]
+    u = torch.randn(M, N, device="cuda").bfloat16()
+    du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(dY, W2, M, N, Kd, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD, out=du, aux=u)
+    ref = (dY.float() @ W2.float().t()) * gelu_slope_ref(u.float())
+    assert rel(du, ref) < 1e-2
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 768), (37, 192), (513, 1024), (64, 1664)])
+def test_layer_norm_fwd_bwd(K, rows, cols):
+    x = torch.randn(rows, cols, device="cuda") * 3 + 1
+    gamma = torch.randn(cols, device="cuda")
+    beta = torch.randn(cols, device="cuda")
+    y, mean, rstd = K.layer_norm_fwd(x, gamma, beta, 1e-5)
+    mu = x.mean(-1, keepdim=True)
+    var = ((x - mu) ** 2).mean(-1, keepdim=True)
+    xh = (x - mu) / torch.sqrt(var + 1e-5)
+    assert rel(y, xh * gamma + beta) < 1e-2
+    assert rel(rstd, 1 / torch.sqrt(var.squeeze(-1) + 1e-5)) < 1e-5
+    dy = torch.randn(rows, cols, device="cuda").bfloat16()
+    dres = torch.randn(rows, cols, device="cuda")
+    dxb = torch.empty(rows, cols, device="cuda", dtype=torch.bfloat16)
+    dx, dg, db = K.layer_norm_bwd(x, mean, rstd, gamma, dy, dres=dres, dx_bf16=dxb)
+    g = dy.float() * gamma
+    dx_ref = (g - g.mean(-1, keepdim=True) - xh * (g * xh).mean(-1, keepdim=True)) / torch.sqrt(
+        var + 1e-5) + dres
+    assert rel(dx, dx_ref) < 1e-4
+    assert rel(dxb, dx_ref) < 1e-2
+    assert rel(dg, (dy.float() * xh).sum(0)) < 1e-4
+    assert rel(db, dy.float().sum(0)) < 1e-4
+    # bit-reproducible
+    dx2, dg2, db2 = K.layer_norm_bwd(x, mean, rstd, gamma, dy, dres=dres)
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_colsum(K, dtype):
+    x = torch.randn(50432 // 8, 3072, device="cuda").to(dtype)
+    out = K.colsum(x)
+    assert rel(out, x.float().sum(0)) < 1e-4
+    assert torch.equal(out, K.colsum(x))
+
+
+def attn_ref(qkv, B, N, H, hd=64):
+    q, k, v = qkv.float().view(B, N, 3, H, hd).permute(2, 0, 3, 1, 4)
+    s = (q @ k.transpose(-1, -2)) / hd ** 0.5
+    p = torch.softmax(s, -1)
+    o = p @ v
+    return o.permute(0, 2, 1, 3).reshape(B * N, H * hd), torch.logsumexp(s, -1)
+
+
+@pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3)])
+def test_attention_fwd_bwd(K, B, N, H):
+    qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
+    out, lse = K.attention_fwd(qkv, B, N, H)
+    qkv_r = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = attn_ref(qkv_r, B, N, H)
+    assert rel(out, o_ref) < 1e-2
+    assert rel(lse / 1.4426950408889634, lse_ref) < 1e-4
+    dout = torch.randn(B * N, H * 64, device="cuda").bfloat16()
+    dqkv = K.attention_bwd(qkv, out, lse, dout, B, N, H)
+    o_ref.backward(dout.float())
+    g = qkv_r.grad
+    for i, name in enumerate("qkv"):
+        sl = slice(i * H * 64, (i + 1) * H * 64)
+        assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
+    assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H))
