@@ -90,7 +90,92 @@ int rp_gemm_plan_create(const RpGemmDesc* desc, RpGemmPlan** plan);
 int rp_gemm_plan_launch(const RpGemmPlan* plan, rp_stream_t stream);
 int rp_gemm_plan_set_max_ctas(RpGemmPlan* plan, int max_ctas);
 void rp_gemm_plan_destroy(RpGemmPlan* plan);
+int rp_gemm_plan_shape(const RpGemmPlan* plan, int64_t* M, int64_t* N, int64_t* K);
 int rp_gemm(const RpGemmDesc* desc, rp_stream_t stream);
+
+/* ------------------------------------------------------------------ LayerNorm / reductions
+ * rp_layer_norm_fwd: ref:proj/core/src/ops.cpp:264-304 (y = x_hat*gamma + beta, two-pass
+ *   population variance). x fp32 [rows, cols] -> y bf16, per-row mean / rstd (fp32).
+ * rp_layer_norm_bwd: ref:proj/core/src/ops.cpp:306-345, fused with the coupling's cotangent
+ *   add: dx = dres + LN^T(dy) (fp32, optional bf16 copy); dgamma/dbeta (+)= deterministic
+ *   column sums. workspace: rp_layer_norm_bwd_workspace_floats(rows, cols) floats.
+ * rp_colsum: ref:proj/core/src/layers.cpp:38-52 (col_sum, the MLP bias grads).
+ */
+int rp_layer_norm_fwd(const float* x, const float* gamma, const float* beta, int64_t rows,
+                      int64_t cols, double eps, uint16_t* y, float* mean, float* rstd,
+                      rp_stream_t stream);
+int rp_layer_norm_bwd(const float* x, const float* mean, const float* rstd, const float* gamma,
+                      const uint16_t* dy, const float* dres, int64_t rows, int64_t cols,
+                      float* dx, uint16_t* dx_bf16, float* dgamma, float* dbeta,
+                      float* workspace, int accumulate, rp_stream_t stream);
+int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols);
+int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t cols, float* out,
+              float* workspace, int accumulate, rp_stream_t stream);
+int64_t rp_colsum_workspace_floats(int64_t rows, int64_t cols);
+
+/* ------------------------------------------------------------------ attention (head_dim 64)
+ * Replaces the per-(batch, head, window) loops of ref:proj/core/src/layers.cpp:150-166
+ * (forward) and :185-208 (VJP). qkv [S*N, 3*H*64] bf16 (q | k | v, head i at column i*64,
+ * layers.cpp:144-146), S independent sequences (batch x windows) of N tokens.
+ * lse: [S][H][N] fp32 (log2 domain), kept instead of the probability tensor.
+ */
+int rp_attention_fwd(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64_t head_dim,
+                     uint16_t* out, float* lse, rp_stream_t stream);
+int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                     const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
+                     uint16_t* dqkv, float* workspace, rp_stream_t stream);
+int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
+
+/* ------------------------------------------------------------------ training engine
+ * Isotropic reversible model and its engines:
+ * step_reprop (mode 1) and step_pareprop (mode 2, two CUDA streams), SGD, optional
+ * data parallelism over NCCL. Parameters are one flat fp32 vector in the order
+ *   embed_w [in,d] | per block: w_qkv [d,3d], w_out [d,d], lnF_gamma [d], lnF_beta [d],
+ *   w1 [d,h], b1 [h], w2 [h,d], b2 [d], lnG_gamma [d], lnG_beta [d] | head_w [d,C]
+ * (weights [in, out] row-major, as ref layers.hpp:43-52, 94-103: y = x . W).
+ */
+typedef struct RpModelConfig {
+  int64_t depth, width, heads, hidden, seq_len, in_dim, num_classes, batch;
+  int64_t window;  /* tokens per attention window; 0 = full attention */
+  uint64_t seed;
+  int device;
+  int r_ctas; /* PaReprop: max CTAs per recompute-lane GEMM (0 = all SMs) */
+  int g_ctas; /* PaReprop: max CTAs per gradient-lane GEMM (0 = all SMs) */
+} RpModelConfig;
+
+typedef struct RpEngine RpEngine;
+int rp_engine_create(const RpModelConfig* cfg, RpEngine** engine);
+void rp_engine_destroy(RpEngine* engine);
+int64_t rp_engine_param_count(const RpEngine* engine);
+int rp_engine_tensor_table(const RpEngine* engine, int64_t* offsets, int64_t* numels,
+                           int64_t capacity);
+int rp_engine_init_params(RpEngine* engine, uint64_t seed);
+int rp_engine_synthetic_batch(RpEngine* engine, uint64_t seed);
+int rp_engine_set_params(RpEngine* engine, const float* host_params);
+int rp_engine_get_params(RpEngine* engine, float* host_params);
+int rp_engine_get_grads(RpEngine* engine, float* host_grads);
+int rp_engine_set_batch(RpEngine* engine, const uint16_t* host_inputs_bf16,
+                        const int32_t* host_labels);
+int rp_engine_set_batch_device(RpEngine* engine, const uint16_t* inputs_bf16,
+                               const int32_t* labels);
+int rp_engine_set_lr(RpEngine* engine, float lr);
+int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
+int rp_engine_step(RpEngine* engine, int mode, int use_graph);
+int rp_engine_sync(RpEngine* engine);
+int rp_engine_read_loss(RpEngine* engine, float* loss);
+void* rp_engine_stream(RpEngine* engine);
+int64_t rp_engine_graph_kernels(const RpEngine* engine, int mode);
+int rp_engine_gemm_profile(RpEngine* engine, int mode, double* ms, double* flops,
+                           int64_t* launches);
+int rp_engine_set_instrument(RpEngine* engine, int on);
+int rp_engine_slot_log(RpEngine* engine, float* out);
+int rp_nccl_unique_id(uint8_t* out128);
+int rp_engine_comm_init(RpEngine* engine, const uint8_t* id128, int world, int rank);
+int rp_engine_rev_forward(RpEngine* engine, int64_t block, const float* i1, const float* i2,
+                          float* o1, float* o2);
+int rp_engine_rev_backward_local(RpEngine* engine, int64_t block, const float* o1,
+                                 const float* o2, const float* d_o1, const float* d_o2,
+                                 float* i1, float* i2, float* d_i1, float* d_i2);
 
 #ifdef __cplusplus
 }

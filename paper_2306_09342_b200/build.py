@@ -30,7 +30,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + str(ROOT / "include"),
           "-I" + str(CSRC)]
 NVFLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-LINK_LIBS = ["-lpthread"]
+LINK_LIBS = ["-lnccl", "-lpthread"]
 
 
 def _sources() -> list[Path]:

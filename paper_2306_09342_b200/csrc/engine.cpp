@@ -1,0 +1,930 @@
+// The reversible training engine (host C++ over the sm_100a kernels).
+//
+// Implements the SPEC's engines module for the isotropic model on one B200:
+//   step_reprop  forward storing only the stage boundary, backward
+//                                     block L..1 with fused recompute + VJP, one lane
+//   step_pareprop  the same work split over two CUDA streams: lane R
+//                                     recomputes block i-1 while lane G runs block i's VJP
+//   sgd_update  per-bucket, overlapped with the backward
+// plus data parallelism over the GPUs of one box: one fp32 gradient bucket per block,
+// ncclAllReduce'd on a comm stream as soon as lane G finishes that block.
+//
+// Memory is a static arena sized at creation; the step never allocates (the paper's
+// "synchronous memory freeing" pitfall, §3.3, cannot occur). The coupled residual
+// stream and all cotangents are fp32; GEMM operands are bf16 shadows.
+//
+// Buffer rotation (block b maps X_b -> X_{b+1}, X_0 = (e, e) is the stored stage input):
+//   X_j.i1 lives in buf1[j % 2], X_j.i2 in buf2[j % 3] (j >= 1); block-b caches in slot[b % 2].
+//   R(b) writes buf1[b%2], buf2[b%3], slot[b%2]: exactly what VJP(b+2) reads, so R(b) waits
+//   on G_done[b+2] -- the capacity-1 rendezvous of SPEC.md:381/415/420 (R at most one
+//   block ahead, <= 2 blocks of caches live).
+// Every kernel's arithmetic is independent of grid size and stream co-residency, so
+// PaReprop reproduces Reprop bit for bit.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/revprop_b200.h"
+#include "kernels.h"
+#include "model_kernels.h"
+
+namespace {
+
+constexpr int kSms = 148;
+
+struct Slot {
+  uint16_t *hF = nullptr, *qkv = nullptr, *att = nullptr, *hG = nullptr, *u = nullptr,
+           *a = nullptr;
+  float *lse = nullptr, *meanF = nullptr, *rstdF = nullptr, *meanG = nullptr, *rstdG = nullptr;
+};
+
+struct BlockPlans {
+  // lane R (recompute) -- also used by the forward with +1 residual sign
+  RpGemmPlan *r_w1 = nullptr, *r_w2 = nullptr, *r_qkv = nullptr, *r_proj = nullptr;
+  RpGemmPlan *f_qkv = nullptr, *f_proj = nullptr, *f_w1 = nullptr, *f_w2 = nullptr;
+  // lane G (VJP)
+  RpGemmPlan *g_dw2 = nullptr, *g_ww2 = nullptr, *g_ww1 = nullptr, *g_dw1 = nullptr,
+             *g_dproj = nullptr, *g_wproj = nullptr, *g_wqkv = nullptr, *g_dqkv = nullptr;
+};
+
+int pick_splits(int64_t M, int64_t N, int64_t K, int bn) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int64_t kb = (K + 63) / 64;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 64; ++s) {
+    if (kb / s < 8) break;  // keep >= 8 k-blocks per split
+    const int64_t units = tiles * s;
+    const double waves = static_cast<double>((units + kSms - 1) / kSms);
+    const double eff = static_cast<double>(units) / (waves * kSms) - 0.004 * s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+struct RpEngine {
+  RpModelConfig cfg{};
+  int64_t B = 0, N = 0, d = 0, h = 0, H = 0, in = 0, C = 0, L = 0, T = 0, W = 0;
+  int64_t P = 0, block_size = 0;
+  std::vector<int64_t> t_off, t_numel;  // flat tensor table
+  int dev = 0;
+  cudaStream_t sG = nullptr, sR = nullptr, sC = nullptr;
+  std::vector<cudaEvent_t> evR, evG;
+  cudaEvent_t evFwd = nullptr, evCommDone = nullptr, evRDone = nullptr, evEmbed = nullptr;
+  std::vector<cudaEvent_t> ts;  // timing events for the slot log (eager, instrumented)
+  bool instrument = false;
+  // parameters
+  float *params = nullptr, *grads = nullptr, *lr = nullptr;
+  uint16_t* pb = nullptr;
+  // data
+  uint16_t* inputs = nullptr;
+  int32_t* labels = nullptr;
+  // activations
+  float* e = nullptr;
+  float* buf1[2] = {nullptr, nullptr};
+  float* buf2[3] = {nullptr, nullptr, nullptr};
+  Slot slot[2];
+  // lane G temporaries
+  float *d1 = nullptr, *d2 = nullptr;
+  uint16_t *d1b = nullptr, *d2b = nullptr, *du = nullptr, *dh = nullptr, *datt = nullptr,
+           *dqkv = nullptr, *deb = nullptr;
+  float *ln_ws = nullptr, *col_ws = nullptr, *split_ws = nullptr, *attn_ws = nullptr;
+  // head
+  float *pooled = nullptr, *logits = nullptr, *dlogits = nullptr, *row_loss = nullptr,
+        *loss = nullptr, *dpooled = nullptr;
+  std::vector<BlockPlans> plans;
+  RpGemmPlan *p_embed = nullptr, *p_embed_w = nullptr;
+  std::vector<RpGemmPlan*> all_plans;
+  // graphs: index by mode (1 reprop, 2 pareprop)
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+  int r_ctas = 0, g_ctas = 0;  // PaReprop SM partition (0 = all)
+  std::vector<void*> allocs;
+  // live GEMM profiling (eager steps only)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+  std::vector<double> prof_flops;
+  size_t prof_used = 0;
+  int64_t graph_kernels[3] = {0, 0, 0};
+};
+
+namespace {
+
+#define RP_TRY(x)                 \
+  do {                            \
+    int rc_ = (x);                \
+    if (rc_ != RP_OK) return rc_; \
+  } while (0)
+
+int cuda_ok(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RP_OK;
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return rp_fail(RP_ERR_CUDA, m.c_str());
+}
+
+template <class T>
+int dalloc(RpEngine* g, T** p, int64_t count) {
+  void* q = nullptr;
+  const size_t bytes = static_cast<size_t>(count > 0 ? count : 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    std::string m = "device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                    cudaGetErrorString(e);
+    return rp_fail(RP_ERR_BUDGET, m.c_str());
+  }
+  g->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return RP_OK;
+}
+
+// tensor index helpers (flat order, SPEC.md:279-282 Model fields)
+enum BlockTensor { kWqkv = 0, kWout, kLnFg, kLnFb, kW1, kB1, kW2, kB2, kLnGg, kLnGb, kPerBlock };
+inline int64_t tix_block(int64_t b, int t) { return 1 + kPerBlock * b + t; }
+
+struct GemmArgs {
+  const uint16_t* A;
+  int64_t lda;
+  int a_mn;
+  const uint16_t* B;
+  int64_t ldb;
+  int b_mn;
+  int64_t M, N, K;
+  int epi;
+  void* out;
+  int64_t ldo;
+  void* out2 = nullptr;
+  const void* aux = nullptr;
+  int64_t ldaux = 0;
+  const float* bias = nullptr;
+  float sign = 1.f;
+  int splits = 1;
+  float* ws = nullptr;
+};
+
+int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
+  RpGemmDesc d{};
+  d.A = a.A;
+  d.lda = a.lda;
+  d.a_mn = a.a_mn;
+  d.B = a.B;
+  d.ldb = a.ldb;
+  d.b_mn = a.b_mn;
+  d.M = a.M;
+  d.N = a.N;
+  d.K = a.K;
+  d.epi = a.epi;
+  d.out = a.out;
+  d.ldo = a.ldo;
+  d.out2 = a.out2;
+  d.ldo2 = a.ldo;
+  d.aux = a.aux;
+  d.ldaux = a.ldaux ? a.ldaux : a.ldo;
+  d.bias = a.bias;
+  d.sign = a.sign;
+  d.splits = a.splits;
+  d.workspace = a.ws;
+  d.max_ctas = 0;
+  d.bn = 256;
+  int rc = rp_gemm_plan_create(&d, out);
+  if (rc != RP_OK) return rp_fail(rc, "engine: gemm plan creation failed");
+  g->all_plans.push_back(*out);
+  return RP_OK;
+}
+
+const uint16_t* wb(const RpEngine* g, int64_t tix) { return g->pb + g->t_off[tix]; }
+const float* wf(const RpEngine* g, int64_t tix) { return g->params + g->t_off[tix]; }
+float* gr(const RpEngine* g, int64_t tix) { return g->grads + g->t_off[tix]; }
+
+float* X1(RpEngine* g, int64_t j) { return j == 0 ? g->e : g->buf1[j % 2]; }
+float* X2(RpEngine* g, int64_t j) { return j == 0 ? g->e : g->buf2[j % 3]; }
+
+int build_plans(RpEngine* g) {
+  const int64_t T = g->T, d = g->d, h = g->h;
+  const int s_qkv = pick_splits(d, 3 * d, T, 256), s_proj = pick_splits(d, d, T, 256),
+            s_w1 = pick_splits(d, h, T, 256), s_w2 = pick_splits(h, d, T, 256),
+            s_emb = pick_splits(g->in, d, T, 256);
+  g->plans.resize(static_cast<size_t>(g->L));
+  for (int64_t b = 0; b < g->L; ++b) {
+    BlockPlans& p = g->plans[static_cast<size_t>(b)];
+    Slot& S = g->slot[b % 2];
+    Slot& F = g->slot[0];  // forward temporaries
+    const uint16_t *Wqkv = wb(g, tix_block(b, kWqkv)), *Wout = wb(g, tix_block(b, kWout)),
+                   *W1 = wb(g, tix_block(b, kW1)), *W2 = wb(g, tix_block(b, kW2));
+    const float *b1 = wf(g, tix_block(b, kB1)), *b2 = wf(g, tix_block(b, kB2));
+    // ---- forward (stores nothing)
+    RP_TRY(mk_plan(g, {F.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, F.qkv, 3 * d},
+                   &p.f_qkv));
+    {
+      GemmArgs a{F.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, b + 1), d};
+      a.aux = X2(g, b);
+      RP_TRY(mk_plan(g, a, &p.f_proj));
+    }
+    {
+      GemmArgs a{F.hF, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU, F.a, h};
+      a.bias = b1;
+      RP_TRY(mk_plan(g, a, &p.f_w1));
+    }
+    {
+      GemmArgs a{F.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, b + 1), d};
+      a.aux = X1(g, b);
+      a.bias = b2;
+      RP_TRY(mk_plan(g, a, &p.f_w2));
+    }
+    // ---- lane R: inverse with caches
+    {
+      GemmArgs a{S.hG, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU, S.a, h};
+      a.out2 = S.u;
+      a.bias = b1;
+      RP_TRY(mk_plan(g, a, &p.r_w1));
+    }
+    RP_TRY(mk_plan(g, {S.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, S.qkv, 3 * d},
+                   &p.r_qkv));
+    if (b > 0) {
+      GemmArgs a{S.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, b), d};
+      a.aux = X1(g, b + 1);
+      a.bias = b2;
+      a.sign = -1.f;
+      RP_TRY(mk_plan(g, a, &p.r_w2));
+      GemmArgs c{S.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, b), d};
+      c.aux = X2(g, b + 1);
+      c.sign = -1.f;
+      RP_TRY(mk_plan(g, c, &p.r_proj));
+    }
+    // ---- lane G: VJPs (layers.cpp:171-220, 241-259)
+    {
+      GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_GELU_BWD, g->du, h};
+      a.aux = S.u;
+      RP_TRY(mk_plan(g, a, &p.g_dw2));  // d_u = gelu'(u) * (d_o1 . W2^T)
+    }
+    {
+      GemmArgs a{S.a, h, 1, g->d1b, d, 1, h, d, T, RP_EPI_F32, gr(g, tix_block(b, kW2)), d};
+      a.splits = s_w2;
+      a.ws = g->split_ws;
+      RP_TRY(mk_plan(g, a, &p.g_ww2));  // dW2 = a^T d_o1
+    }
+    {
+      GemmArgs a{S.hG, d, 1, g->du, h, 1, d, h, T, RP_EPI_F32, gr(g, tix_block(b, kW1)), h};
+      a.splits = s_w1;
+      a.ws = g->split_ws;
+      RP_TRY(mk_plan(g, a, &p.g_ww1));  // dW1 = hG^T d_u
+    }
+    RP_TRY(mk_plan(g, {g->du, h, 0, W1, h, 0, T, d, h, RP_EPI_BF16, g->dh, d}, &p.g_dw1));
+    RP_TRY(mk_plan(g, {g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_BF16, g->datt, d}, &p.g_dproj));
+    {
+      GemmArgs a{S.att, d, 1, g->d2b, d, 1, d, d, T, RP_EPI_F32, gr(g, tix_block(b, kWout)), d};
+      a.splits = s_proj;
+      a.ws = g->split_ws;
+      RP_TRY(mk_plan(g, a, &p.g_wproj));
+    }
+    {
+      GemmArgs a{S.hF, d, 1, g->dqkv, 3 * d, 1, d, 3 * d, T, RP_EPI_F32,
+                 gr(g, tix_block(b, kWqkv)), 3 * d};
+      a.splits = s_qkv;
+      a.ws = g->split_ws;
+      RP_TRY(mk_plan(g, a, &p.g_wqkv));
+    }
+    RP_TRY(mk_plan(g, {g->dqkv, 3 * d, 0, Wqkv, 3 * d, 0, T, d, 3 * d, RP_EPI_BF16, g->dh, d},
+                   &p.g_dqkv));
+  }
+  // embedding: e = x . embed_w ; d_embed_w = x^T . (d_i1 + d_i2)
+  RP_TRY(mk_plan(g, {g->inputs, g->in, 0, wb(g, 0), d, 1, T, d, g->in, RP_EPI_F32, g->e, d},
+                 &g->p_embed));
+  {
+    GemmArgs a{g->inputs, g->in, 1, g->deb, d, 1, g->in, d, T, RP_EPI_F32, gr(g, 0), d};
+    a.splits = s_emb;
+    a.ws = g->split_ws;
+    RP_TRY(mk_plan(g, a, &g->p_embed_w));
+  }
+  return RP_OK;
+}
+
+// GEMM timing (live roofline): when g->prof is set, every plan launch is bracketed by
+// CUDA events on its own stream; rp_engine_gemm_profile() sums durations and FLOPs.
+struct GemmProf {
+  cudaEvent_t a, b;
+  double flops;
+};
+thread_local RpEngine* t_prof_engine = nullptr;
+
+int launch(RpGemmPlan* p, cudaStream_t s);
+
+int launch(RpGemmPlan* p, cudaStream_t s) {
+  RpEngine* g = t_prof_engine;
+  if (!g || !g->prof) return rp_gemm_plan_launch(p, s);
+  if (g->prof_used == g->prof_ev.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    g->prof_ev.push_back({a, b});
+    g->prof_flops.push_back(0.0);
+  }
+  auto& ev = g->prof_ev[g->prof_used];
+  int64_t M, N, K;
+  rp_gemm_plan_shape(p, &M, &N, &K);
+  g->prof_flops[g->prof_used] = 2.0 * static_cast<double>(M) * N * K;
+  ++g->prof_used;
+  cudaEventRecord(ev.first, s);
+  const int rc = rp_gemm_plan_launch(p, s);
+  cudaEventRecord(ev.second, s);
+  return rc;
+}
+
+int ln_fwd(RpEngine* g, const float* x, int64_t tg, int64_t tb, uint16_t* y, float* mean,
+           float* rstd, cudaStream_t s) {
+  return rp_layer_norm_fwd(x, wf(g, tg), wf(g, tb), g->T, g->d, 1e-5, y, mean, rstd, s);
+}
+
+int attn_fwd(RpEngine* g, const uint16_t* qkv, uint16_t* att, float* lse, cudaStream_t s) {
+  return rp_attention_fwd(qkv, g->T / g->W, g->W, g->H, 64, att, lse, s);
+}
+
+void mark(RpEngine* g, int lane, int64_t b, int which, cudaStream_t s) {
+  if (!g->instrument) return;
+  cudaEventRecord(g->ts[static_cast<size_t>(((lane * g->L) + b) * 2 + which)], s);
+}
+
+int forward(RpEngine* g, cudaStream_t s) {
+  RP_TRY(launch(g->p_embed, s));
+  Slot& F = g->slot[0];
+  for (int64_t b = 0; b < g->L; ++b) {
+    BlockPlans& p = g->plans[static_cast<size_t>(b)];
+    RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), F.hF, F.meanF, F.rstdF, s));
+    RP_TRY(launch(p.f_qkv, s));
+    RP_TRY(attn_fwd(g, F.qkv, F.att, F.lse, s));
+    RP_TRY(launch(p.f_proj, s));  // o2 = i2 + F(i1)
+    RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), F.hF, F.meanF,
+                  F.rstdF, s));
+    RP_TRY(launch(p.f_w1, s));
+    RP_TRY(launch(p.f_w2, s));  // o1 = i1 + G(o2)
+  }
+  return RP_OK;
+}
+
+int head(RpEngine* g, cudaStream_t s) {
+  const int64_t B = g->B, d = g->d, C = g->C;
+  const float* hw = wf(g, 1 + kPerBlock * g->L);
+  RP_TRY(rpk_pool(X1(g, g->L), X2(g, g->L), B, g->N, d, g->pooled, s));
+  RP_TRY(rpk_simt_gemm(B, C, d, g->pooled, d, 1, hw, C, 1, g->logits, C, s));
+  RP_TRY(rpk_cross_entropy(g->logits, g->labels, B, C, g->dlogits, g->row_loss, g->loss, s));
+  RP_TRY(rpk_simt_gemm(d, C, B, g->pooled, 1, d, g->dlogits, C, 1, gr(g, 1 + kPerBlock * g->L),
+                       C, s));
+  RP_TRY(rpk_simt_gemm(B, d, C, g->dlogits, C, 1, hw, 1, C, g->dpooled, d, s));
+  RP_TRY(rpk_spread(g->dpooled, B, g->N, d, g->d1, g->d2, g->d1b, g->d2b, s));
+  return RP_OK;
+}
+
+// Lane R: recompute block b's input and caches from its output X_{b+1}.
+int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  Slot& S = g->slot[b % 2];
+  mark(g, 0, b, 0, s);
+  RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), S.hG, S.meanG,
+                S.rstdG, s));
+  RP_TRY(launch(p.r_w1, s));
+  if (b > 0) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
+  RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), S.hF, S.meanF, S.rstdF, s));
+  RP_TRY(launch(p.r_qkv, s));
+  RP_TRY(attn_fwd(g, S.qkv, S.att, S.lse, s));
+  if (b > 0) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
+  mark(g, 0, b, 1, s);
+  return RP_OK;
+}
+
+// Lane G: the VJP half of rev_backward_local, G-path before F-path.
+int lane_g(RpEngine* g, int64_t b, cudaStream_t s) {
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  Slot& S = g->slot[b % 2];
+  const int64_t T = g->T, d = g->d, h = g->h;
+  mark(g, 1, b, 0, s);
+  // ---- G = MLP VJP with d_o1 (layers.cpp:241-259)
+  RP_TRY(launch(p.g_dw2, s));
+  RP_TRY(launch(p.g_ww2, s));
+  RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
+  RP_TRY(launch(p.g_ww1, s));
+  RP_TRY(rp_colsum(g->du, 1, T, h, gr(g, tix_block(b, kB1)), g->col_ws, 0, s));
+  RP_TRY(launch(p.g_dw1, s));
+  // d_o2t = d_o2 + LN_G^T(d_hG)   (in place in d2 / d2b)
+  RP_TRY(rp_layer_norm_bwd(X2(g, b + 1), S.meanG, S.rstdG, wf(g, tix_block(b, kLnGg)), g->dh,
+                           g->d2, T, d, g->d2, g->d2b, gr(g, tix_block(b, kLnGg)),
+                           gr(g, tix_block(b, kLnGb)), g->ln_ws, 0, s));
+  // ---- F = attention VJP with d_o2t (layers.cpp:171-220)
+  RP_TRY(launch(p.g_dproj, s));
+  RP_TRY(launch(p.g_wproj, s));
+  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / g->W, g->W, g->H, 64, g->dqkv,
+                          g->attn_ws, s));
+  RP_TRY(launch(p.g_wqkv, s));
+  RP_TRY(launch(p.g_dqkv, s));
+  // d_i1 = d_o1 + LN_F^T(d_hF)    (in place in d1 / d1b); d_i2 = d_o2t (already in d2)
+  RP_TRY(rp_layer_norm_bwd(X1(g, b), S.meanF, S.rstdF, wf(g, tix_block(b, kLnFg)), g->dh, g->d1,
+                           T, d, g->d1, g->d1b, gr(g, tix_block(b, kLnFg)),
+                           gr(g, tix_block(b, kLnFb)), g->ln_ws, 0, s));
+  mark(g, 1, b, 1, s);
+  return RP_OK;
+}
+
+// bucket b (block params) -> allreduce (DP) -> SGD, on the comm stream
+int bucket_update(RpEngine* g, int64_t off, int64_t n, cudaStream_t s) {
+  if (g->world > 1) {
+    ncclResult_t r = ncclAllReduce(g->grads + off, g->grads + off, static_cast<size_t>(n),
+                                   ncclFloat32, ncclSum, g->comm, s);
+    if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
+  }
+  return rpk_sgd(g->params + off, g->grads + off, g->pb + off, n, g->lr,
+                 1.0f / static_cast<float>(g->world), s);
+}
+
+int enqueue_step(RpEngine* g, int mode) {
+  cudaStream_t sG = g->sG, sR = g->sR, sC = g->sC;
+  t_prof_engine = g;
+  g->prof_used = 0;
+  RP_TRY(forward(g, sG));
+  RP_TRY(head(g, sG));
+  RP_TRY(cuda_ok(cudaEventRecord(g->evFwd, sG), "record"));
+  // the head bucket can go as soon as the head backward is done
+  RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evFwd, 0), "wait"));
+  const int64_t head_off = g->t_off[1 + kPerBlock * g->L];
+  RP_TRY(bucket_update(g, head_off, g->d * g->C, sC));
+  if (mode == 2) {
+    RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evFwd, 0), "wait"));
+    for (int64_t b = g->L - 1; b >= 0; --b) {
+      if (b + 2 <= g->L - 1)
+        RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evG[static_cast<size_t>(b + 2)], 0), "wait"));
+      RP_TRY(lane_r(g, b, sR));
+      RP_TRY(cuda_ok(cudaEventRecord(g->evR[static_cast<size_t>(b)], sR), "record"));
+      RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
+      RP_TRY(lane_g(g, b, sG));
+      RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
+      RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
+      RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
+    }
+    RP_TRY(cuda_ok(cudaEventRecord(g->evRDone, sR), "record"));
+  } else {
+    for (int64_t b = g->L - 1; b >= 0; --b) {
+      RP_TRY(lane_r(g, b, sG));
+      RP_TRY(lane_g(g, b, sG));
+      RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
+      RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
+      RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
+    }
+  }
+  // embedding backward: e fed both halves -> d_e = d_i1 + d_i2
+  RP_TRY(rpk_add_to_bf16(g->d1, g->d2, g->deb, g->T * g->d, sG));
+  RP_TRY(launch(g->p_embed_w, sG));
+  RP_TRY(cuda_ok(cudaEventRecord(g->evEmbed, sG), "record"));
+  RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evEmbed, 0), "wait"));
+  RP_TRY(bucket_update(g, 0, g->in * g->d, sC));
+  if (g->world > 1) {
+    ncclResult_t r = ncclAllReduce(g->loss, g->loss, 1, ncclFloat32, ncclAvg, g->comm, sC);
+    if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
+  }
+  RP_TRY(cuda_ok(cudaEventRecord(g->evCommDone, sC), "record"));
+  RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evCommDone, 0), "wait"));
+  if (mode == 2) RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evRDone, 0), "wait"));
+  return rp_check_launch("engine step");
+}
+
+void set_partition(RpEngine* g, int mode) {
+  const int r = (mode == 2) ? g->r_ctas : 0;
+  const int gg = (mode == 2) ? g->g_ctas : 0;
+  for (auto& p : g->plans) {
+    for (RpGemmPlan* q : {p.r_w1, p.r_w2, p.r_qkv, p.r_proj})
+      if (q) rp_gemm_plan_set_max_ctas(q, r);
+    for (RpGemmPlan* q : {p.g_dw2, p.g_ww2, p.g_ww1, p.g_dw1, p.g_dproj, p.g_wproj, p.g_wqkv,
+                          p.g_dqkv})
+      if (q) rp_gemm_plan_set_max_ctas(q, gg);
+  }
+}
+
+}  // namespace
+
+extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
+  if (!c || !out) return rp_fail(RP_ERR_CONTRACT, "engine_create: null argument");
+  *out = nullptr;
+  if (c->depth < 1 || c->width < 16 || c->heads < 1 || c->width % c->heads ||
+      c->width / c->heads != 64 || c->hidden < 16 || c->seq_len < 1 || c->in_dim < 8 ||
+      c->num_classes < 1 || c->batch < 1)
+    return rp_fail(RP_ERR_CONFIG, "engine_create: invalid model config (head_dim must be 64)");
+  if (c->width % 16 || c->hidden % 16 || c->in_dim % 16)
+    return rp_fail(RP_ERR_CONFIG, "engine_create: width/hidden/in_dim must be multiples of 16");
+  const int64_t W = c->window > 0 ? c->window : c->seq_len;
+  if (c->seq_len % W) return rp_fail(RP_ERR_SHAPE, "attention: sequence length not divisible by window");
+  RpEngine* g = new RpEngine();
+  g->cfg = *c;
+  g->B = c->batch;
+  g->N = c->seq_len;
+  g->d = c->width;
+  g->h = c->hidden;
+  g->H = c->heads;
+  g->in = c->in_dim;
+  g->C = c->num_classes;
+  g->L = c->depth;
+  g->W = W;
+  g->T = g->B * g->N;
+  g->dev = c->device;
+  const int64_t d = g->d, h = g->h, T = g->T;
+  auto fail = [&](int rc) {
+    rp_engine_destroy(g);
+    return rc;
+  };
+  if (cudaSetDevice(g->dev) != cudaSuccess) return fail(rp_fail(RP_ERR_CUDA, "cudaSetDevice failed"));
+  // flat tensor table
+  auto add = [&](int64_t n) {
+    const int64_t off = g->t_off.empty() ? 0 : g->t_off.back() + g->t_numel.back();
+    g->t_off.push_back(off);
+    g->t_numel.push_back(n);
+  };
+  add(g->in * d);
+  for (int64_t b = 0; b < g->L; ++b) {
+    add(d * 3 * d);
+    add(d * d);
+    add(d);
+    add(d);
+    add(d * h);
+    add(h);
+    add(h * d);
+    add(d);
+    add(d);
+    add(d);
+  }
+  add(d * g->C);
+  g->P = g->t_off.back() + g->t_numel.back();
+  g->block_size = 4 * d * d + 2 * d * h + h + 5 * d;
+  int rc = RP_OK;
+  if ((rc = cuda_ok(cudaStreamCreateWithFlags(&g->sG, cudaStreamNonBlocking), "stream")) ||
+      (rc = cuda_ok(cudaStreamCreateWithFlags(&g->sR, cudaStreamNonBlocking), "stream")) ||
+      (rc = cuda_ok(cudaStreamCreateWithFlags(&g->sC, cudaStreamNonBlocking), "stream")))
+    return fail(rc);
+  g->evR.resize(static_cast<size_t>(g->L));
+  g->evG.resize(static_cast<size_t>(g->L));
+  for (auto* v : {&g->evR, &g->evG})
+    for (auto& e : *v) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed})
+    cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+  g->ts.resize(static_cast<size_t>(4 * g->L));
+  for (auto& e : g->ts) cudaEventCreate(&e);
+  // arena
+  if ((rc = dalloc(g, &g->params, g->P)) || (rc = dalloc(g, &g->grads, g->P)) ||
+      (rc = dalloc(g, &g->pb, g->P)) || (rc = dalloc(g, &g->lr, 1)) ||
+      (rc = dalloc(g, &g->inputs, T * g->in)) || (rc = dalloc(g, &g->labels, g->B)) ||
+      (rc = dalloc(g, &g->e, T * d)) || (rc = dalloc(g, &g->buf1[0], T * d)) ||
+      (rc = dalloc(g, &g->buf1[1], T * d)) || (rc = dalloc(g, &g->buf2[0], T * d)) ||
+      (rc = dalloc(g, &g->buf2[1], T * d)) || (rc = dalloc(g, &g->buf2[2], T * d)))
+    return fail(rc);
+  for (Slot& S : g->slot) {
+    if ((rc = dalloc(g, &S.hF, T * d)) || (rc = dalloc(g, &S.qkv, T * 3 * d)) ||
+        (rc = dalloc(g, &S.att, T * d)) || (rc = dalloc(g, &S.hG, T * d)) ||
+        (rc = dalloc(g, &S.u, T * h)) || (rc = dalloc(g, &S.a, T * h)) ||
+        (rc = dalloc(g, &S.lse, T * g->H)) || (rc = dalloc(g, &S.meanF, T)) ||
+        (rc = dalloc(g, &S.rstdF, T)) || (rc = dalloc(g, &S.meanG, T)) ||
+        (rc = dalloc(g, &S.rstdG, T)))
+      return fail(rc);
+  }
+  int64_t split_ws = 0;
+  for (auto mn : {std::pair<int64_t, int64_t>{d, 3 * d}, {d, d}, {d, h}, {h, d}, {g->in, d}}) {
+    const int s = pick_splits(mn.first, mn.second, T, 256);
+    if (s > 1) split_ws = std::max<int64_t>(split_ws, s * mn.first * mn.second);
+  }
+  const int64_t col_ws = rp_colsum_workspace_floats(T, h > d ? h : d);
+  if ((rc = dalloc(g, &g->d1, T * d)) || (rc = dalloc(g, &g->d2, T * d)) ||
+      (rc = dalloc(g, &g->d1b, T * d)) || (rc = dalloc(g, &g->d2b, T * d)) ||
+      (rc = dalloc(g, &g->du, T * h)) || (rc = dalloc(g, &g->dh, T * d)) ||
+      (rc = dalloc(g, &g->datt, T * d)) || (rc = dalloc(g, &g->dqkv, T * 3 * d)) ||
+      (rc = dalloc(g, &g->deb, T * d)) ||
+      (rc = dalloc(g, &g->ln_ws, rp_layer_norm_bwd_workspace_floats(T, d))) ||
+      (rc = dalloc(g, &g->col_ws, col_ws)) || (rc = dalloc(g, &g->split_ws, split_ws)) ||
+      (rc = dalloc(g, &g->attn_ws, rp_attention_bwd_workspace_floats(T / W, W, g->H))) ||
+      (rc = dalloc(g, &g->pooled, g->B * d)) || (rc = dalloc(g, &g->logits, g->B * g->C)) ||
+      (rc = dalloc(g, &g->dlogits, g->B * g->C)) || (rc = dalloc(g, &g->row_loss, g->B)) ||
+      (rc = dalloc(g, &g->loss, 1)) || (rc = dalloc(g, &g->dpooled, g->B * d)))
+    return fail(rc);
+  if ((rc = build_plans(g))) return fail(rc);
+  // default PaReprop SM partition: recompute : VJP work is ~1 : 2
+  g->r_ctas = c->r_ctas > 0 ? c->r_ctas : 0;
+  g->g_ctas = c->g_ctas > 0 ? c->g_ctas : 0;
+  // initial parameters + synthetic batch from the counter RNG
+  if ((rc = rp_engine_init_params(g, c->seed)) || (rc = rp_engine_synthetic_batch(g, c->seed)))
+    return fail(rc);
+  const float lr0 = 0.f;
+  cudaMemcpy(g->lr, &lr0, sizeof(float), cudaMemcpyHostToDevice);
+  cudaMemset(g->grads, 0, static_cast<size_t>(g->P) * sizeof(float));
+  if ((rc = cuda_ok(cudaDeviceSynchronize(), "engine_create"))) return fail(rc);
+  *out = g;
+  return RP_OK;
+}
+
+extern "C" void rp_engine_destroy(RpEngine* g) {
+  if (!g) return;
+  cudaDeviceSynchronize();
+  for (auto& x : g->graph)
+    if (x) cudaGraphExecDestroy(x);
+  for (RpGemmPlan* p : g->all_plans) rp_gemm_plan_destroy(p);
+  for (void* p : g->allocs) cudaFree(p);
+  for (auto* v : {&g->evR, &g->evG, &g->ts})
+    for (auto& e : *v)
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {g->sG, g->sR, g->sC})
+    if (s) cudaStreamDestroy(s);
+  if (g->comm) ncclCommDestroy(g->comm);
+  delete g;
+}
+
+extern "C" int64_t rp_engine_param_count(const RpEngine* g) { return g ? g->P : -1; }
+
+extern "C" int rp_engine_tensor_table(const RpEngine* g, int64_t* offsets, int64_t* numels,
+                                      int64_t cap) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  const int64_t n = static_cast<int64_t>(g->t_off.size());
+  if (cap < n) return rp_fail(RP_ERR_SHAPE, "tensor table capacity too small");
+  for (int64_t i = 0; i < n; ++i) {
+    offsets[i] = g->t_off[static_cast<size_t>(i)];
+    numels[i] = g->t_numel[static_cast<size_t>(i)];
+  }
+  return static_cast<int>(n);
+}
+
+extern "C" int rp_engine_init_params(RpEngine* g, uint64_t seed) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  // weights trunc-normal(0.02), biases zero; LayerNorm gamma = 1, beta = 0.
+  for (size_t j = 0; j < g->t_off.size(); ++j) {
+    int kind = 0;
+    if (j >= 1 && j < 1 + static_cast<size_t>(kPerBlock * g->L)) {
+      const int t = static_cast<int>((j - 1) % kPerBlock);
+      if (t == kB1 || t == kB2 || t == kLnFb || t == kLnGb) kind = 1;
+      if (t == kLnFg || t == kLnGg) kind = 2;
+    }
+    RP_TRY(rpk_init_tensor(g->params + g->t_off[j], g->t_numel[j], seed, j, kind, 0.02, g->sG));
+  }
+  RP_TRY(rpk_f32_to_bf16(g->params, g->pb, g->P, g->sG));
+  return cuda_ok(cudaStreamSynchronize(g->sG), "init_params");
+}
+
+extern "C" int rp_engine_synthetic_batch(RpEngine* g, uint64_t seed) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  RP_TRY(rpk_init_inputs(g->inputs, g->T * g->in, seed, g->sG));
+  std::vector<int32_t> lab(static_cast<size_t>(g->B));
+  // labels: Rng(seed, 3<<56).next_int(0, C) in batch order (rng.hpp:53-57)
+  for (int64_t b = 0; b < g->B; ++b)
+    lab[static_cast<size_t>(b)] = static_cast<int32_t>(
+        rp_rng_u64_host(seed, 3ull << 56, static_cast<uint64_t>(b)) % static_cast<uint64_t>(g->C));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->labels, lab.data(), lab.size() * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, g->sG),
+                 "labels"));
+  return cuda_ok(cudaStreamSynchronize(g->sG), "synthetic_batch");
+}
+
+extern "C" int rp_engine_set_params(RpEngine* g, const float* host) {
+  if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->params, host, static_cast<size_t>(g->P) * 4,
+                                 cudaMemcpyHostToDevice, g->sG),
+                 "set_params"));
+  RP_TRY(rpk_f32_to_bf16(g->params, g->pb, g->P, g->sG));
+  return cuda_ok(cudaStreamSynchronize(g->sG), "set_params");
+}
+
+extern "C" int rp_engine_get_params(RpEngine* g, float* host) {
+  if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  return cuda_ok(cudaMemcpy(host, g->params, static_cast<size_t>(g->P) * 4, cudaMemcpyDeviceToHost),
+                 "get_params");
+}
+
+extern "C" int rp_engine_get_grads(RpEngine* g, float* host) {
+  if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  return cuda_ok(cudaMemcpy(host, g->grads, static_cast<size_t>(g->P) * 4, cudaMemcpyDeviceToHost),
+                 "get_grads");
+}
+
+// inputs: bf16 [B, N, in_dim] (host, ideally pinned), labels int32 [B]; async on the
+// engine's stream (the next step is ordered after it).
+extern "C" int rp_engine_set_batch(RpEngine* g, const uint16_t* inputs, const int32_t* labels) {
+  if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->inputs, inputs, static_cast<size_t>(g->T * g->in) * 2,
+                                 cudaMemcpyHostToDevice, g->sG),
+                 "set_batch inputs"));
+  return cuda_ok(cudaMemcpyAsync(g->labels, labels, static_cast<size_t>(g->B) * 4,
+                                 cudaMemcpyHostToDevice, g->sG),
+                 "set_batch labels");
+}
+
+extern "C" int rp_engine_set_batch_device(RpEngine* g, const uint16_t* inputs,
+                                          const int32_t* labels) {
+  if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->inputs, inputs, static_cast<size_t>(g->T * g->in) * 2,
+                                 cudaMemcpyDeviceToDevice, g->sG),
+                 "set_batch inputs"));
+  return cuda_ok(cudaMemcpyAsync(g->labels, labels, static_cast<size_t>(g->B) * 4,
+                                 cudaMemcpyDeviceToDevice, g->sG),
+                 "set_batch labels");
+}
+
+extern "C" int rp_engine_set_lr(RpEngine* g, float lr) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  return cuda_ok(cudaMemcpyAsync(g->lr, &lr, sizeof(float), cudaMemcpyHostToDevice, g->sG),
+                 "set_lr");
+}
+
+extern "C" int rp_engine_set_partition(RpEngine* g, int r_ctas, int g_ctas) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  g->r_ctas = r_ctas;
+  g->g_ctas = g_ctas;
+  if (g->graph[2]) {
+    cudaGraphExecDestroy(g->graph[2]);
+    g->graph[2] = nullptr;
+  }
+  return RP_OK;
+}
+
+// mode: 1 = Reprop, 2 = PaReprop. use_graph: capture once, then replay.
+// The step is asynchronous on the engine stream; rp_engine_sync / read_loss wait for it.
+extern "C" int rp_engine_step(RpEngine* g, int mode, int use_graph) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  if (mode != 1 && mode != 2) return rp_fail(RP_ERR_CONFIG, "step: mode must be 1 (reprop) or 2 (pareprop)");
+  set_partition(g, mode);
+  if (!use_graph || g->instrument) return enqueue_step(g, mode);
+  if (!g->graph[mode]) {
+    cudaGraph_t graph = nullptr;
+    RP_TRY(cuda_ok(cudaStreamBeginCapture(g->sG, cudaStreamCaptureModeThreadLocal), "capture"));
+    const int rc = enqueue_step(g, mode);
+    const cudaError_t e = cudaStreamEndCapture(g->sG, &graph);
+    if (rc != RP_OK) return rc;
+    RP_TRY(cuda_ok(e, "end capture"));
+    RP_TRY(cuda_ok(cudaGraphInstantiate(&g->graph[mode], graph, 0), "graph instantiate"));
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(graph, nodes.data(), &nn);
+    int64_t kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      if (t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    g->graph_kernels[mode] = kernels;
+    cudaGraphDestroy(graph);
+  }
+  return cuda_ok(cudaGraphLaunch(g->graph[mode], g->sG), "graph launch");
+}
+
+extern "C" int rp_engine_sync(RpEngine* g) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  const cudaError_t e = cudaStreamSynchronize(g->sG);
+  if (e != cudaSuccess) {
+    std::string m = std::string("pipeline lane failed: ") + cudaGetErrorString(e);
+    return rp_fail(RP_ERR_SCHEDULER, m.c_str());
+  }
+  return RP_OK;
+}
+
+extern "C" int rp_engine_read_loss(RpEngine* g, float* loss) {
+  if (!g || !loss) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(cuda_ok(cudaMemcpyAsync(loss, g->loss, sizeof(float), cudaMemcpyDeviceToHost, g->sG),
+                 "read_loss"));
+  return rp_engine_sync(g);
+}
+
+// Kernel launches per captured step (counted from the CUDA graph's kernel nodes).
+extern "C" int64_t rp_engine_graph_kernels(const RpEngine* g, int mode) {
+  return (g && mode >= 1 && mode <= 2) ? g->graph_kernels[mode] : -1;
+}
+
+// Runs one eager step with every tcgen05 GEMM launch bracketed by CUDA events on its own
+// stream; returns the summed GEMM time (ms), FLOPs and launch count of that step.
+extern "C" int rp_engine_gemm_profile(RpEngine* g, int mode, double* ms, double* flops,
+                                      int64_t* launches) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  set_partition(g, mode);
+  g->prof = true;
+  const int rc = enqueue_step(g, mode);
+  g->prof = false;
+  RP_TRY(rc);
+  RP_TRY(rp_engine_sync(g));
+  double t = 0.0, f = 0.0;
+  for (size_t i = 0; i < g->prof_used; ++i) {
+    float x = 0.f;
+    cudaEventElapsedTime(&x, g->prof_ev[i].first, g->prof_ev[i].second);
+    t += x;
+    f += g->prof_flops[i];
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (launches) *launches = static_cast<int64_t>(g->prof_used);
+  return RP_OK;
+}
+
+extern "C" void* rp_engine_stream(RpEngine* g) { return g ? static_cast<void*>(g->sG) : nullptr; }
+
+// Instrumented slot log (eager mode): per lane (0 = R, 1 = G) and block, start/end in ms
+// relative to the first R slot. out: [2][L][2] floats.
+extern "C" int rp_engine_set_instrument(RpEngine* g, int on) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  g->instrument = on != 0;
+  return RP_OK;
+}
+
+extern "C" int rp_engine_slot_log(RpEngine* g, float* out) {
+  if (!g || !out) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(rp_engine_sync(g));
+  cudaEvent_t ref = g->ts[static_cast<size_t>((0 * g->L + (g->L - 1)) * 2)];
+  for (int lane = 0; lane < 2; ++lane)
+    for (int64_t b = 0; b < g->L; ++b)
+      for (int w = 0; w < 2; ++w) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ref, g->ts[static_cast<size_t>(((lane * g->L) + b) * 2 + w)]);
+        out[(lane * g->L + b) * 2 + w] = ms;
+      }
+  return RP_OK;
+}
+
+// ---------------------------------------------------------------- data parallel (NCCL)
+extern "C" int rp_nccl_unique_id(uint8_t* out128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return rp_fail(RP_ERR_CUDA, ncclGetErrorString(r));
+  std::memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return RP_OK;
+}
+
+extern "C" int rp_engine_comm_init(RpEngine* g, const uint8_t* id128, int world, int rank) {
+  if (!g || !id128) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return rp_fail(RP_ERR_CONFIG, "bad world/rank");
+  if (world == 1) return RP_OK;
+  ncclUniqueId id;
+  std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+  cudaSetDevice(g->dev);
+  ncclResult_t r = ncclCommInitRank(&g->comm, world, id, rank);
+  if (r != ncclSuccess) return rp_fail(RP_ERR_CUDA, ncclGetErrorString(r));
+  g->world = world;
+  g->rank = rank;
+  for (auto& x : g->graph)
+    if (x) {
+      cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
+  return RP_OK;
+}
+
+// ---------------------------------------------------------------- block-level entry points
+// (revcore on device pointers owned by the caller; params are the engine's block b)
+// rev_forward: (i1, i2) -> (o1, o2), fp32 [T, d]
+extern "C" int rp_engine_rev_forward(RpEngine* g, int64_t b, const float* i1, const float* i2,
+                                     float* o1, float* o2) {
+  if (!g || b < 0 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block");
+  cudaStream_t s = g->sG;
+  const size_t bytes = static_cast<size_t>(g->T * g->d) * 4;
+  // stage the pair into X_b (b's input slots) so the forward plans can be reused
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, b), i1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  if (b > 0) RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, b), i2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  else if (i1 != i2) return rp_fail(RP_ERR_CONTRACT, "block 0 input is the duplicated embedding (i1 == i2)");
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  Slot& F = g->slot[0];
+  RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(launch(p.f_qkv, s));
+  RP_TRY(attn_fwd(g, F.qkv, F.att, F.lse, s));
+  RP_TRY(launch(p.f_proj, s));
+  RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(launch(p.f_w1, s));
+  RP_TRY(launch(p.f_w2, s));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(o1, X1(g, b + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(o2, X2(g, b + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}
+
+// rev_backward_local for block b >= 1:
+// (o1, o2, d_o1, d_o2) -> (i1, i2, d_i1, d_i2) + the block's grads in the engine grad buffer.
+extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float* o1,
+                                            const float* o2, const float* d_o1,
+                                            const float* d_o2, float* i1, float* i2,
+                                            float* d_i1, float* d_i2) {
+  if (!g || b < 1 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block (b >= 1)");
+  cudaStream_t s = g->sG;
+  const int64_t n = g->T * g->d;
+  const size_t bytes = static_cast<size_t>(n) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, b + 1), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, b + 1), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d1, d_o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d2, d_o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(rpk_f32_to_bf16(g->d1, g->d1b, n, s));
+  RP_TRY(rpk_f32_to_bf16(g->d2, g->d2b, n, s));
+  set_partition(g, 1);
+  RP_TRY(lane_r(g, b, s));
+  RP_TRY(lane_g(g, b, s));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i1, X1(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i2, X2(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_i1, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_i2, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}

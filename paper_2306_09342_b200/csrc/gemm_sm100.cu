@@ -491,6 +491,14 @@ extern "C" int rp_gemm_plan_set_max_ctas(RpGemmPlan* p, int max_ctas) {
 
 extern "C" void rp_gemm_plan_destroy(RpGemmPlan* p) { delete p; }
 
+extern "C" int rp_gemm_plan_shape(const RpGemmPlan* p, int64_t* M, int64_t* N, int64_t* K) {
+  if (!p) return RP_ERR_CONTRACT;
+  *M = p->sh.M;
+  *N = p->sh.N;
+  *K = p->sh.K;
+  return RP_OK;
+}
+
 extern "C" int rp_gemm(const RpGemmDesc* d, rp_stream_t stream) {
   RpGemmPlan* p = nullptr;
   int rc = rp_gemm_plan_create(d, &p);

@@ -1,0 +1,257 @@
+// Model glue kernels of the isotropic reversible model:
+// parameter init (counter RNG of ref:proj/core/include/revprop/rng.hpp:13-71), fp32->bf16
+// weight shadow, SGD, the head (fuse-average, mean-pool, logits, cross-entropy and their
+// VJPs) and small element-wise helpers. All are HBM- or launch-bound; none sits on the
+// tensor-core critical path. Every reduction has a fixed order (no atomics).
+#include "../../include/revprop_b200.h"
+#include "kernels.h"
+#include "model_kernels.h"
+#include "ptx.cuh"
+
+namespace rp {
+
+// ------------------------------------------------------------- counter RNG (rng.hpp)
+__host__ __device__ __forceinline__ uint64_t rng_mix(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xff51afd7ed558ccdULL;
+  z ^= z >> 33;
+  z *= 0xc4ceb9fe1a85ec53ULL;
+  z ^= z >> 33;
+  return z;
+}
+// Rng(seed, stream).next_u64() at `counter` (rng.hpp:27-33)
+__host__ __device__ __forceinline__ uint64_t rng_u64(uint64_t seed, uint64_t stream,
+                                                     uint64_t counter) {
+  uint64_t h = rng_mix(seed ^ 0x9e3779b97f4a7c15ULL);
+  h = rng_mix(h ^ (stream * 0xbf58476d1ce4e5b9ULL + 0x94d049bb133111ebULL));
+  h = rng_mix(h ^ (counter * 0x2545f4914f6cdd1dULL + 0xd6e8feb86659fd93ULL));
+  return h;
+}
+// next_normal at counters (c, c+1) (rng.hpp:38-42)
+__device__ __forceinline__ double rng_normal(uint64_t seed, uint64_t stream, uint64_t c) {
+  const double u1 = static_cast<double>((rng_u64(seed, stream, c) >> 11) + 1) * 0x1.0p-53;
+  const double u2 = static_cast<double>(rng_u64(seed, stream, c + 1) >> 11) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+// Parameter element e of flat tensor j: Rng(seed, (1<<56)|(j<<32)|e).next_trunc_normal(sigma)
+// (trunc normal at +-2 sigma, rng.hpp:45-50); kinds: 0 trunc-normal, 1 zeros, 2 ones.
+__global__ void init_tensor_kernel(float* __restrict__ p, int64_t n, uint64_t seed,
+                                   uint64_t tensor_idx, int kind, double sigma) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v;
+    if (kind == 1) {
+      v = 0.f;
+    } else if (kind == 2) {
+      v = 1.f;
+    } else {
+      const uint64_t stream = (1ull << 56) | (tensor_idx << 32) | static_cast<uint64_t>(e);
+      double z = 0.0;
+      for (uint64_t c = 0;; c += 2) {
+        z = rng_normal(seed, stream, c);
+        if (z >= -2.0 && z <= 2.0) break;
+      }
+      v = static_cast<float>(z * sigma);
+    }
+    p[e] = v;
+  }
+}
+
+// Synthetic input element e: Rng(seed, (2<<56)|e).next_normal(), stored as bf16.
+__global__ void init_inputs_kernel(__nv_bfloat16* __restrict__ x, int64_t n, uint64_t seed) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t stream = (2ull << 56) | static_cast<uint64_t>(e);
+    x[e] = __float2bfloat16_rn(static_cast<float>(rng_normal(seed, stream, 0)));
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// SGD: theta <- theta - lr * scale * g, fp32 master + bf16 shadow.
+// lr is read from device memory so a captured CUDA graph can change it between steps.
+__global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
+                           __nv_bfloat16* __restrict__ pb, int64_t n,
+                           const float* __restrict__ lr, float scale) {
+  const float step = lr[0] * scale;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = p[i] - step * g[i];
+    p[i] = v;
+    pb[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// fuse(average) + mean_tokens (layers.cpp:276-280 -> ops.cpp:408-427):
+// pooled[b][c] = (sum_n (o1 + o2) * 0.5) * (1/N), summed in token order.
+__global__ void pool_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
+                            int64_t B, int64_t N, int64_t d, float* __restrict__ pooled) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= B * d) return;
+  const int64_t b = i / d, c = i % d;
+  const float* p1 = o1 + b * N * d + c;
+  const float* p2 = o2 + b * N * d + c;
+  float s = 0.f;
+  for (int64_t n = 0; n < N; ++n) s += (p1[n * d] + p2[n * d]) * 0.5f;
+  pooled[i] = s * (1.0f / static_cast<float>(N));
+}
+
+// C[M,N] (+)= sum_k A(m,k) B(k,n), fp32 SIMT, 16x16 tiles; A(m,k) = A[m*sam + k*sak].
+__global__ void simt_gemm_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A,
+                                 int64_t sam, int64_t sak, const float* __restrict__ Bm,
+                                 int64_t sbk, int64_t sbn, float* __restrict__ Cm, int64_t ldc) {
+  __shared__ float as[16][17], bs[16][17];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t m = blockIdx.y * 16 + ty, n = blockIdx.x * 16 + tx;
+  float acc = 0.f;
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    const int64_t ka = k0 + tx, kb = k0 + ty;
+    as[ty][tx] = (m < M && ka < K) ? A[m * sam + ka * sak] : 0.f;
+    bs[ty][tx] = (kb < K && n < N) ? Bm[kb * sbk + n * sbn] : 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc += as[ty][k] * bs[k][tx];
+    __syncthreads();
+  }
+  if (m < M && n < N) Cm[m * ldc + n] = acc;
+}
+
+// Mean cross-entropy, log-sum-exp stabilised. One warp per row:
+// d_logits = (softmax - onehot) / B; row_loss[b] = lse - logit[label].
+__global__ void ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels,
+                          int64_t B, int64_t C, float* __restrict__ d_logits,
+                          float* __restrict__ row_loss) {
+  const int64_t b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const float* lr = logits + b * C;
+  float mx = -INFINITY;
+  for (int64_t c = lane; c < C; c += 32) mx = fmaxf(mx, lr[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+  for (int64_t c = lane; c < C; c += 32) s += expf(lr[c] - mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float lse = mx + logf(s);
+  const int32_t y = labels[b];
+  const float invB = 1.0f / static_cast<float>(B);
+  for (int64_t c = lane; c < C; c += 32) {
+    const float p = expf(lr[c] - lse);
+    d_logits[b * C + c] = (p - (c == y ? 1.f : 0.f)) * invB;
+  }
+  if (lane == 0) row_loss[b] = lse - lr[y];
+}
+
+// loss = (1/B) sum_b row_loss[b], fixed order, optionally * 1/world for DP averaging
+__global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int64_t B,
+                                   float* __restrict__ loss) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < B; i += blockDim.x) s += row_loss[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += red[i];
+    loss[0] = t / static_cast<float>(B);
+  }
+}
+
+// spread_tokens + fuse_vjp(average) (ops.cpp:429-447, layers.cpp:289-293):
+// d_o1 = d_o2 = (d_pooled[b] * (1/N)) * 0.5, written fp32 (both) + bf16 (both).
+__global__ void spread_kernel(const float* __restrict__ d_pooled, int64_t B, int64_t N,
+                              int64_t d, float* __restrict__ d1, float* __restrict__ d2,
+                              __nv_bfloat16* __restrict__ d1b, __nv_bfloat16* __restrict__ d2b) {
+  const int64_t total = B * N * d;
+  const float invN = 1.0f / static_cast<float>(N);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = i % d, b = i / (N * d);
+    const float v = (d_pooled[b * d + c] * invN) * 0.5f;
+    d1[i] = v;
+    d2[i] = v;
+    const __nv_bfloat16 vb = __float2bfloat16_rn(v);
+    d1b[i] = vb;
+    d2b[i] = vb;
+  }
+}
+
+// out = bf16(a + b)  (embedding cotangent: e feeds both halves of the coupled pair)
+__global__ void add_to_bf16_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                   __nv_bfloat16* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(a[i] + b[i]);
+}
+
+static inline unsigned grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+uint64_t rp_rng_u64_host(uint64_t seed, uint64_t stream, uint64_t counter) {
+  return rng_u64(seed, stream, counter);
+}
+
+int rpk_init_tensor(float* p, int64_t n, uint64_t seed, uint64_t tensor_idx, int kind,
+                    double sigma, cudaStream_t s) {
+  init_tensor_kernel<<<grid_for(n), 256, 0, s>>>(p, n, seed, tensor_idx, kind, sigma);
+  return rp_check_launch("init_tensor");
+}
+int rpk_init_inputs(uint16_t* x, int64_t n, uint64_t seed, cudaStream_t s) {
+  init_inputs_kernel<<<grid_for(n), 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(x), n, seed);
+  return rp_check_launch("init_inputs");
+}
+int rpk_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t s) {
+  f32_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(in, reinterpret_cast<__nv_bfloat16*>(out), n);
+  return rp_check_launch("f32_to_bf16");
+}
+int rpk_sgd(float* p, const float* g, uint16_t* pb, int64_t n, const float* lr, float scale,
+            cudaStream_t s) {
+  sgd_kernel<<<grid_for(n), 256, 0, s>>>(p, g, reinterpret_cast<__nv_bfloat16*>(pb), n, lr,
+                                         scale);
+  return rp_check_launch("sgd");
+}
+int rpk_pool(const float* o1, const float* o2, int64_t B, int64_t N, int64_t d, float* pooled,
+             cudaStream_t s) {
+  pool_kernel<<<static_cast<unsigned>((B * d + 255) / 256), 256, 0, s>>>(o1, o2, B, N, d, pooled);
+  return rp_check_launch("pool");
+}
+int rpk_simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t sam, int64_t sak,
+                  const float* B, int64_t sbk, int64_t sbn, float* C, int64_t ldc,
+                  cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((N + 15) / 16), static_cast<unsigned>((M + 15) / 16));
+  simt_gemm_kernel<<<grid, dim3(16, 16), 0, s>>>(M, N, K, A, sam, sak, B, sbk, sbn, C, ldc);
+  return rp_check_launch("simt_gemm");
+}
+int rpk_cross_entropy(const float* logits, const int32_t* labels, int64_t B, int64_t C,
+                      float* d_logits, float* row_loss, float* loss, cudaStream_t s) {
+  ce_kernel<<<static_cast<unsigned>((B + 7) / 8), 256, 0, s>>>(logits, labels, B, C, d_logits,
+                                                              row_loss);
+  loss_reduce_kernel<<<1, 256, 0, s>>>(row_loss, B, loss);
+  return rp_check_launch("cross_entropy");
+}
+int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1, float* d2,
+               uint16_t* d1b, uint16_t* d2b, cudaStream_t s) {
+  spread_kernel<<<grid_for(B * N * d), 256, 0, s>>>(d_pooled, B, N, d, d1, d2,
+                                                    reinterpret_cast<__nv_bfloat16*>(d1b),
+                                                    reinterpret_cast<__nv_bfloat16*>(d2b));
+  return rp_check_launch("spread");
+}
+int rpk_add_to_bf16(const float* a, const float* b, uint16_t* out, int64_t n, cudaStream_t s) {
+  add_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(a, b, reinterpret_cast<__nv_bfloat16*>(out), n);
+  return rp_check_launch("add_to_bf16");
+}

@@ -1,0 +1,257 @@
+"""Python front end of the C++ training engine (include/revprop_b200.h, csrc/engine.cpp).
+
+Mirrors the reference's engines module: `step_reprop`, `step_pareprop`,
+`sgd_update`, on the isotropic reversible model of SPEC.md:270-335. All arithmetic runs in
+the sm_100a library; this module only moves host arrays and calls the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+
+REPROP, PAREPROP = 1, 2
+
+
+class ModelConfigC(C.Structure):
+    _fields_ = [("depth", C.c_int64), ("width", C.c_int64), ("heads", C.c_int64),
+                ("hidden", C.c_int64), ("seq_len", C.c_int64), ("in_dim", C.c_int64),
+                ("num_classes", C.c_int64), ("batch", C.c_int64), ("window", C.c_int64),
+                ("seed", C.c_uint64), ("device", C.c_int), ("r_ctas", C.c_int),
+                ("g_ctas", C.c_int)]
+
+
+@dataclass
+class ModelConfig:
+    """SPEC.md:275-278 (isotropic) plus the per-GPU batch."""
+    depth: int = 12
+    width: int = 768
+    heads: int = 12
+    hidden: int = 3072
+    seq_len: int = 197
+    in_dim: int = 768
+    num_classes: int = 1000
+    batch: int = 256
+    window: int = 0
+    seed: int = 0
+    device: int = 0
+    r_ctas: int = 0
+    g_ctas: int = 0
+
+
+PRESETS = {
+    # BASELINE.json configs
+    "revvit-ti": dict(depth=12, width=192, heads=3, hidden=768, seq_len=197, batch=8),
+    "revvit-b": dict(depth=12, width=768, heads=12, hidden=3072, seq_len=197, batch=256),
+    "revvit-l": dict(depth=24, width=1024, heads=16, hidden=4096, seq_len=197, batch=256),
+    "rev-roberta-base": dict(depth=12, width=768, heads=12, hidden=3072, seq_len=512,
+                             batch=64, num_classes=2),
+}
+
+
+def _fn(name, restype, argtypes):
+    f = getattr(lib(), name)
+    f.restype, f.argtypes = restype, argtypes
+    return f
+
+
+_P, _I64, _I = C.c_void_p, C.c_int64, C.c_int
+_API = {
+    "rp_engine_create": (_I, [C.POINTER(ModelConfigC), C.POINTER(_P)]),
+    "rp_engine_destroy": (None, [_P]),
+    "rp_engine_param_count": (_I64, [_P]),
+    "rp_engine_tensor_table": (_I, [_P, _P, _P, _I64]),
+    "rp_engine_init_params": (_I, [_P, C.c_uint64]),
+    "rp_engine_synthetic_batch": (_I, [_P, C.c_uint64]),
+    "rp_engine_set_params": (_I, [_P, _P]),
+    "rp_engine_get_params": (_I, [_P, _P]),
+    "rp_engine_get_grads": (_I, [_P, _P]),
+    "rp_engine_set_batch": (_I, [_P, _P, _P]),
+    "rp_engine_set_batch_device": (_I, [_P, _P, _P]),
+    "rp_engine_set_lr": (_I, [_P, C.c_float]),
+    "rp_engine_set_partition": (_I, [_P, _I, _I]),
+    "rp_engine_step": (_I, [_P, _I, _I]),
+    "rp_engine_sync": (_I, [_P]),
+    "rp_engine_read_loss": (_I, [_P, C.POINTER(C.c_float)]),
+    "rp_engine_stream": (_P, [_P]),
+    "rp_engine_graph_kernels": (_I64, [_P, _I]),
+    "rp_engine_gemm_profile": (_I, [_P, _I, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.POINTER(_I64)]),
+    "rp_engine_set_instrument": (_I, [_P, _I]),
+    "rp_engine_slot_log": (_I, [_P, _P]),
+    "rp_nccl_unique_id": (_I, [_P]),
+    "rp_engine_comm_init": (_I, [_P, _P, _I, _I]),
+    "rp_engine_rev_forward": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "rp_engine_rev_backward_local": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
+}
+_bound = {}
+
+
+def api(name):
+    if name not in _bound:
+        r, a = _API[name]
+        _bound[name] = _fn(name, r, a)
+    return _bound[name]
+
+
+def exported_symbols():
+    return list(_API)
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16 bit patterns (uint16)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u >> 16) & 1) + 0x7FFF
+    return ((u + r) >> 16).astype(np.uint16)
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    return (bf16_bits(x).astype(np.uint32) << 16).view(np.float32)
+
+
+class Engine:
+    """One GPU's training engine. `step(mode)` runs forward + backward + (allreduce) + SGD."""
+
+    def __init__(self, cfg: ModelConfig):
+        self.cfg = cfg
+        c = ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
+                         cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
+                         cfg.g_ctas)
+        h = C.c_void_p()
+        check(api("rp_engine_create")(C.byref(c), C.byref(h)), "engine_create")
+        self._h = h
+        self.n_params = api("rp_engine_param_count")(h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            api("rp_engine_destroy")(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def tensor_table(self):
+        cap = 1 + 10 * self.cfg.depth + 1
+        off = np.zeros(cap, np.int64)
+        num = np.zeros(cap, np.int64)
+        n = api("rp_engine_tensor_table")(self._h, _np_ptr(off), _np_ptr(num), cap)
+        if n < 0:
+            check(n)
+        return off[:n], num[:n]
+
+    def set_params(self, flat: np.ndarray):
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        assert a.size == self.n_params
+        check(api("rp_engine_set_params")(self._h, _np_ptr(a)), "set_params")
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.n_params, np.float32)
+        check(api("rp_engine_get_params")(self._h, _np_ptr(out)), "get_params")
+        return out
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.n_params, np.float32)
+        check(api("rp_engine_get_grads")(self._h, _np_ptr(out)), "get_grads")
+        return out
+
+    def set_batch(self, inputs_bf16: np.ndarray, labels: np.ndarray):
+        x = np.ascontiguousarray(inputs_bf16, dtype=np.uint16)
+        y = np.ascontiguousarray(labels, dtype=np.int32)
+        check(api("rp_engine_set_batch")(self._h, _np_ptr(x), _np_ptr(y)), "set_batch")
+        self.sync()  # host buffers may be freed by the caller afterwards
+
+    def set_batch_ptr(self, inputs_ptr: int, labels_ptr: int):
+        """Async H2D from caller-owned (pinned) host memory."""
+        check(api("rp_engine_set_batch")(self._h, C.c_void_p(inputs_ptr), C.c_void_p(labels_ptr)),
+              "set_batch")
+
+    def set_batch_device(self, inputs_ptr: int, labels_ptr: int):
+        check(api("rp_engine_set_batch_device")(self._h, C.c_void_p(inputs_ptr),
+                                                C.c_void_p(labels_ptr)), "set_batch_device")
+
+    def synthetic_batch(self, seed: int):
+        check(api("rp_engine_synthetic_batch")(self._h, seed), "synthetic_batch")
+
+    def set_lr(self, lr: float):
+        check(api("rp_engine_set_lr")(self._h, lr), "set_lr")
+
+    def set_partition(self, r_ctas: int, g_ctas: int):
+        check(api("rp_engine_set_partition")(self._h, r_ctas, g_ctas), "set_partition")
+
+    def step(self, mode=REPROP, graph=True):
+        check(api("rp_engine_step")(self._h, mode, int(graph)), "step")
+
+    def sync(self):
+        check(api("rp_engine_sync")(self._h), "sync")
+
+    def loss(self) -> float:
+        v = C.c_float()
+        check(api("rp_engine_read_loss")(self._h, C.byref(v)), "read_loss")
+        return v.value
+
+    @property
+    def stream_ptr(self) -> int:
+        return api("rp_engine_stream")(self._h)
+
+    def graph_kernels(self, mode) -> int:
+        return int(api("rp_engine_graph_kernels")(self._h, mode))
+
+    def gemm_profile(self, mode):
+        """(ms, flops, launches) of every tcgen05 GEMM in one eager step."""
+        ms, fl, n = C.c_double(), C.c_double(), C.c_int64()
+        check(api("rp_engine_gemm_profile")(self._h, mode, C.byref(ms), C.byref(fl), C.byref(n)),
+              "gemm_profile")
+        return ms.value, fl.value, n.value
+
+    def set_instrument(self, on: bool):
+        check(api("rp_engine_set_instrument")(self._h, int(on)), "instrument")
+
+    def slot_log(self) -> np.ndarray:
+        out = np.zeros((2, self.cfg.depth, 2), np.float32)
+        check(api("rp_engine_slot_log")(self._h, _np_ptr(out)), "slot_log")
+        return out
+
+    def comm_init(self, uid: bytes, world: int, rank: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(api("rp_engine_comm_init")(self._h, buf, world, rank), "comm_init")
+
+    # revcore on caller-owned device pointers (torch tensors)
+    def rev_forward(self, b, i1, i2, o1, o2):
+        check(api("rp_engine_rev_forward")(self._h, b, i1.data_ptr(), i2.data_ptr(),
+                                           o1.data_ptr(), o2.data_ptr()), "rev_forward")
+
+    def rev_backward_local(self, b, o1, o2, d_o1, d_o2, i1, i2, d_i1, d_i2):
+        check(api("rp_engine_rev_backward_local")(
+            self._h, b, o1.data_ptr(), o2.data_ptr(), d_o1.data_ptr(), d_o2.data_ptr(),
+            i1.data_ptr(), i2.data_ptr(), d_i1.data_ptr(), d_i2.data_ptr()), "rev_backward_local")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(api("rp_nccl_unique_id")(buf), "nccl_unique_id")
+    return bytes(buf)
+
+
+def step_reprop(engine: Engine, graph=True):
+    """SPEC.md:369-377."""
+    engine.step(REPROP, graph)
+
+
+def step_pareprop(engine: Engine, graph=True):
+    """SPEC.md:378-386."""
+    engine.step(PAREPROP, graph)

@@ -1,0 +1,196 @@
+"""Engine-level parity on the B200 against the CPU oracle (oracle/revprop_oracle.py, itself
+pinned to the compiled reference in tests/test_oracle.py).
+
+Tolerance (stated, bf16 operands / fp32 accumulate vs f64 oracle on the same bf16-rounded
+weights and inputs): per tensor max|gpu - ref| / max|ref| <= 2e-2 for recomputed
+activations and outputs, <= 5e-2 for parameter gradients, relative L2 <= 2e-2; PaReprop vs
+Reprop on the GPU: bit-identical.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import revprop_oracle as O  # noqa: E402
+
+TOL_ACT = 2e-2
+TOL_GRAD = 5e-2
+TOL_L2 = 2e-2
+
+
+def maxrel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def l2rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def make(cfg_kw, batch, seed=0):
+    from paper_2306_09342_b200.engine import Engine, ModelConfig, bf16_round
+    cfg = ModelConfig(batch=batch, **cfg_kw)
+    eng = Engine(cfg)
+    mc = O.ModelConfig(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
+                       cfg.num_classes, cfg.window or None)
+    p32 = O.init_params(mc, seed, np.float32)
+    eng.set_params(p32)
+    # the oracle sees what the GPU computes with: bf16 matrices, fp32 vectors
+    pref = p32.astype(np.float64)
+    off = 0
+    for name, shape in O.tensor_shapes(mc):
+        n = int(np.prod(shape))
+        if len(shape) == 2:
+            pref[off:off + n] = bf16_round(p32[off:off + n])
+        off += n
+    return eng, mc, p32, pref
+
+
+TI = dict(depth=2, width=192, heads=3, hidden=768, seq_len=197, in_dim=768, num_classes=1000)
+BW = dict(depth=2, width=768, heads=12, hidden=3072, seq_len=197, in_dim=768, num_classes=1000)
+
+
+def per_tensor(mc, a, b, tol):
+    worst = []
+    off = 0
+    for name, shape in O.tensor_shapes(mc):
+        n = int(np.prod(shape))
+        r = maxrel(a[off:off + n], b[off:off + n])
+        worst.append((r, name))
+        assert r <= tol, (name, r)
+        off += n
+    return max(worst)
+
+
+@pytest.mark.parametrize("cfg", [TI, BW], ids=["ti", "b-width"])
+def test_block_forward_and_backward_local(cfg):
+    from paper_2306_09342_b200.engine import bf16_round
+    eng, mc, p32, pref = make(cfg, batch=2)
+    _, blocks, _ = O.blocks_of(mc, pref)
+    T, d = 2 * mc.seq_len, mc.width
+    rng = np.random.default_rng(1)
+    i1 = rng.standard_normal((2, mc.seq_len, d)).astype(np.float32)
+    i2 = rng.standard_normal((2, mc.seq_len, d)).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    o1g, o2g = torch.empty(T, d, device="cuda"), torch.empty(T, d, device="cuda")
+    eng.rev_forward(1, t(i1), t(i2), o1g, o2g)
+    o1r, o2r = O.rev_forward(blocks[1], i1.astype(np.float64), i2.astype(np.float64))
+    assert maxrel(o1g.cpu().numpy().reshape(o1r.shape), o1r) < TOL_ACT
+    assert maxrel(o2g.cpu().numpy().reshape(o2r.shape), o2r) < TOL_ACT
+    # rev_backward_local from the GPU's own outputs
+    o1 = o1g.cpu().numpy().reshape(o1r.shape)
+    o2 = o2g.cpu().numpy().reshape(o2r.shape)
+    d1 = rng.standard_normal(o1.shape).astype(np.float32) * 1e-2
+    d2 = rng.standard_normal(o1.shape).astype(np.float32) * 1e-2
+    outs = [torch.empty(T, d, device="cuda") for _ in range(4)]
+    eng.rev_backward_local(1, t(o1), t(o2), t(d1), t(d2), *outs)
+    (ri1, ri2), (rd1, rd2), (fg, gg) = O.rev_backward_local(
+        blocks[1], o1.astype(np.float64), o2.astype(np.float64),
+        bf16_round(d1).astype(np.float64), bf16_round(d2).astype(np.float64))
+    gi1, gi2, gd1, gd2 = (o.cpu().numpy().reshape(o1.shape) for o in outs)
+    # recomputed inputs match the true inputs (round trip) and the oracle's recompute
+    assert maxrel(gi1, i1) < 1e-3 and maxrel(gi2, i2) < 1e-3
+    assert maxrel(gi1, ri1) < TOL_ACT and maxrel(gi2, ri2) < TOL_ACT
+    assert maxrel(gd1, rd1) < TOL_ACT and maxrel(gd2, rd2) < TOL_ACT
+    assert l2rel(gd1, rd1) < TOL_L2 and l2rel(gd2, rd2) < TOL_L2
+    g = eng.grads()
+    from oracle.ref import block_slice
+    gb = block_slice(mc, g, 1)
+    ref = np.concatenate([np.ravel(x) for x in (
+        fg["d_w_qkv"], fg["d_w_out"], fg["d_ln_gamma"], fg["d_ln_beta"], gg["d_w1"], gg["d_b1"],
+        gg["d_w2"], gg["d_b2"], gg["d_ln_gamma"], gg["d_ln_beta"])])
+    off = 0
+    for name in O.BLOCK_TENSORS:
+        n = {"w_qkv": 3 * d * d, "w_out": d * d, "w1": d * mc.hidden, "b1": mc.hidden,
+             "w2": mc.hidden * d}.get(name, d)
+        assert maxrel(gb[off:off + n], ref[off:off + n]) < TOL_GRAD, name
+        off += n
+
+
+@pytest.mark.parametrize("cfg,batch", [(TI, 8), (BW, 2)], ids=["ti-b8", "b-width-b2"])
+def test_step_grads_match_oracle(cfg, batch):
+    from paper_2306_09342_b200.engine import REPROP, bf16_bits, bf16_round
+    eng, mc, p32, pref = make(cfg, batch=batch)
+    x, lab = O.synthetic_batch(mc, batch, seed=11)
+    xb = bf16_bits(x)
+    eng.set_batch(xb, lab)
+    eng.set_lr(0.0)
+    eng.step(REPROP, graph=False)
+    loss = eng.loss()
+    g = eng.grads()
+    r = O.step(mc, pref, bf16_round(x).astype(np.float64), lab)
+    assert abs(loss - r.loss) / abs(r.loss) < 1e-3
+    per_tensor(mc, g, r.grads, TOL_GRAD)
+    assert l2rel(g, r.grads) < TOL_L2
+    np.testing.assert_array_equal(eng.params(), p32)  # lr = 0 leaves the model unchanged
+
+
+def test_pareprop_bit_identical_to_reprop():
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits
+    cfg = dict(TI, depth=4)
+    eng, mc, p32, _ = make(cfg, batch=8)
+    x, lab = O.synthetic_batch(mc, 8, seed=3)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    results = []
+    for mode, graph, part in [(REPROP, False, None), (PAREPROP, False, None),
+                              (REPROP, True, None), (PAREPROP, True, None),
+                              (PAREPROP, True, (40, 100)), (PAREPROP, False, (7, 13))]:
+        if part:
+            eng.set_partition(*part)
+        eng.step(mode, graph=graph)
+        results.append((eng.loss(), eng.grads()))
+    l0, g0 = results[0]
+    for l, g in results[1:]:
+        assert l == l0
+        np.testing.assert_array_equal(g, g0)
+
+
+def test_sgd_descent():
+    """SPEC.md:395 / acceptance 9: loss falls over 20 SGD steps on one fixed batch."""
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits
+    cfg = dict(TI, depth=2, num_classes=10)
+    losses = {}
+    for mode in (REPROP, PAREPROP):
+        eng, mc, p32, _ = make(cfg, batch=8)
+        x, lab = O.synthetic_batch(mc, 8, seed=5)
+        eng.set_batch(bf16_bits(x), lab)
+        eng.set_lr(0.5)
+        ls = []
+        for _ in range(20):
+            eng.step(mode)
+            ls.append(eng.loss())
+        losses[mode] = ls
+        eng.close()
+    assert losses[REPROP][-1] < 0.8 * losses[REPROP][0], losses[REPROP]
+    assert losses[REPROP] == losses[PAREPROP]
+
+
+def test_slot_log_shape():
+    """Acceptance 7: lane G waits for lane R of the same block; R(i-1) overlaps G(i)."""
+    from paper_2306_09342_b200.engine import PAREPROP, bf16_bits
+    cfg = dict(TI, depth=3)
+    eng, mc, p32, _ = make(cfg, batch=8)
+    x, lab = O.synthetic_batch(mc, 8, seed=3)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_instrument(True)
+    eng.step(PAREPROP, graph=False)
+    log = eng.slot_log()  # [lane][block][start, end]
+    R, G = log[0], log[1]
+    for b in range(3):
+        assert G[b, 0] >= R[b, 1] - 1e-3  # G_b starts after R_b ends
+    for b in range(2):
+        assert R[b, 0] <= G[b + 1, 1]  # R_{b} starts before G_{b+1} ends (overlap slot)
+
+
+def test_errors_map_to_reference_classes():
+    from paper_2306_09342_b200 import _capi
+    from paper_2306_09342_b200.engine import Engine, ModelConfig
+    with pytest.raises(_capi.ConfigError):
+        Engine(ModelConfig(depth=1, width=100, heads=3, hidden=256, batch=1))
+    with pytest.raises(_capi.ShapeError):
+        Engine(ModelConfig(depth=1, width=128, heads=2, hidden=256, seq_len=10, window=3, batch=1))
