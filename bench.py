@@ -281,7 +281,7 @@ def main_ours(a, rank, world, local_rank):
 
     # ---- live roofline of the dominant kernel (the tcgen05 GEMM), one eager step
     pk = peaks()
-    gms, gflops, glaunch = eng.gemm_profile(PAREPROP)
+    gms, gflops, glaunch = eng.gemm_profile(REPROP)  # kernels serialised: clean durations
     ach = gflops / (gms / 1e3) / 1e12
     mf, hf = model_flops_per_img(dict(p, in_dim=cfg.in_dim, num_classes=cfg.num_classes))
     per_gpu = img_p / world

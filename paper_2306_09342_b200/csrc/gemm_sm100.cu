@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "gemm.h"
+#include "kernels.h"
 #include "ptx.cuh"
 
 namespace rp {
@@ -392,15 +393,15 @@ struct RpGemmPlan {
 };
 
 extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
-  if (!d || !out) return RP_ERR_CONTRACT;
+  if (!d || !out) return rp_fail(RP_ERR_CONTRACT, "gemm: null descriptor");
   *out = nullptr;
   const int64_t M = d->M, N = d->N, K = d->K;
-  if (M <= 0 || N <= 0 || K <= 0) return RP_ERR_SHAPE;
-  if (N % 16 != 0) return RP_ERR_SHAPE;
+  if (M <= 0 || N <= 0 || K <= 0) return rp_fail(RP_ERR_SHAPE, "gemm: empty M/N/K");
+  if (N % 16 != 0) return rp_fail(RP_ERR_SHAPE, "gemm: N must be a multiple of 16");
   if (d->lda % 8 || d->ldb % 8 || d->ldo % (d->epi == RP_EPI_F32 || d->epi == RP_EPI_RESID ? 4 : 8))
-    return RP_ERR_SHAPE;
+    return rp_fail(RP_ERR_SHAPE, "gemm: leading dimensions must be 16-byte multiples");
   if ((reinterpret_cast<uintptr_t>(d->A) | reinterpret_cast<uintptr_t>(d->B)) & 15)
-    return RP_ERR_SHAPE;
+    return rp_fail(RP_ERR_SHAPE, "gemm: operands must be 16-byte aligned");
   const int bn = (d->bn == 128) ? 128 : 256;
   RpGemmPlan* p = new RpGemmPlan();
   p->bn = bn;
@@ -414,7 +415,7 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   if (splits > p->sh.k_blocks) splits = p->sh.k_blocks;
   if (splits > 1 && d->epi != RP_EPI_F32) {
     delete p;
-    return RP_ERR_CONTRACT;
+    return rp_fail(RP_ERR_CONTRACT, "gemm: split-K needs the fp32 (wgrad) epilogue");
   }
   p->sh.splits = splits;
   p->ep.out = d->out;
@@ -431,7 +432,7 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   if (splits > 1) {
     if (!d->workspace || d->ldo != N) {
       delete p;
-      return RP_ERR_CONTRACT;
+      return rp_fail(RP_ERR_CONTRACT, "gemm: split-K needs a workspace and ldo == N");
     }
     p->ep.out = d->workspace;  // partials [splits][M][N]
     p->red_out = static_cast<float*>(d->out);
@@ -451,12 +452,12 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   }
   if (rc != RP_OK) {
     delete p;
-    return rc;
+    return rp_fail(rc, "gemm: cuTensorMapEncodeTiled failed");
   }
   p->kern = bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi) : pick<128>(d->a_mn, d->b_mn, d->epi);
   if (!p->kern) {
     delete p;
-    return RP_ERR_CONFIG;
+    return rp_fail(RP_ERR_CONFIG, "gemm: unknown epilogue");
   }
   p->smem = bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes;
   const int units = p->sh.m_tiles * p->sh.n_tiles * splits;
@@ -470,6 +471,7 @@ extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!p) return RP_ERR_CONTRACT;
   p->kern<<<p->grid, kThreads, p->smem, stream>>>(p->tmA, p->tmB, p->sh, p->ep);
+  if (cudaPeekAtLastError() != cudaSuccess) return rp_check_launch("gemm");
   if (p->sh.splits > 1) {
     const int64_t n4 = p->red_n / 4;
     int blocks = static_cast<int>((n4 + 255) / 256);
@@ -478,7 +480,7 @@ extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
                                                      p->sh.splits, p->ep.split_stride, n4,
                                                      p->red_out);
   }
-  return cudaPeekAtLastError() == cudaSuccess ? RP_OK : RP_ERR_CUDA;
+  return rp_check_launch("gemm");
 }
 
 extern "C" int rp_gemm_plan_set_max_ctas(RpGemmPlan* p, int max_ctas) {
