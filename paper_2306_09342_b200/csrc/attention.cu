@@ -86,15 +86,18 @@ __device__ __forceinline__ void load_b_kn(uint32_t base, int k0, int nc, uint32_
   ldsm_x4_t(base + swz(k0 + (l & 15), nc + (l >> 4)), b);
 }
 
-// S(16 x 64) = A(16 x 64, regs) . B^T where B tile [64 n][64 k] in smem rows nb..nb+63
+// S(16 x 64) = A(16 x 64, regs) . B^T where B tile [64 n][64 k] in smem rows nb..nb+63;
+// n16 blocks at or beyond `valid` rows of B are skipped (their S entries stay 0 and are
+// masked by the caller).
 __device__ __forceinline__ void mm_abt(const uint32_t (*a)[4], uint32_t bbase, int nb,
-                                       float (*s)[4]) {
+                                       float (*s)[4], int valid = 64) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
     for (int np = 0; np < 4; ++np) {
+      if (16 * np >= valid) break;
       uint32_t b[4];
       load_b_nk(bbase, nb + 16 * np, 2 * ks, b);
       mma16816(s[2 * np], a[ks], b[0], b[1]);
@@ -103,11 +106,13 @@ __device__ __forceinline__ void mm_abt(const uint32_t (*a)[4], uint32_t bbase, i
   }
 }
 
-// acc(16 x 64) += P(16 x 64 k, C-fragment layout) . B where B tile [64 k][64 n] rows kb..
+// acc(16 x 64) += P(16 x 64 k, C-fragment layout) . B where B tile [64 k][64 n] rows kb..;
+// k16 steps at or beyond `valid` are skipped (P is zero there).
 __device__ __forceinline__ void mm_pb(const float (*p)[4], uint32_t bbase, int kb,
-                                      float (*acc)[4]) {
+                                      float (*acc)[4], int valid = 64) {
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
+    if (16 * ks >= valid) break;
     uint32_t a[4];
     a[0] = pack_bf16x2(p[2 * ks][0], p[2 * ks][1]);
     a[1] = pack_bf16x2(p[2 * ks][2], p[2 * ks][3]);
@@ -151,6 +156,7 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (q0 + warp * 16 >= g.N) return;  // all 16 rows are padding (no block syncs follow)
   const int gq = lane >> 2, tq = lane & 3;
   const uint32_t bQ = smem_u32(sQ), bK = smem_u32(sK), bV = smem_u32(sV);
   uint32_t qa[4][4];
@@ -164,7 +170,8 @@ __global__ void __launch_bounds__(128)
 
   for (int kt = 0; kt < npad; kt += kTile) {
     float s[8][4];
-    mm_abt(qa, bK, kt, s);
+    const int valid = g.N - kt;
+    mm_abt(qa, bK, kt, s, valid);
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(128)
         o[nt][e] *= corr[e >> 1];
       }
     }
-    mm_pb(s, bV, kt, o);
+    mm_pb(s, bV, kt, o, valid);
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -280,6 +287,7 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (k0 + warp * 16 >= g.N) return;  // padding keys only
   const int tq = lane & 3, gq = lane >> 2;
   const uint32_t bK = smem_u32(sK), bV = smem_u32(sV), bQ = smem_u32(sQ), bO = smem_u32(sO);
   uint32_t ka[4][4], va[4][4];
@@ -296,8 +304,9 @@ __global__ void __launch_bounds__(128)
 
   for (int qt = 0; qt < npad; qt += kTile) {
     float st[8][4], dpt[8][4];
-    mm_abt(ka, bQ, qt, st);   // S^T [16 keys][64 queries]
-    mm_abt(va, bO, qt, dpt);  // dP^T = V . dO^T
+    const int valid = g.N - qt;
+    mm_abt(ka, bQ, qt, st, valid);   // S^T [16 keys][64 queries]
+    mm_abt(va, bO, qt, dpt, valid);  // dP^T = V . dO^T
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
@@ -308,8 +317,8 @@ __global__ void __launch_bounds__(128)
         dpt[nt][e] = p * (dpt[nt][e] - sD[q]) * g.scale;
       }
     }
-    mm_pb(st, bO, qt, dv);   // dV += P^T . dO
-    mm_pb(dpt, bQ, qt, dk);  // dK += dS^T . Q
+    mm_pb(st, bO, qt, dv, valid);   // dV += P^T . dO
+    mm_pb(dpt, bQ, qt, dk, valid);  // dK += dS^T . Q
   }
   const int rowa = k0 + warp * 16 + gq;
 #pragma unroll
@@ -356,6 +365,7 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (q0 + warp * 16 >= g.N) return;  // padding queries only
   const int tq = lane & 3, gq = lane >> 2;
   const uint32_t bQ = smem_u32(sQ), bO = smem_u32(sO), bK = smem_u32(sK), bV = smem_u32(sV);
   uint32_t qa[4][4], oa[4][4];
@@ -379,8 +389,9 @@ __global__ void __launch_bounds__(128)
 
   for (int kt = 0; kt < npad; kt += kTile) {
     float s[8][4], dp[8][4];
-    mm_abt(qa, bK, kt, s);
-    mm_abt(oa, bV, kt, dp);
+    const int valid = g.N - kt;
+    mm_abt(qa, bK, kt, s, valid);
+    mm_abt(oa, bV, kt, dp, valid);
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(128)
         s[nt][e] = p * (dp[nt][e] - dr[e >> 1]) * g.scale;
       }
     }
-    mm_pb(s, bK, kt, dq);  // dQ += dS . K
+    mm_pb(s, bK, kt, dq, valid);  // dQ += dS . K
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {

@@ -28,7 +28,7 @@ namespace rp {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 
 template <int BN>
 struct GemmCfg {
@@ -37,7 +37,8 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 256;
+  static constexpr int kEpiBytes = 8 * 4096;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
 };
 
 struct GemmShape {
@@ -45,79 +46,173 @@ struct GemmShape {
   int32_t m_tiles, n_tiles, k_blocks, splits;
 };
 
+// ---------------------------------------------------------------- epilogue
+// Each epilogue warp owns 32 accumulator rows (its TMEM lane quarter) and half of the BN
+// columns, processed in 32x32 chunks. tcgen05.ld gives one row per thread; the chunk is
+// bounced through a warp-private, XOR-swizzled 4 KB smem tile so that every global load
+// (residual / saved pre-activation) and store is row-contiguous across the warp (coalesced)
+// and every smem access is bank-conflict free.
+constexpr int kEpiWarps = 8;
+constexpr int kEpiStage = 4096;  // bytes per warp
+
+// fp32 tile: 32 rows x 128 B, 16 B chunk c of row r at r*128 + ((c ^ (r & 7)) << 4)
+__device__ __forceinline__ uint32_t sw32(int r, int c) {
+  return static_cast<uint32_t>(r * 128 + ((c ^ (r & 7)) << 4));
+}
+// bf16 tile: 32 rows x 64 B, chunk c (0..3) of row r at r*64 + ((c ^ ((r >> 1) & 3)) << 4)
+__device__ __forceinline__ uint32_t sw16(int r, int c) {
+  return static_cast<uint32_t>(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
+// row-owner -> staging (fp32 values)
+__device__ __forceinline__ void stage_rows_f32(uint32_t st, int lane, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    sts128(st + sw32(lane, c),
+           make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+                      __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3])));
+}
+// row-owner -> staging (bf16 values)
+__device__ __forceinline__ void stage_rows_bf16(uint32_t st, int lane, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    sts128(st + sw16(lane, c),
+           make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                      pack_bf16x2(v[8 * c + 4], v[8 * c + 5]),
+                      pack_bf16x2(v[8 * c + 6], v[8 * c + 7])));
+}
+// staging -> global, coalesced: 8 lanes per 128 B fp32 row
+__device__ __forceinline__ void store_tile_f32(uint32_t st, int lane, float* g, int64_t ld,
+                                               int64_t row0, int64_t rows_left) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    const uint4 x = lds128(st + sw32(r, c));
+    if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 4 * c) = x;
+  }
+}
+// staging -> global, coalesced: 4 lanes per 64 B bf16 row
+__device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bfloat16* g,
+                                                int64_t ld, int64_t row0, int64_t rows_left) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = (lane >> 2) + 8 * i, c = lane & 3;
+    const uint4 x = lds128(st + sw16(r, c));
+    if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 8 * c) = x;
+  }
+}
+// global -> staging (coalesced) -> row-owner registers
+__device__ __forceinline__ void load_rows_f32(uint32_t st, int lane, const float* g, int64_t ld,
+                                              int64_t row0, int64_t rows_left, float* out) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (r < rows_left) x = *reinterpret_cast<const uint4*>(g + (row0 + r) * ld + 4 * c);
+    sts128(st + sw32(r, c), x);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 x = lds128(st + sw32(lane, c));
+    out[4 * c] = __uint_as_float(x.x);
+    out[4 * c + 1] = __uint_as_float(x.y);
+    out[4 * c + 2] = __uint_as_float(x.z);
+    out[4 * c + 3] = __uint_as_float(x.w);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void load_rows_bf16(uint32_t st, int lane, const __nv_bfloat16* g,
+                                               int64_t ld, int64_t row0, int64_t rows_left,
+                                               float* out) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = (lane >> 2) + 8 * i, c = lane & 3;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (r < rows_left) x = *reinterpret_cast<const uint4*>(g + (row0 + r) * ld + 8 * c);
+    sts128(st + sw16(r, c), x);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 x = lds128(st + sw16(lane, c));
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = unpack_bf16x2(w[k]);
+      out[8 * c + 2 * k] = f.x;
+      out[8 * c + 2 * k + 1] = f.y;
+    }
+  }
+  __syncwarp();
+}
+
+// One 32x32 chunk: rows [row0, row0+32), cols [col, col+32); v = this lane's row.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShape& sh,
-                                               int64_t row, int64_t col, int split,
-                                               const float* v) {
-  if (row >= sh.M || col >= sh.N) return;
+                                               uint32_t st, int lane, int64_t row0,
+                                               int64_t col, int split, float* v) {
+  const int64_t rows_left = sh.M - row0;
   if constexpr (EPI == RP_EPI_BF16) {
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + row * ep.ldo + col);
-    o[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                      pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-    o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
-                      pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+    stage_rows_bf16(st, lane, v);
+    __syncwarp();
+    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_F32) {
-    float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
-                                          static_cast<int64_t>(split) * ep.split_stride +
-                                          row * ep.ldo + col);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    stage_rows_f32(st, lane, v);
+    __syncwarp();
+    store_tile_f32(st, lane,
+                   static_cast<float*>(ep.out) + static_cast<int64_t>(split) * ep.split_stride + col,
+                   ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_BIAS_GELU) {
-    float u[16], a[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      u[i] = v[i] + (ep.bias ? ep.bias[col + i] : 0.0f);
-      a[i] = gelu_tanh(u[i]);
+    for (int i = 0; i < 32; ++i) v[i] += ep.bias ? __ldg(ep.bias + col + i) : 0.0f;
+    if (ep.out2) {  // pre-activation u (kept for the backward's gelu')
+      stage_rows_bf16(st, lane, v);
+      __syncwarp();
+      store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2, row0,
+                      rows_left);
+      __syncwarp();
     }
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + row * ep.ldo + col);
-    o[0] = make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]),
-                      pack_bf16x2(a[4], a[5]), pack_bf16x2(a[6], a[7]));
-    o[1] = make_uint4(pack_bf16x2(a[8], a[9]), pack_bf16x2(a[10], a[11]),
-                      pack_bf16x2(a[12], a[13]), pack_bf16x2(a[14], a[15]));
-    if (ep.out2) {
-      uint4* o2 =
-          reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out2) + row * ep.ldo2 + col);
-      o2[0] = make_uint4(pack_bf16x2(u[0], u[1]), pack_bf16x2(u[2], u[3]),
-                         pack_bf16x2(u[4], u[5]), pack_bf16x2(u[6], u[7]));
-      o2[1] = make_uint4(pack_bf16x2(u[8], u[9]), pack_bf16x2(u[10], u[11]),
-                         pack_bf16x2(u[12], u[13]), pack_bf16x2(u[14], u[15]));
-    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
+    stage_rows_bf16(st, lane, v);
+    __syncwarp();
+    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_RESID) {
-    const float4* r =
-        reinterpret_cast<const float4*>(static_cast<const float*>(ep.aux) + row * ep.ldaux + col);
-    float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + row * ep.ldo + col);
+    float r[32];
+    load_rows_f32(st, lane, static_cast<const float*>(ep.aux) + col, ep.ldaux, row0, rows_left, r);
     const float s = ep.sign;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 rv = r[i];
-      float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
-      if (ep.bias) {
-        b0 = ep.bias[col + 4 * i];
-        b1 = ep.bias[col + 4 * i + 1];
-        b2 = ep.bias[col + 4 * i + 2];
-        b3 = ep.bias[col + 4 * i + 3];
-      }
-      o[i] = make_float4(rv.x + s * (v[4 * i] + b0), rv.y + s * (v[4 * i + 1] + b1),
-                         rv.z + s * (v[4 * i + 2] + b2), rv.w + s * (v[4 * i + 3] + b3));
-    }
+    for (int i = 0; i < 32; ++i)
+      v[i] = r[i] + s * (v[i] + (ep.bias ? __ldg(ep.bias + col + i) : 0.0f));
+    stage_rows_f32(st, lane, v);
+    __syncwarp();
+    store_tile_f32(st, lane, static_cast<float*>(ep.out) + col, ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_GELU_BWD) {
-    const uint4* up = reinterpret_cast<const uint4*>(
-        static_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ldaux + col);
-    const uint4 u0 = up[0], u1 = up[1];
-    const uint32_t uu[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-    float d[16];
+    float u[32];
+    load_rows_bf16(st, lane, static_cast<const __nv_bfloat16*>(ep.aux) + col, ep.ldaux, row0,
+                   rows_left, u);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float2 f = unpack_bf16x2(uu[i]);
-      d[2 * i] = v[2 * i] * gelu_tanh_slope(f.x);
-      d[2 * i + 1] = v[2 * i + 1] * gelu_tanh_slope(f.y);
-    }
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + row * ep.ldo + col);
-    o[0] = make_uint4(pack_bf16x2(d[0], d[1]), pack_bf16x2(d[2], d[3]),
-                      pack_bf16x2(d[4], d[5]), pack_bf16x2(d[6], d[7]));
-    o[1] = make_uint4(pack_bf16x2(d[8], d[9]), pack_bf16x2(d[10], d[11]),
-                      pack_bf16x2(d[12], d[13]), pack_bf16x2(d[14], d[15]));
+    for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_slope_fast(u[i]);
+    stage_rows_bf16(st, lane, v);
+    __syncwarp();
+    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
   }
+  __syncwarp();
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -132,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* sEpi = smem + S * Cfg::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -150,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -243,8 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5; warp w reads TMEM lanes [32*(w%4), +32)
+    // ---------------- epilogue warps 2..9: warp w reads TMEM lanes [32*(w%4), +32),
+    // column half (w-2)/4 of the tile
     const uint32_t q = warp & 3u;
+    const int half = (static_cast<int>(warp) - 2) >> 2;
+    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -254,12 +353,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * BN);
-      const int64_t row = m0 + q * 32 + lane;
+      const int64_t row0 = m0 + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(tbase + c, v);
-        epilogue_chunk<EPI>(ep, sh, row, n0 + c, split, v);
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        float v[32];
+        tmem_ld32(tbase + c, v);
+        if (row0 < sh.M && n0 + c < sh.N)
+          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -397,7 +497,7 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   *out = nullptr;
   const int64_t M = d->M, N = d->N, K = d->K;
   if (M <= 0 || N <= 0 || K <= 0) return rp_fail(RP_ERR_SHAPE, "gemm: empty M/N/K");
-  if (N % 16 != 0) return rp_fail(RP_ERR_SHAPE, "gemm: N must be a multiple of 16");
+  if (N % 32 != 0) return rp_fail(RP_ERR_SHAPE, "gemm: N must be a multiple of 32");
   if (d->lda % 8 || d->ldb % 8 || d->ldo % (d->epi == RP_EPI_F32 || d->epi == RP_EPI_RESID ? 4 : 8))
     return rp_fail(RP_ERR_SHAPE, "gemm: leading dimensions must be 16-byte multiples");
   if ((reinterpret_cast<uintptr_t>(d->A) | reinterpret_cast<uintptr_t>(d->B)) & 15)

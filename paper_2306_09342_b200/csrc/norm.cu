@@ -18,7 +18,7 @@
 namespace rp {
 
 constexpr int kLnWarps = 8;        // rows per CTA in the forward
-constexpr int kLnBwdRows = 64;     // rows per CTA in the backward (one dgamma/dbeta partial)
+constexpr int kLnBwdRows = 128;    // rows per dgamma/dbeta partial
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -79,103 +79,99 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   }
 }
 
-// Backward: CTA = 8 warps over kLnBwdRows consecutive rows (warp w: rows w, w+8, ...).
-// dgamma/dbeta: per-lane register accumulation in row order, then warps combined in
-// warp order -> one partial per CTA: part[blk][0][c] = dgamma, part[blk][1][c] = dbeta.
+// Backward, row part: one warp per row, all loads issued before the reductions, no
+// column accumulators (keeps ~60 registers -> full occupancy; the kernel is HBM-bound).
 template <int V>
 __global__ void __launch_bounds__(kLnWarps * 32)
-    ln_bwd_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
-                  const float* __restrict__ rstd_in, const float* __restrict__ gamma,
-                  const __nv_bfloat16* __restrict__ dy, const float* __restrict__ dres,
-                  int64_t rows, int cols, float* __restrict__ dx,
-                  __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ part) {
-  extern __shared__ float red[];  // [kLnWarps][2][cols]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    ln_bwd_dx_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
+                     const float* __restrict__ rstd_in, const float* __restrict__ gamma,
+                     const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
+                     int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kLnWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
   const int c4 = cols >> 2;
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
-  float4 ag[V], ab[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    ag[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const float inv_n = 1.0f / static_cast<float>(cols);
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
-  for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
-    const int64_t row = r0 + rr;
-    if (row >= rows) break;
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
-    const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
-    float4 h[V], d[V];
-    float sg = 0.f, sgh = 0.f;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const int c = lane + 32 * i;
-      if (c < c4) {
-        const float4 xv = xr[c];
-        const uint2 dv = dyr[c];
-        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
-        d[i] = make_float4(d01.x, d01.y, d23.x, d23.y);
-        h[i] = make_float4((xv.x - mean) * rstd, (xv.y - mean) * rstd, (xv.z - mean) * rstd,
-                           (xv.w - mean) * rstd);
-        const float4 g = g4[c];
-        const float gx = d[i].x * g.x, gy = d[i].y * g.y, gz = d[i].z * g.z, gw = d[i].w * g.w;
-        sg += (gx + gy) + (gz + gw);
-        sgh += (gx * h[i].x + gy * h[i].y) + (gz * h[i].z + gw * h[i].w);
-        ag[i].x += d[i].x * h[i].x;
-        ag[i].y += d[i].y * h[i].y;
-        ag[i].z += d[i].z * h[i].z;
-        ag[i].w += d[i].w * h[i].w;
-        ab[i].x += d[i].x;
-        ab[i].y += d[i].y;
-        ab[i].z += d[i].z;
-        ab[i].w += d[i].w;
-      }
-    }
-    const float gm = warp_sum(sg) * inv_n;
-    const float ghm = warp_sum(sgh) * inv_n;
-    float4* dxr = reinterpret_cast<float4*>(dx + row * cols);
-    const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
-    uint2* dxb = dx_bf16 ? reinterpret_cast<uint2*>(dx_bf16 + row * cols) : nullptr;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const int c = lane + 32 * i;
-      if (c < c4) {
-        const float4 g = g4[c];
-        float4 o;
-        o.x = (d[i].x * g.x - gm - h[i].x * ghm) * rstd;
-        o.y = (d[i].y * g.y - gm - h[i].y * ghm) * rstd;
-        o.z = (d[i].z * g.z - gm - h[i].z * ghm) * rstd;
-        o.w = (d[i].w * g.w - gm - h[i].w * ghm) * rstd;
-        if (drr) {
-          const float4 r = drr[c];
-          o.x += r.x;
-          o.y += r.y;
-          o.z += r.z;
-          o.w += r.w;
-        }
-        dxr[c] = o;
-        if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
-      }
-    }
-  }
-  // combine warps in fixed order
+  const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
+  const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
+  const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
+  float4 xv[V], rv[V];
+  uint2 dv[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const int c = lane + 32 * i;
     if (c < c4) {
-      reinterpret_cast<float4*>(red + (warp * 2 + 0) * cols)[c] = ag[i];
-      reinterpret_cast<float4*>(red + (warp * 2 + 1) * cols)[c] = ab[i];
+      xv[i] = xr[c];
+      dv[i] = dyr[c];
+      rv[i] = drr ? drr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
-    const int which = c / cols, col = c % cols;
-    float s = red[which * cols + col];
-    for (int w = 1; w < kLnWarps; ++w) s += red[(w * 2 + which) * cols + col];
-    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = s;
+  const float mean = mean_in[row], rstd = rstd_in[row];
+  float sg = 0.f, sgh = 0.f;
+  float4 h[V], g[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    if (c < c4) {
+      const float2 d01 = unpack_bf16x2(dv[i].x), d23 = unpack_bf16x2(dv[i].y);
+      const float4 gm = g4[c];
+      h[i] = make_float4((xv[i].x - mean) * rstd, (xv[i].y - mean) * rstd,
+                         (xv[i].z - mean) * rstd, (xv[i].w - mean) * rstd);
+      g[i] = make_float4(d01.x * gm.x, d01.y * gm.y, d23.x * gm.z, d23.y * gm.w);
+      sg += (g[i].x + g[i].y) + (g[i].z + g[i].w);
+      sgh += (g[i].x * h[i].x + g[i].y * h[i].y) + (g[i].z * h[i].z + g[i].w * h[i].w);
+    }
   }
+  const float inv_n = 1.0f / static_cast<float>(cols);
+  const float gm = warp_sum(sg) * inv_n;
+  const float ghm = warp_sum(sgh) * inv_n;
+  float4* dxr = reinterpret_cast<float4*>(dx + row * cols);
+  uint2* dxb = dx_bf16 ? reinterpret_cast<uint2*>(dx_bf16 + row * cols) : nullptr;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = lane + 32 * i;
+    if (c < c4) {
+      float4 o;
+      o.x = (g[i].x - gm - h[i].x * ghm) * rstd + rv[i].x;
+      o.y = (g[i].y - gm - h[i].y * ghm) * rstd + rv[i].y;
+      o.z = (g[i].z - gm - h[i].z * ghm) * rstd + rv[i].z;
+      o.w = (g[i].w - gm - h[i].w * ghm) * rstd + rv[i].w;
+      dxr[c] = o;
+      if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+    }
+  }
+}
+
+// Backward, column part (stage 1): CTA (rb, cb) sums dgamma = dy*x_hat and dbeta = dy
+// over rows [rb*RPB, (rb+1)*RPB) in row order for 4*256 columns -> part[rb][2][cols].
+__global__ void __launch_bounds__(256)
+    ln_bwd_dgb_partial_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
+                              const float* __restrict__ rstd_in,
+                              const __nv_bfloat16* __restrict__ dy, int64_t rows, int cols,
+                              int rpb, float* __restrict__ part) {
+  const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
+  if (c >= cols) return;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
+  int64_t r1 = r0 + rpb;
+  if (r1 > rows) r1 = rows;
+  float4 ag = make_float4(0.f, 0.f, 0.f, 0.f), ab = ag;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float4 xv = *reinterpret_cast<const float4*>(x + r * cols + c);
+    const uint2 dv = *reinterpret_cast<const uint2*>(dy + r * cols + c);
+    const float m = mean_in[r], s = rstd_in[r];
+    const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+    ag.x += d01.x * ((xv.x - m) * s);
+    ag.y += d01.y * ((xv.y - m) * s);
+    ag.z += d23.x * ((xv.z - m) * s);
+    ag.w += d23.y * ((xv.w - m) * s);
+    ab.x += d01.x;
+    ab.y += d01.y;
+    ab.z += d23.x;
+    ab.w += d23.y;
+  }
+  float* p = part + static_cast<int64_t>(blockIdx.x) * 2 * cols;
+  *reinterpret_cast<float4*>(p + c) = ag;
+  *reinterpret_cast<float4*>(p + cols + c) = ab;
 }
 
 // Stage 1 of a deterministic column sum over a [rows, cols] matrix (fp32 or bf16):
@@ -248,18 +244,10 @@ static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_
 template <int V>
 static void launch_ln_bwd(const float* x, const float* mean, const float* rstd,
                           const float* gamma, const __nv_bfloat16* dy, const float* dres,
-                          int64_t rows, int cols, float* dx, __nv_bfloat16* dxb, float* part,
-                          cudaStream_t s) {
-  const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
-  const int smem = kLnWarps * 2 * cols * static_cast<int>(sizeof(float));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(ln_bwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kLnWarps * 2 * 2048 * 4);
-    attr_set = true;
-  }
-  ln_bwd_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, smem, s>>>(
-      x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+                          int64_t rows, int cols, float* dx, __nv_bfloat16* dxb, cudaStream_t s) {
+  const int64_t blocks = (rows + kLnWarps - 1) / kLnWarps;
+  ln_bwd_dx_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, 0, s>>>(
+      x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb);
 }
 
 }  // namespace rp
@@ -305,18 +293,27 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
                                  int accumulate, rp_stream_t stream) {
   if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma,
-                 reinterpret_cast<const __nv_bfloat16*>(dy), dres, rows, static_cast<int>(cols),
-                 dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16), workspace, s);
-  const int64_t nparts = rp_ln_bwd_num_parts(rows);
-  // workspace holds [nparts][2][cols] (dgamma | dbeta partials)
-  const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
-  if (dgamma)
-    colsum_final_kernel<<<gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(cols), 2 * cols,
-                                           dgamma, accumulate);
-  if (dbeta)
-    colsum_final_kernel<<<gb, 256, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
-                                           2 * cols, dbeta, accumulate);
+  const __nv_bfloat16* dyb = reinterpret_cast<const __nv_bfloat16*>(dy);
+  if (dgamma || dbeta) {  // column sums first: dx may overwrite x's partner buffers in place
+    const int64_t nparts = rp_ln_bwd_num_parts(rows);
+    dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
+    ln_bwd_dgb_partial_kernel<<<grid, 256, 0, s>>>(x, mean, rstd, dyb, rows,
+                                                   static_cast<int>(cols), kLnBwdRows, workspace);
+    const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
+    if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
+      colsum_final_kernel<<<2 * gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(2 * cols),
+                                                 2 * cols, dgamma, accumulate);
+    } else {
+      if (dgamma)
+        colsum_final_kernel<<<gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(cols),
+                                               2 * cols, dgamma, accumulate);
+      if (dbeta)
+        colsum_final_kernel<<<gb, 256, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
+                                               2 * cols, dbeta, accumulate);
+    }
+  }
+  RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols), dx,
+                 reinterpret_cast<__nv_bfloat16*>(dx_bf16), s);
   return rp_check_launch("layer_norm_bwd");
 }
 
