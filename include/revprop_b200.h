@@ -125,6 +125,8 @@ int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
                      const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
                      uint16_t* dqkv, float* workspace, rp_stream_t stream);
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
+/* 0 (default): tcgen05 kernels where they apply (N <= 256); 1: warp-level mma.sync only */
+int rp_set_attention_impl(int impl);
 
 /* ------------------------------------------------------------------ training engine
  * Isotropic reversible model and its engines:

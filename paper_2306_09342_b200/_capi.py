@@ -86,6 +86,7 @@ _SIGS = {
     "rp_attention_fwd": (_I, [_P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "rp_attention_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "rp_attention_bwd_workspace_floats": (_I64, [_I64, _I64, _I64]),
+    "rp_set_attention_impl": (_I, [_I]),
 }
 
 

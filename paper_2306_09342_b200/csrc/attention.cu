@@ -448,11 +448,24 @@ static int attn_check(int64_t B, int64_t N, int64_t H, int64_t hd) {
 
 // qkv [B*N, 3*H*64] bf16 -> out [B*N, H*64] bf16, lse [B][H][N] (log2 domain).
 // B here is the number of independent sequences (batch x windows).
+int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, uint16_t* out,
+                        float* lse, cudaStream_t stream);
+static int g_attn_impl = 0;  // 0 = tcgen05 where it applies (N <= 256), 1 = mma.sync only
+
+extern "C" int rp_set_attention_impl(int impl) {
+  g_attn_impl = impl;
+  return RP_OK;
+}
+
 extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64_t H,
                                 int64_t head_dim, uint16_t* out, float* lse,
                                 rp_stream_t stream) {
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
+  if (g_attn_impl == 0 && N <= 256) {
+    rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, static_cast<cudaStream_t>(stream));
+    if (rc != RP_ERR_CONFIG) return rc;
+  }
   const AttnGeom g = make_geom(B, N, H);
   const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
   const int smem = (kTile + 2 * npad) * kRowBytes;

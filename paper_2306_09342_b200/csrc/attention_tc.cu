@@ -1,0 +1,247 @@
+// tcgen05 attention forward for short sequences (N <= 256 keys, head_dim 64).
+//
+// Same contract as attn_fwd_kernel in attention.cu (ref:proj/core/src/layers.cpp:150-166:
+// scores = (q k^T) * 1/sqrt(hd), row softmax, probs . v), but the two products run on the
+// 5th-gen tensor cores with TMEM accumulators:
+//   S = Q K^T      tcgen05.mma kind::f16, A = Q (smem), B = K (smem)  -> TMEM cols [0, Nk)
+//   softmax        4 warps, one query row per thread, exact (the whole key row fits):
+//                  pass 1 row max, pass 2 p = exp2(s*scale*log2e - m) -> bf16 P written
+//                  back into TMEM over the already-consumed S columns [0, Nk/2)
+//   O = P V        tcgen05.mma with A = P straight from TMEM, B = V (smem, MN-major)
+//                  -> TMEM cols [192, 256)
+// One CTA per (sequence, head, 128-query tile): 80 KB smem + 256 TMEM columns, so two
+// CTAs share an SM and one's loads overlap the other's softmax. Keys beyond N (the next
+// sequence's rows, or TMA zero fill past the end) are masked to -inf.
+#include <mutex>
+
+#include "../../include/revprop_b200.h"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace rp {
+namespace attn_tc {
+
+constexpr int kThreads = 160;  // warps 0-3 softmax / epilogue, warp 4 TMA + MMA issue
+constexpr int kTmemCols = 256;
+constexpr int kOCol = 192;
+
+struct Geom {
+  int B, N, H, Nk;  // sequences, tokens, heads, padded key count (multiple of 32, <= 256)
+  int64_t ld_o;
+  float scale_log2;
+};
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]   (A K-major, 16-bit elements packed two per column)
+__device__ __forceinline__ void umma_ts_bf16(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_kv, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse, Geom g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;                 // 128 x 128 B
+  uint8_t* sK = sQ + 128 * 128;       // Nk x 128 B
+  uint8_t* sV = sK + 256 * 128;       // Nk x 128 B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 256 * 128);
+  uint64_t* bar_load = bars;      // TMA bytes
+  uint64_t* bar_s = bars + 1;     // S ready (tcgen05.commit)
+  uint64_t* bar_p = bars + 2;     // P written to TMEM (4 warp arrivals)
+  uint64_t* bar_o = bars + 3;     // O ready (tcgen05.commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int q0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
+  const int Nk = g.Nk;
+  if (warp == 4) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_kv);
+      mbar_init(bar_load, 1);
+      mbar_init(bar_s, 1);
+      mbar_init(bar_p, 4);
+      mbar_init(bar_o, 1);
+      fence_barrier_init();
+    }
+    tmem_alloc(tmem_slot, kTmemCols);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int row_seq = b * g.N;  // first row of this sequence in qkv [T, 3d]
+  const int d = g.H * 64;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // ---- loads: Q tile, K and V rows [0, Nk) of this sequence / head
+      mbar_arrive_expect_tx(bar_load, (128 + 2 * Nk) * 128);
+      tma_load_2d(sQ, &tm_q, bar_load, h * 64, row_seq + q0);
+      tma_load_2d(sK, &tm_kv, bar_load, d + h * 64, row_seq);
+      tma_load_2d(sV, &tm_kv, bar_load, 2 * d + h * 64, row_seq);
+      mbar_wait(bar_load, 0);
+      tc_fence_after();
+      // ---- S = Q K^T : M = 128, N = Nk, K = 64 (4 x 16)
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
+      const uint32_t aq = smem_u32(sQ), bk = smem_u32(sK), bv = smem_u32(sV);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, make_sdesc_sw128(aq + kk * 32, 16, 1024),
+                  make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+      umma_commit(bar_s);
+      // ---- O = P V : M = 128, N = 64, K = Nk (Nk/16 steps); A = P in TMEM cols [0, Nk/2)
+      mbar_wait(bar_p, 0);
+      tc_fence_after();
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      for (int ks = 0; ks < Nk / 16; ++ks)
+        umma_ts_bf16(tmem + kOCol, tmem + static_cast<uint32_t>(ks * 8),
+                     make_sdesc_sw128(bv + ks * 2048, 8192, 1024), idesc_o, ks > 0 ? 1u : 0u);
+      umma_commit(bar_o);
+    }
+  } else {
+    // ---- softmax: warp w owns TMEM lanes / query rows [32w, 32w+32)
+    const uint32_t lane_base = tmem + ((warp * 32u) << 16);
+    mbar_wait(bar_s, 0);
+    tc_fence_after();
+    const int valid = g.N;  // keys >= N are masked
+    float m = -INFINITY;
+    for (int c = 0; c < Nk; c += 32) {
+      float v[32];
+      tmem_ld32(lane_base + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c + i < valid) m = fmaxf(m, v[i]);
+    }
+    const float ms = m * g.scale_log2;
+    float l = 0.f;
+    for (int c = 0; c < Nk; c += 32) {
+      float v[32];
+      tmem_ld32(lane_base + c, v);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float p0 = (c + 2 * i < valid) ? exp2f(v[2 * i] * g.scale_log2 - ms) : 0.f;
+        const float p1 = (c + 2 * i + 1 < valid) ? exp2f(v[2 * i + 1] * g.scale_log2 - ms) : 0.f;
+        l += p0 + p1;
+        pk[i] = pack_bf16x2(p0, p1);
+      }
+      // P columns [c/2, c/2+16) lie inside S columns already read by this thread
+      tmem_st16(lane_base + c / 2, pk);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_p);
+    // ---- epilogue: O / l -> bf16 att rows; lse = m*scale*log2e + log2(l)
+    mbar_wait(bar_o, 0);
+    tc_fence_after();
+    float o[32];
+    const int row = q0 + static_cast<int>(warp) * 32 + static_cast<int>(lane);
+    const float inv = 1.0f / l;
+    __nv_bfloat16* orow = out + (static_cast<int64_t>(row_seq) + row) * g.ld_o + h * 64;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      tmem_ld32(lane_base + kOCol + half * 32, o);
+      if (row < g.N) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + half * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16x2(o[8 * j] * inv, o[8 * j + 1] * inv),
+                              pack_bf16x2(o[8 * j + 2] * inv, o[8 * j + 3] * inv),
+                              pack_bf16x2(o[8 * j + 4] * inv, o[8 * j + 5] * inv),
+                              pack_bf16x2(o[8 * j + 6] * inv, o[8 * j + 7] * inv));
+      }
+    }
+    if (row < g.N) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = ms + log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 4) tmem_dealloc(tmem, kTmemCols);
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return RP_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? RP_OK
+             : RP_ERR_CUDA;
+}
+
+}  // namespace attn_tc
+}  // namespace rp
+
+using namespace rp;
+
+// Returns RP_ERR_CONFIG (without launching) when the shape is outside the tcgen05 path;
+// the caller then uses the mma.sync kernel.
+int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, uint16_t* out,
+                        float* lse, cudaStream_t stream) {
+  using namespace attn_tc;
+  if (N > 256 || N < 1) return RP_ERR_CONFIG;
+  Geom g;
+  g.B = static_cast<int>(S);
+  g.N = static_cast<int>(N);
+  g.H = static_cast<int>(H);
+  g.Nk = static_cast<int>((N + 31) / 32 * 32);
+  g.ld_o = H * 64;
+  g.scale_log2 = (1.0f / 8.0f) * 1.4426950408889634f;
+  const int64_t T = S * N, cols = 3 * H * 64;
+  CUtensorMap mq, mkv;
+  if (make_map(&mq, qkv, T, cols, 128) || make_map(&mkv, qkv, T, cols, static_cast<uint32_t>(g.Nk)))
+    return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
+  const int smem = 1024 + (128 + 2 * 256) * 128 + 64;
+  static std::once_flag once;
+  std::call_once(once, [smem] {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(H),
+            static_cast<unsigned>(S));
+  attn_fwd_tc_kernel<<<grid, kThreads, smem, stream>>>(
+      mq, mkv, reinterpret_cast<__nv_bfloat16*>(out), lse, g);
+  return rp_check_launch("attention_fwd_tc");
+}

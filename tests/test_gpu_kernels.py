@@ -171,10 +171,15 @@ def attn_ref(qkv, B, N, H, hd=64):
     return o.permute(0, 2, 1, 3).reshape(B * N, H * hd), torch.logsumexp(s, -1)
 
 
-@pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3)])
-def test_attention_fwd_bwd(K, B, N, H):
+@pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3),
+                                   (3, 256, 2), (2, 129, 1)])
+def test_attention_fwd_bwd(K, B, N, H, impl):
+    from paper_2306_09342_b200 import _capi
+    _capi.lib().rp_set_attention_impl(impl)
     qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
     out, lse = K.attention_fwd(qkv, B, N, H)
+    _capi.lib().rp_set_attention_impl(0)
     qkv_r = qkv.float().requires_grad_(True)
     o_ref, lse_ref = attn_ref(qkv_r, B, N, H)
     assert rel(out, o_ref) < 1e-2
