@@ -1,0 +1,47 @@
+"""Launch each hot kernel once at the RevViT-B block shapes (T = 256*197), for ncu:
+
+    ncu --set full -k regex:<kernel> -c 1 python -m paper_2306_09342_b200.ncu_targets
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _capi, kernels as K
+from ._capi import RP_EPI_BIAS_GELU, RP_EPI_GELU_BWD, RP_EPI_RESID
+
+
+def main():
+    _capi.lib()
+    B, N, d, h, H = 256, 197, 768, 3072, 12
+    T = B * N
+    bf = torch.bfloat16
+    dev = "cuda"
+    qkv = torch.randn(T, 3 * d, device=dev).to(bf)
+    att = torch.empty(T, d, device=dev, dtype=bf)
+    lse = torch.empty(B, H, N, device=dev)
+    dO = torch.randn(T, d, device=dev).to(bf)
+    x = torch.randn(T, d, device=dev).to(bf)
+    x3 = torch.randn(T, h, device=dev).to(bf)
+    W1 = (0.02 * torch.randn(d, h, device=dev)).to(bf)
+    W2 = (0.02 * torch.randn(h, d, device=dev)).to(bf)
+    res = torch.randn(T, d, device=dev)
+    a = torch.empty(T, h, device=dev, dtype=bf)
+    u = torch.empty(T, h, device=dev, dtype=bf)
+    b1 = torch.zeros(h, device=dev)
+    xf = torch.randn(T, d, device=dev)
+    g = torch.ones(d, device=dev)
+    bt = torch.zeros(d, device=dev)
+    for _ in range(2):  # second iteration is the profiled one under -s/-c filters
+        K.attention_fwd(qkv, B, N, H, out=att, lse=lse)
+        K.attention_bwd(qkv, att, lse, dO, B, N, H)
+        K.gemm(x, W1, T, h, d, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU, out=a, out2=u, bias=b1)
+        K.gemm(x3, W2, T, d, h, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=res, aux=res)
+        K.gemm(x, W2, T, h, d, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD, out=a, aux=u)
+        y, mean, rstd = K.layer_norm_fwd(xf, g, bt)
+        K.layer_norm_bwd(xf, mean, rstd, g, y, dres=res, dx=res)
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
