@@ -10,7 +10,10 @@
 //   O = P V        tcgen05.mma with A = P straight from TMEM, B = V (smem, MN-major)
 //                  -> TMEM cols [192, 256)
 // One CTA per (sequence, head, 128-query tile): 80 KB smem + 256 TMEM columns, so two
-// CTAs share an SM and one's loads overlap the other's softmax. Keys beyond N (the next
+// CTAs share an SM and one's loads overlap the other's softmax. Eight softmax warps: warp
+// w reads TMEM lane quarter w%4 and key half w/4; the two halves exchange row max / sum
+// through smem. P of key half k is written over that half's own (consumed) S columns,
+// so no warp overwrites columns another warp may still be reading. Keys beyond N (the next
 // sequence's rows, or TMA zero fill past the end) are masked to -inf.
 #include <mutex>
 
@@ -21,7 +24,7 @@
 namespace rp {
 namespace attn_tc {
 
-constexpr int kThreads = 160;  // warps 0-3 softmax / epilogue, warp 4 TMA + MMA issue
+constexpr int kThreads = 288;  // warps 0-7 softmax / epilogue, warp 8 TMA + MMA issue
 constexpr int kTmemCols = 256;
 constexpr int kOCol = 192;
 
@@ -30,6 +33,18 @@ struct Geom {
   int64_t ld_o;
   float scale_log2;
 };
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                   taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -62,7 +77,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint8_t* sQ = smem;                 // 128 x 128 B
   uint8_t* sK = sQ + 128 * 128;       // Nk x 128 B
   uint8_t* sV = sK + 256 * 128;       // Nk x 128 B
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 256 * 128);
+  float* red = reinterpret_cast<float*>(sV + 256 * 128);  // [2 halves][128 rows] x 2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);
   uint64_t* bar_load = bars;      // TMA bytes
   uint64_t* bar_s = bars + 1;     // S ready (tcgen05.commit)
   uint64_t* bar_p = bars + 2;     // P written to TMEM (4 warp arrivals)
@@ -72,13 +88,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int q0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
   const int Nk = g.Nk;
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_kv);
       mbar_init(bar_load, 1);
       mbar_init(bar_s, 1);
-      mbar_init(bar_p, 4);
+      mbar_init(bar_p, 8);
       mbar_init(bar_o, 1);
       fence_barrier_init();
     }
@@ -91,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int row_seq = b * g.N;  // first row of this sequence in qkv [T, 3d]
   const int d = g.H * 64;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       // ---- loads: Q tile, K and V rows [0, Nk) of this sequence / head
       mbar_arrive_expect_tx(bar_load, (128 + 2 * Nk) * 128);
@@ -112,71 +128,97 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(bar_p, 0);
       tc_fence_after();
       const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
-      for (int ks = 0; ks < Nk / 16; ++ks)
-        umma_ts_bf16(tmem + kOCol, tmem + static_cast<uint32_t>(ks * 8),
+      const int half = Nk / 2;
+      for (int ks = 0; ks < Nk / 16; ++ks) {
+        // key half 0: P at cols [0, half/2); key half 1: P at cols [half, half + half/2)
+        const int kcol = ks * 16 < half ? ks * 8 : half + (ks * 16 - half) / 2;
+        umma_ts_bf16(tmem + kOCol, tmem + static_cast<uint32_t>(kcol),
                      make_sdesc_sw128(bv + ks * 2048, 8192, 1024), idesc_o, ks > 0 ? 1u : 0u);
+      }
       umma_commit(bar_o);
     }
   } else {
-    // ---- softmax: warp w owns TMEM lanes / query rows [32w, 32w+32)
-    const uint32_t lane_base = tmem + ((warp * 32u) << 16);
+    // ---- softmax: warp w owns TMEM lanes / query rows [32(w%4), +32) and key half w/4
+    const int q = static_cast<int>(warp & 3u), kh = static_cast<int>(warp >> 2);
+    const int half = Nk / 2;
+    const int c0 = kh * half;
+    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(q) * 32u) << 16);
+    const int rloc = q * 32 + static_cast<int>(lane);
     mbar_wait(bar_s, 0);
     tc_fence_after();
     const int valid = g.N;  // keys >= N are masked
-    float m = -INFINITY;
-    for (int c = 0; c < Nk; c += 32) {
-      float v[32];
-      tmem_ld32(lane_base + c, v);
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int c = c0; c < c0 + half; c += 16) {
+      float v[16];
+      tmem_ld16(lane_base + c, v);
+      if (c + 16 <= valid) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (c + i < valid) m = fmaxf(m, v[i]);
-    }
-    const float ms = m * g.scale_log2;
-    float l = 0.f;
-    for (int c = 0; c < Nk; c += 32) {
-      float v[32];
-      tmem_ld32(lane_base + c, v);
-      uint32_t pk[16];
+        for (int i = 0; i < 16; ++i) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float p0 = (c + 2 * i < valid) ? exp2f(v[2 * i] * g.scale_log2 - ms) : 0.f;
-        const float p1 = (c + 2 * i + 1 < valid) ? exp2f(v[2 * i + 1] * g.scale_log2 - ms) : 0.f;
-        l += p0 + p1;
-        pk[i] = pack_bf16x2(p0, p1);
+        for (int i = 0; i < 16; ++i)
+          if (c + i < valid) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
       }
-      // P columns [c/2, c/2+16) lie inside S columns already read by this thread
-      tmem_st16(lane_base + c / 2, pk);
+    }
+    red[kh * 128 + rloc] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    named_bar(1, 256);
+    const float m = fmaxf(red[rloc], red[128 + rloc]);
+    const float ms = m * g.scale_log2;
+    float l4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = c0; c < c0 + half; c += 16) {
+      float v[16];
+      tmem_ld16(lane_base + c, v);
+      uint32_t pk[8];
+      if (c + 16 <= valid) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float p0 = exp2f(v[2 * i] * g.scale_log2 - ms);
+          const float p1 = exp2f(v[2 * i + 1] * g.scale_log2 - ms);
+          l4[i & 3] += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float p0 = (c + 2 * i < valid) ? exp2f(v[2 * i] * g.scale_log2 - ms) : 0.f;
+          const float p1 = (c + 2 * i + 1 < valid) ? exp2f(v[2 * i + 1] * g.scale_log2 - ms) : 0.f;
+          l4[i & 3] += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+      }
+      // P columns [c0 + (c - c0)/2, +8) lie inside this warp's own, already-read S columns
+      tmem_st8(lane_base + c0 + (c - c0) / 2, pk);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(bar_p);
-    // ---- epilogue: O / l -> bf16 att rows; lse = m*scale*log2e + log2(l)
+    red[256 + kh * 128 + rloc] = (l4[0] + l4[1]) + (l4[2] + l4[3]);
+    named_bar(1, 256);
+    const float l = red[256 + rloc] + red[256 + 128 + rloc];
+    // ---- epilogue: O / l -> bf16 att (32 of the 64 head columns per warp)
     mbar_wait(bar_o, 0);
     tc_fence_after();
     float o[32];
-    const int row = q0 + static_cast<int>(warp) * 32 + static_cast<int>(lane);
+    const int row = q0 + rloc;
     const float inv = 1.0f / l;
-    __nv_bfloat16* orow = out + (static_cast<int64_t>(row_seq) + row) * g.ld_o + h * 64;
+    tmem_ld32(lane_base + kOCol + kh * 32, o);
+    if (row < g.N) {
+      __nv_bfloat16* orow = out + (static_cast<int64_t>(row_seq) + row) * g.ld_o + h * 64 + kh * 32;
+      uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      tmem_ld32(lane_base + kOCol + half * 32, o);
-      if (row < g.N) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + half * 32);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(pack_bf16x2(o[8 * j] * inv, o[8 * j + 1] * inv),
-                              pack_bf16x2(o[8 * j + 2] * inv, o[8 * j + 3] * inv),
-                              pack_bf16x2(o[8 * j + 4] * inv, o[8 * j + 5] * inv),
-                              pack_bf16x2(o[8 * j + 6] * inv, o[8 * j + 7] * inv));
-      }
+      for (int j = 0; j < 4; ++j)
+        dst[j] = make_uint4(pack_bf16x2(o[8 * j] * inv, o[8 * j + 1] * inv),
+                            pack_bf16x2(o[8 * j + 2] * inv, o[8 * j + 3] * inv),
+                            pack_bf16x2(o[8 * j + 4] * inv, o[8 * j + 5] * inv),
+                            pack_bf16x2(o[8 * j + 6] * inv, o[8 * j + 7] * inv));
+      if (kh == 0) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = ms + log2f(l);
     }
-    if (row < g.N) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = ms + log2f(l);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 4) tmem_dealloc(tmem, kTmemCols);
+  if (warp == 8) tmem_dealloc(tmem, kTmemCols);
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -234,7 +276,7 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   CUtensorMap mq, mkv;
   if (make_map(&mq, qkv, T, cols, 128) || make_map(&mkv, qkv, T, cols, static_cast<uint32_t>(g.Nk)))
     return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
-  const int smem = 1024 + (128 + 2 * 256) * 128 + 64;
+  const int smem = 1024 + (128 + 2 * 256) * 128 + 4 * 128 * 4 + 64;
   static std::once_flag once;
   std::call_once(once, [smem] {
     cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -115,16 +115,48 @@ __device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bflo
     if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 8 * c) = x;
   }
 }
-// global -> staging (coalesced) -> row-owner registers
-__device__ __forceinline__ void load_rows_f32(uint32_t st, int lane, const float* g, int64_t ld,
-                                              int64_t row0, int64_t rows_left, float* out) {
+// Epilogue inputs of one 32x32 chunk, fetched one chunk ahead (software pipelining) so
+// the global-load latency of the residual / saved pre-activation / bias overlaps the
+// previous chunk's math and stores.
+struct ChunkIn {
+  uint4 aux[8];    // fp32 residual: 8 x 16 B per lane; bf16 u: first 4 used
+  float4 bias[8];  // 32 bias values (identical across lanes; broadcast loads)
+};
+
+template <int EPI>
+__device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
+                                               int64_t rows_left, int64_t col, ChunkIn& in) {
+  if constexpr (EPI == RP_EPI_RESID) {
+    const float* g = static_cast<const float*>(ep.aux) + col;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = (lane >> 3) + 4 * i, c = lane & 7;
-    uint4 x = make_uint4(0, 0, 0, 0);
-    if (r < rows_left) x = *reinterpret_cast<const uint4*>(g + (row0 + r) * ld + 4 * c);
-    sts128(st + sw32(r, c), x);
+    for (int i = 0; i < 8; ++i) {
+      const int r = (lane >> 3) + 4 * i, c = lane & 7;
+      in.aux[i] = r < rows_left
+                      ? *reinterpret_cast<const uint4*>(g + (row0 + r) * ep.ldaux + 4 * c)
+                      : make_uint4(0, 0, 0, 0);
+    }
+  } else if constexpr (EPI == RP_EPI_GELU_BWD) {
+    const __nv_bfloat16* g = static_cast<const __nv_bfloat16*>(ep.aux) + col;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = (lane >> 2) + 8 * i, c = lane & 3;
+      in.aux[i] = r < rows_left
+                      ? __ldg(reinterpret_cast<const uint4*>(g + (row0 + r) * ep.ldaux + 8 * c))
+                      : make_uint4(0, 0, 0, 0);
+    }
   }
+  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_BIAS_GELU) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      in.bias[i] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col) + i)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// prefetched coalesced aux -> staging -> row-owner registers
+__device__ __forceinline__ void aux_rows_f32(uint32_t st, int lane, const ChunkIn& in, float* out) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sts128(st + sw32((lane >> 3) + 4 * i, lane & 7), in.aux[i]);
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -136,16 +168,9 @@ __device__ __forceinline__ void load_rows_f32(uint32_t st, int lane, const float
   }
   __syncwarp();
 }
-__device__ __forceinline__ void load_rows_bf16(uint32_t st, int lane, const __nv_bfloat16* g,
-                                               int64_t ld, int64_t row0, int64_t rows_left,
-                                               float* out) {
+__device__ __forceinline__ void aux_rows_bf16(uint32_t st, int lane, const ChunkIn& in, float* out) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = (lane >> 2) + 8 * i, c = lane & 3;
-    uint4 x = make_uint4(0, 0, 0, 0);
-    if (r < rows_left) x = *reinterpret_cast<const uint4*>(g + (row0 + r) * ld + 8 * c);
-    sts128(st + sw16(r, c), x);
-  }
+  for (int i = 0; i < 4; ++i) sts128(st + sw16((lane >> 2) + 8 * i, lane & 3), in.aux[i]);
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -161,11 +186,17 @@ __device__ __forceinline__ void load_rows_bf16(uint32_t st, int lane, const __nv
   __syncwarp();
 }
 
+__device__ __forceinline__ float bias_at(const ChunkIn& in, int i) {
+  const float4 b = in.bias[i >> 2];
+  return (i & 3) == 0 ? b.x : (i & 3) == 1 ? b.y : (i & 3) == 2 ? b.z : b.w;
+}
+
 // One 32x32 chunk: rows [row0, row0+32), cols [col, col+32); v = this lane's row.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShape& sh,
                                                uint32_t st, int lane, int64_t row0,
-                                               int64_t col, int split, float* v) {
+                                               int64_t col, int split, float* v,
+                                               const ChunkIn& in) {
   const int64_t rows_left = sh.M - row0;
   if constexpr (EPI == RP_EPI_BF16) {
     stage_rows_bf16(st, lane, v);
@@ -179,7 +210,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
                    ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_BIAS_GELU) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += ep.bias ? __ldg(ep.bias + col + i) : 0.0f;
+    for (int i = 0; i < 32; ++i) v[i] += bias_at(in, i);
     if (ep.out2) {  // pre-activation u (kept for the backward's gelu')
       stage_rows_bf16(st, lane, v);
       __syncwarp();
@@ -194,18 +225,16 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
     store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_RESID) {
     float r[32];
-    load_rows_f32(st, lane, static_cast<const float*>(ep.aux) + col, ep.ldaux, row0, rows_left, r);
+    aux_rows_f32(st, lane, in, r);
     const float s = ep.sign;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      v[i] = r[i] + s * (v[i] + (ep.bias ? __ldg(ep.bias + col + i) : 0.0f));
+    for (int i = 0; i < 32; ++i) v[i] = r[i] + s * (v[i] + bias_at(in, i));
     stage_rows_f32(st, lane, v);
     __syncwarp();
     store_tile_f32(st, lane, static_cast<float*>(ep.out) + col, ep.ldo, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_GELU_BWD) {
     float u[32];
-    load_rows_bf16(st, lane, static_cast<const __nv_bfloat16*>(ep.aux) + col, ep.ldaux, row0,
-                   rows_left, u);
+    aux_rows_bf16(st, lane, in, u);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_slope_fast(u[i]);
     stage_rows_bf16(st, lane, v);
@@ -354,12 +383,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * BN);
       const int64_t row0 = m0 + q * 32;
+      const int c_begin = half * (BN / 2), c_end = (half + 1) * (BN / 2);
+      const bool rows_ok = row0 < sh.M;
+      ChunkIn nxt;
+      if (rows_ok && n0 + c_begin < sh.N)
+        prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c_begin, nxt);
 #pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+      for (int c = c_begin; c < c_end; c += 32) {
         float v[32];
         tmem_ld32(tbase + c, v);
-        if (row0 < sh.M && n0 + c < sh.N)
-          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v);
+        const ChunkIn cur = nxt;
+        if (rows_ok && c + 32 < c_end && n0 + c + 32 < sh.N)
+          prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + 32, nxt);
+        if (rows_ok && n0 + c < sh.N)
+          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
       }
       tc_fence_before();
       __syncwarp();
