@@ -221,6 +221,289 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 8) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ======================================================================= backward
+// Two kernels, each output element owned by one CTA (no atomics, bit-reproducible):
+//   dq kernel   (CTA per 128-query tile):  S = Q K^T, dP = dO V^T (TMEM),
+//               dS = P * (dP - D) * scale with P = exp2(S*scale*log2e - lse) -> bf16 in TMEM,
+//               dQ = dS K (A from TMEM)
+//   dkdv kernel (CTA per 128-key tile):    S^T = K Q^T, dP^T = V dO^T (TMEM),
+//               P^T, dS^T -> bf16 in TMEM, dV = P^T dO, dK = dS^T Q (A from TMEM)
+// (ref:proj/core/src/layers.cpp:185-208; softmax VJP ops.cpp:206-225.)
+// TMEM: S at [0, 256), dP at [256, 512); the packed bf16 products overwrite the low half of
+// each warp's own, already-read columns; accumulators live in columns no one reads any more.
+constexpr int kBwdThreads = 288;  // warps 0-7 elementwise, warp 8 TMA + MMA
+
+struct BwdGeom {
+  int B, N, H, Nk;
+  int64_t ld_o;       // d_out / dqkv column pitch helpers
+  int64_t ld_qkv;
+  float scale, scale_log2;
+};
+
+// dS (or P^T / dS^T) packed column for key/query column c of the warp's half [c0, c0+half)
+__device__ __forceinline__ int packed_col(int c, int c0) { return c0 + (c - c0) / 2; }
+__device__ __forceinline__ int ts_acol(int ks, int half) {
+  return ks * 16 < half ? ks * 8 : half + (ks * 16 - half) / 2;
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q128,
+                          const __grid_constant__ CUtensorMap tm_kv,
+                          const __grid_constant__ CUtensorMap tm_do128,
+                          const float* __restrict__ lse, const float* __restrict__ Dg,
+                          __nv_bfloat16* __restrict__ dqkv, BwdGeom g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;              // 128 x 128 B
+  uint8_t* sO = sQ + 128 * 128;    // dO tile
+  uint8_t* sK = sO + 128 * 128;    // Nk x 128 B
+  uint8_t* sV = sK + 256 * 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 256 * 128);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_s = bars + 1;
+  uint64_t* bar_p = bars + 2;
+  uint64_t* bar_o = bars + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int q0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
+  const int Nk = g.Nk, half = Nk / 2;
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q128);
+      tma_prefetch_desc(&tm_kv);
+      tma_prefetch_desc(&tm_do128);
+      mbar_init(bar_load, 1);
+      mbar_init(bar_s, 1);
+      mbar_init(bar_p, 8);
+      mbar_init(bar_o, 1);
+      fence_barrier_init();
+    }
+    tmem_alloc(tmem_slot, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int row_seq = b * g.N;
+  const int d = g.H * 64;
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bar_load, (256 + 2 * Nk) * 128);
+      tma_load_2d(sQ, &tm_q128, bar_load, h * 64, row_seq + q0);
+      tma_load_2d(sO, &tm_do128, bar_load, h * 64, row_seq + q0);
+      tma_load_2d(sK, &tm_kv, bar_load, d + h * 64, row_seq);
+      tma_load_2d(sV, &tm_kv, bar_load, 2 * d + h * 64, row_seq);
+      mbar_wait(bar_load, 0);
+      tc_fence_after();
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
+      const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO), bk = smem_u32(sK), bv = smem_u32(sV);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, make_sdesc_sw128(aq + kk * 32, 16, 1024),
+                  make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem + 256, make_sdesc_sw128(ao + kk * 32, 16, 1024),
+                  make_sdesc_sw128(bv + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+      umma_commit(bar_s);
+      mbar_wait(bar_p, 0);
+      tc_fence_after();
+      // dQ = dS K : M = 128, N = 64, K = Nk; B = K rows [key][hd] -> MN-major
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      for (int ks = 0; ks < Nk / 16; ++ks)
+        umma_ts_bf16(tmem + 256, tmem + static_cast<uint32_t>(ts_acol(ks, half)),
+                     make_sdesc_sw128(bk + ks * 2048, 8192, 1024), idesc_o, ks > 0 ? 1u : 0u);
+      umma_commit(bar_o);
+    }
+  } else {
+    const int q = static_cast<int>(warp & 3u), kh = static_cast<int>(warp >> 2);
+    const int c0 = kh * half;
+    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(q) * 32u) << 16);
+    const int row = q0 + q * 32 + static_cast<int>(lane);
+    const bool row_ok = row < g.N;
+    const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
+    const float lr = row_ok ? lse[hb + row] : 0.f;
+    const float dr = row_ok ? Dg[hb + row] : 0.f;
+    mbar_wait(bar_s, 0);
+    tc_fence_after();
+    const int valid = g.N;
+    for (int c = c0; c < c0 + half; c += 16) {
+      float s[16], dp[16];
+      tmem_ld16(lane_base + c, s);
+      tmem_ld16(lane_base + 256 + c, dp);
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k0 = c + 2 * i;
+        const float p0 = k0 < valid ? exp2f(s[2 * i] * g.scale_log2 - lr) : 0.f;
+        const float p1 = k0 + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - lr) : 0.f;
+        pk[i] = pack_bf16x2(p0 * (dp[2 * i] - dr) * g.scale, p1 * (dp[2 * i + 1] - dr) * g.scale);
+      }
+      tmem_st8(lane_base + packed_col(c, c0), pk);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_p);
+    mbar_wait(bar_o, 0);
+    tc_fence_after();
+    float o[32];
+    tmem_ld32(lane_base + 256 + kh * 32, o);
+    if (row_ok) {
+      uint4* dst = reinterpret_cast<uint4*>(dqkv + (static_cast<int64_t>(row_seq) + row) * g.ld_qkv +
+                                            h * 64 + kh * 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        dst[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                            pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                            pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_kv128,
+                            const __grid_constant__ CUtensorMap tm_qNk,
+                            const __grid_constant__ CUtensorMap tm_doNk,
+                            const float* __restrict__ lse, const float* __restrict__ Dg,
+                            __nv_bfloat16* __restrict__ dqkv, BwdGeom g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sK = smem;              // key tile 128 x 128 B
+  uint8_t* sV = sK + 128 * 128;
+  uint8_t* sQ = sV + 128 * 128;    // all queries Nq x 128 B
+  uint8_t* sO = sQ + 256 * 128;    // all dO rows
+  float* sL = reinterpret_cast<float*>(sO + 256 * 128);
+  float* sD = sL + 256;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_s = bars + 1;
+  uint64_t* bar_p = bars + 2;
+  uint64_t* bar_o = bars + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int k0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
+  const int Nq = g.Nk, half = Nq / 2;
+  const int row_seq = b * g.N;
+  const int d = g.H * 64;
+  const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_kv128);
+      tma_prefetch_desc(&tm_qNk);
+      tma_prefetch_desc(&tm_doNk);
+      mbar_init(bar_load, 1);
+      mbar_init(bar_s, 1);
+      mbar_init(bar_p, 8);
+      mbar_init(bar_o, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(bar_load, (256 + 2 * Nq) * 128);
+      tma_load_2d(sK, &tm_kv128, bar_load, d + h * 64, row_seq + k0);
+      tma_load_2d(sV, &tm_kv128, bar_load, 2 * d + h * 64, row_seq + k0);
+      tma_load_2d(sQ, &tm_qNk, bar_load, h * 64, row_seq);
+      tma_load_2d(sO, &tm_doNk, bar_load, h * 64, row_seq);
+    }
+    tmem_alloc(tmem_slot, 512);
+  } else {
+    for (int i = threadIdx.x; i < Nq; i += 256) {
+      sL[i] = i < g.N ? lse[hb + i] : 0.f;
+      sD[i] = i < g.N ? Dg[hb + i] : 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_wait(bar_load, 0);
+      tc_fence_after();
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nq), false, false);
+      const uint32_t ak = smem_u32(sK), av = smem_u32(sV), bq = smem_u32(sQ), bo = smem_u32(sO);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, make_sdesc_sw128(ak + kk * 32, 16, 1024),
+                  make_sdesc_sw128(bq + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem + 256, make_sdesc_sw128(av + kk * 32, 16, 1024),
+                  make_sdesc_sw128(bo + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+      umma_commit(bar_s);
+      mbar_wait(bar_p, 0);
+      tc_fence_after();
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      for (int ks = 0; ks < Nq / 16; ++ks) {
+        const uint32_t ac = static_cast<uint32_t>(ts_acol(ks, half));
+        // dV = P^T dO  (B = dO rows [query][hd], MN-major) -> cols [192, 256)
+        umma_ts_bf16(tmem + 192, tmem + ac, make_sdesc_sw128(bo + ks * 2048, 8192, 1024),
+                     idesc_o, ks > 0 ? 1u : 0u);
+        // dK = dS^T Q  (B = Q rows, MN-major) -> cols [448, 512)
+        umma_ts_bf16(tmem + 448, tmem + 256 + ac, make_sdesc_sw128(bq + ks * 2048, 8192, 1024),
+                     idesc_o, ks > 0 ? 1u : 0u);
+      }
+      umma_commit(bar_o);
+    }
+  } else {
+    const int qd = static_cast<int>(warp & 3u), qh = static_cast<int>(warp >> 2);
+    const int c0 = qh * half;
+    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(qd) * 32u) << 16);
+    const int key = k0 + qd * 32 + static_cast<int>(lane);
+    mbar_wait(bar_s, 0);
+    tc_fence_after();
+    const int valid = g.N;
+    for (int c = c0; c < c0 + half; c += 16) {
+      float s[16], dp[16];
+      tmem_ld16(lane_base + c, s);
+      tmem_ld16(lane_base + 256 + c, dp);
+      uint32_t pp[8], pd[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int qa = c + 2 * i;
+        const float p0 = qa < valid ? exp2f(s[2 * i] * g.scale_log2 - sL[qa]) : 0.f;
+        const float p1 = qa + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - sL[qa + 1]) : 0.f;
+        pp[i] = pack_bf16x2(p0, p1);
+        pd[i] = pack_bf16x2(p0 * (dp[2 * i] - sD[qa]) * g.scale,
+                            p1 * (dp[2 * i + 1] - sD[qa + 1]) * g.scale);
+      }
+      tmem_st8(lane_base + packed_col(c, c0), pp);
+      tmem_st8(lane_base + 256 + packed_col(c, c0), pd);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_p);
+    mbar_wait(bar_o, 0);
+    tc_fence_after();
+    // warp half qh writes columns [32 qh, 32 qh + 32) of dK and dV for its 32 keys
+    float o[32];
+    const bool key_ok = key < g.N;
+    __nv_bfloat16* base = dqkv + (static_cast<int64_t>(row_seq) + key) * g.ld_qkv + h * 64 + qh * 32;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // 0: dK (cols 448), 1: dV (cols 192)
+      tmem_ld32(lane_base + (which == 0 ? 448 : 192) + qh * 32, o);
+      if (key_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(base + (which == 0 ? d : 2 * d));
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
+                              pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                              pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                              pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -286,4 +569,44 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   attn_fwd_tc_kernel<<<grid, kThreads, smem, stream>>>(
       mq, mkv, reinterpret_cast<__nv_bfloat16*>(out), lse, g);
   return rp_check_launch("attention_fwd_tc");
+}
+
+// Backward on the tcgen05 path (N <= 256). D = rowsum(dO * O) must already be in `Dg`.
+int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                        const float* Dg, int64_t S, int64_t N, int64_t H, uint16_t* dqkv,
+                        cudaStream_t stream) {
+  using namespace attn_tc;
+  if (N > 256 || N < 1) return RP_ERR_CONFIG;
+  BwdGeom g;
+  g.B = static_cast<int>(S);
+  g.N = static_cast<int>(N);
+  g.H = static_cast<int>(H);
+  g.Nk = static_cast<int>((N + 31) / 32 * 32);
+  g.ld_o = H * 64;
+  g.ld_qkv = 3 * H * 64;
+  g.scale = 1.0f / 8.0f;
+  g.scale_log2 = g.scale * 1.4426950408889634f;
+  const int64_t T = S * N;
+  CUtensorMap q128, kvNk, do128, kv128, qNk, doNk;
+  if (make_map(&q128, qkv, T, 3 * H * 64, 128) ||
+      make_map(&kvNk, qkv, T, 3 * H * 64, static_cast<uint32_t>(g.Nk)) ||
+      make_map(&do128, dout, T, H * 64, 128) || make_map(&kv128, qkv, T, 3 * H * 64, 128) ||
+      make_map(&qNk, qkv, T, 3 * H * 64, static_cast<uint32_t>(g.Nk)) ||
+      make_map(&doNk, dout, T, H * 64, static_cast<uint32_t>(g.Nk)))
+    return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
+  const int smem_dq = 1024 + (256 + 2 * 256) * 128 + 64;
+  const int smem_kv = 1024 + (256 + 2 * 256) * 128 + 2 * 256 * 4 + 64;
+  static std::once_flag once;
+  std::call_once(once, [smem_dq, smem_kv] {
+    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem_kv);
+  });
+  dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(H),
+            static_cast<unsigned>(S));
+  attn_bwd_dkdv_tc_kernel<<<grid, kBwdThreads, smem_kv, stream>>>(
+      kv128, qNk, doNk, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  attn_bwd_dq_tc_kernel<<<grid, kBwdThreads, smem_dq, stream>>>(
+      q128, kvNk, do128, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  return rp_check_launch("attention_bwd_tc");
 }

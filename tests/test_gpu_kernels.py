@@ -179,7 +179,6 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
     _capi.lib().rp_set_attention_impl(impl)
     qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
     out, lse = K.attention_fwd(qkv, B, N, H)
-    _capi.lib().rp_set_attention_impl(0)
     qkv_r = qkv.float().requires_grad_(True)
     o_ref, lse_ref = attn_ref(qkv_r, B, N, H)
     assert rel(out, o_ref) < 1e-2
@@ -192,3 +191,4 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
         sl = slice(i * H * 64, (i + 1) * H * 64)
         assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
     assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H))
+    _capi.lib().rp_set_attention_impl(0)
