@@ -18,7 +18,7 @@
 namespace rp {
 
 constexpr int kLnWarps = 8;        // rows per CTA in the forward
-constexpr int kLnBwdRows = 128;    // rows per dgamma/dbeta partial
+constexpr int kLnBwdRows = 64;     // rows per dgamma/dbeta partial
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -155,7 +155,33 @@ __global__ void __launch_bounds__(256)
   int64_t r1 = r0 + rpb;
   if (r1 > rows) r1 = rows;
   float4 ag = make_float4(0.f, 0.f, 0.f, 0.f), ab = ag;
-  for (int64_t r = r0; r < r1; ++r) {
+  // rows in order; 4 rows' loads in flight per iteration (same association order)
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    float4 xv[4];
+    uint2 dv[4];
+    float m[4], s[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      xv[j] = *reinterpret_cast<const float4*>(x + (r + j) * cols + c);
+      dv[j] = *reinterpret_cast<const uint2*>(dy + (r + j) * cols + c);
+      m[j] = mean_in[r + j];
+      s[j] = rstd_in[r + j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 d01 = unpack_bf16x2(dv[j].x), d23 = unpack_bf16x2(dv[j].y);
+      ag.x += d01.x * ((xv[j].x - m[j]) * s[j]);
+      ag.y += d01.y * ((xv[j].y - m[j]) * s[j]);
+      ag.z += d23.x * ((xv[j].z - m[j]) * s[j]);
+      ag.w += d23.y * ((xv[j].w - m[j]) * s[j]);
+      ab.x += d01.x;
+      ab.y += d01.y;
+      ab.z += d23.x;
+      ab.w += d23.y;
+    }
+  }
+  for (; r < r1; ++r) {
     const float4 xv = *reinterpret_cast<const float4*>(x + r * cols + c);
     const uint2 dv = *reinterpret_cast<const uint2*>(dy + r * cols + c);
     const float m = mean_in[r], s = rstd_in[r];

@@ -1,0 +1,34 @@
+"""Reprop vs PaReprop step time across per-GPU batch sizes (§3.3: the gain comes
+from GPU under-utilisation, largest at small batch).
+
+    python -m paper_2306_09342_b200.sweep_batch [--batches 8,16,32,64,128,256]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+
+from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from .sweep_partition import time_steps
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--preset", default="revvit-b")
+    ap.add_argument("--batches", default="8,16,32,64,128,256")
+    ap.add_argument("--steps", type=int, default=10)
+    a = ap.parse_args(argv)
+    for B in [int(x) for x in a.batches.split(",")]:
+        p = dict(PRESETS[a.preset], batch=B)
+        eng = Engine(ModelConfig(**p))
+        eng.set_lr(1e-4)
+        r = time_steps(eng, REPROP, a.steps)
+        q = time_steps(eng, PAREPROP, a.steps)
+        print(json.dumps({"batch": B, "reprop_ms": r, "pareprop_ms": q,
+                          "reprop_img_s": B * 1e3 / r, "pareprop_img_s": B * 1e3 / q,
+                          "gain_pct": 100 * (r / q - 1)}), flush=True)
+        eng.close()
+
+
+if __name__ == "__main__":
+    main()
