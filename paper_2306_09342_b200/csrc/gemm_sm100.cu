@@ -115,83 +115,66 @@ __device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bflo
     if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 8 * c) = x;
   }
 }
-// Epilogue inputs of one 32x32 chunk, fetched one chunk ahead (software pipelining) so
-// the global-load latency of the residual / saved pre-activation / bias overlaps the
-// previous chunk's math and stores.
+// Epilogue inputs of one chunk, fetched one chunk ahead (software pipelining) so the
+// global-load latency of the residual / saved pre-activation overlaps the previous chunk.
+// A chunk is 32 rows x 128 B: 32 fp32 columns (fp32 outputs) or 64 bf16 columns (bf16
+// outputs), so every staged row is one full 128-byte line.
 struct ChunkIn {
-  uint4 aux[8];    // fp32 residual: 8 x 16 B per lane; bf16 u: first 4 used
-  float4 bias[8];  // 32 bias values (identical across lanes; broadcast loads)
+  uint4 aux[8];  // 32 rows x 128 B of the residual (fp32) or of u (bf16), coalesced
 };
 
 template <int EPI>
 __device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
                                                int64_t rows_left, int64_t col, ChunkIn& in) {
-  if constexpr (EPI == RP_EPI_RESID) {
-    const float* g = static_cast<const float*>(ep.aux) + col;
+  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_GELU_BWD) {
+    const int esz = EPI == RP_EPI_RESID ? 4 : 2;
+    const uint8_t* g = static_cast<const uint8_t*>(ep.aux) + col * esz;
+    const int64_t ldb = ep.ldaux * esz;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = (lane >> 3) + 4 * i, c = lane & 7;
-      in.aux[i] = r < rows_left
-                      ? *reinterpret_cast<const uint4*>(g + (row0 + r) * ep.ldaux + 4 * c)
-                      : make_uint4(0, 0, 0, 0);
+      in.aux[i] = r < rows_left ? *reinterpret_cast<const uint4*>(g + (row0 + r) * ldb + 16 * c)
+                                : make_uint4(0, 0, 0, 0);
     }
-  } else if constexpr (EPI == RP_EPI_GELU_BWD) {
-    const __nv_bfloat16* g = static_cast<const __nv_bfloat16*>(ep.aux) + col;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = (lane >> 2) + 8 * i, c = lane & 3;
-      in.aux[i] = r < rows_left
-                      ? __ldg(reinterpret_cast<const uint4*>(g + (row0 + r) * ep.ldaux + 8 * c))
-                      : make_uint4(0, 0, 0, 0);
-    }
-  }
-  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_BIAS_GELU) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      in.bias[i] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col) + i)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
-// prefetched coalesced aux -> staging -> row-owner registers
-__device__ __forceinline__ void aux_rows_f32(uint32_t st, int lane, const ChunkIn& in, float* out) {
+// staging (32 x 128 B, swizzled) -> global, 8 lanes per row: 4 full lines per instruction
+__device__ __forceinline__ void store_tile(uint32_t st, int lane, void* g, int64_t ldb,
+                                           int64_t row0, int64_t rows_left) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    const uint4 x = lds128(st + sw32(r, c));
+    if (r < rows_left)
+      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(g) + (row0 + r) * ldb + 16 * c) = x;
+  }
+}
+// prefetched coalesced aux -> staging -> this lane's row (8 x 16 B)
+__device__ __forceinline__ void aux_rows(uint32_t st, int lane, const ChunkIn& in, uint4* row) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) sts128(st + sw32((lane >> 3) + 4 * i, lane & 7), in.aux[i]);
   __syncwarp();
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 x = lds128(st + sw32(lane, c));
-    out[4 * c] = __uint_as_float(x.x);
-    out[4 * c + 1] = __uint_as_float(x.y);
-    out[4 * c + 2] = __uint_as_float(x.z);
-    out[4 * c + 3] = __uint_as_float(x.w);
-  }
+  for (int c = 0; c < 8; ++c) row[c] = lds128(st + sw32(lane, c));
   __syncwarp();
 }
-__device__ __forceinline__ void aux_rows_bf16(uint32_t st, int lane, const ChunkIn& in, float* out) {
+// this lane's 64 bf16 values -> staging
+__device__ __forceinline__ void stage_row_bf16x64(uint32_t st, int lane, const float* v) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) sts128(st + sw16((lane >> 2) + 8 * i, lane & 3), in.aux[i]);
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint4 x = lds128(st + sw16(lane, c));
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = unpack_bf16x2(w[k]);
-      out[8 * c + 2 * k] = f.x;
-      out[8 * c + 2 * k + 1] = f.y;
-    }
-  }
-  __syncwarp();
+  for (int c = 0; c < 8; ++c)
+    sts128(st + sw32(lane, c),
+           make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                      pack_bf16x2(v[8 * c + 4], v[8 * c + 5]),
+                      pack_bf16x2(v[8 * c + 6], v[8 * c + 7])));
 }
 
-__device__ __forceinline__ float bias_at(const ChunkIn& in, int i) {
-  const float4 b = in.bias[i >> 2];
-  return (i & 3) == 0 ? b.x : (i & 3) == 1 ? b.y : (i & 3) == 2 ? b.z : b.w;
-}
+template <int EPI>
+struct EpiTraits {
+  static constexpr int kCW = (EPI == RP_EPI_F32 || EPI == RP_EPI_RESID) ? 32 : 64;
+};
 
-// One 32x32 chunk: rows [row0, row0+32), cols [col, col+32); v = this lane's row.
+// One chunk: rows [row0, row0+32), cols [col, col+CW); v = this lane's row (CW values).
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShape& sh,
                                                uint32_t st, int lane, int64_t row0,
@@ -199,47 +182,71 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
                                                const ChunkIn& in) {
   const int64_t rows_left = sh.M - row0;
   if constexpr (EPI == RP_EPI_BF16) {
-    stage_rows_bf16(st, lane, v);
+    stage_row_bf16x64(st, lane, v);
     __syncwarp();
-    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_F32) {
     stage_rows_f32(st, lane, v);
     __syncwarp();
-    store_tile_f32(st, lane,
-                   static_cast<float*>(ep.out) + static_cast<int64_t>(split) * ep.split_stride + col,
-                   ep.ldo, row0, rows_left);
+    store_tile(st, lane,
+               static_cast<float*>(ep.out) + static_cast<int64_t>(split) * ep.split_stride + col,
+               ep.ldo * 4, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_BIAS_GELU) {
+    if (ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += bias_at(in, i);
+      for (int i = 0; i < 16; ++i) {
+        const float4 b = __ldg(b4 + i);
+        v[4 * i] += b.x;
+        v[4 * i + 1] += b.y;
+        v[4 * i + 2] += b.z;
+        v[4 * i + 3] += b.w;
+      }
+    }
     if (ep.out2) {  // pre-activation u (kept for the backward's gelu')
-      stage_rows_bf16(st, lane, v);
+      stage_row_bf16x64(st, lane, v);
       __syncwarp();
-      store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2, row0,
-                      rows_left);
+      store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0,
+                 rows_left);
       __syncwarp();
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
-    stage_rows_bf16(st, lane, v);
+    for (int i = 0; i < 64; ++i) v[i] = gelu_tanh_fast(v[i]);
+    stage_row_bf16x64(st, lane, v);
     __syncwarp();
-    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_RESID) {
-    float r[32];
-    aux_rows_f32(st, lane, in, r);
+    uint4 rr[8];
+    aux_rows(st, lane, in, rr);
     const float s = ep.sign;
+    const float4* b4 = ep.bias ? reinterpret_cast<const float4*>(ep.bias + col) : nullptr;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = r[i] + s * (v[i] + bias_at(in, i));
+    for (int c = 0; c < 8; ++c) {
+      const float4 b = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + b.x);
+      v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + b.y);
+      v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + b.z);
+      v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + b.w);
+    }
     stage_rows_f32(st, lane, v);
     __syncwarp();
-    store_tile_f32(st, lane, static_cast<float*>(ep.out) + col, ep.ldo, row0, rows_left);
+    store_tile(st, lane, static_cast<float*>(ep.out) + col, ep.ldo * 4, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_GELU_BWD) {
-    float u[32];
-    aux_rows_bf16(st, lane, in, u);
+    uint4 uu[8];
+    aux_rows(st, lane, in, uu);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_slope_fast(u[i]);
-    stage_rows_bf16(st, lane, v);
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t w[4] = {uu[c].x, uu[c].y, uu[c].z, uu[c].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = unpack_bf16x2(w[k]);
+        v[8 * c + 2 * k] *= gelu_tanh_slope_fast(f.x);
+        v[8 * c + 2 * k + 1] *= gelu_tanh_slope_fast(f.y);
+      }
+    }
+    stage_row_bf16x64(st, lane, v);
     __syncwarp();
-    store_tile_bf16(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo, row0, rows_left);
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
   }
   __syncwarp();
 }
@@ -384,17 +391,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * BN);
       const int64_t row0 = m0 + q * 32;
       const int c_begin = half * (BN / 2), c_end = (half + 1) * (BN / 2);
+      constexpr int CW = EpiTraits<EPI>::kCW;
       const bool rows_ok = row0 < sh.M;
       ChunkIn nxt;
       if (rows_ok && n0 + c_begin < sh.N)
         prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c_begin, nxt);
 #pragma unroll 1
-      for (int c = c_begin; c < c_end; c += 32) {
-        float v[32];
+      for (int c = c_begin; c < c_end; c += CW) {
+        float v[CW];
         tmem_ld32(tbase + c, v);
+        if constexpr (CW == 64) tmem_ld32(tbase + c + 32, v + 32);
         const ChunkIn cur = nxt;
-        if (rows_ok && c + 32 < c_end && n0 + c + 32 < sh.N)
-          prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + 32, nxt);
+        if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
+          prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
         if (rows_ok && n0 + c < sh.N)
           epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
       }
@@ -534,7 +543,7 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   *out = nullptr;
   const int64_t M = d->M, N = d->N, K = d->K;
   if (M <= 0 || N <= 0 || K <= 0) return rp_fail(RP_ERR_SHAPE, "gemm: empty M/N/K");
-  if (N % 32 != 0) return rp_fail(RP_ERR_SHAPE, "gemm: N must be a multiple of 32");
+  if (N % 64 != 0) return rp_fail(RP_ERR_SHAPE, "gemm: N must be a multiple of 64");
   if (d->lda % 8 || d->ldb % 8 || d->ldo % (d->epi == RP_EPI_F32 || d->epi == RP_EPI_RESID ? 4 : 8))
     return rp_fail(RP_ERR_SHAPE, "gemm: leading dimensions must be 16-byte multiples");
   if ((reinterpret_cast<uintptr_t>(d->A) | reinterpret_cast<uintptr_t>(d->B)) & 15)
