@@ -504,6 +504,330 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------- persistent backward
+// Same math as attn_bwd_dq_tc_kernel / attn_bwd_dkdv_tc_kernel, but one CTA per SM loops
+// over work items (tile, head, sequence) and double-buffers the TMA loads: item i+1's
+// operands stream in while item i is being computed. Per-item barrier phases are i & 1.
+struct BwdItems {
+  int ntile;  // tiles per (sequence, head)
+  int nitems;
+};
+
+__device__ __forceinline__ void item_coords(int item, int ntile, int H, int& tile, int& h,
+                                            int& b) {
+  tile = item % ntile;
+  const int bh = item / ntile;
+  h = bh % H;
+  b = bh / H;
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dq_tc_persistent(const __grid_constant__ CUtensorMap tm_q128,
+                              const __grid_constant__ CUtensorMap tm_kv,
+                              const __grid_constant__ CUtensorMap tm_do128,
+                              const float* __restrict__ lse, const float* __restrict__ Dg,
+                              __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdItems it) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kBuf = (256 + 2 * 256) * 128;  // Q tile | dO tile | K | V
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kBuf);
+  uint64_t* bar_load = bars;  // [2]
+  uint64_t* bar_s = bars + 2;
+  uint64_t* bar_p = bars + 3;
+  uint64_t* bar_o = bars + 4;
+  uint64_t* bar_e = bars + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Nk = g.Nk, half = Nk / 2;
+  const int d = g.H * 64;
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q128);
+      tma_prefetch_desc(&tm_kv);
+      tma_prefetch_desc(&tm_do128);
+      mbar_init(&bar_load[0], 1);
+      mbar_init(&bar_load[1], 1);
+      mbar_init(bar_s, 1);
+      mbar_init(bar_p, 8);
+      mbar_init(bar_o, 1);
+      mbar_init(bar_e, 8);
+      fence_barrier_init();
+    }
+    tmem_alloc(tmem_slot, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 8) {
+    if (lane == 0) {
+      auto issue_load = [&](int item, int buf) {
+        int tile, h, b;
+        item_coords(item, it.ntile, g.H, tile, h, b);
+        uint8_t* base = smem + buf * kBuf;
+        const int row_seq = b * g.N;
+        mbar_arrive_expect_tx(&bar_load[buf], (256 + 2 * Nk) * 128);
+        tma_load_2d(base, &tm_q128, &bar_load[buf], h * 64, row_seq + tile * 128);
+        tma_load_2d(base + 128 * 128, &tm_do128, &bar_load[buf], h * 64, row_seq + tile * 128);
+        tma_load_2d(base + 256 * 128, &tm_kv, &bar_load[buf], d + h * 64, row_seq);
+        tma_load_2d(base + 512 * 128, &tm_kv, &bar_load[buf], 2 * d + h * 64, row_seq);
+      };
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      int k = 0;
+      if (static_cast<int>(blockIdx.x) < it.nitems) issue_load(blockIdx.x, 0);
+      for (int item = blockIdx.x; item < it.nitems; item += gridDim.x, ++k) {
+        const int buf = k & 1;
+        if (item + static_cast<int>(gridDim.x) < it.nitems) issue_load(item + gridDim.x, buf ^ 1);
+        mbar_wait(&bar_load[buf], (k >> 1) & 1);
+        if (k > 0) mbar_wait(bar_e, (k - 1) & 1);  // previous epilogue done with TMEM
+        tc_fence_after();
+        const uint32_t base = smem_u32(smem + buf * kBuf);
+        const uint32_t aq = base, ao = base + 128 * 128, bk = base + 256 * 128,
+                       bv = base + 512 * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem, make_sdesc_sw128(aq + kk * 32, 16, 1024),
+                    make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem + 256, make_sdesc_sw128(ao + kk * 32, 16, 1024),
+                    make_sdesc_sw128(bv + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        umma_commit(bar_s);
+        mbar_wait(bar_p, k & 1);
+        tc_fence_after();
+        for (int ks = 0; ks < Nk / 16; ++ks)
+          umma_ts_bf16(tmem + 256, tmem + static_cast<uint32_t>(ts_acol(ks, half)),
+                       make_sdesc_sw128(bk + ks * 2048, 8192, 1024), idesc_o, ks > 0 ? 1u : 0u);
+        umma_commit(bar_o);
+        mbar_wait(bar_o, k & 1);  // smem buffer free for the load after next
+      }
+    }
+  } else {
+    const int q = static_cast<int>(warp & 3u), kh = static_cast<int>(warp >> 2);
+    const int c0 = kh * half;
+    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(q) * 32u) << 16);
+    int k = 0;
+    for (int item = blockIdx.x; item < it.nitems; item += gridDim.x, ++k) {
+      int tile, h, b;
+      item_coords(item, it.ntile, g.H, tile, h, b);
+      const int row_seq = b * g.N;
+      const int row = tile * 128 + q * 32 + static_cast<int>(lane);
+      const bool row_ok = row < g.N;
+      const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
+      const float lr = row_ok ? lse[hb + row] : 0.f;
+      const float dr = row_ok ? Dg[hb + row] : 0.f;
+      mbar_wait(bar_s, k & 1);
+      tc_fence_after();
+      const int valid = g.N;
+      for (int c = c0; c < c0 + half; c += 16) {
+        float s[16], dp[16];
+        tmem_ld16(lane_base + c, s);
+        tmem_ld16(lane_base + 256 + c, dp);
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int k0 = c + 2 * i;
+          const float p0 = k0 < valid ? exp2f(s[2 * i] * g.scale_log2 - lr) : 0.f;
+          const float p1 = k0 + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - lr) : 0.f;
+          pk[i] = pack_bf16x2(p0 * (dp[2 * i] - dr) * g.scale, p1 * (dp[2 * i + 1] - dr) * g.scale);
+        }
+        tmem_st8(lane_base + packed_col(c, c0), pk);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p);
+      mbar_wait(bar_o, k & 1);
+      tc_fence_after();
+      float o[32];
+      tmem_ld32(lane_base + 256 + kh * 32, o);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_e);
+      if (row_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(
+            dqkv + (static_cast<int64_t>(row_seq) + row) * g.ld_qkv + h * 64 + kh * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
+                              pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                              pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                              pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dkdv_tc_persistent(const __grid_constant__ CUtensorMap tm_kv128,
+                                const __grid_constant__ CUtensorMap tm_qNk,
+                                const __grid_constant__ CUtensorMap tm_doNk,
+                                const float* __restrict__ lse, const float* __restrict__ Dg,
+                                __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdItems it) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kBuf = (256 + 2 * 256) * 128;  // K tile | V tile | Q | dO
+  float* sLD = reinterpret_cast<float*>(smem + 2 * kBuf);  // [2 bufs][lse 256 | D 256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + 2 * 512);
+  uint64_t* bar_load = bars;  // [2]
+  uint64_t* bar_s = bars + 2;
+  uint64_t* bar_p = bars + 3;
+  uint64_t* bar_o = bars + 4;
+  uint64_t* bar_e = bars + 5;
+  uint64_t* bar_ld = bars + 6;  // [2] lse/D staged by the elementwise warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Nq = g.Nk, half = Nq / 2;
+  const int d = g.H * 64;
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_kv128);
+      tma_prefetch_desc(&tm_qNk);
+      tma_prefetch_desc(&tm_doNk);
+      mbar_init(&bar_load[0], 1);
+      mbar_init(&bar_load[1], 1);
+      mbar_init(bar_s, 1);
+      mbar_init(bar_p, 8);
+      mbar_init(bar_o, 1);
+      mbar_init(bar_e, 8);
+      fence_barrier_init();
+    }
+    tmem_alloc(tmem_slot, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 8) {
+    if (lane == 0) {
+      auto issue_load = [&](int item, int buf) {
+        int tile, h, b;
+        item_coords(item, it.ntile, g.H, tile, h, b);
+        uint8_t* base = smem + buf * kBuf;
+        const int row_seq = b * g.N;
+        mbar_arrive_expect_tx(&bar_load[buf], (256 + 2 * Nq) * 128);
+        tma_load_2d(base, &tm_kv128, &bar_load[buf], d + h * 64, row_seq + tile * 128);
+        tma_load_2d(base + 128 * 128, &tm_kv128, &bar_load[buf], 2 * d + h * 64,
+                    row_seq + tile * 128);
+        tma_load_2d(base + 256 * 128, &tm_qNk, &bar_load[buf], h * 64, row_seq);
+        tma_load_2d(base + 512 * 128, &tm_doNk, &bar_load[buf], h * 64, row_seq);
+      };
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nq), false, false);
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      int k = 0;
+      if (static_cast<int>(blockIdx.x) < it.nitems) issue_load(blockIdx.x, 0);
+      for (int item = blockIdx.x; item < it.nitems; item += gridDim.x, ++k) {
+        const int buf = k & 1;
+        if (item + static_cast<int>(gridDim.x) < it.nitems) issue_load(item + gridDim.x, buf ^ 1);
+        mbar_wait(&bar_load[buf], (k >> 1) & 1);
+        if (k > 0) mbar_wait(bar_e, (k - 1) & 1);
+        tc_fence_after();
+        const uint32_t base = smem_u32(smem + buf * kBuf);
+        const uint32_t ak = base, av = base + 128 * 128, bq = base + 256 * 128,
+                       bo = base + 512 * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem, make_sdesc_sw128(ak + kk * 32, 16, 1024),
+                    make_sdesc_sw128(bq + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem + 256, make_sdesc_sw128(av + kk * 32, 16, 1024),
+                    make_sdesc_sw128(bo + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        umma_commit(bar_s);
+        mbar_wait(bar_p, k & 1);
+        tc_fence_after();
+        for (int ks = 0; ks < Nq / 16; ++ks) {
+          const uint32_t ac = static_cast<uint32_t>(ts_acol(ks, half));
+          umma_ts_bf16(tmem + 192, tmem + ac, make_sdesc_sw128(bo + ks * 2048, 8192, 1024),
+                       idesc_o, ks > 0 ? 1u : 0u);
+          umma_ts_bf16(tmem + 448, tmem + 256 + ac, make_sdesc_sw128(bq + ks * 2048, 8192, 1024),
+                       idesc_o, ks > 0 ? 1u : 0u);
+        }
+        umma_commit(bar_o);
+        mbar_wait(bar_o, k & 1);
+      }
+    }
+  } else {
+    const int qd = static_cast<int>(warp & 3u), qh = static_cast<int>(warp >> 2);
+    const int c0 = qh * half;
+    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(qd) * 32u) << 16);
+    int k = 0;
+    for (int item = blockIdx.x; item < it.nitems; item += gridDim.x, ++k) {
+      int tile, h, b;
+      item_coords(item, it.ntile, g.H, tile, h, b);
+      const int row_seq = b * g.N;
+      const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
+      float* sL = sLD + (k & 1) * 512;
+      float* sD = sL + 256;
+      for (int i = threadIdx.x; i < Nq; i += 256) {
+        sL[i] = i < g.N ? lse[hb + i] : 0.f;
+        sD[i] = i < g.N ? Dg[hb + i] : 0.f;
+      }
+      named_bar(2, 256);
+      const int key = tile * 128 + qd * 32 + static_cast<int>(lane);
+      mbar_wait(bar_s, k & 1);
+      tc_fence_after();
+      const int valid = g.N;
+      for (int c = c0; c < c0 + half; c += 16) {
+        float s[16], dp[16];
+        tmem_ld16(lane_base + c, s);
+        tmem_ld16(lane_base + 256 + c, dp);
+        uint32_t pp[8], pd[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int qa = c + 2 * i;
+          const float p0 = qa < valid ? exp2f(s[2 * i] * g.scale_log2 - sL[qa]) : 0.f;
+          const float p1 = qa + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - sL[qa + 1]) : 0.f;
+          pp[i] = pack_bf16x2(p0, p1);
+          pd[i] = pack_bf16x2(p0 * (dp[2 * i] - sD[qa]) * g.scale,
+                              p1 * (dp[2 * i + 1] - sD[qa + 1]) * g.scale);
+        }
+        tmem_st8(lane_base + packed_col(c, c0), pp);
+        tmem_st8(lane_base + 256 + packed_col(c, c0), pd);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p);
+      mbar_wait(bar_o, k & 1);
+      tc_fence_after();
+      float o[32], o2[32];
+      tmem_ld32(lane_base + 448 + qh * 32, o);   // dK
+      tmem_ld32(lane_base + 192 + qh * 32, o2);  // dV
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_e);
+      if (key < g.N) {
+        __nv_bfloat16* base =
+            dqkv + (static_cast<int64_t>(row_seq) + key) * g.ld_qkv + h * 64 + qh * 32;
+        uint4* dk = reinterpret_cast<uint4*>(base + d);
+        uint4* dv = reinterpret_cast<uint4*>(base + 2 * d);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dk[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                             pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                             pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+          dv[j] = make_uint4(pack_bf16x2(o2[8 * j], o2[8 * j + 1]),
+                             pack_bf16x2(o2[8 * j + 2], o2[8 * j + 3]),
+                             pack_bf16x2(o2[8 * j + 4], o2[8 * j + 5]),
+                             pack_bf16x2(o2[8 * j + 6], o2[8 * j + 7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -594,19 +918,26 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* dout, const float* 
       make_map(&qNk, qkv, T, 3 * H * 64, static_cast<uint32_t>(g.Nk)) ||
       make_map(&doNk, dout, T, H * 64, static_cast<uint32_t>(g.Nk)))
     return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
-  const int smem_dq = 1024 + (256 + 2 * 256) * 128 + 64;
-  const int smem_kv = 1024 + (256 + 2 * 256) * 128 + 2 * 256 * 4 + 64;
+  const int smem_dq = 1024 + 2 * (256 + 2 * 256) * 128 + 128;
+  const int smem_kv = 1024 + 2 * (256 + 2 * 256) * 128 + 2 * 512 * 4 + 128;
   static std::once_flag once;
+  static int nsm = 148;
   std::call_once(once, [smem_dq, smem_kv] {
-    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
-    cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem_kv);
+    cudaFuncSetAttribute(attn_bwd_dq_tc_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem_dq);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tc_persistent,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   });
-  dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(H),
-            static_cast<unsigned>(S));
-  attn_bwd_dkdv_tc_kernel<<<grid, kBwdThreads, smem_kv, stream>>>(
-      kv128, qNk, doNk, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
-  attn_bwd_dq_tc_kernel<<<grid, kBwdThreads, smem_dq, stream>>>(
-      q128, kvNk, do128, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  BwdItems items;
+  items.ntile = static_cast<int>((N + 127) / 128);
+  items.nitems = static_cast<int>(S * H) * items.ntile;
+  const unsigned grid = static_cast<unsigned>(items.nitems < nsm ? items.nitems : nsm);
+  attn_bwd_dkdv_tc_persistent<<<grid, kBwdThreads, smem_kv, stream>>>(
+      kv128, qNk, doNk, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g, items);
+  attn_bwd_dq_tc_persistent<<<grid, kBwdThreads, smem_dq, stream>>>(
+      q128, kvNk, do128, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g, items);
   return rp_check_launch("attention_bwd_tc");
 }
