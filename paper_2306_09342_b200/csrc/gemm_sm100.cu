@@ -424,6 +424,202 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, Cfg::kTmemCols);
 }
 
+// ============================================================ 2-SM (CTA pair) variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile. CTA r loads
+// A rows [m0 + 128 r, +128) and B rows [n0 + 128 r, +128) into its own smem; the leader
+// (r = 0) issues tcgen05.mma.cta_group::2 (M = 256, N = 256) which reads both CTAs'
+// halves; each CTA's TMEM receives its 128 accumulator rows. Per SM this moves 32 KB of
+// operands per 128x256x64 step instead of 48 KB, which is what the L2 can sustain.
+template <int EPI>
+struct Gemm2Cfg {
+  static constexpr int kStages = 6;
+  static constexpr int kHalfBytes = 128 * kBK * 2;         // 16 KB: one A or B half stage
+  static constexpr int kStageBytes = 2 * kHalfBytes;       // per CTA
+  static constexpr int kTmemCols = 512;                    // 2 x 256 accumulator columns
+  static constexpr int kEpiBytes = 8 * 4096;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+};
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_sm100_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB, const GemmShape sh,
+                          const GemmEpi ep) {
+  using Cfg = Gemm2Cfg<EPI>;
+  constexpr int S = Cfg::kStages;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kHalfBytes;
+  uint8_t* sEpi = smem + S * Cfg::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + Cfg::kEpiBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);  // both CTAs' epilogue warps (leader's copy)
+    }
+    fence_barrier_init();
+  }
+  cluster_sync_all();
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles = sh.m_tiles * sh.n_tiles;  // m_tiles counts 256-row pair tiles
+  const int units = tiles * sh.splits;
+  const int cluster_id = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs, each its own halves)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cluster_id; u < units; u += nclusters) {
+        const int split = u / tiles, tile = u % tiles;
+        const int m0 = (tile / sh.n_tiles) * 256 + 128 * static_cast<int>(rank);
+        const int n0 = (tile % sh.n_tiles) * BN + 128 * static_cast<int>(rank);
+        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
+        const int kb1 =
+            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::kStageBytes);
+          uint8_t* a = sA + stage * Cfg::kHalfBytes;
+          uint8_t* b = sB + stage * Cfg::kHalfBytes;
+          const int k0 = kb * kBK;
+          if constexpr (A_MN) {
+            tma_load_2d_2sm(a, &tmA, lbar, m0, k0);
+            tma_load_2d_2sm(a + 8192, &tmA, lbar, m0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(a, &tmA, lbar, k0, m0);
+          }
+          if constexpr (B_MN) {
+            tma_load_2d_2sm(b, &tmB, lbar, n0, k0);
+            tma_load_2d_2sm(b + 8192, &tmB, lbar, n0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(b, &tmB, lbar, k0, n0);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cluster_id; u < units; u += nclusters) {
+        const int split = u / tiles;
+        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
+        const int kb1 =
+            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kHalfBytes);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kHalfBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            umma_bf16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm_mc(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9 (both CTAs; this CTA's 128 rows of the tile)
+    const uint32_t q = warp & 3u;
+    const int half = (static_cast<int>(warp) - 2) >> 2;
+    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage);
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cluster_id; u < units; u += nclusters) {
+      const int split = u / tiles, tile = u % tiles;
+      const int64_t m0 = static_cast<int64_t>(tile / sh.n_tiles) * 256 + 128 * rank;
+      const int64_t n0 = static_cast<int64_t>(tile % sh.n_tiles) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * BN);
+      const int64_t row0 = m0 + q * 32;
+      const int c_begin = half * (BN / 2), c_end = (half + 1) * (BN / 2);
+      constexpr int CW = EpiTraits<EPI>::kCW;
+      const bool rows_ok = row0 < sh.M;
+      ChunkIn nxt;
+      if (rows_ok && n0 + c_begin < sh.N)
+        prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c_begin, nxt);
+#pragma unroll 1
+      for (int c = c_begin; c < c_end; c += CW) {
+        float v[CW];
+        tmem_ld32(tbase + c, v);
+        if constexpr (CW == 64) tmem_ld32(tbase + c + 32, v + 32);
+        const ChunkIn cur = nxt;
+        if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
+          prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
+        if (rows_ok && n0 + c < sh.N)
+          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty0 + static_cast<uint32_t>(acc * 8));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_2sm(tmem_base, Cfg::kTmemCols);
+}
+
 // Deterministic split-K reduction: out[i] = sum_{s=0..S-1} part[s][i], fixed order.
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
                                      int64_t stride, int64_t n4, float* __restrict__ out) {
@@ -502,6 +698,36 @@ static GemmKernelPtr pick_epi(int epi) {
   return nullptr;
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+static GemmKernelPtr kernel_ptr_2sm() {
+  static std::once_flag once;
+  auto k = &gemm_sm100_2sm_kernel<A_MN, B_MN, EPI>;
+  std::call_once(once, [k] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Gemm2Cfg<EPI>::kSmemBytes);
+  });
+  return reinterpret_cast<GemmKernelPtr>(k);
+}
+
+template <bool A_MN, bool B_MN>
+static GemmKernelPtr pick_epi_2sm(int epi) {
+  switch (epi) {
+    case RP_EPI_BF16: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BF16>();
+    case RP_EPI_F32: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_F32>();
+    case RP_EPI_BIAS_GELU: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU>();
+    case RP_EPI_RESID: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_RESID>();
+    case RP_EPI_GELU_BWD: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_GELU_BWD>();
+  }
+  return nullptr;
+}
+
+static GemmKernelPtr pick_2sm(bool a_mn, bool b_mn, int epi) {
+  if (!a_mn && !b_mn) return pick_epi_2sm<false, false>(epi);
+  if (!a_mn && b_mn) return pick_epi_2sm<false, true>(epi);
+  if (a_mn && !b_mn) return pick_epi_2sm<true, false>(epi);
+  return pick_epi_2sm<true, true>(epi);
+}
+
 template <int BN>
 static GemmKernelPtr pick(bool a_mn, bool b_mn, int epi) {
   if (!a_mn && !b_mn) return pick_epi<BN, false, false>(epi);
@@ -531,12 +757,15 @@ struct RpGemmPlan {
   GemmEpi ep;
   GemmKernelPtr kern;
   int bn;
+  bool two_sm;
   int grid;
   int smem;
   // split-K reduction (only when splits > 1)
   float* red_out;
   int64_t red_n;
 };
+
+extern "C" int rp_gemm_plan_set_max_ctas(RpGemmPlan* p, int max_ctas);
 
 extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   if (!d || !out) return rp_fail(RP_ERR_CONTRACT, "gemm: null descriptor");
@@ -548,13 +777,15 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
     return rp_fail(RP_ERR_SHAPE, "gemm: leading dimensions must be 16-byte multiples");
   if ((reinterpret_cast<uintptr_t>(d->A) | reinterpret_cast<uintptr_t>(d->B)) & 15)
     return rp_fail(RP_ERR_SHAPE, "gemm: operands must be 16-byte aligned");
+  const bool two_sm = d->bn == 512;  // CTA-pair 256x256 tiles
   const int bn = (d->bn == 128) ? 128 : 256;
   RpGemmPlan* p = new RpGemmPlan();
   p->bn = bn;
+  p->two_sm = two_sm;
   p->sh.M = M;
   p->sh.N = N;
   p->sh.K = K;
-  p->sh.m_tiles = static_cast<int32_t>((M + kBM - 1) / kBM);
+  p->sh.m_tiles = static_cast<int32_t>((M + (two_sm ? 255 : kBM - 1)) / (two_sm ? 256 : kBM));
   p->sh.n_tiles = static_cast<int32_t>((N + bn - 1) / bn);
   p->sh.k_blocks = static_cast<int32_t>((K + kBK - 1) / kBK);
   int splits = d->splits < 1 ? 1 : d->splits;
@@ -594,21 +825,22 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
     if (d->b_mn)
       rc = encode_map(&p->tmB, d->B, K, N, d->ldb, 64);
     else
-      rc = encode_map(&p->tmB, d->B, N, K, d->ldb, static_cast<uint32_t>(bn));
+      rc = encode_map(&p->tmB, d->B, N, K, d->ldb, two_sm ? 128u : static_cast<uint32_t>(bn));
   }
   if (rc != RP_OK) {
     delete p;
     return rp_fail(rc, "gemm: cuTensorMapEncodeTiled failed");
   }
-  p->kern = bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi) : pick<128>(d->a_mn, d->b_mn, d->epi);
+  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, d->epi)
+                   : (bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi)
+                                : pick<128>(d->a_mn, d->b_mn, d->epi));
   if (!p->kern) {
     delete p;
     return rp_fail(RP_ERR_CONFIG, "gemm: unknown epilogue");
   }
-  p->smem = bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes;
-  const int units = p->sh.m_tiles * p->sh.n_tiles * splits;
-  int cap = d->max_ctas > 0 ? d->max_ctas : num_sms();
-  p->grid = units < cap ? units : cap;
+  p->smem = two_sm ? Gemm2Cfg<RP_EPI_F32>::kSmemBytes
+                   : (bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes);
+  rp_gemm_plan_set_max_ctas(p, d->max_ctas);
   *out = p;
   return RP_OK;
 }
@@ -632,8 +864,14 @@ extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
 extern "C" int rp_gemm_plan_set_max_ctas(RpGemmPlan* p, int max_ctas) {
   if (!p) return RP_ERR_CONTRACT;
   const int units = p->sh.m_tiles * p->sh.n_tiles * p->sh.splits;
-  const int cap = max_ctas > 0 ? max_ctas : num_sms();
-  p->grid = units < cap ? units : cap;
+  int cap = max_ctas > 0 ? max_ctas : num_sms();
+  if (p->two_sm) {  // one unit per CTA pair; grid is a whole number of clusters
+    int pairs = cap / 2;
+    if (pairs < 1) pairs = 1;
+    p->grid = 2 * (units < pairs ? units : pairs);
+  } else {
+    p->grid = units < cap ? units : cap;
+  }
   return RP_OK;
 }
 

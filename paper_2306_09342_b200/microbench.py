@@ -101,6 +101,18 @@ def main(argv=None):
              lambda: K.gemm(x3, W2, T, d, h, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=yo, aux=res,
                             bias=b2),
              lambda: torch.matmul(x3, W2))
+    # the same forward shapes on CTA pairs (cta_group::2, 256x256 tiles)
+    gemm_row("fwd_qkv_2sm", T, 3 * d, d,
+             lambda: K.gemm(x, Wqkv, T, 3 * d, d, a_mn=0, b_mn=1, epi=RP_EPI_BF16, out=qkv, bn=512))
+    gemm_row("fwd_w1_gelu_2sm", T, h, d,
+             lambda: K.gemm(x, W1, T, h, d, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU, out=aa,
+                            out2=uu, bias=b1, bn=512))
+    gemm_row("fwd_w2_resid_2sm", T, d, h,
+             lambda: K.gemm(x3, W2, T, d, h, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=yo, aux=res,
+                            bias=b2, bn=512))
+    gemm_row("fwd_proj_resid_2sm", T, d, d,
+             lambda: K.gemm(x, Wo, T, d, d, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=yo, aux=res,
+                            bn=512))
     # dgrad
     du = torch.empty(T, h, device=dev, dtype=bf)
     gemm_row("dgrad_w2_gelu", T, h, d,
@@ -114,15 +126,22 @@ def main(argv=None):
              lambda: K.gemm(qkv, Wqkv, T, d, 3 * d, a_mn=0, b_mn=0, epi=RP_EPI_BF16, out=dh),
              lambda: torch.matmul(qkv, Wqkv.t()))
     # wgrad (split-K)
-    for name, A_, B_, M, Nn, splits in [("wgrad_w1", x, x3, d, h, 2), ("wgrad_w2", x3, x, h, d, 2),
-                                        ("wgrad_qkv", x, qkv, d, 3 * d, 3),
-                                        ("wgrad_proj", x, x, d, d, 8)]:
+    gemm_row("dgrad_w2_gelu_2sm", T, h, d,
+             lambda: K.gemm(x, W2, T, h, d, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD, out=du, aux=uu,
+                            bn=512))
+    gemm_row("dgrad_w1_2sm", T, d, h,
+             lambda: K.gemm(x3, W1, T, d, h, a_mn=0, b_mn=0, epi=RP_EPI_BF16, out=dh, bn=512))
+    for name, A_, B_, M, Nn, splits, bnn in [
+            ("wgrad_w1", x, x3, d, h, 2, 256), ("wgrad_w2", x3, x, h, d, 2, 256),
+            ("wgrad_qkv", x, qkv, d, 3 * d, 8, 256), ("wgrad_proj", x, x, d, d, 8, 256),
+            ("wgrad_w1_2sm", x, x3, d, h, 4, 512), ("wgrad_w2_2sm", x3, x, h, d, 4, 512),
+            ("wgrad_qkv_2sm", x, qkv, d, 3 * d, 8, 512), ("wgrad_proj_2sm", x, x, d, d, 16, 512)]:
         o = torch.empty(M, Nn, device=dev)
         ws = torch.empty(splits * M * Nn, device=dev)
         gemm_row(f"{name}_s{splits}", M, Nn, T,
-                 lambda A_=A_, B_=B_, M=M, Nn=Nn, o=o, ws=ws, s=splits: K.gemm(
+                 lambda A_=A_, B_=B_, M=M, Nn=Nn, o=o, ws=ws, s=splits, bnn=bnn: K.gemm(
                      A_, B_, M, Nn, T, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=s,
-                     workspace=ws),
+                     workspace=ws, bn=bnn),
                  lambda A_=A_, B_=B_: torch.matmul(A_.t(), B_))
 
     # memory-bound kernels

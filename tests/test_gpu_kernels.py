@@ -36,7 +36,7 @@ SHAPES = [(296, 512, 200), (128, 256, 64), (1000, 768, 768), (264, 2304, 136)]
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("bn", [256, 128])
+@pytest.mark.parametrize("bn", [256, 128, 512], ids=["128x256", "128x128", "2sm-256x256"])
 def test_gemm_majors_bf16(K, a_mn, b_mn, shape, bn):
     from paper_2306_09342_b200._capi import RP_EPI_BF16
     M, N, Kd = shape
@@ -58,31 +58,35 @@ def test_gemm_persistent_grid_independent(K):
     A = torch.randn(Kd, M, device="cuda").bfloat16()
     Bm = torch.randn(Kd, N, device="cuda").bfloat16()
     outs = []
-    for cap in (0, 5, 37):
+    for bn, cap in ((256, 0), (256, 5), (256, 37), (512, 0), (512, 6), (512, 38)):
         o = torch.empty(M, N, device="cuda")
         ws = torch.empty(4 * M * N, device="cuda")
         K.gemm(A, Bm, M, N, Kd, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=4, workspace=ws,
-               max_ctas=cap)
+               max_ctas=cap, bn=bn)
         outs.append(o)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert torch.equal(outs[3], outs[4]) and torch.equal(outs[3], outs[5])
     ref = A.float().t() @ Bm.float()
     assert rel(outs[0], ref) < 1e-4
 
 
+@pytest.mark.parametrize("bn", [256, 512])
 @pytest.mark.parametrize("splits", [1, 3, 8])
-def test_gemm_wgrad_splitk(K, splits):
+def test_gemm_wgrad_splitk(K, splits, bn):
     from paper_2306_09342_b200._capi import RP_EPI_F32
     T, M, N = 5000, 384, 768
     X = torch.randn(T, M, device="cuda").bfloat16()
     dY = torch.randn(T, N, device="cuda").bfloat16()
     o = torch.empty(M, N, device="cuda")
     ws = torch.empty(splits * M * N, device="cuda")
-    K.gemm(X, dY, M, N, T, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=splits, workspace=ws)
+    K.gemm(X, dY, M, N, T, a_mn=1, b_mn=1, epi=RP_EPI_F32, out=o, splits=splits, workspace=ws,
+           bn=bn)
     ref = X.float().t() @ dY.float()
     assert rel(o, ref) < 1e-4
 
 
-def test_gemm_bias_gelu(K):
+@pytest.mark.parametrize("bn", [256, 512])
+def test_gemm_bias_gelu(K, bn):
     from paper_2306_09342_b200._capi import RP_EPI_BIAS_GELU
     M, N, Kd = 515, 1024, 192
     A = torch.randn(M, Kd, device="cuda").bfloat16()
@@ -90,14 +94,15 @@ def test_gemm_bias_gelu(K):
     bias = torch.randn(N, device="cuda")
     a = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU, out=a, out2=u, bias=bias)
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU, out=a, out2=u, bias=bias, bn=bn)
     uref = A.float() @ W.float() + bias
     assert rel(u, uref) < 1e-2
     assert rel(a, gelu_ref(uref)) < 1e-2
 
 
+@pytest.mark.parametrize("bn", [256, 512])
 @pytest.mark.parametrize("sign", [1.0, -1.0])
-def test_gemm_residual(K, sign):
+def test_gemm_residual(K, sign, bn):
     from paper_2306_09342_b200._capi import RP_EPI_RESID
     M, N, Kd = 700, 768, 3072
     A = torch.randn(M, Kd, device="cuda").bfloat16()
@@ -106,24 +111,25 @@ def test_gemm_residual(K, sign):
     res = torch.randn(M, N, device="cuda")
     out = torch.empty(M, N, device="cuda")
     K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=out, aux=res, bias=bias,
-           sign=sign)
+           sign=sign, bn=bn)
     ref = res + sign * (A.float() @ W.float() + bias)
     assert rel(out, ref) < 1e-4
     # in place (out aliases the residual), as the inverse uses it
     res2 = res.clone()
     K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=res2, aux=res2, bias=bias,
-           sign=sign)
+           sign=sign, bn=bn)
     assert torch.equal(res2, out)
 
 
-def test_gemm_gelu_bwd(K):
+@pytest.mark.parametrize("bn", [256, 512])
+def test_gemm_gelu_bwd(K, bn):
     from paper_2306_09342_b200._capi import RP_EPI_GELU_BWD
     M, N, Kd = 640, 3072, 768
     dY = torch.randn(M, Kd, device="cuda").bfloat16()
     W2 = (0.05 * torch.randn(N, Kd, device="cuda")).bfloat16()  # W2 is [h, d] = [N][K]
     u = torch.randn(M, N, device="cuda").bfloat16()
     du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    K.gemm(dY, W2, M, N, Kd, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD, out=du, aux=u)
+    K.gemm(dY, W2, M, N, Kd, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD, out=du, aux=u, bn=bn)
     ref = (dY.float() @ W2.float().t()) * gelu_slope_ref(u.float())
     assert rel(du, ref) < 1e-2
 
