@@ -42,6 +42,36 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// two 16-column TMEM loads behind one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, float* a, float* b) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(ta), "r"(tb)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    a[i] = __uint_as_float(r[i]);
+    b[i] = __uint_as_float(r[16 + i]);
+  }
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -172,16 +202,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (c + 16 <= valid) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float p0 = exp2f(v[2 * i] * g.scale_log2 - ms);
-          const float p1 = exp2f(v[2 * i + 1] * g.scale_log2 - ms);
+          const float p0 = ex2(fmaf(v[2 * i], g.scale_log2, -ms));
+          const float p1 = ex2(fmaf(v[2 * i + 1], g.scale_log2, -ms));
           l4[i & 3] += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
         }
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float p0 = (c + 2 * i < valid) ? exp2f(v[2 * i] * g.scale_log2 - ms) : 0.f;
-          const float p1 = (c + 2 * i + 1 < valid) ? exp2f(v[2 * i + 1] * g.scale_log2 - ms) : 0.f;
+          const float p0 = (c + 2 * i < valid) ? ex2(fmaf(v[2 * i], g.scale_log2, -ms)) : 0.f;
+          const float p1 = (c + 2 * i + 1 < valid) ? ex2(fmaf(v[2 * i + 1], g.scale_log2, -ms)) : 0.f;
           l4[i & 3] += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
         }
@@ -244,264 +274,6 @@ struct BwdGeom {
 __device__ __forceinline__ int packed_col(int c, int c0) { return c0 + (c - c0) / 2; }
 __device__ __forceinline__ int ts_acol(int ks, int half) {
   return ks * 16 < half ? ks * 8 : half + (ks * 16 - half) / 2;
-}
-
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q128,
-                          const __grid_constant__ CUtensorMap tm_kv,
-                          const __grid_constant__ CUtensorMap tm_do128,
-                          const float* __restrict__ lse, const float* __restrict__ Dg,
-                          __nv_bfloat16* __restrict__ dqkv, BwdGeom g) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem;              // 128 x 128 B
-  uint8_t* sO = sQ + 128 * 128;    // dO tile
-  uint8_t* sK = sO + 128 * 128;    // Nk x 128 B
-  uint8_t* sV = sK + 256 * 128;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 256 * 128);
-  uint64_t* bar_load = bars;
-  uint64_t* bar_s = bars + 1;
-  uint64_t* bar_p = bars + 2;
-  uint64_t* bar_o = bars + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int q0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
-  const int Nk = g.Nk, half = Nk / 2;
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_q128);
-      tma_prefetch_desc(&tm_kv);
-      tma_prefetch_desc(&tm_do128);
-      mbar_init(bar_load, 1);
-      mbar_init(bar_s, 1);
-      mbar_init(bar_p, 8);
-      mbar_init(bar_o, 1);
-      fence_barrier_init();
-    }
-    tmem_alloc(tmem_slot, 512);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int row_seq = b * g.N;
-  const int d = g.H * 64;
-  if (warp == 8) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar_load, (256 + 2 * Nk) * 128);
-      tma_load_2d(sQ, &tm_q128, bar_load, h * 64, row_seq + q0);
-      tma_load_2d(sO, &tm_do128, bar_load, h * 64, row_seq + q0);
-      tma_load_2d(sK, &tm_kv, bar_load, d + h * 64, row_seq);
-      tma_load_2d(sV, &tm_kv, bar_load, 2 * d + h * 64, row_seq);
-      mbar_wait(bar_load, 0);
-      tc_fence_after();
-      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
-      const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO), bk = smem_u32(sK), bv = smem_u32(sV);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem, make_sdesc_sw128(aq + kk * 32, 16, 1024),
-                  make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem + 256, make_sdesc_sw128(ao + kk * 32, 16, 1024),
-                  make_sdesc_sw128(bv + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-      umma_commit(bar_s);
-      mbar_wait(bar_p, 0);
-      tc_fence_after();
-      // dQ = dS K : M = 128, N = 64, K = Nk; B = K rows [key][hd] -> MN-major
-      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
-      for (int ks = 0; ks < Nk / 16; ++ks)
-        umma_ts_bf16(tmem + 256, tmem + static_cast<uint32_t>(ts_acol(ks, half)),
-                     make_sdesc_sw128(bk + ks * 2048, 8192, 1024), idesc_o, ks > 0 ? 1u : 0u);
-      umma_commit(bar_o);
-    }
-  } else {
-    const int q = static_cast<int>(warp & 3u), kh = static_cast<int>(warp >> 2);
-    const int c0 = kh * half;
-    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(q) * 32u) << 16);
-    const int row = q0 + q * 32 + static_cast<int>(lane);
-    const bool row_ok = row < g.N;
-    const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
-    const float lr = row_ok ? lse[hb + row] : 0.f;
-    const float dr = row_ok ? Dg[hb + row] : 0.f;
-    mbar_wait(bar_s, 0);
-    tc_fence_after();
-    const int valid = g.N;
-    for (int c = c0; c < c0 + half; c += 16) {
-      float s[16], dp[16];
-      tmem_ld16(lane_base + c, s);
-      tmem_ld16(lane_base + 256 + c, dp);
-      uint32_t pk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int k0 = c + 2 * i;
-        const float p0 = k0 < valid ? exp2f(s[2 * i] * g.scale_log2 - lr) : 0.f;
-        const float p1 = k0 + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - lr) : 0.f;
-        pk[i] = pack_bf16x2(p0 * (dp[2 * i] - dr) * g.scale, p1 * (dp[2 * i + 1] - dr) * g.scale);
-      }
-      tmem_st8(lane_base + packed_col(c, c0), pk);
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_p);
-    mbar_wait(bar_o, 0);
-    tc_fence_after();
-    float o[32];
-    tmem_ld32(lane_base + 256 + kh * 32, o);
-    if (row_ok) {
-      uint4* dst = reinterpret_cast<uint4*>(dqkv + (static_cast<int64_t>(row_seq) + row) * g.ld_qkv +
-                                            h * 64 + kh * 32);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        dst[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
-                            pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
-                            pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, 512);
-}
-
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_kv128,
-                            const __grid_constant__ CUtensorMap tm_qNk,
-                            const __grid_constant__ CUtensorMap tm_doNk,
-                            const float* __restrict__ lse, const float* __restrict__ Dg,
-                            __nv_bfloat16* __restrict__ dqkv, BwdGeom g) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sK = smem;              // key tile 128 x 128 B
-  uint8_t* sV = sK + 128 * 128;
-  uint8_t* sQ = sV + 128 * 128;    // all queries Nq x 128 B
-  uint8_t* sO = sQ + 256 * 128;    // all dO rows
-  float* sL = reinterpret_cast<float*>(sO + 256 * 128);
-  float* sD = sL + 256;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
-  uint64_t* bar_load = bars;
-  uint64_t* bar_s = bars + 1;
-  uint64_t* bar_p = bars + 2;
-  uint64_t* bar_o = bars + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int k0 = blockIdx.x * 128, h = blockIdx.y, b = blockIdx.z;
-  const int Nq = g.Nk, half = Nq / 2;
-  const int row_seq = b * g.N;
-  const int d = g.H * 64;
-  const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_kv128);
-      tma_prefetch_desc(&tm_qNk);
-      tma_prefetch_desc(&tm_doNk);
-      mbar_init(bar_load, 1);
-      mbar_init(bar_s, 1);
-      mbar_init(bar_p, 8);
-      mbar_init(bar_o, 1);
-      fence_barrier_init();
-      mbar_arrive_expect_tx(bar_load, (256 + 2 * Nq) * 128);
-      tma_load_2d(sK, &tm_kv128, bar_load, d + h * 64, row_seq + k0);
-      tma_load_2d(sV, &tm_kv128, bar_load, 2 * d + h * 64, row_seq + k0);
-      tma_load_2d(sQ, &tm_qNk, bar_load, h * 64, row_seq);
-      tma_load_2d(sO, &tm_doNk, bar_load, h * 64, row_seq);
-    }
-    tmem_alloc(tmem_slot, 512);
-  } else {
-    for (int i = threadIdx.x; i < Nq; i += 256) {
-      sL[i] = i < g.N ? lse[hb + i] : 0.f;
-      sD[i] = i < g.N ? Dg[hb + i] : 0.f;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (warp == 8) {
-    if (lane == 0) {
-      mbar_wait(bar_load, 0);
-      tc_fence_after();
-      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nq), false, false);
-      const uint32_t ak = smem_u32(sK), av = smem_u32(sV), bq = smem_u32(sQ), bo = smem_u32(sO);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem, make_sdesc_sw128(ak + kk * 32, 16, 1024),
-                  make_sdesc_sw128(bq + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem + 256, make_sdesc_sw128(av + kk * 32, 16, 1024),
-                  make_sdesc_sw128(bo + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-      umma_commit(bar_s);
-      mbar_wait(bar_p, 0);
-      tc_fence_after();
-      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
-      for (int ks = 0; ks < Nq / 16; ++ks) {
-        const uint32_t ac = static_cast<uint32_t>(ts_acol(ks, half));
-        // dV = P^T dO  (B = dO rows [query][hd], MN-major) -> cols [192, 256)
-        umma_ts_bf16(tmem + 192, tmem + ac, make_sdesc_sw128(bo + ks * 2048, 8192, 1024),
-                     idesc_o, ks > 0 ? 1u : 0u);
-        // dK = dS^T Q  (B = Q rows, MN-major) -> cols [448, 512)
-        umma_ts_bf16(tmem + 448, tmem + 256 + ac, make_sdesc_sw128(bq + ks * 2048, 8192, 1024),
-                     idesc_o, ks > 0 ? 1u : 0u);
-      }
-      umma_commit(bar_o);
-    }
-  } else {
-    const int qd = static_cast<int>(warp & 3u), qh = static_cast<int>(warp >> 2);
-    const int c0 = qh * half;
-    const uint32_t lane_base = tmem + ((static_cast<uint32_t>(qd) * 32u) << 16);
-    const int key = k0 + qd * 32 + static_cast<int>(lane);
-    mbar_wait(bar_s, 0);
-    tc_fence_after();
-    const int valid = g.N;
-    for (int c = c0; c < c0 + half; c += 16) {
-      float s[16], dp[16];
-      tmem_ld16(lane_base + c, s);
-      tmem_ld16(lane_base + 256 + c, dp);
-      uint32_t pp[8], pd[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int qa = c + 2 * i;
-        const float p0 = qa < valid ? exp2f(s[2 * i] * g.scale_log2 - sL[qa]) : 0.f;
-        const float p1 = qa + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - sL[qa + 1]) : 0.f;
-        pp[i] = pack_bf16x2(p0, p1);
-        pd[i] = pack_bf16x2(p0 * (dp[2 * i] - sD[qa]) * g.scale,
-                            p1 * (dp[2 * i + 1] - sD[qa + 1]) * g.scale);
-      }
-      tmem_st8(lane_base + packed_col(c, c0), pp);
-      tmem_st8(lane_base + 256 + packed_col(c, c0), pd);
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_p);
-    mbar_wait(bar_o, 0);
-    tc_fence_after();
-    // warp half qh writes columns [32 qh, 32 qh + 32) of dK and dV for its 32 keys
-    float o[32];
-    const bool key_ok = key < g.N;
-    __nv_bfloat16* base = dqkv + (static_cast<int64_t>(row_seq) + key) * g.ld_qkv + h * 64 + qh * 32;
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {  // 0: dK (cols 448), 1: dV (cols 192)
-      tmem_ld32(lane_base + (which == 0 ? 448 : 192) + qh * 32, o);
-      if (key_ok) {
-        uint4* dst = reinterpret_cast<uint4*>(base + (which == 0 ? d : 2 * d));
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
-                              pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
-                              pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
-                              pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------- persistent backward
@@ -621,17 +393,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(bar_s, k & 1);
       tc_fence_after();
       const int valid = g.N;
+      const float nds = -dr * g.scale;  // dS = P * (dP*scale - D*scale)
       for (int c = c0; c < c0 + half; c += 16) {
         float s[16], dp[16];
-        tmem_ld16(lane_base + c, s);
-        tmem_ld16(lane_base + 256 + c, dp);
+        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s, dp);
         uint32_t pk[8];
+        if (c + 16 <= valid) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int k0 = c + 2 * i;
-          const float p0 = k0 < valid ? exp2f(s[2 * i] * g.scale_log2 - lr) : 0.f;
-          const float p1 = k0 + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - lr) : 0.f;
-          pk[i] = pack_bf16x2(p0 * (dp[2 * i] - dr) * g.scale, p1 * (dp[2 * i + 1] - dr) * g.scale);
+          for (int i = 0; i < 8; ++i) {
+            const float p0 = ex2(fmaf(s[2 * i], g.scale_log2, -lr));
+            const float p1 = ex2(fmaf(s[2 * i + 1], g.scale_log2, -lr));
+            pk[i] = pack_bf16x2(p0 * fmaf(dp[2 * i], g.scale, nds),
+                                p1 * fmaf(dp[2 * i + 1], g.scale, nds));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int k0 = c + 2 * i;
+            const float p0 = k0 < valid ? ex2(fmaf(s[2 * i], g.scale_log2, -lr)) : 0.f;
+            const float p1 = k0 + 1 < valid ? ex2(fmaf(s[2 * i + 1], g.scale_log2, -lr)) : 0.f;
+            pk[i] = pack_bf16x2(p0 * fmaf(dp[2 * i], g.scale, nds),
+                                p1 * fmaf(dp[2 * i + 1], g.scale, nds));
+          }
         }
         tmem_st8(lane_base + packed_col(c, c0), pk);
       }
@@ -766,28 +549,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
       float* sL = sLD + (k & 1) * 512;
       float* sD = sL + 256;
-      for (int i = threadIdx.x; i < Nq; i += 256) {
-        sL[i] = i < g.N ? lse[hb + i] : 0.f;
-        sD[i] = i < g.N ? Dg[hb + i] : 0.f;
+      for (int i = threadIdx.x; i < Nq; i += 256) {  // -lse and -D*scale per query
+        sL[i] = i < g.N ? -lse[hb + i] : -INFINITY;
+        sD[i] = i < g.N ? -Dg[hb + i] * g.scale : 0.f;
       }
       named_bar(2, 256);
       const int key = tile * 128 + qd * 32 + static_cast<int>(lane);
       mbar_wait(bar_s, k & 1);
       tc_fence_after();
-      const int valid = g.N;
       for (int c = c0; c < c0 + half; c += 16) {
         float s[16], dp[16];
-        tmem_ld16(lane_base + c, s);
-        tmem_ld16(lane_base + 256 + c, dp);
+        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s, dp);
         uint32_t pp[8], pd[8];
+        const float4* l4 = reinterpret_cast<const float4*>(sL + c);
+        const float4* d4 = reinterpret_cast<const float4*>(sD + c);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int qa = c + 2 * i;
-          const float p0 = qa < valid ? exp2f(s[2 * i] * g.scale_log2 - sL[qa]) : 0.f;
-          const float p1 = qa + 1 < valid ? exp2f(s[2 * i + 1] * g.scale_log2 - sL[qa + 1]) : 0.f;
-          pp[i] = pack_bf16x2(p0, p1);
-          pd[i] = pack_bf16x2(p0 * (dp[2 * i] - sD[qa]) * g.scale,
-                              p1 * (dp[2 * i + 1] - sD[qa + 1]) * g.scale);
+        for (int j = 0; j < 4; ++j) {
+          const float4 nl = l4[j], nd = d4[j];
+          const float la[4] = {nl.x, nl.y, nl.z, nl.w}, da[4] = {nd.x, nd.y, nd.z, nd.w};
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int e = 4 * j + 2 * t;  // masked queries carry -lse = -inf -> p = 0
+            const float p0 = ex2(fmaf(s[e], g.scale_log2, la[2 * t]));
+            const float p1 = ex2(fmaf(s[e + 1], g.scale_log2, la[2 * t + 1]));
+            pp[2 * j + t] = pack_bf16x2(p0, p1);
+            pd[2 * j + t] = pack_bf16x2(p0 * fmaf(dp[e], g.scale, da[2 * t]),
+                                        p1 * fmaf(dp[e + 1], g.scale, da[2 * t + 1]));
+          }
         }
         tmem_st8(lane_base + packed_col(c, c0), pp);
         tmem_st8(lane_base + 256 + packed_col(c, c0), pd);

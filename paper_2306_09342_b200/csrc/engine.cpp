@@ -53,16 +53,22 @@ struct BlockPlans {
              *g_dproj = nullptr, *g_wproj = nullptr, *g_wqkv = nullptr, *g_dqkv = nullptr;
 };
 
+// GEMM tiling used by the engine: CTA-pair (cta_group::2) 256 x 256 tiles.
+constexpr int kGemmBn = 512;
+
 int pick_splits(int64_t M, int64_t N, int64_t K, int bn) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  const bool pair = bn == 512;
+  const int tm = pair ? 256 : 128, tn = pair ? 256 : bn;
+  const int slots = pair ? kSms / 2 : kSms;
+  const int64_t tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
   const int64_t kb = (K + 63) / 64;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 64; ++s) {
     if (kb / s < 8) break;  // keep >= 8 k-blocks per split
     const int64_t units = tiles * s;
-    const double waves = static_cast<double>((units + kSms - 1) / kSms);
-    const double eff = static_cast<double>(units) / (waves * kSms) - 0.004 * s;
+    const double waves = static_cast<double>((units + slots - 1) / slots);
+    const double eff = static_cast<double>(units) / (waves * slots) - 0.004 * s;
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = s;
@@ -197,7 +203,7 @@ int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   d.splits = a.splits;
   d.workspace = a.ws;
   d.max_ctas = 0;
-  d.bn = 256;
+  d.bn = kGemmBn;
   int rc = rp_gemm_plan_create(&d, out);
   if (rc != RP_OK) return rp_fail(rc, "engine: gemm plan creation failed");
   g->all_plans.push_back(*out);
@@ -213,9 +219,9 @@ float* X2(RpEngine* g, int64_t j) { return j == 0 ? g->e : g->buf2[j % 3]; }
 
 int build_plans(RpEngine* g) {
   const int64_t T = g->T, d = g->d, h = g->h;
-  const int s_qkv = pick_splits(d, 3 * d, T, 256), s_proj = pick_splits(d, d, T, 256),
-            s_w1 = pick_splits(d, h, T, 256), s_w2 = pick_splits(h, d, T, 256),
-            s_emb = pick_splits(g->in, d, T, 256);
+  const int s_qkv = pick_splits(d, 3 * d, T, kGemmBn), s_proj = pick_splits(d, d, T, kGemmBn),
+            s_w1 = pick_splits(d, h, T, kGemmBn), s_w2 = pick_splits(h, d, T, kGemmBn),
+            s_emb = pick_splits(g->in, d, T, kGemmBn);
   g->plans.resize(static_cast<size_t>(g->L));
   for (int64_t b = 0; b < g->L; ++b) {
     BlockPlans& p = g->plans[static_cast<size_t>(b)];
@@ -594,7 +600,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   }
   int64_t split_ws = 0;
   for (auto mn : {std::pair<int64_t, int64_t>{d, 3 * d}, {d, d}, {d, h}, {h, d}, {g->in, d}}) {
-    const int s = pick_splits(mn.first, mn.second, T, 256);
+    const int s = pick_splits(mn.first, mn.second, T, kGemmBn);
     if (s > 1) split_ws = std::max<int64_t>(split_ws, s * mn.first * mn.second);
   }
   const int64_t col_ws = rp_colsum_workspace_floats(T, h > d ? h : d);
