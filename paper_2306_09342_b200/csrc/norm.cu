@@ -142,6 +142,98 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   }
 }
 
+// Backward, fused: the row kernel above plus dgamma / dbeta partial sums. Each warp keeps
+// its column sums in its own shared-memory row ([2][cols] floats, read-modify-write per
+// row it owns: rows w, w+8, ... of the CTA's kLnBwdRows), then the CTA combines its 8 warp
+// rows in warp order -> part[blk][2][cols]. Fixed association order, no atomics, and no
+// second pass over x and dy.
+template <int V>
+__global__ void __launch_bounds__(kLnWarps * 32, 2)
+    ln_bwd_fused_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
+                        const float* __restrict__ rstd_in, const float* __restrict__ gamma,
+                        const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
+                        int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16,
+                        float* __restrict__ part) {
+  extern __shared__ float acc[];  // [kLnWarps][2][cols]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c4 = cols >> 2;
+  float4* ag = reinterpret_cast<float4*>(acc + warp * 2 * cols);
+  float4* ab = reinterpret_cast<float4*>(acc + warp * 2 * cols + cols);
+  for (int c = lane; c < c4; c += 32) {
+    ag[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ab[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float inv_n = 1.0f / static_cast<float>(cols);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
+  for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
+    const int64_t row = r0 + rr;
+    if (row >= rows) break;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
+    const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    // pass 1: row sums (loads stay in L1 for pass 2)
+    float sg = 0.f, sgh = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + 32 * i;
+      if (c < c4) {
+        const float4 xv = xr[c];
+        const uint2 dv = dyr[c];
+        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+        const float4 gm = g4[c];
+        const float gx = d01.x * gm.x, gy = d01.y * gm.y, gz = d23.x * gm.z, gw = d23.y * gm.w;
+        sg += (gx + gy) + (gz + gw);
+        sgh += (gx * ((xv.x - mean) * rstd) + gy * ((xv.y - mean) * rstd)) +
+               (gz * ((xv.z - mean) * rstd) + gw * ((xv.w - mean) * rstd));
+      }
+    }
+    const float gmn = warp_sum(sg) * inv_n;
+    const float ghm = warp_sum(sgh) * inv_n;
+    // pass 2: dx = dres + (g - mean(g) - x_hat mean(g x_hat)) rstd; column sums
+    const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
+    float4* dxr = reinterpret_cast<float4*>(dx + row * cols);
+    uint2* dxb = dx_bf16 ? reinterpret_cast<uint2*>(dx_bf16 + row * cols) : nullptr;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + 32 * i;
+      if (c < c4) {
+        const float4 xv = xr[c];
+        const uint2 dv = dyr[c];
+        const float4 rv = drr ? drr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+        const float4 gm = g4[c];
+        const float hx = (xv.x - mean) * rstd, hy = (xv.y - mean) * rstd,
+                    hz = (xv.z - mean) * rstd, hw = (xv.w - mean) * rstd;
+        float4 o;
+        o.x = (d01.x * gm.x - gmn - hx * ghm) * rstd + rv.x;
+        o.y = (d01.y * gm.y - gmn - hy * ghm) * rstd + rv.y;
+        o.z = (d23.x * gm.z - gmn - hz * ghm) * rstd + rv.z;
+        o.w = (d23.y * gm.w - gmn - hw * ghm) * rstd + rv.w;
+        dxr[c] = o;
+        if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+        float4 a = ag[c], bb = ab[c];
+        a.x += d01.x * hx;
+        a.y += d01.y * hy;
+        a.z += d23.x * hz;
+        a.w += d23.y * hw;
+        bb.x += d01.x;
+        bb.y += d01.y;
+        bb.z += d23.x;
+        bb.w += d23.y;
+        ag[c] = a;
+        ab[c] = bb;
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
+    float t = acc[c];
+    for (int w = 1; w < kLnWarps; ++w) t += acc[w * 2 * cols + c];
+    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = t;
+  }
+}
+
 // Backward, column part (stage 1): CTA (rb, cb) sums dgamma = dy*x_hat and dbeta = dy
 // over rows [rb*RPB, (rb+1)*RPB) in row order for 4*256 columns -> part[rb][2][cols].
 __global__ void __launch_bounds__(256)
@@ -268,6 +360,23 @@ static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_
 }
 
 template <int V>
+static void launch_ln_bwd_fused(const float* x, const float* mean, const float* rstd,
+                                const float* gamma, const __nv_bfloat16* dy, const float* dres,
+                                int64_t rows, int cols, float* dx, __nv_bfloat16* dxb,
+                                float* part, cudaStream_t s) {
+  const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
+  const int smem = kLnWarps * 2 * cols * static_cast<int>(sizeof(float));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ln_bwd_fused_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kLnWarps * 2 * 2048 * 4);
+    attr = true;
+  }
+  ln_bwd_fused_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, smem, s>>>(
+      x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+}
+
+template <int V>
 static void launch_ln_bwd(const float* x, const float* mean, const float* rstd,
                           const float* gamma, const __nv_bfloat16* dy, const float* dres,
                           int64_t rows, int cols, float* dx, __nv_bfloat16* dxb, cudaStream_t s) {
@@ -320,11 +429,11 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
   if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* dyb = reinterpret_cast<const __nv_bfloat16*>(dy);
-  if (dgamma || dbeta) {  // column sums first: dx may overwrite x's partner buffers in place
+  if (dgamma || dbeta) {
     const int64_t nparts = rp_ln_bwd_num_parts(rows);
-    dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
-    ln_bwd_dgb_partial_kernel<<<grid, 256, 0, s>>>(x, mean, rstd, dyb, rows,
-                                                   static_cast<int>(cols), kLnBwdRows, workspace);
+    RP_LN_DISPATCH(launch_ln_bwd_fused, x, mean, rstd, gamma, dyb, dres, rows,
+                   static_cast<int>(cols), dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16),
+                   workspace, s);
     const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
       colsum_final_kernel<<<2 * gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(2 * cols),
@@ -337,9 +446,10 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
         colsum_final_kernel<<<gb, 256, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
                                                2 * cols, dbeta, accumulate);
     }
+  } else {
+    RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols),
+                   dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16), s);
   }
-  RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols), dx,
-                 reinterpret_cast<__nv_bfloat16*>(dx_bf16), s);
   return rp_check_launch("layer_norm_bwd");
 }
 
