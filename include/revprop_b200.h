@@ -59,7 +59,9 @@ enum {
   RP_EPI_F32 = 1,       /* out(f32)  = acc  (split-K allowed: workspace [S][M][N]) */
   RP_EPI_BIAS_GELU = 2, /* u = acc + bias; out(bf16) = gelu(u); out2(bf16) = u    */
   RP_EPI_RESID = 3,     /* out(f32) = aux(f32) + sign * (acc + bias)              */
-  RP_EPI_GELU_BWD = 4   /* out(bf16) = acc * gelu'(aux(bf16) u)                   */
+  RP_EPI_GELU_BWD = 4,  /* out(bf16) = acc * gelu'(aux(bf16) u)                   */
+  RP_EPI_BIAS_GELU_SLOPE = 5, /* u = acc + bias; out(bf16) = gelu(u); out2(bf16) = gelu'(u) */
+  RP_EPI_MUL = 6        /* out(bf16) = acc * aux(bf16)  (MLP dgrad with the saved slope) */
 };
 
 typedef struct RpGemmDesc {

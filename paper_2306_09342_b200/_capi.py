@@ -48,7 +48,8 @@ class DeviceError(Error):
 _CODE_TO_EXC = {1: ShapeError, 2: ContractError, 3: ConfigError, 4: BudgetError,
                 5: SchedulerError, 6: AccountingError, 7: DeviceError}
 
-RP_EPI_BF16, RP_EPI_F32, RP_EPI_BIAS_GELU, RP_EPI_RESID, RP_EPI_GELU_BWD = range(5)
+(RP_EPI_BF16, RP_EPI_F32, RP_EPI_BIAS_GELU, RP_EPI_RESID, RP_EPI_GELU_BWD,
+ RP_EPI_BIAS_GELU_SLOPE, RP_EPI_MUL) = range(7)
 
 
 class GemmDesc(C.Structure):

@@ -250,8 +250,8 @@ int build_plans(RpEngine* g) {
       RP_TRY(mk_plan(g, a, &p.f_w2));
     }
     // ---- lane R: inverse with caches
-    {
-      GemmArgs a{S.hG, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU, S.a, h};
+    {  // keeps gelu'(u) (not u) for the MLP dgrad: slot.u holds the slope
+      GemmArgs a{S.hG, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU_SLOPE, S.a, h};
       a.out2 = S.u;
       a.bias = b1;
       RP_TRY(mk_plan(g, a, &p.r_w1));
@@ -271,7 +271,7 @@ int build_plans(RpEngine* g) {
     }
     // ---- lane G: VJPs (layers.cpp:171-220, 241-259)
     {
-      GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_GELU_BWD, g->du, h};
+      GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_MUL, g->du, h};
       a.aux = S.u;
       RP_TRY(mk_plan(g, a, &p.g_dw2));  // d_u = gelu'(u) * (d_o1 . W2^T)
     }

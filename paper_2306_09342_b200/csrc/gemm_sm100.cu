@@ -126,7 +126,7 @@ struct ChunkIn {
 template <int EPI>
 __device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
                                                int64_t rows_left, int64_t col, ChunkIn& in) {
-  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_GELU_BWD) {
+  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_GELU_BWD || EPI == RP_EPI_MUL) {
     const int esz = EPI == RP_EPI_RESID ? 4 : 2;
     const uint8_t* g = static_cast<const uint8_t*>(ep.aux) + col * esz;
     const int64_t ldb = ep.ldaux * esz;
@@ -231,6 +231,44 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
     stage_rows_f32(st, lane, v);
     __syncwarp();
     store_tile(st, lane, static_cast<float*>(ep.out) + col, ep.ldo * 4, row0, rows_left);
+  } else if constexpr (EPI == RP_EPI_BIAS_GELU_SLOPE) {
+    if (ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float4 b = __ldg(b4 + i);
+        v[4 * i] += b.x;
+        v[4 * i + 1] += b.y;
+        v[4 * i + 2] += b.z;
+        v[4 * i + 3] += b.w;
+      }
+    }
+    float sl[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) gelu_and_slope_fast(v[i], v[i], sl[i]);
+    stage_row_bf16x64(st, lane, sl);
+    __syncwarp();
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0, rows_left);
+    __syncwarp();
+    stage_row_bf16x64(st, lane, v);
+    __syncwarp();
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
+  } else if constexpr (EPI == RP_EPI_MUL) {
+    uint4 uu[8];
+    aux_rows(st, lane, in, uu);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t w[4] = {uu[c].x, uu[c].y, uu[c].z, uu[c].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = unpack_bf16x2(w[k]);
+        v[8 * c + 2 * k] *= f.x;
+        v[8 * c + 2 * k + 1] *= f.y;
+      }
+    }
+    stage_row_bf16x64(st, lane, v);
+    __syncwarp();
+    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
   } else if constexpr (EPI == RP_EPI_GELU_BWD) {
     uint4 uu[8];
     aux_rows(st, lane, in, uu);
@@ -694,6 +732,8 @@ static GemmKernelPtr pick_epi(int epi) {
     case RP_EPI_BIAS_GELU: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_BIAS_GELU>();
     case RP_EPI_RESID: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_RESID>();
     case RP_EPI_GELU_BWD: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_GELU_BWD>();
+    case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
+    case RP_EPI_MUL: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_MUL>();
   }
   return nullptr;
 }
@@ -717,6 +757,8 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
     case RP_EPI_BIAS_GELU: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU>();
     case RP_EPI_RESID: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_RESID>();
     case RP_EPI_GELU_BWD: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_GELU_BWD>();
+    case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
+    case RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_MUL>();
   }
   return nullptr;
 }

@@ -322,30 +322,29 @@ __global__ void __launch_bounds__(256)
   *reinterpret_cast<float4*>(part + static_cast<int64_t>(blockIdx.x) * cols + c) = acc;
 }
 
-// Stage 2: out[c] (+)= sum_p part[p][c] in a fixed order. CTA = 8 warps x 32 columns;
-// warp w owns parts {w, w+8, ...} with 4 interleaved accumulators; combined in order.
-__global__ void __launch_bounds__(256)
+// Stage 2: out[c] (+)= sum_p part[p][c] in a fixed order. CTA = 32 warps x 32 columns;
+// warp w owns parts {w, w+32, ...} with 2 interleaved accumulators; combined in order.
+constexpr int kFinWarps = 32;
+__global__ void __launch_bounds__(kFinWarps * 32)
     colsum_final_kernel(const float* __restrict__ part, int64_t nparts, int cols, int64_t ld,
                         float* __restrict__ out, int accumulate) {
-  __shared__ float red[8][32];
+  __shared__ float red[kFinWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float a0 = 0.f, a1 = 0.f;
   if (c < cols) {
     int64_t p = warp;
-    for (; p + 24 < nparts; p += 32) {
+    for (; p + kFinWarps < nparts; p += 2 * kFinWarps) {
       a0 += part[p * ld + c];
-      a1 += part[(p + 8) * ld + c];
-      a2 += part[(p + 16) * ld + c];
-      a3 += part[(p + 24) * ld + c];
+      a1 += part[(p + kFinWarps) * ld + c];
     }
-    for (; p < nparts; p += 8) a0 += part[p * ld + c];
+    for (; p < nparts; p += kFinWarps) a0 += part[p * ld + c];
   }
-  red[warp][lane] = (a0 + a1) + (a2 + a3);
+  red[warp][lane] = a0 + a1;
   __syncthreads();
   if (warp == 0 && c < cols) {
     float s = red[0][lane];
-    for (int w = 1; w < 8; ++w) s += red[w][lane];
+    for (int w = 1; w < kFinWarps; ++w) s += red[w][lane];
     out[c] = accumulate ? out[c] + s : s;
   }
 }
@@ -436,14 +435,14 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
                    workspace, s);
     const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
-      colsum_final_kernel<<<2 * gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(2 * cols),
+      colsum_final_kernel<<<2 * gb, kFinWarps * 32, 0, s>>>(workspace, nparts, static_cast<int>(2 * cols),
                                                  2 * cols, dgamma, accumulate);
     } else {
       if (dgamma)
-        colsum_final_kernel<<<gb, 256, 0, s>>>(workspace, nparts, static_cast<int>(cols),
+        colsum_final_kernel<<<gb, kFinWarps * 32, 0, s>>>(workspace, nparts, static_cast<int>(cols),
                                                2 * cols, dgamma, accumulate);
       if (dbeta)
-        colsum_final_kernel<<<gb, 256, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
+        colsum_final_kernel<<<gb, kFinWarps * 32, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
                                                2 * cols, dbeta, accumulate);
     }
   } else {
@@ -477,7 +476,7 @@ extern "C" int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t c
     colsum_partial_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(in), rows,
                                                       static_cast<int>(cols), kColRpb,
                                                       workspace);
-  colsum_final_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(
+  colsum_final_kernel<<<static_cast<unsigned>((cols + 31) / 32), kFinWarps * 32, 0, s>>>(
       workspace, nparts, static_cast<int>(cols), cols, out, accumulate);
   return rp_check_launch("col_sum");
 }

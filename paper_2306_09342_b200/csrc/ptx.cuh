@@ -181,6 +181,16 @@ __device__ __forceinline__ float gelu_tanh_fast(float x) {
   const float t = tanh_fast(c * (x + a * x * x * x));
   return 0.5f * x * (1.0f + t);
 }
+// gelu(x) and gelu'(x) sharing one MUFU.TANH (the recompute epilogue keeps the slope
+// for the backward instead of the pre-activation).
+__device__ __forceinline__ void gelu_and_slope_fast(float x, float& g, float& s) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float x2 = x * x;
+  const float t = tanh_fast(c * x * fmaf(a, x2, 1.0f));
+  const float hx = 0.5f * x;
+  g = fmaf(hx, t, hx);
+  s = fmaf(hx * (c * fmaf(3.0f * a, x2, 1.0f)), fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
+}
 __device__ __forceinline__ float gelu_tanh_slope_fast(float x) {
   const float c = 0.7978845608028654f, a = 0.044715f;
   const float t = tanh_fast(c * (x + a * x * x * x));

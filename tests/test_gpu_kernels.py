@@ -122,6 +122,28 @@ def test_gemm_residual(K, sign, bn):
 
 
 @pytest.mark.parametrize("bn", [256, 512])
+def test_gemm_gelu_slope_then_mul(K, bn):
+    """Recompute epilogue keeps gelu'(u); the MLP dgrad multiplies by it."""
+    from paper_2306_09342_b200._capi import RP_EPI_BIAS_GELU_SLOPE, RP_EPI_MUL
+    M, N, Kd = 600, 1024, 256
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    W = (0.1 * torch.randn(Kd, N, device="cuda")).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    a = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    sl = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU_SLOPE, out=a, out2=sl, bias=bias,
+           bn=bn)
+    uref = A.float() @ W.float() + bias
+    assert rel(a, gelu_ref(uref)) < 1e-2
+    assert rel(sl, gelu_slope_ref(uref)) < 1e-2
+    dY = torch.randn(M, 512, device="cuda").bfloat16()
+    W2 = (0.05 * torch.randn(N, 512, device="cuda")).bfloat16()
+    du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(dY, W2, M, N, 512, a_mn=0, b_mn=0, epi=RP_EPI_MUL, out=du, aux=sl, bn=bn)
+    assert rel(du, (dY.float() @ W2.float().t()) * sl.float()) < 1e-2
+
+
+@pytest.mark.parametrize("bn", [256, 512])
 def test_gemm_gelu_bwd(K, bn):
     from paper_2306_09342_b200._capi import RP_EPI_GELU_BWD
     M, N, Kd = 640, 3072, 768
