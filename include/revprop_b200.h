@@ -42,6 +42,8 @@ enum {
 };
 
 const char* rp_last_error(void);
+/* Programmatic dependent launch between consecutive kernels: 1 (default) on, 0 off. */
+int rp_set_pdl(int on);
 /* Library build / device information: writes "sm_100a ..." into buf. */
 int rp_version(char* buf, int len);
 
@@ -164,6 +166,7 @@ int rp_engine_set_batch_device(RpEngine* engine, const uint16_t* inputs_bf16,
                                const int32_t* labels);
 int rp_engine_set_lr(RpEngine* engine, float lr);
 int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
+int rp_engine_invalidate_graphs(RpEngine* engine);
 int rp_engine_step(RpEngine* engine, int mode, int use_graph);
 int rp_engine_sync(RpEngine* engine);
 int rp_engine_read_loss(RpEngine* engine, float* loss);

@@ -74,6 +74,7 @@ _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double
 _SIGS = {
     "rp_last_error": (C.c_char_p, []),
     "rp_version": (_I, [C.c_char_p, _I]),
+    "rp_set_pdl": (_I, [_I]),
     "rp_gemm": (_I, [C.POINTER(GemmDesc), _P]),
     "rp_gemm_plan_create": (_I, [C.POINTER(GemmDesc), C.POINTER(_P)]),
     "rp_gemm_plan_launch": (_I, [_P, _P]),

@@ -1,0 +1,43 @@
+"""Same-process A/B of whole-step time: Reprop / PaReprop x PDL on / off (device-timed,
+CUDA graphs), so clock / power-cap drift between boxes does not enter the comparison.
+
+    python -m paper_2306_09342_b200.ab_step [--rounds 3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+
+from . import _capi
+from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from .sweep_partition import time_steps
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--preset", default="revvit-b")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--rounds", type=int, default=3)
+    a = ap.parse_args(argv)
+    p = dict(PRESETS[a.preset])
+    if a.batch:
+        p["batch"] = a.batch
+    eng = Engine(ModelConfig(**p))
+    eng.set_lr(1e-4)
+    res = {}
+    for r in range(a.rounds):
+        for pdl in (1, 0):
+            _capi.lib().rp_set_pdl(pdl)
+            eng.invalidate_graphs()
+            for mode, name in ((REPROP, "reprop"), (PAREPROP, "pareprop")):
+                ms = time_steps(eng, mode, a.steps)
+                res.setdefault(f"{name}_pdl{pdl}", []).append(ms)
+    _capi.lib().rp_set_pdl(1)
+    B = p["batch"]
+    out = {k: {"ms": min(v), "img_s": B * 1e3 / min(v)} for k, v in res.items()}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

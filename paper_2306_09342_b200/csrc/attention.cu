@@ -21,6 +21,7 @@
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.h"
 
 namespace rp {
 
@@ -142,6 +143,9 @@ struct AttnGeom {
 __global__ void __launch_bounds__(128)
     attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, AttnGeom g) {
+  pdl_trigger();
+  pdl_wait();
+
   extern __shared__ __align__(128) uint8_t sm[];
   const int npad = (g.N + kTile - 1) / kTile * kTile;
   uint8_t* sQ = sm;
@@ -231,6 +235,9 @@ __global__ void __launch_bounds__(128)
 __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out,
                                     const __nv_bfloat16* __restrict__ dout,
                                     float* __restrict__ D, AttnGeom g) {
+  pdl_trigger();
+  pdl_wait();
+
   const int64_t total = static_cast<int64_t>(g.B) * g.N * g.H;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -262,6 +269,9 @@ __global__ void __launch_bounds__(128)
                          const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                          const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv,
                          AttnGeom g) {
+  pdl_trigger();
+  pdl_wait();
+
   extern __shared__ __align__(128) uint8_t sm[];
   const int npad = (g.N + kTile - 1) / kTile * kTile;
   uint8_t* sK = sm;
@@ -348,6 +358,9 @@ __global__ void __launch_bounds__(128)
                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                        const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv,
                        AttnGeom g) {
+  pdl_trigger();
+  pdl_wait();
+
   extern __shared__ __align__(128) uint8_t sm[];
   const int npad = (g.N + kTile - 1) / kTile * kTile;
   uint8_t* sQ = sm;
@@ -475,9 +488,9 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
   if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem))) return rc;
   dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
             static_cast<unsigned>(B));
-  attn_fwd_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse,
-      g);
+  launch_k(attn_fwd_kernel, grid, dim3(128), smem, static_cast<cudaStream_t>(stream),
+           reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse,
+           g);
   return rp_check_launch("attention_fwd");
 }
 
@@ -497,7 +510,7 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   const int64_t total = B * N * H;
   int blocks = static_cast<int>((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  attn_bwd_dot_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(out),
+  launch_k(attn_bwd_dot_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(out),
                                              reinterpret_cast<const __nv_bfloat16*>(dout),
                                              workspace, g);
   if (g_attn_impl == 0 && N <= 256) {
@@ -512,10 +525,10 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dq_kernel), smem_q))) return rc;
   dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
             static_cast<unsigned>(B));
-  attn_bwd_dkdv_kernel<<<grid, 128, smem_kv, s>>>(
+  launch_k(attn_bwd_dkdv_kernel, dim3(grid), dim3(128), smem_kv, s, 
       reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
       lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
-  attn_bwd_dq_kernel<<<grid, 128, smem_q, s>>>(
+  launch_k(attn_bwd_dq_kernel, dim3(grid), dim3(128), smem_q, s, 
       reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
       lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
   return rp_check_launch("attention_bwd");

@@ -20,6 +20,7 @@
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.h"
 
 namespace rp {
 namespace attn_tc {
@@ -101,6 +102,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_kv, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse, Geom g) {
+  pdl_trigger();
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
   const int row_seq = b * g.N;  // first row of this sequence in qkv [T, 3d]
   const int d = g.H * 64;
 
@@ -299,6 +303,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                               const __grid_constant__ CUtensorMap tm_do128,
                               const float* __restrict__ lse, const float* __restrict__ Dg,
                               __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdItems it) {
+  pdl_trigger();
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -332,6 +338,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
   if (warp == 8) {
     if (lane == 0) {
       auto issue_load = [&](int item, int buf) {
@@ -453,6 +460,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                 const __grid_constant__ CUtensorMap tm_doNk,
                                 const float* __restrict__ lse, const float* __restrict__ Dg,
                                 __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdItems it) {
+  pdl_trigger();
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -488,6 +497,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
   if (warp == 8) {
     if (lane == 0) {
       auto issue_load = [&](int item, int buf) {
@@ -678,7 +688,7 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   });
   dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(H),
             static_cast<unsigned>(S));
-  attn_fwd_tc_kernel<<<grid, kThreads, smem, stream>>>(
+  launch_k(attn_fwd_tc_kernel, dim3(grid), dim3(kThreads), smem, stream, 
       mq, mkv, reinterpret_cast<__nv_bfloat16*>(out), lse, g);
   return rp_check_launch("attention_fwd_tc");
 }
@@ -723,9 +733,9 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* dout, const float* 
   items.ntile = static_cast<int>((N + 127) / 128);
   items.nitems = static_cast<int>(S * H) * items.ntile;
   const unsigned grid = static_cast<unsigned>(items.nitems < nsm ? items.nitems : nsm);
-  attn_bwd_dkdv_tc_persistent<<<grid, kBwdThreads, smem_kv, stream>>>(
+  launch_k(attn_bwd_dkdv_tc_persistent, dim3(grid), dim3(kBwdThreads), smem_kv, stream, 
       kv128, qNk, doNk, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g, items);
-  attn_bwd_dq_tc_persistent<<<grid, kBwdThreads, smem_dq, stream>>>(
+  launch_k(attn_bwd_dq_tc_persistent, dim3(grid), dim3(kBwdThreads), smem_dq, stream, 
       q128, kvNk, do128, lse, Dg, reinterpret_cast<__nv_bfloat16*>(dqkv), g, items);
   return rp_check_launch("attention_bwd_tc");
 }

@@ -743,6 +743,18 @@ extern "C" int rp_engine_set_lr(RpEngine* g, float lr) {
                  "set_lr");
 }
 
+// Drop captured graphs (e.g. after toggling rp_set_pdl); the next step recaptures.
+extern "C" int rp_engine_invalidate_graphs(RpEngine* g) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  RP_TRY(cuda_ok(cudaStreamSynchronize(g->sG), "sync"));
+  for (auto& x : g->graph)
+    if (x) {
+      cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
+  return RP_OK;
+}
+
 extern "C" int rp_engine_set_partition(RpEngine* g, int r_ctas, int g_ctas) {
   if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
   g->r_ctas = r_ctas;

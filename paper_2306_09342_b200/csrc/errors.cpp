@@ -24,6 +24,17 @@ int rp_check_launch(const char* what) {
 
 extern "C" const char* rp_last_error(void) { return g_last_error.c_str(); }
 
+namespace rp {
+static bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+}  // namespace rp
+
+// Programmatic dependent launch on (1, default) or off (0) for all kernels of the library.
+extern "C" int rp_set_pdl(int on) {
+  rp::g_pdl = on != 0;
+  return RP_OK;
+}
+
 extern "C" int rp_version(char* buf, int len) {
   const char* v = "revprop_b200 0.1 (sm_100a: tcgen05/TMEM/TMA GEMM, fused LN, attention)";
   if (buf && len > 0) {

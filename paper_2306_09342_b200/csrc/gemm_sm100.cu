@@ -23,6 +23,7 @@
 #include "gemm.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.h"
 
 namespace rp {
 
@@ -294,6 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const GemmShape sh,
                       const GemmEpi ep) {
+  pdl_trigger();
+
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   const int tiles = sh.m_tiles * sh.n_tiles;
   const int units = tiles * sh.splits;
@@ -483,6 +487,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_sm100_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmB, const GemmShape sh,
                           const GemmEpi ep) {
+  pdl_trigger();
+
   using Cfg = Gemm2Cfg<EPI>;
   constexpr int S = Cfg::kStages;
   constexpr int BN = 256;
@@ -522,6 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   const int tiles = sh.m_tiles * sh.n_tiles;  // m_tiles counts 256-row pair tiles
   const int units = tiles * sh.splits;
@@ -661,6 +668,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // Deterministic split-K reduction: out[i] = sum_{s=0..S-1} part[s][i], fixed order.
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
                                      int64_t stride, int64_t n4, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float4 acc = reinterpret_cast<const float4*>(part)[i];
@@ -890,13 +900,13 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
 extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!p) return RP_ERR_CONTRACT;
-  p->kern<<<p->grid, kThreads, p->smem, stream>>>(p->tmA, p->tmB, p->sh, p->ep);
+  launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->sh, p->ep);
   if (cudaPeekAtLastError() != cudaSuccess) return rp_check_launch("gemm");
   if (p->sh.splits > 1) {
     const int64_t n4 = p->red_n / 4;
     int blocks = static_cast<int>((n4 + 255) / 256);
     if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float*>(p->ep.out),
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, static_cast<const float*>(p->ep.out),
                                                      p->sh.splits, p->ep.split_stride, n4,
                                                      p->red_out);
   }

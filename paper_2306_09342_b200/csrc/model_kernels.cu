@@ -7,6 +7,7 @@
 #include "kernels.h"
 #include "model_kernels.h"
 #include "ptx.cuh"
+#include "launch.h"
 
 namespace rp {
 
@@ -38,6 +39,9 @@ __device__ __forceinline__ double rng_normal(uint64_t seed, uint64_t stream, uin
 // (trunc normal at +-2 sigma, rng.hpp:45-50); kinds: 0 trunc-normal, 1 zeros, 2 ones.
 __global__ void init_tensor_kernel(float* __restrict__ p, int64_t n, uint64_t seed,
                                    uint64_t tensor_idx, int kind, double sigma) {
+  pdl_trigger();
+  pdl_wait();
+
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float v;
@@ -60,6 +64,9 @@ __global__ void init_tensor_kernel(float* __restrict__ p, int64_t n, uint64_t se
 
 // Synthetic input element e: Rng(seed, (2<<56)|e).next_normal(), stored as bf16.
 __global__ void init_inputs_kernel(__nv_bfloat16* __restrict__ x, int64_t n, uint64_t seed) {
+  pdl_trigger();
+  pdl_wait();
+
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t stream = (2ull << 56) | static_cast<uint64_t>(e);
@@ -69,6 +76,9 @@ __global__ void init_inputs_kernel(__nv_bfloat16* __restrict__ x, int64_t n, uin
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
                                    int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = __float2bfloat16_rn(in[i]);
@@ -79,6 +89,9 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
                            __nv_bfloat16* __restrict__ pb, int64_t n,
                            const float* __restrict__ lr, float scale) {
+  pdl_trigger();
+  pdl_wait();
+
   const float step = lr[0] * scale;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -92,6 +105,9 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
 // pooled[b][c] = (sum_n (o1 + o2) * 0.5) * (1/N), summed in token order.
 __global__ void pool_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
                             int64_t B, int64_t N, int64_t d, float* __restrict__ pooled) {
+  pdl_trigger();
+  pdl_wait();
+
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= B * d) return;
   const int64_t b = i / d, c = i % d;
@@ -106,6 +122,9 @@ __global__ void pool_kernel(const float* __restrict__ o1, const float* __restric
 __global__ void simt_gemm_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A,
                                  int64_t sam, int64_t sak, const float* __restrict__ Bm,
                                  int64_t sbk, int64_t sbn, float* __restrict__ Cm, int64_t ldc) {
+  pdl_trigger();
+  pdl_wait();
+
   __shared__ float as[16][17], bs[16][17];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t m = blockIdx.y * 16 + ty, n = blockIdx.x * 16 + tx;
@@ -127,6 +146,9 @@ __global__ void simt_gemm_kernel(int64_t M, int64_t N, int64_t K, const float* _
 __global__ void ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels,
                           int64_t B, int64_t C, float* __restrict__ d_logits,
                           float* __restrict__ row_loss) {
+  pdl_trigger();
+  pdl_wait();
+
   const int64_t b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -152,6 +174,9 @@ __global__ void ce_kernel(const float* __restrict__ logits, const int32_t* __res
 // loss = (1/B) sum_b row_loss[b], fixed order, optionally * 1/world for DP averaging
 __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int64_t B,
                                    float* __restrict__ loss) {
+  pdl_trigger();
+  pdl_wait();
+
   __shared__ float red[256];
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < B; i += blockDim.x) s += row_loss[i];
@@ -169,6 +194,9 @@ __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int64_t B
 __global__ void spread_kernel(const float* __restrict__ d_pooled, int64_t B, int64_t N,
                               int64_t d, float* __restrict__ d1, float* __restrict__ d2,
                               __nv_bfloat16* __restrict__ d1b, __nv_bfloat16* __restrict__ d2b) {
+  pdl_trigger();
+  pdl_wait();
+
   const int64_t total = B * N * d;
   const float invN = 1.0f / static_cast<float>(N);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -186,6 +214,9 @@ __global__ void spread_kernel(const float* __restrict__ d_pooled, int64_t B, int
 // out = bf16(a + b)  (embedding cotangent: e feeds both halves of the coupled pair)
 __global__ void add_to_bf16_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                    __nv_bfloat16* __restrict__ out, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = __float2bfloat16_rn(a[i] + b[i]);
@@ -208,50 +239,50 @@ uint64_t rp_rng_u64_host(uint64_t seed, uint64_t stream, uint64_t counter) {
 
 int rpk_init_tensor(float* p, int64_t n, uint64_t seed, uint64_t tensor_idx, int kind,
                     double sigma, cudaStream_t s) {
-  init_tensor_kernel<<<grid_for(n), 256, 0, s>>>(p, n, seed, tensor_idx, kind, sigma);
+  launch_k(init_tensor_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, n, seed, tensor_idx, kind, sigma);
   return rp_check_launch("init_tensor");
 }
 int rpk_init_inputs(uint16_t* x, int64_t n, uint64_t seed, cudaStream_t s) {
-  init_inputs_kernel<<<grid_for(n), 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(x), n, seed);
+  launch_k(init_inputs_kernel, dim3(grid_for(n)), dim3(256), 0, s, reinterpret_cast<__nv_bfloat16*>(x), n, seed);
   return rp_check_launch("init_inputs");
 }
 int rpk_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t s) {
-  f32_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(in, reinterpret_cast<__nv_bfloat16*>(out), n);
+  launch_k(f32_to_bf16_kernel, dim3(grid_for(n)), dim3(256), 0, s, in, reinterpret_cast<__nv_bfloat16*>(out), n);
   return rp_check_launch("f32_to_bf16");
 }
 int rpk_sgd(float* p, const float* g, uint16_t* pb, int64_t n, const float* lr, float scale,
             cudaStream_t s) {
-  sgd_kernel<<<grid_for(n), 256, 0, s>>>(p, g, reinterpret_cast<__nv_bfloat16*>(pb), n, lr,
+  launch_k(sgd_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, g, reinterpret_cast<__nv_bfloat16*>(pb), n, lr,
                                          scale);
   return rp_check_launch("sgd");
 }
 int rpk_pool(const float* o1, const float* o2, int64_t B, int64_t N, int64_t d, float* pooled,
              cudaStream_t s) {
-  pool_kernel<<<static_cast<unsigned>((B * d + 255) / 256), 256, 0, s>>>(o1, o2, B, N, d, pooled);
+  launch_k(pool_kernel, dim3(static_cast<unsigned>((B * d + 255) / 256)), dim3(256), 0, s, o1, o2, B, N, d, pooled);
   return rp_check_launch("pool");
 }
 int rpk_simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t sam, int64_t sak,
                   const float* B, int64_t sbk, int64_t sbn, float* C, int64_t ldc,
                   cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((N + 15) / 16), static_cast<unsigned>((M + 15) / 16));
-  simt_gemm_kernel<<<grid, dim3(16, 16), 0, s>>>(M, N, K, A, sam, sak, B, sbk, sbn, C, ldc);
+  launch_k(simt_gemm_kernel, dim3(grid), dim3(16, 16), 0, s, M, N, K, A, sam, sak, B, sbk, sbn, C, ldc);
   return rp_check_launch("simt_gemm");
 }
 int rpk_cross_entropy(const float* logits, const int32_t* labels, int64_t B, int64_t C,
                       float* d_logits, float* row_loss, float* loss, cudaStream_t s) {
-  ce_kernel<<<static_cast<unsigned>((B + 7) / 8), 256, 0, s>>>(logits, labels, B, C, d_logits,
+  launch_k(ce_kernel, dim3(static_cast<unsigned>((B + 7) / 8)), dim3(256), 0, s, logits, labels, B, C, d_logits,
                                                               row_loss);
-  loss_reduce_kernel<<<1, 256, 0, s>>>(row_loss, B, loss);
+  launch_k(loss_reduce_kernel, dim3(1), dim3(256), 0, s, row_loss, B, loss);
   return rp_check_launch("cross_entropy");
 }
 int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1, float* d2,
                uint16_t* d1b, uint16_t* d2b, cudaStream_t s) {
-  spread_kernel<<<grid_for(B * N * d), 256, 0, s>>>(d_pooled, B, N, d, d1, d2,
+  launch_k(spread_kernel, dim3(grid_for(B * N * d)), dim3(256), 0, s, d_pooled, B, N, d, d1, d2,
                                                     reinterpret_cast<__nv_bfloat16*>(d1b),
                                                     reinterpret_cast<__nv_bfloat16*>(d2b));
   return rp_check_launch("spread");
 }
 int rpk_add_to_bf16(const float* a, const float* b, uint16_t* out, int64_t n, cudaStream_t s) {
-  add_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(a, b, reinterpret_cast<__nv_bfloat16*>(out), n);
+  launch_k(add_to_bf16_kernel, dim3(grid_for(n)), dim3(256), 0, s, a, b, reinterpret_cast<__nv_bfloat16*>(out), n);
   return rp_check_launch("add_to_bf16");
 }

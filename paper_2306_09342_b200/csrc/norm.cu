@@ -14,6 +14,7 @@
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.h"
 
 namespace rp {
 
@@ -33,6 +34,9 @@ __global__ void __launch_bounds__(kLnWarps * 32)
                   const float* __restrict__ beta, int64_t rows, int cols, float eps,
                   __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                   float* __restrict__ rstd_out) {
+  pdl_trigger();
+  pdl_wait();
+
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * kLnWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -87,6 +91,9 @@ __global__ void __launch_bounds__(kLnWarps * 32)
                      const float* __restrict__ rstd_in, const float* __restrict__ gamma,
                      const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
                      int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16) {
+  pdl_trigger();
+  pdl_wait();
+
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * kLnWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -154,17 +161,19 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2)
                         const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
                         int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16,
                         float* __restrict__ part) {
-  extern __shared__ float acc[];  // [kLnWarps][2][cols]
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float acc[];  // [2][cols]: the CTA's running dgamma | dbeta partial
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c4 = cols >> 2;
-  float4* ag = reinterpret_cast<float4*>(acc + warp * 2 * cols);
-  float4* ab = reinterpret_cast<float4*>(acc + warp * 2 * cols + cols);
-  for (int c = lane; c < c4; c += 32) {
-    ag[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    ab[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
   const float inv_n = 1.0f / static_cast<float>(cols);
+  float4 ag[V], ab[V];  // this lane's column sums over the warp's rows (row order)
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    ag[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ab[i] = ag[i];
+  }
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
   for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
     const int64_t row = r0 + rr;
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2)
     const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
     const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
     const float mean = mean_in[row], rstd = rstd_in[row];
-    // pass 1: row sums (loads stay in L1 for pass 2)
+    // pass 1: row sums (x and dy stay in L1 for pass 2)
     float sg = 0.f, sgh = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
@@ -212,26 +221,43 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2)
         o.w = (d23.y * gm.w - gmn - hw * ghm) * rstd + rv.w;
         dxr[c] = o;
         if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
-        float4 a = ag[c], bb = ab[c];
-        a.x += d01.x * hx;
-        a.y += d01.y * hy;
-        a.z += d23.x * hz;
-        a.w += d23.y * hw;
-        bb.x += d01.x;
-        bb.y += d01.y;
-        bb.z += d23.x;
-        bb.w += d23.y;
-        ag[c] = a;
-        ab[c] = bb;
+        ag[i].x += d01.x * hx;
+        ag[i].y += d01.y * hy;
+        ag[i].z += d23.x * hz;
+        ag[i].w += d23.y * hw;
+        ab[i].x += d01.x;
+        ab[i].y += d01.y;
+        ab[i].z += d23.x;
+        ab[i].w += d23.y;
       }
     }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
-    float t = acc[c];
-    for (int w = 1; w < kLnWarps; ++w) t += acc[w * 2 * cols + c];
-    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = t;
+  // combine the 8 warps in warp order through one [2][cols] buffer
+  for (int w = 0; w < kLnWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const int c = lane + 32 * i;
+        if (c < c4) {
+          float4* pg = reinterpret_cast<float4*>(acc) + c;
+          float4* pb = reinterpret_cast<float4*>(acc + cols) + c;
+          if (w == 0) {
+            *pg = ag[i];
+            *pb = ab[i];
+          } else {
+            float4 tg = *pg, tb = *pb;
+            tg.x += ag[i].x; tg.y += ag[i].y; tg.z += ag[i].z; tg.w += ag[i].w;
+            tb.x += ab[i].x; tb.y += ab[i].y; tb.z += ab[i].z; tb.w += ab[i].w;
+            *pg = tg;
+            *pb = tb;
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
+  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x)
+    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = acc[c];
 }
 
 // Backward, column part (stage 1): CTA (rb, cb) sums dgamma = dy*x_hat and dbeta = dy
@@ -241,6 +267,9 @@ __global__ void __launch_bounds__(256)
                               const float* __restrict__ rstd_in,
                               const __nv_bfloat16* __restrict__ dy, int64_t rows, int cols,
                               int rpb, float* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
+
   const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
   if (c >= cols) return;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
@@ -298,6 +327,9 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     colsum_partial_kernel(const T* __restrict__ in, int64_t rows, int cols, int rpb,
                           float* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
+
   const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
   if (c >= cols) return;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
@@ -328,6 +360,9 @@ constexpr int kFinWarps = 32;
 __global__ void __launch_bounds__(kFinWarps * 32)
     colsum_final_kernel(const float* __restrict__ part, int64_t nparts, int cols, int64_t ld,
                         float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
+
   __shared__ float red[kFinWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -354,7 +389,7 @@ static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_
                           int cols, float eps, __nv_bfloat16* y, float* mean, float* rstd,
                           cudaStream_t s) {
   const int64_t blocks = (rows + kLnWarps - 1) / kLnWarps;
-  ln_fwd_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, 0, s>>>(x, g, b, rows, cols,
+  launch_k(ln_fwd_kernel<V>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32), 0, s, x, g, b, rows, cols,
                                                                            eps, y, mean, rstd);
 }
 
@@ -364,14 +399,8 @@ static void launch_ln_bwd_fused(const float* x, const float* mean, const float* 
                                 int64_t rows, int cols, float* dx, __nv_bfloat16* dxb,
                                 float* part, cudaStream_t s) {
   const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
-  const int smem = kLnWarps * 2 * cols * static_cast<int>(sizeof(float));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ln_bwd_fused_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kLnWarps * 2 * 2048 * 4);
-    attr = true;
-  }
-  ln_bwd_fused_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, smem, s>>>(
+  const int smem = 2 * cols * static_cast<int>(sizeof(float));
+  launch_k(ln_bwd_fused_kernel<V>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32), smem, s, 
       x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
 }
 
@@ -380,7 +409,7 @@ static void launch_ln_bwd(const float* x, const float* mean, const float* rstd,
                           const float* gamma, const __nv_bfloat16* dy, const float* dres,
                           int64_t rows, int cols, float* dx, __nv_bfloat16* dxb, cudaStream_t s) {
   const int64_t blocks = (rows + kLnWarps - 1) / kLnWarps;
-  ln_bwd_dx_kernel<V><<<static_cast<unsigned>(blocks), kLnWarps * 32, 0, s>>>(
+  launch_k(ln_bwd_dx_kernel<V>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32), 0, s, 
       x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb);
 }
 
@@ -435,14 +464,14 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
                    workspace, s);
     const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
-      colsum_final_kernel<<<2 * gb, kFinWarps * 32, 0, s>>>(workspace, nparts, static_cast<int>(2 * cols),
+      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts, static_cast<int>(2 * cols),
                                                  2 * cols, dgamma, accumulate);
     } else {
       if (dgamma)
-        colsum_final_kernel<<<gb, kFinWarps * 32, 0, s>>>(workspace, nparts, static_cast<int>(cols),
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts, static_cast<int>(cols),
                                                2 * cols, dgamma, accumulate);
       if (dbeta)
-        colsum_final_kernel<<<gb, kFinWarps * 32, 0, s>>>(workspace + cols, nparts, static_cast<int>(cols),
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols, nparts, static_cast<int>(cols),
                                                2 * cols, dbeta, accumulate);
     }
   } else {
@@ -470,13 +499,13 @@ extern "C" int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t c
   const int64_t nparts = (rows + kColRpb - 1) / kColRpb;
   dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
   if (in_is_bf16)
-    colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+    launch_k(colsum_partial_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, 
         static_cast<const __nv_bfloat16*>(in), rows, static_cast<int>(cols), kColRpb, workspace);
   else
-    colsum_partial_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(in), rows,
+    launch_k(colsum_partial_kernel<float>, dim3(grid), dim3(256), 0, s, static_cast<const float*>(in), rows,
                                                       static_cast<int>(cols), kColRpb,
                                                       workspace);
-  colsum_final_kernel<<<static_cast<unsigned>((cols + 31) / 32), kFinWarps * 32, 0, s>>>(
+  launch_k(colsum_final_kernel, dim3(static_cast<unsigned>((cols + 31) / 32)), dim3(kFinWarps * 32), 0, s, 
       workspace, nparts, static_cast<int>(cols), cols, out, accumulate);
   return rp_check_launch("col_sum");
 }

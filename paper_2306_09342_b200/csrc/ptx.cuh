@@ -279,3 +279,16 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar, uint16_t mask)
       : "memory");
 }
 }  // namespace rp
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the step calls pdl_trigger() on entry (the next kernel in the stream may
+// be scheduled once all CTAs of this grid have started) and pdl_wait() after its
+// data-independent prologue (barrier init, TMEM alloc, descriptor prefetch) and before it
+// touches global memory written by its predecessor. pdl_wait() is a no-op for a kernel
+// that was not launched with the programmatic-serialization attribute.
+namespace rp {
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+}  // namespace rp

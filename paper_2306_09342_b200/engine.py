@@ -74,6 +74,7 @@ _API = {
     "rp_engine_set_batch_device": (_I, [_P, _P, _P]),
     "rp_engine_set_lr": (_I, [_P, C.c_float]),
     "rp_engine_set_partition": (_I, [_P, _I, _I]),
+    "rp_engine_invalidate_graphs": (_I, [_P]),
     "rp_engine_step": (_I, [_P, _I, _I]),
     "rp_engine_sync": (_I, [_P]),
     "rp_engine_read_loss": (_I, [_P, C.POINTER(C.c_float)]),
@@ -192,6 +193,9 @@ class Engine:
 
     def set_partition(self, r_ctas: int, g_ctas: int):
         check(api("rp_engine_set_partition")(self._h, r_ctas, g_ctas), "set_partition")
+
+    def invalidate_graphs(self):
+        check(api("rp_engine_invalidate_graphs")(self._h), "invalidate_graphs")
 
     def step(self, mode=REPROP, graph=True):
         check(api("rp_engine_step")(self._h, mode, int(graph)), "step")
