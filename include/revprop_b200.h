@@ -42,7 +42,7 @@ enum {
 };
 
 const char* rp_last_error(void);
-/* Programmatic dependent launch between consecutive kernels: 1 (default) on, 0 off. */
+/* Programmatic dependent launch between consecutive kernels: 1 on, 0 (default) off. */
 int rp_set_pdl(int on);
 /* Library build / device information: writes "sm_100a ..." into buf. */
 int rp_version(char* buf, int len);

@@ -73,6 +73,42 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, float* a, 
   }
 }
 
+// four 16-column TMEM loads behind one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld16x4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                            float* a, float* b, float* c, float* d) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%64];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%65];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%66];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%67];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
+        "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+        "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
+        "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
+        "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(t0), "r"(t1), "r"(t2), "r"(t3)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    a[i] = __uint_as_float(r[i]);
+    b[i] = __uint_as_float(r[16 + i]);
+    c[i] = __uint_as_float(r[32 + i]);
+    d[i] = __uint_as_float(r[48 + i]);
+  }
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -182,9 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     const int valid = g.N;  // keys >= N are masked
     float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    for (int c = c0; c < c0 + half; c += 16) {
-      float v[16];
-      tmem_ld16(lane_base + c, v);
+    auto max_chunk = [&](int c, const float* v) {
       if (c + 16 <= valid) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
@@ -193,15 +227,30 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int i = 0; i < 16; ++i)
           if (c + i < valid) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
       }
+    };
+    {
+      int c = c0;
+      for (; c + 64 <= c0 + half; c += 64) {
+        float v0[16], v1[16], v2[16], v3[16];
+        tmem_ld16x4(lane_base + c, lane_base + c + 16, lane_base + c + 32, lane_base + c + 48, v0,
+                    v1, v2, v3);
+        max_chunk(c, v0);
+        max_chunk(c + 16, v1);
+        max_chunk(c + 32, v2);
+        max_chunk(c + 48, v3);
+      }
+      for (; c < c0 + half; c += 16) {
+        float v[16];
+        tmem_ld16(lane_base + c, v);
+        max_chunk(c, v);
+      }
     }
     red[kh * 128 + rloc] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     named_bar(1, 256);
     const float m = fmaxf(red[rloc], red[128 + rloc]);
     const float ms = m * g.scale_log2;
     float l4[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int c = c0; c < c0 + half; c += 16) {
-      float v[16];
-      tmem_ld16(lane_base + c, v);
+    auto p_chunk = [&](int c, const float* v) {
       uint32_t pk[8];
       if (c + 16 <= valid) {
 #pragma unroll
@@ -222,6 +271,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       // P columns [c0 + (c - c0)/2, +8) lie inside this warp's own, already-read S columns
       tmem_st8(lane_base + c0 + (c - c0) / 2, pk);
+    };
+    {
+      int c = c0;
+      for (; c + 32 <= c0 + half; c += 32) {
+        float v0[16], v1[16];
+        tmem_ld16x2(lane_base + c, lane_base + c + 16, v0, v1);
+        p_chunk(c, v0);
+        p_chunk(c + 16, v1);
+      }
+      for (; c < c0 + half; c += 16) {
+        float v[16];
+        tmem_ld16(lane_base + c, v);
+        p_chunk(c, v);
+      }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc_fence_before();
@@ -401,9 +464,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       const int valid = g.N;
       const float nds = -dr * g.scale;  // dS = P * (dP*scale - D*scale)
-      for (int c = c0; c < c0 + half; c += 16) {
-        float s[16], dp[16];
-        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s, dp);
+      auto ds_chunk = [&](int c, const float* s, const float* dp) {
         uint32_t pk[8];
         if (c + 16 <= valid) {
 #pragma unroll
@@ -424,6 +485,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         tmem_st8(lane_base + packed_col(c, c0), pk);
+      };
+      int c = c0;
+      for (; c + 32 <= c0 + half; c += 32) {
+        float s0[16], d0[16], s1[16], d1[16];
+        tmem_ld16x4(lane_base + c, lane_base + 256 + c, lane_base + c + 16,
+                    lane_base + 256 + c + 16, s0, d0, s1, d1);
+        ds_chunk(c, s0, d0);
+        ds_chunk(c + 16, s1, d1);
+      }
+      for (; c < c0 + half; c += 16) {
+        float s0[16], d0[16];
+        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s0, d0);
+        ds_chunk(c, s0, d0);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -567,9 +641,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int key = tile * 128 + qd * 32 + static_cast<int>(lane);
       mbar_wait(bar_s, k & 1);
       tc_fence_after();
-      for (int c = c0; c < c0 + half; c += 16) {
-        float s[16], dp[16];
-        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s, dp);
+      auto pds_chunk = [&](int c, const float* s, const float* dp) {
         uint32_t pp[8], pd[8];
         const float4* l4 = reinterpret_cast<const float4*>(sL + c);
         const float4* d4 = reinterpret_cast<const float4*>(sD + c);
@@ -589,6 +661,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         tmem_st8(lane_base + packed_col(c, c0), pp);
         tmem_st8(lane_base + 256 + packed_col(c, c0), pd);
+      };
+      int c = c0;
+      for (; c + 32 <= c0 + half; c += 32) {
+        float s0[16], d0[16], s1[16], d1[16];
+        tmem_ld16x4(lane_base + c, lane_base + 256 + c, lane_base + c + 16,
+                    lane_base + 256 + c + 16, s0, d0, s1, d1);
+        pds_chunk(c, s0, d0);
+        pds_chunk(c + 16, s1, d1);
+      }
+      for (; c < c0 + half; c += 16) {
+        float s0[16], d0[16];
+        tmem_ld16x2(lane_base + c, lane_base + 256 + c, s0, d0);
+        pds_chunk(c, s0, d0);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();

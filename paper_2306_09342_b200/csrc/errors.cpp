@@ -25,7 +25,7 @@ int rp_check_launch(const char* what) {
 extern "C" const char* rp_last_error(void) { return g_last_error.c_str(); }
 
 namespace rp {
-static bool g_pdl = true;
+static bool g_pdl = false;  // measured: no gain for this step (see profiles/)
 bool pdl_enabled() { return g_pdl; }
 }  // namespace rp
 

@@ -457,27 +457,26 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
   if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* dyb = reinterpret_cast<const __nv_bfloat16*>(dy);
-  if (dgamma || dbeta) {
+  if (dgamma || dbeta) {  // column partials first (reads x, dy before dx may alias dres)
     const int64_t nparts = rp_ln_bwd_num_parts(rows);
-    RP_LN_DISPATCH(launch_ln_bwd_fused, x, mean, rstd, gamma, dyb, dres, rows,
-                   static_cast<int>(cols), dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16),
-                   workspace, s);
+    dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
+    launch_k(ln_bwd_dgb_partial_kernel, grid, dim3(256), 0, s, x, mean, rstd, dyb, rows,
+             static_cast<int>(cols), kLnBwdRows, workspace);
     const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
-      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts, static_cast<int>(2 * cols),
-                                                 2 * cols, dgamma, accumulate);
+      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
+               static_cast<int>(2 * cols), 2 * cols, dgamma, accumulate);
     } else {
       if (dgamma)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts, static_cast<int>(cols),
-                                               2 * cols, dgamma, accumulate);
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
+                 static_cast<int>(cols), 2 * cols, dgamma, accumulate);
       if (dbeta)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols, nparts, static_cast<int>(cols),
-                                               2 * cols, dbeta, accumulate);
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols,
+                 nparts, static_cast<int>(cols), 2 * cols, dbeta, accumulate);
     }
-  } else {
-    RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols),
-                   dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16), s);
   }
+  RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols), dx,
+                 reinterpret_cast<__nv_bfloat16*>(dx_bf16), s);
   return rp_check_launch("layer_norm_bwd");
 }
 
