@@ -147,6 +147,7 @@ typedef struct RpModelConfig {
   int device;
   int r_ctas; /* PaReprop: max CTAs per recompute-lane GEMM (0 = all SMs) */
   int g_ctas; /* PaReprop: max CTAs per gradient-lane GEMM (0 = all SMs) */
+  int lane_priority; /* 1: gradient lane high / recompute lane low stream priority */
 } RpModelConfig;
 
 typedef struct RpEngine RpEngine;

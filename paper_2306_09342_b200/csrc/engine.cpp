@@ -569,9 +569,21 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   g->P = g->t_off.back() + g->t_numel.back();
   g->block_size = 4 * d * d + 2 * d * h + h + 5 * d;
   int rc = RP_OK;
-  if ((rc = cuda_ok(cudaStreamCreateWithFlags(&g->sG, cudaStreamNonBlocking), "stream")) ||
-      (rc = cuda_ok(cudaStreamCreateWithFlags(&g->sR, cudaStreamNonBlocking), "stream")) ||
-      (rc = cuda_ok(cudaStreamCreateWithFlags(&g->sC, cudaStreamNonBlocking), "stream")))
+  // Lane G (the critical path) gets the highest stream priority, lane R and the comm /
+  // SGD stream the lowest: the block scheduler then fills idle SMs and kernel tails with
+  // recompute work instead of letting it compete with the gradient lane.
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  const bool use_prio = c->lane_priority != 0;
+  if ((rc = cuda_ok(cudaStreamCreateWithPriority(&g->sG, cudaStreamNonBlocking,
+                                                 use_prio ? prio_hi : 0),
+                    "stream")) ||
+      (rc = cuda_ok(cudaStreamCreateWithPriority(&g->sR, cudaStreamNonBlocking,
+                                                 use_prio ? prio_lo : 0),
+                    "stream")) ||
+      (rc = cuda_ok(cudaStreamCreateWithPriority(&g->sC, cudaStreamNonBlocking,
+                                                 use_prio ? prio_lo : 0),
+                    "stream")))
     return fail(rc);
   g->evR.resize(static_cast<size_t>(g->L));
   g->evG.resize(static_cast<size_t>(g->L));

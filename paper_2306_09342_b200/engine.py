@@ -22,7 +22,7 @@ class ModelConfigC(C.Structure):
                 ("hidden", C.c_int64), ("seq_len", C.c_int64), ("in_dim", C.c_int64),
                 ("num_classes", C.c_int64), ("batch", C.c_int64), ("window", C.c_int64),
                 ("seed", C.c_uint64), ("device", C.c_int), ("r_ctas", C.c_int),
-                ("g_ctas", C.c_int)]
+                ("g_ctas", C.c_int), ("lane_priority", C.c_int)]
 
 
 @dataclass
@@ -41,6 +41,7 @@ class ModelConfig:
     device: int = 0
     r_ctas: int = 0
     g_ctas: int = 0
+    lane_priority: int = 1
 
 
 PRESETS = {
@@ -125,7 +126,7 @@ class Engine:
         self.cfg = cfg
         c = ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
                          cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
-                         cfg.g_ctas)
+                         cfg.g_ctas, cfg.lane_priority)
         h = C.c_void_p()
         check(api("rp_engine_create")(C.byref(c), C.byref(h)), "engine_create")
         self._h = h

@@ -17,17 +17,20 @@ def main(argv=None):
     ap.add_argument("--preset", default="revvit-b")
     ap.add_argument("--batches", default="8,16,32,64,128,256")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--priorities", default="1,0")
     a = ap.parse_args(argv)
     for B in [int(x) for x in a.batches.split(",")]:
-        p = dict(PRESETS[a.preset], batch=B)
-        eng = Engine(ModelConfig(**p))
-        eng.set_lr(1e-4)
-        r = time_steps(eng, REPROP, a.steps)
-        q = time_steps(eng, PAREPROP, a.steps)
-        print(json.dumps({"batch": B, "reprop_ms": r, "pareprop_ms": q,
-                          "reprop_img_s": B * 1e3 / r, "pareprop_img_s": B * 1e3 / q,
-                          "gain_pct": 100 * (r / q - 1)}), flush=True)
-        eng.close()
+        for prio in [int(x) for x in a.priorities.split(",")]:
+            p = dict(PRESETS[a.preset], batch=B)
+            eng = Engine(ModelConfig(lane_priority=prio, **p))
+            eng.set_lr(1e-4)
+            r = time_steps(eng, REPROP, a.steps)
+            q = time_steps(eng, PAREPROP, a.steps)
+            print(json.dumps({"batch": B, "lane_priority": prio, "reprop_ms": r,
+                              "pareprop_ms": q, "reprop_img_s": B * 1e3 / r,
+                              "pareprop_img_s": B * 1e3 / q,
+                              "gain_pct": 100 * (r / q - 1)}), flush=True)
+            eng.close()
 
 
 if __name__ == "__main__":
