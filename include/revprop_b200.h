@@ -148,7 +148,14 @@ typedef struct RpModelConfig {
   int r_ctas; /* PaReprop: max CTAs per recompute-lane GEMM (0 = all SMs) */
   int g_ctas; /* PaReprop: max CTAs per gradient-lane GEMM (0 = all SMs) */
   int lane_priority; /* 1: gradient lane high / recompute lane low stream priority */
+  int optimizer;     /* 0: SGD, 1: AdamW */
+  float beta1, beta2, adam_eps, weight_decay;
 } RpModelConfig;
+
+/* Ledger-predicted peak activation bytes of an engine (mode 0 vanilla, 1 reprop,
+ * 2 pareprop) and the per-block footprint, from the config alone (no device needed). */
+int rp_activation_bytes(const RpModelConfig* cfg, int mode, int64_t* peak_bytes,
+                        int64_t* block_footprint_bytes);
 
 typedef struct RpEngine RpEngine;
 int rp_engine_create(const RpModelConfig* cfg, RpEngine** engine);
@@ -168,6 +175,8 @@ int rp_engine_set_batch_device(RpEngine* engine, const uint16_t* inputs_bf16,
 int rp_engine_set_lr(RpEngine* engine, float lr);
 int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
 int rp_engine_invalidate_graphs(RpEngine* engine);
+int rp_engine_enable_vanilla(RpEngine* engine);
+/* mode: 0 vanilla (needs rp_engine_enable_vanilla), 1 reprop, 2 pareprop */
 int rp_engine_step(RpEngine* engine, int mode, int use_graph);
 int rp_engine_sync(RpEngine* engine);
 int rp_engine_read_loss(RpEngine* engine, float* loss);

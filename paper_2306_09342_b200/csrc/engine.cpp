@@ -113,7 +113,7 @@ struct RpEngine {
   RpGemmPlan *p_embed = nullptr, *p_embed_w = nullptr;
   std::vector<RpGemmPlan*> all_plans;
   // graphs: index by mode (1 reprop, 2 pareprop)
-  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};  // by mode: 0 vanilla, 1, 2
   // NCCL
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
@@ -125,6 +125,14 @@ struct RpEngine {
   std::vector<double> prof_flops;
   size_t prof_used = 0;
   int64_t graph_kernels[3] = {0, 0, 0};
+  // Vanilla engine: every block's input pair is stored in the forward
+  float *stash1 = nullptr, *stash2 = nullptr;  // X_1..X_L, [L][T*d] each
+  bool vanilla_ready = false, vmode = false;
+  std::vector<RpGemmPlan*> vf_proj, vf_w2;
+  // optimizer: 0 SGD, 1 AdamW
+  int optimizer = 0;
+  float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f, wd = 0.f;
+  float *adam_m = nullptr, *adam_v = nullptr, *step_t = nullptr;
 };
 
 namespace {
@@ -214,8 +222,15 @@ const uint16_t* wb(const RpEngine* g, int64_t tix) { return g->pb + g->t_off[tix
 const float* wf(const RpEngine* g, int64_t tix) { return g->params + g->t_off[tix]; }
 float* gr(const RpEngine* g, int64_t tix) { return g->grads + g->t_off[tix]; }
 
-float* X1(RpEngine* g, int64_t j) { return j == 0 ? g->e : g->buf1[j % 2]; }
-float* X2(RpEngine* g, int64_t j) { return j == 0 ? g->e : g->buf2[j % 3]; }
+// X_j storage: rotating buffers for Reprop / PaReprop, the stash for Vanilla.
+float* X1(RpEngine* g, int64_t j) {
+  if (j == 0) return g->e;
+  return g->vmode ? g->stash1 + (j - 1) * g->T * g->d : g->buf1[j % 2];
+}
+float* X2(RpEngine* g, int64_t j) {
+  if (j == 0) return g->e;
+  return g->vmode ? g->stash2 + (j - 1) * g->T * g->d : g->buf2[j % 3];
+}
 
 int build_plans(RpEngine* g) {
   const int64_t T = g->T, d = g->d, h = g->h;
@@ -370,11 +385,11 @@ int forward(RpEngine* g, cudaStream_t s) {
     RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), F.hF, F.meanF, F.rstdF, s));
     RP_TRY(launch(p.f_qkv, s));
     RP_TRY(attn_fwd(g, F.qkv, F.att, F.lse, s));
-    RP_TRY(launch(p.f_proj, s));  // o2 = i2 + F(i1)
+    RP_TRY(launch(g->vmode ? g->vf_proj[static_cast<size_t>(b)] : p.f_proj, s));  // o2 = i2 + F(i1)
     RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), F.hF, F.meanF,
                   F.rstdF, s));
     RP_TRY(launch(p.f_w1, s));
-    RP_TRY(launch(p.f_w2, s));  // o1 = i1 + G(o2)
+    RP_TRY(launch(g->vmode ? g->vf_w2[static_cast<size_t>(b)] : p.f_w2, s));  // o1 = i1 + G(o2)
   }
   return RP_OK;
 }
@@ -400,11 +415,11 @@ int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
   RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), S.hG, S.meanG,
                 S.rstdG, s));
   RP_TRY(launch(p.r_w1, s));
-  if (b > 0) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
+  if (b > 0 && !g->vmode) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
   RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), S.hF, S.meanF, S.rstdF, s));
   RP_TRY(launch(p.r_qkv, s));
   RP_TRY(attn_fwd(g, S.qkv, S.att, S.lse, s));
-  if (b > 0) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
+  if (b > 0 && !g->vmode) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
   mark(g, 0, b, 1, s);
   return RP_OK;
 }
@@ -448,14 +463,28 @@ int bucket_update(RpEngine* g, int64_t off, int64_t n, cudaStream_t s) {
                                    ncclFloat32, ncclSum, g->comm, s);
     if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
   }
+  if (g->optimizer == 1)
+    return rpk_adamw(g->params + off, g->grads + off, g->pb + off, g->adam_m + off,
+                     g->adam_v + off, n, g->lr, g->step_t, g->beta1, g->beta2, g->eps, g->wd,
+                     1.0f / static_cast<float>(g->world), s);
   return rpk_sgd(g->params + off, g->grads + off, g->pb + off, n, g->lr,
                  1.0f / static_cast<float>(g->world), s);
 }
 
+int enqueue_step_impl(RpEngine* g, int mode);
+
 int enqueue_step(RpEngine* g, int mode) {
+  g->vmode = mode == 0;
+  const int rc = enqueue_step_impl(g, mode == 0 ? 1 : mode);
+  g->vmode = false;
+  return rc;
+}
+
+int enqueue_step_impl(RpEngine* g, int mode) {
   cudaStream_t sG = g->sG, sR = g->sR, sC = g->sC;
   t_prof_engine = g;
   g->prof_used = 0;
+  if (g->optimizer == 1) RP_TRY(rpk_add_scalar(g->step_t, 1.0f, sG));
   RP_TRY(forward(g, sG));
   RP_TRY(head(g, sG));
   RP_TRY(cuda_ok(cudaEventRecord(g->evFwd, sG), "record"));
@@ -515,6 +544,39 @@ void set_partition(RpEngine* g, int mode) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- activation ledger
+// Bytes of activation storage each engine keeps live at its peak (SPEC.md:346-349
+// MemoryLedger semantics, ref:proj/core/include/revprop/ledger.hpp:18-62), from the
+// arena plan of this engine: stored stage boundary, per-block recompute footprint,
+// cotangents and lane-G temporaries. Parameters, gradients and split-K / reduction
+// workspaces are excluded (they do not scale with depth or batch in the same way).
+//   mode 0 vanilla   stores every block's input pair + one block's caches
+//   mode 1 reprop    stage input + stage output + one block footprint
+//   mode 2 pareprop  reprop + one more block footprint (rendezvous depth 1)
+extern "C" int rp_activation_bytes(const RpModelConfig* c, int mode, int64_t* out_peak,
+                                   int64_t* out_block_footprint) {
+  if (!c || !out_peak) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  if (mode < 0 || mode > 2) return rp_fail(RP_ERR_CONFIG, "mode must be 0, 1 or 2");
+  const int64_t T = c->batch * c->seq_len, d = c->width, h = c->hidden, H = c->heads;
+  const int64_t pair = 2 * T * d * 4;  // one coupled (i1, i2) fp32 pair
+  // block footprint: recomputed input pair + F caches (hF, qkv, att: bf16; lse, LN stats)
+  // + G caches (hG, slope, a: bf16; LN stats)
+  const int64_t cache_f = T * d * 2 + T * 3 * d * 2 + T * d * 2 + T * H * 4 + 2 * T * 4;
+  const int64_t cache_g = T * d * 2 + 2 * T * h * 2 + 2 * T * 4;
+  const int64_t block = pair + cache_f + cache_g;
+  const int64_t stage = T * d * 4 /* embedding e, shared by i1 = i2 */ + pair /* output */;
+  const int64_t cot = 2 * T * d * 4 + 2 * T * d * 2;                        // d_out pair
+  const int64_t temps = T * h * 2 + 2 * T * d * 2 + T * 3 * d * 2 + T * d * 2;  // du,dh,datt,dqkv,de
+  int64_t peak = 0;
+  if (mode == 0)
+    peak = T * d * 4 + c->depth * pair + (block - pair) + cot + temps;
+  else
+    peak = stage + (mode == 2 ? 2 : 1) * block + cot + temps;
+  *out_peak = peak;
+  if (out_block_footprint) *out_block_footprint = block;
+  return RP_OK;
+}
 
 extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   if (!c || !out) return rp_fail(RP_ERR_CONTRACT, "engine_create: null argument");
@@ -629,6 +691,21 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
       (rc = dalloc(g, &g->loss, 1)) || (rc = dalloc(g, &g->dpooled, g->B * d)))
     return fail(rc);
   if ((rc = build_plans(g))) return fail(rc);
+  g->optimizer = c->optimizer;
+  if (c->optimizer == 1) {
+    g->beta1 = c->beta1;
+    g->beta2 = c->beta2;
+    g->eps = c->adam_eps;
+    g->wd = c->weight_decay;
+    if ((rc = dalloc(g, &g->adam_m, g->P)) || (rc = dalloc(g, &g->adam_v, g->P)) ||
+        (rc = dalloc(g, &g->step_t, 1)))
+      return fail(rc);
+    cudaMemset(g->adam_m, 0, static_cast<size_t>(g->P) * 4);
+    cudaMemset(g->adam_v, 0, static_cast<size_t>(g->P) * 4);
+    cudaMemset(g->step_t, 0, 4);
+  } else if (c->optimizer != 0) {
+    return fail(rp_fail(RP_ERR_CONFIG, "optimizer must be 0 (SGD) or 1 (AdamW)"));
+  }
   // default PaReprop SM partition: recompute : VJP work is ~1 : 2
   g->r_ctas = c->r_ctas > 0 ? c->r_ctas : 0;
   g->g_ctas = c->g_ctas > 0 ? c->g_ctas : 0;
@@ -755,6 +832,40 @@ extern "C" int rp_engine_set_lr(RpEngine* g, float lr) {
                  "set_lr");
 }
 
+// Allocates the Vanilla stash (every block's input pair, 2 L T d fp32) and its forward
+// plans; afterwards rp_engine_step(engine, 0, ...) runs store-everything training.
+extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  if (g->vanilla_ready) return RP_OK;
+  const int64_t n = g->L * g->T * g->d;
+  RP_TRY(dalloc(g, &g->stash1, n));
+  RP_TRY(dalloc(g, &g->stash2, n));
+  const int64_t T = g->T, d = g->d, h = g->h;
+  Slot& F = g->slot[0];
+  g->vmode = true;
+  g->vf_proj.resize(static_cast<size_t>(g->L));
+  g->vf_w2.resize(static_cast<size_t>(g->L));
+  for (int64_t b = 0; b < g->L; ++b) {
+    GemmArgs a{F.att, d, 0, wb(g, tix_block(b, kWout)), d, 1, T, d, d, RP_EPI_RESID,
+               X2(g, b + 1), d};
+    a.aux = X2(g, b);
+    int rc = mk_plan(g, a, &g->vf_proj[static_cast<size_t>(b)]);
+    if (rc == RP_OK) {
+      GemmArgs c{F.a, h, 0, wb(g, tix_block(b, kW2)), d, 1, T, d, h, RP_EPI_RESID, X1(g, b + 1), d};
+      c.aux = X1(g, b);
+      c.bias = wf(g, tix_block(b, kB2));
+      rc = mk_plan(g, c, &g->vf_w2[static_cast<size_t>(b)]);
+    }
+    if (rc != RP_OK) {
+      g->vmode = false;
+      return rc;
+    }
+  }
+  g->vmode = false;
+  g->vanilla_ready = true;
+  return RP_OK;
+}
+
 // Drop captured graphs (e.g. after toggling rp_set_pdl); the next step recaptures.
 extern "C" int rp_engine_invalidate_graphs(RpEngine* g) {
   if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
@@ -782,7 +893,10 @@ extern "C" int rp_engine_set_partition(RpEngine* g, int r_ctas, int g_ctas) {
 // The step is asynchronous on the engine stream; rp_engine_sync / read_loss wait for it.
 extern "C" int rp_engine_step(RpEngine* g, int mode, int use_graph) {
   if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
-  if (mode != 1 && mode != 2) return rp_fail(RP_ERR_CONFIG, "step: mode must be 1 (reprop) or 2 (pareprop)");
+  if (mode < 0 || mode > 2)
+    return rp_fail(RP_ERR_CONFIG, "step: mode must be 0 (vanilla), 1 (reprop) or 2 (pareprop)");
+  if (mode == 0 && !g->vanilla_ready)
+    return rp_fail(RP_ERR_CONTRACT, "step: vanilla mode needs rp_engine_enable_vanilla()");
   set_partition(g, mode);
   if (!use_graph || g->instrument) return enqueue_step(g, mode);
   if (!g->graph[mode]) {
@@ -828,7 +942,7 @@ extern "C" int rp_engine_read_loss(RpEngine* g, float* loss) {
 
 // Kernel launches per captured step (counted from the CUDA graph's kernel nodes).
 extern "C" int64_t rp_engine_graph_kernels(const RpEngine* g, int mode) {
-  return (g && mode >= 1 && mode <= 2) ? g->graph_kernels[mode] : -1;
+  return (g && mode >= 0 && mode <= 2) ? g->graph_kernels[mode] : -1;
 }
 
 // Runs one eager step with every tcgen05 GEMM launch bracketed by CUDA events on its own

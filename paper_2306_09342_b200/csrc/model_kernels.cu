@@ -101,6 +101,37 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
   }
 }
 
+// AdamW (decoupled weight decay), bias-corrected with the device step counter t.
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
+                             __nv_bfloat16* __restrict__ pb, float* __restrict__ m,
+                             float* __restrict__ v, int64_t n, const float* __restrict__ lr,
+                             const float* __restrict__ t, float b1, float b2, float eps,
+                             float wd, float scale) {
+  pdl_trigger();
+  pdl_wait();
+  const float step = lr[0];
+  const float tt = t[0];
+  const float c1 = 1.0f / (1.0f - powf(b1, tt)), c2 = 1.0f / (1.0f - powf(b2, tt));
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float gi = g[i] * scale;
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float upd = (mi * c1) / (sqrtf(vi * c2) + eps) + wd * p[i];
+    const float pv = p[i] - step * upd;
+    p[i] = pv;
+    pb[i] = __float2bfloat16_rn(pv);
+  }
+}
+
+__global__ void add_scalar_kernel(float* x, float a) {
+  pdl_trigger();
+  pdl_wait();
+  x[0] += a;
+}
+
 // fuse(average) + mean_tokens (layers.cpp:276-280 -> ops.cpp:408-427):
 // pooled[b][c] = (sum_n (o1 + o2) * 0.5) * (1/N), summed in token order.
 __global__ void pool_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
@@ -255,6 +286,17 @@ int rpk_sgd(float* p, const float* g, uint16_t* pb, int64_t n, const float* lr, 
   launch_k(sgd_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, g, reinterpret_cast<__nv_bfloat16*>(pb), n, lr,
                                          scale);
   return rp_check_launch("sgd");
+}
+int rpk_adamw(float* p, const float* g, uint16_t* pb, float* m, float* v, int64_t n,
+              const float* lr, const float* t, float b1, float b2, float eps, float wd,
+              float scale, cudaStream_t s) {
+  launch_k(adamw_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, g,
+           reinterpret_cast<__nv_bfloat16*>(pb), m, v, n, lr, t, b1, b2, eps, wd, scale);
+  return rp_check_launch("adamw");
+}
+int rpk_add_scalar(float* x, float a, cudaStream_t s) {
+  launch_k(add_scalar_kernel, dim3(1), dim3(1), 0, s, x, a);
+  return rp_check_launch("add_scalar");
 }
 int rpk_pool(const float* o1, const float* o2, int64_t B, int64_t N, int64_t d, float* pooled,
              cudaStream_t s) {

@@ -20,3 +20,7 @@ int rpk_cross_entropy(const float* logits, const int32_t* labels, int64_t B, int
 int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1, float* d2,
                uint16_t* d1b, uint16_t* d2b, cudaStream_t s);
 int rpk_add_to_bf16(const float* a, const float* b, uint16_t* out, int64_t n, cudaStream_t s);
+int rpk_adamw(float* p, const float* g, uint16_t* pb, float* m, float* v, int64_t n,
+              const float* lr, const float* t, float b1, float b2, float eps, float wd,
+              float scale, cudaStream_t s);
+int rpk_add_scalar(float* x, float a, cudaStream_t s);

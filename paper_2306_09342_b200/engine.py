@@ -22,7 +22,9 @@ class ModelConfigC(C.Structure):
                 ("hidden", C.c_int64), ("seq_len", C.c_int64), ("in_dim", C.c_int64),
                 ("num_classes", C.c_int64), ("batch", C.c_int64), ("window", C.c_int64),
                 ("seed", C.c_uint64), ("device", C.c_int), ("r_ctas", C.c_int),
-                ("g_ctas", C.c_int), ("lane_priority", C.c_int)]
+                ("g_ctas", C.c_int), ("lane_priority", C.c_int), ("optimizer", C.c_int),
+                ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
+                ("weight_decay", C.c_float)]
 
 
 @dataclass
@@ -42,6 +44,11 @@ class ModelConfig:
     r_ctas: int = 0
     g_ctas: int = 0
     lane_priority: int = 1
+    optimizer: int = 0          # 0 SGD, 1 AdamW
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    weight_decay: float = 0.0
 
 
 PRESETS = {
@@ -63,6 +70,7 @@ def _fn(name, restype, argtypes):
 _P, _I64, _I = C.c_void_p, C.c_int64, C.c_int
 _API = {
     "rp_engine_create": (_I, [C.POINTER(ModelConfigC), C.POINTER(_P)]),
+    "rp_activation_bytes": (_I, [C.POINTER(ModelConfigC), _I, C.POINTER(_I64), C.POINTER(_I64)]),
     "rp_engine_destroy": (None, [_P]),
     "rp_engine_param_count": (_I64, [_P]),
     "rp_engine_tensor_table": (_I, [_P, _P, _P, _I64]),
@@ -76,6 +84,7 @@ _API = {
     "rp_engine_set_lr": (_I, [_P, C.c_float]),
     "rp_engine_set_partition": (_I, [_P, _I, _I]),
     "rp_engine_invalidate_graphs": (_I, [_P]),
+    "rp_engine_enable_vanilla": (_I, [_P]),
     "rp_engine_step": (_I, [_P, _I, _I]),
     "rp_engine_sync": (_I, [_P]),
     "rp_engine_read_loss": (_I, [_P, C.POINTER(C.c_float)]),
@@ -124,9 +133,7 @@ class Engine:
 
     def __init__(self, cfg: ModelConfig):
         self.cfg = cfg
-        c = ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
-                         cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
-                         cfg.g_ctas, cfg.lane_priority)
+        c = _cfg_c(cfg)
         h = C.c_void_p()
         check(api("rp_engine_create")(C.byref(c), C.byref(h)), "engine_create")
         self._h = h
@@ -195,6 +202,10 @@ class Engine:
     def set_partition(self, r_ctas: int, g_ctas: int):
         check(api("rp_engine_set_partition")(self._h, r_ctas, g_ctas), "set_partition")
 
+    def enable_vanilla(self):
+        """Allocate the store-everything stash so step(VANILLA) works."""
+        check(api("rp_engine_enable_vanilla")(self._h), "enable_vanilla")
+
     def invalidate_graphs(self):
         check(api("rp_engine_invalidate_graphs")(self._h), "invalidate_graphs")
 
@@ -244,6 +255,37 @@ class Engine:
         check(api("rp_engine_rev_backward_local")(
             self._h, b, o1.data_ptr(), o2.data_ptr(), d_o1.data_ptr(), d_o2.data_ptr(),
             i1.data_ptr(), i2.data_ptr(), d_i1.data_ptr(), d_i2.data_ptr()), "rev_backward_local")
+
+
+def _cfg_c(cfg: "ModelConfig") -> ModelConfigC:
+    return ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
+                        cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
+                        cfg.g_ctas, cfg.lane_priority, cfg.optimizer, cfg.beta1, cfg.beta2,
+                        cfg.adam_eps, cfg.weight_decay)
+
+
+VANILLA = 0
+
+
+def activation_bytes(cfg: "ModelConfig", mode: int):
+    """(peak activation bytes, block footprint) the ledger predicts for an engine mode."""
+    peak, blk = C.c_int64(), C.c_int64()
+    c = _cfg_c(cfg)
+    check(api("rp_activation_bytes")(C.byref(c), mode, C.byref(peak), C.byref(blk)),
+          "activation_bytes")
+    return peak.value, blk.value
+
+
+def probe_max_batch(cfg: "ModelConfig", mode: int, budget_bytes: int) -> int:
+    """SPEC.md:462-470: doubling search over batch against the ledger-predicted peak;
+    returns the largest feasible power of two (BudgetError if batch 1 does not fit)."""
+    from dataclasses import replace
+    b = 1
+    if activation_bytes(replace(cfg, batch=1), mode)[0] > budget_bytes:
+        raise _capi.BudgetError("batch 1 exceeds the byte budget")
+    while activation_bytes(replace(cfg, batch=2 * b), mode)[0] <= budget_bytes:
+        b *= 2
+    return b
 
 
 def nccl_unique_id() -> bytes:

@@ -84,3 +84,37 @@ def test_engine_config_errors(capi):
         Engine(ModelConfig(depth=0))
     with pytest.raises(capi.ConfigError, match="head_dim"):
         Engine(ModelConfig(width=768, heads=8))
+
+
+def test_activation_ledger_spec_invariants(capi):
+    """SPEC.md acceptance 4 and 5 on the engine's ledger: Reprop/PaReprop peaks are flat in
+    depth, Vanilla grows by one stored fp32 pair per block, PaReprop costs at most two extra
+    block footprints; probe_max_batch follows SPEC.md:462-470.
+
+    The Vanilla/Reprop ratio crosses 3 at depth 32 here, not 16 as SPEC.md:500 states for
+    the CPU reference: one block's recompute footprint on the GPU (bf16 caches incl. the
+    h = 4d MLP activations) is ~4.5 stored input pairs, so Reprop's constant term is larger."""
+    import numpy as np
+    from dataclasses import replace
+    from paper_2306_09342_b200.engine import (PAREPROP, REPROP, VANILLA, ModelConfig,
+                                              activation_bytes, probe_max_batch)
+    base = ModelConfig(depth=2, width=192, heads=3, hidden=768, seq_len=197, batch=64)
+    depths = [2, 4, 8, 16]
+    peaks = {m: [activation_bytes(replace(base, depth=L), m)[0] for L in depths]
+             for m in (VANILLA, REPROP, PAREPROP)}
+    _, block = activation_bytes(base, REPROP)
+    slope = {m: np.polyfit(depths, peaks[m], 1)[0] for m in peaks}
+    pair = 2 * base.batch * base.seq_len * base.width * 4
+    assert abs(slope[VANILLA] - pair) < 1e-6 * pair  # one stored pair per block
+    assert abs(slope[REPROP]) < 0.1 * block and abs(slope[PAREPROP]) < 0.1 * block
+    ratio16 = peaks[VANILLA][-1] / peaks[REPROP][-1]
+    ratio32 = (activation_bytes(replace(base, depth=32), VANILLA)[0] /
+               activation_bytes(replace(base, depth=32), REPROP)[0])
+    assert 2 < ratio16 < ratio32 and ratio32 > 3
+    for r, p in zip(peaks[REPROP], peaks[PAREPROP]):
+        assert r <= p <= r + 2 * block
+    budget = activation_bytes(replace(base, batch=8), REPROP)[0]
+    assert probe_max_batch(base, REPROP, budget) == 8
+    assert probe_max_batch(replace(base, depth=16), VANILLA, budget) < 8
+    with pytest.raises(capi.BudgetError):
+        probe_max_batch(base, REPROP, 1000)

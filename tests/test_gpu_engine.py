@@ -33,7 +33,7 @@ def l2rel(a, b):
 
 def make(cfg_kw, batch, seed=0):
     from paper_2306_09342_b200.engine import Engine, ModelConfig, bf16_round
-    cfg = ModelConfig(batch=batch, **cfg_kw)
+    cfg = ModelConfig(**dict(cfg_kw, batch=batch))
     eng = Engine(cfg)
     mc = O.ModelConfig(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
                        cfg.num_classes, cfg.window or None)
@@ -194,3 +194,68 @@ def test_errors_map_to_reference_classes():
         Engine(ModelConfig(depth=1, width=100, heads=3, hidden=256, batch=1))
     with pytest.raises(_capi.ShapeError):
         Engine(ModelConfig(depth=1, width=128, heads=2, hidden=256, seq_len=10, window=3, batch=1))
+
+
+def test_vanilla_engine_matches_reprop_and_oracle():
+    """SPEC.md:360-368 / acceptance 3: store-everything gradients agree with Reprop (they
+    differ only by the inverse's rounding) and with the oracle."""
+    from paper_2306_09342_b200.engine import REPROP, VANILLA, bf16_bits, bf16_round
+    eng, mc, p32, pref = make(dict(TI, depth=3), batch=4)
+    x, lab = O.synthetic_batch(mc, 4, seed=21)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    eng.enable_vanilla()
+    eng.step(REPROP, graph=False)
+    g_r, l_r = eng.grads(), eng.loss()
+    eng.step(VANILLA, graph=False)
+    g_v, l_v = eng.grads(), eng.loss()
+    eng.step(VANILLA, graph=True)
+    assert np.array_equal(eng.grads(), g_v)
+    assert abs(l_v - l_r) < 1e-5 * abs(l_r)
+    assert l2rel(g_v, g_r) < 1e-3
+    r = O.step(mc, pref, bf16_round(x).astype(np.float64), lab)
+    per_tensor(mc, g_v, r.grads, TOL_GRAD)
+
+
+def test_adamw_descent_and_lane_identity():
+    """AdamW instead of SPEC's SGD: loss falls; PaReprop == Reprop bit-exact."""
+    from paper_2306_09342_b200.engine import (PAREPROP, REPROP, Engine, ModelConfig, bf16_bits)
+    mc = O.ModelConfig(2, 192, 3, 768, 197, 768, 10)
+    x, lab = O.synthetic_batch(mc, 8, seed=5)
+    p32 = O.init_params(mc, 0, np.float32)
+    out = {}
+    for mode in (REPROP, PAREPROP):
+        eng = Engine(ModelConfig(depth=2, width=192, heads=3, hidden=768, seq_len=197,
+                                 num_classes=10, batch=8, optimizer=1, weight_decay=0.01))
+        eng.set_params(p32)
+        eng.set_batch(bf16_bits(x), lab)
+        eng.set_lr(1e-3)
+        ls = []
+        for _ in range(15):
+            eng.step(mode)
+            ls.append(eng.loss())
+        out[mode] = (ls, eng.params())
+        eng.close()
+    assert out[REPROP][0][-1] < 0.8 * out[REPROP][0][0], out[REPROP][0]
+    assert out[REPROP][0] == out[PAREPROP][0]
+    np.testing.assert_array_equal(out[REPROP][1], out[PAREPROP][1])
+
+
+def test_windowed_attention_and_long_sequence_steps():
+    """Windowed attention (layers.cpp:119-122) and a 512-token sequence (Rev-RoBERTa config,
+    mma.sync attention path) through the whole step, against the oracle."""
+    from paper_2306_09342_b200.engine import REPROP, bf16_bits, bf16_round
+    for cfg, B in [(dict(depth=2, width=128, heads=2, hidden=512, seq_len=64, in_dim=256,
+                         num_classes=7, window=16), 4),
+                   (dict(depth=2, width=128, heads=2, hidden=512, seq_len=512, in_dim=256,
+                         num_classes=2), 2)]:
+        eng, mc, p32, pref = make(cfg, batch=B)
+        x, lab = O.synthetic_batch(mc, B, seed=8)
+        eng.set_batch(bf16_bits(x), lab)
+        eng.set_lr(0.0)
+        eng.step(REPROP, graph=False)
+        r = O.step(mc, pref, bf16_round(x).astype(np.float64), lab)
+        assert abs(eng.loss() - r.loss) < 1e-3 * abs(r.loss)
+        per_tensor(mc, eng.grads(), r.grads, TOL_GRAD)
+        assert l2rel(eng.grads(), r.grads) < TOL_L2
+        eng.close()
