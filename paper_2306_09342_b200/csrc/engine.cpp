@@ -793,14 +793,20 @@ extern "C" int rp_engine_set_params(RpEngine* g, const float* host) {
 
 extern "C" int rp_engine_get_params(RpEngine* g, float* host) {
   if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
-  return cuda_ok(cudaMemcpy(host, g->params, static_cast<size_t>(g->P) * 4, cudaMemcpyDeviceToHost),
-                 "get_params");
+  // ordered after the engine's pending work (its streams are non-blocking: a plain
+  // cudaMemcpy on the legacy stream would not wait for an in-flight step)
+  RP_TRY(cuda_ok(cudaMemcpyAsync(host, g->params, static_cast<size_t>(g->P) * 4,
+                                 cudaMemcpyDeviceToHost, g->sG),
+                 "get_params"));
+  return rp_engine_sync(g);
 }
 
 extern "C" int rp_engine_get_grads(RpEngine* g, float* host) {
   if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
-  return cuda_ok(cudaMemcpy(host, g->grads, static_cast<size_t>(g->P) * 4, cudaMemcpyDeviceToHost),
-                 "get_grads");
+  RP_TRY(cuda_ok(cudaMemcpyAsync(host, g->grads, static_cast<size_t>(g->P) * 4,
+                                 cudaMemcpyDeviceToHost, g->sG),
+                 "get_grads"));
+  return rp_engine_sync(g);
 }
 
 // inputs: bf16 [B, N, in_dim] (host, ideally pinned), labels int32 [B]; async on the

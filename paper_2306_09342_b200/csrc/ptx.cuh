@@ -174,27 +174,40 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// tanh-GELU with the hardware tanh (MUFU.TANH, |rel err| < 2^-10.9): used in the GEMM
-// epilogues whose outputs are stored as bf16 anyway (8 mantissa bits).
-__device__ __forceinline__ float gelu_tanh_fast(float x) {
-  const float c = 0.7978845608028654f, a = 0.044715f;
-  const float t = tanh_fast(c * (x + a * x * x * x));
-  return 0.5f * x * (1.0f + t);
+// tanh-GELU in its sigmoid form, 0.5 (1 + tanh z) = sigma(2z) = 1 / (1 + 2^(-2 z log2 e)),
+// on MUFU.EX2 + MUFU.RCP (both ~1 ulp): unlike 0.5 (1 + tanh.approx z), whose absolute
+// error (~2^-11) does not shrink with the result and adds up coherently in the bias-gradient
+// column sums, every term here is relative-accurate, including 1 - sigma = e * sigma.
+struct GeluParts {
+  float s;   // sigma(2z) = 0.5 (1 + tanh z)
+  float om;  // 1 - s
+};
+__device__ __forceinline__ GeluParts gelu_parts(float x, float x2) {
+  const float c2l = 2.0f * 0.7978845608028654f * 1.4426950408889634f, a = 0.044715f;
+  // e = 2^(-2 z log2 e); the clamp keeps e finite so that e * s stays 1 for very negative z
+  const float arg = fminf(-c2l * x * fmaf(a, x2, 1.0f), 64.0f);
+  float e, s;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(arg));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(1.0f + e));
+  return {s, e * s};
 }
-// gelu(x) and gelu'(x) sharing one MUFU.TANH (the recompute epilogue keeps the slope
-// for the backward instead of the pre-activation).
-__device__ __forceinline__ void gelu_and_slope_fast(float x, float& g, float& s) {
+__device__ __forceinline__ float gelu_tanh_fast(float x) {
+  return x * gelu_parts(x, x * x).s;
+}
+// gelu(x) and gelu'(x) from one sigmoid (the recompute epilogue keeps the slope for the
+// backward instead of the pre-activation):
+//   gelu' = s + x * 2 z' * s (1 - s),  z' = c (1 + 3 a x^2)
+__device__ __forceinline__ void gelu_and_slope_fast(float x, float& g, float& sl) {
   const float c = 0.7978845608028654f, a = 0.044715f;
   const float x2 = x * x;
-  const float t = tanh_fast(c * x * fmaf(a, x2, 1.0f));
-  const float hx = 0.5f * x;
-  g = fmaf(hx, t, hx);
-  s = fmaf(hx * (c * fmaf(3.0f * a, x2, 1.0f)), fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
+  const GeluParts p = gelu_parts(x, x2);
+  g = x * p.s;
+  sl = fmaf(x * (2.0f * c) * fmaf(3.0f * a, x2, 1.0f), p.s * p.om, p.s);
 }
 __device__ __forceinline__ float gelu_tanh_slope_fast(float x) {
-  const float c = 0.7978845608028654f, a = 0.044715f;
-  const float t = tanh_fast(c * (x + a * x * x * x));
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
+  float g, sl;
+  gelu_and_slope_fast(x, g, sl);
+  return sl;
 }
 // tanh-GELU exactly as ref:proj/core/src/ops.cpp:227-262 (constants ops.cpp:11-12),
 // evaluated in fp32.
