@@ -463,9 +463,9 @@ static int attn_check(int64_t B, int64_t N, int64_t H, int64_t hd) {
 // B here is the number of independent sequences (batch x windows).
 int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, uint16_t* out,
                         float* lse, cudaStream_t stream);
-int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* dout, const float* lse,
-                        const float* Dg, int64_t S, int64_t N, int64_t H, uint16_t* dqkv,
-                        cudaStream_t stream);
+int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
+                        const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
+                        uint16_t* dqkv, cudaStream_t stream);
 static int g_attn_impl = 0;  // 0 = tcgen05 where it applies (N <= 256), 1 = mma.sync only
 
 extern "C" int rp_set_attention_impl(int impl) {
@@ -507,16 +507,16 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   if (rc) return rc;
   const AttnGeom g = make_geom(B, N, H);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (g_attn_impl == 0 && N <= 256) {  // tcgen05 path computes D itself
+    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s);
+    if (rc != RP_ERR_CONFIG) return rc;
+  }
   const int64_t total = B * N * H;
   int blocks = static_cast<int>((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   launch_k(attn_bwd_dot_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(out),
                                              reinterpret_cast<const __nv_bfloat16*>(dout),
                                              workspace, g);
-  if (g_attn_impl == 0 && N <= 256) {
-    rc = rp_attention_bwd_tc(qkv, dout, lse, workspace, B, N, H, dqkv, s);
-    if (rc != RP_ERR_CONFIG) return rc;
-  }
   const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
   const int smem_kv = 2 * kTile * kRowBytes + 2 * npad * kRowBytes + 2 * npad * 4;
   const int smem_q = 2 * kTile * kRowBytes + 2 * npad * kRowBytes;
