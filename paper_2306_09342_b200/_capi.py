@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librevprop_b200.so"
+_LIB_PATH = Path(os.environ.get("RP_LIB") or
+                 Path(__file__).resolve().parent / "_lib" / "librevprop_b200.so")  # RP_LIB: A/B builds
 
 
 class Error(RuntimeError):

@@ -109,9 +109,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tma_load_2d(base + 32768, &tm_kv, &bar_load[buf], d + h * 64, row_seq);
         tma_load_2d(base + 65536, &tm_kv, &bar_load[buf], 2 * d + h * 64, row_seq);
       };
-      auto ready = [](uint64_t* bar, uint32_t parity) {
-        return mbar_try_wait(smem_u32(bar), parity) != 0;
-      };
+      auto ready = [](const uint64_t* bar, uint32_t parity) { return mbar_test(bar, parity); };
       const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
       const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
       int jS = 0, jP = 0, kL = 0;

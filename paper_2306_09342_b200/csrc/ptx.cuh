@@ -46,6 +46,19 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
       : "memory");
   return ok;
 }
+// Non-blocking probe (mbarrier.test_wait never suspends the thread; try_wait may sleep
+// until the phase completes or a timeout): for event loops that poll several barriers.
+__device__ __forceinline__ bool mbar_test(const uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Blocking wait with a watchdog: a pipeline bug traps (kernel error) instead of
 // hanging the device. The bound (~2^34 cycles, several seconds) is never reached by a
 // healthy kernel.
