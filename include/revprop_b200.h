@@ -112,6 +112,15 @@ int rp_layer_norm_bwd(const float* x, const float* mean, const float* rstd, cons
                       const uint16_t* dy, const float* dres, int64_t rows, int64_t cols,
                       float* dx, uint16_t* dx_bf16, float* dgamma, float* dbeta,
                       float* workspace, int accumulate, rp_stream_t stream);
+/* Same, plus (dx_colsum != NULL) dx_colsum[c] = sum_r dx[r][c] of the produced cotangent: the
+ * next reversible block's MLP output-bias gradient (ref:proj/core/src/layers.cpp:38-52
+ * col_sum over the same d_o1), computed in the same single pass over x, dy and dres. */
+int rp_layer_norm_bwd_ex(const float* x, const float* mean, const float* rstd, const float* gamma,
+                         const uint16_t* dy, const float* dres, int64_t rows, int64_t cols,
+                         float* dx, uint16_t* dx_bf16, float* dgamma, float* dbeta,
+                         float* dx_colsum, float* workspace, int accumulate, rp_stream_t stream);
+/* 1 (default): single-pass backward; 0: row kernel + separate column-sum pass (A/B only). */
+int rp_set_ln_bwd_impl(int impl);
 int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols);
 int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t cols, float* out,
               float* workspace, int accumulate, rp_stream_t stream);
@@ -131,6 +140,9 @@ int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
 /* 0 (default): tcgen05 kernels where they apply (N <= 256); 1: warp-level mma.sync only */
 int rp_set_attention_impl(int impl);
+/* Diagnostics: clock64 timeline of CTA 0 of the tcgen05 attention backward (tools/trace_attn.py);
+ * on != 0 arms the trace, out1024 (may be NULL) receives the last one. */
+int rp_attn_trace(int on, long long* out1024);
 
 /* ------------------------------------------------------------------ training engine
  * Isotropic reversible model and its engines:

@@ -83,6 +83,9 @@ _SIGS = {
     "rp_gemm_plan_destroy": (None, [_P]),
     "rp_layer_norm_fwd": (_I, [_P, _P, _P, _I64, _I64, _D, _P, _P, _P, _P]),
     "rp_layer_norm_bwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _I, _P]),
+    "rp_layer_norm_bwd_ex": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I,
+                                  _P]),
+    "rp_set_ln_bwd_impl": (_I, [_I]),
     "rp_layer_norm_bwd_workspace_floats": (_I64, [_I64, _I64]),
     "rp_colsum": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _P]),
     "rp_colsum_workspace_floats": (_I64, [_I64, _I64]),

@@ -425,7 +425,10 @@ int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
 }
 
 // Lane G: the VJP half of rev_backward_local, G-path before F-path.
-int lane_g(RpEngine* g, int64_t b, cudaStream_t s) {
+// own_b2: this block's MLP output-bias grad from its incoming d_o1 (a column-sum pass);
+// in a step only the top block needs it, every other block's b2 grad is produced by the
+// block above in the same pass that writes its d_o1 (next_b2, the F-path LN backward).
+int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   Slot& S = g->slot[b % 2];
   const int64_t T = g->T, d = g->d, h = g->h;
@@ -433,7 +436,7 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s) {
   // ---- G = MLP VJP with d_o1 (layers.cpp:241-259)
   RP_TRY(launch(p.g_dw2, s));
   RP_TRY(launch(p.g_ww2, s));
-  RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
+  if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_ww1, s));
   RP_TRY(rp_colsum(g->du, 1, T, h, gr(g, tix_block(b, kB1)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_dw1, s));
@@ -449,9 +452,10 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s) {
   RP_TRY(launch(p.g_wqkv, s));
   RP_TRY(launch(p.g_dqkv, s));
   // d_i1 = d_o1 + LN_F^T(d_hF)    (in place in d1 / d1b); d_i2 = d_o2t (already in d2)
-  RP_TRY(rp_layer_norm_bwd(X1(g, b), S.meanF, S.rstdF, wf(g, tix_block(b, kLnFg)), g->dh, g->d1,
-                           T, d, g->d1, g->d1b, gr(g, tix_block(b, kLnFg)),
-                           gr(g, tix_block(b, kLnFb)), g->ln_ws, 0, s));
+  RP_TRY(rp_layer_norm_bwd_ex(X1(g, b), S.meanF, S.rstdF, wf(g, tix_block(b, kLnFg)), g->dh,
+                              g->d1, T, d, g->d1, g->d1b, gr(g, tix_block(b, kLnFg)),
+                              gr(g, tix_block(b, kLnFb)),
+                              next_b2 ? gr(g, tix_block(b - 1, kB2)) : nullptr, g->ln_ws, 0, s));
   mark(g, 1, b, 1, s);
   return RP_OK;
 }
@@ -500,7 +504,7 @@ int enqueue_step_impl(RpEngine* g, int mode) {
       RP_TRY(lane_r(g, b, sR));
       RP_TRY(cuda_ok(cudaEventRecord(g->evR[static_cast<size_t>(b)], sR), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
-      RP_TRY(lane_g(g, b, sG));
+      RP_TRY(lane_g(g, b, sG, b == g->L - 1, b > 0));
       RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
       RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
@@ -509,7 +513,7 @@ int enqueue_step_impl(RpEngine* g, int mode) {
   } else {
     for (int64_t b = g->L - 1; b >= 0; --b) {
       RP_TRY(lane_r(g, b, sG));
-      RP_TRY(lane_g(g, b, sG));
+      RP_TRY(lane_g(g, b, sG, b == g->L - 1, b > 0));
       RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
       RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
@@ -1071,7 +1075,7 @@ extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float*
   RP_TRY(rpk_f32_to_bf16(g->d2, g->d2b, n, s));
   set_partition(g, 1);
   RP_TRY(lane_r(g, b, s));
-  RP_TRY(lane_g(g, b, s));
+  RP_TRY(lane_g(g, b, s, true, false));
   RP_TRY(cuda_ok(cudaMemcpyAsync(i1, X1(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(i2, X2(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_i1, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));

@@ -11,6 +11,8 @@
 // SPEC.md:234) and a bf16 copy of dx_total emitted for the next GEMM.
 // All reductions have a fixed association order that depends only on the problem shape,
 // never on the launch or stream co-residency, so results are bit-reproducible.
+#include <mutex>
+
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -149,115 +151,105 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   }
 }
 
-// Backward, fused: the row kernel above plus dgamma / dbeta partial sums. Each warp keeps
-// its column sums in its own shared-memory row ([2][cols] floats, read-modify-write per
-// row it owns: rows w, w+8, ... of the CTA's kLnBwdRows), then the CTA combines its 8 warp
-// rows in warp order -> part[blk][2][cols]. Fixed association order, no atomics, and no
-// second pass over x and dy.
-template <int V>
-__global__ void __launch_bounds__(kLnWarps * 32, 2)
-    ln_bwd_fused_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
+// Backward, single pass: dx (and its bf16 copy) plus the column sums dgamma = sum dy*x_hat,
+// dbeta = sum dy and, optionally, sum dx (the next block's MLP output-bias gradient, which
+// is the column sum of exactly this cotangent). One warp per row, all loads issued before
+// the row reductions; each warp accumulates its rows' column sums in its own shared-memory
+// rows (read-modify-write, the warp's rows in order), and the CTA combines its 8 warps in
+// warp order -> part[blk][NACC][cols]. Fixed association order, no atomics, one read of x,
+// dy and dres.
+template <int V, int NACC>
+__global__ void __launch_bounds__(kLnWarps * 32)
+    ln_bwd_1pass_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
                         const float* __restrict__ rstd_in, const float* __restrict__ gamma,
                         const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
                         int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16,
                         float* __restrict__ part) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ float acc[];  // [2][cols]: the CTA's running dgamma | dbeta partial
+  extern __shared__ float4 acc4[];  // [warp][NACC][cols/4]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c4 = cols >> 2;
+  float4* my = acc4 + static_cast<int64_t>(warp) * NACC * c4;
+  for (int i = lane; i < NACC * c4; i += 32) my[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
   const float inv_n = 1.0f / static_cast<float>(cols);
-  float4 ag[V], ab[V];  // this lane's column sums over the warp's rows (row order)
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    ag[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    ab[i] = ag[i];
-  }
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
   for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
     const int64_t row = r0 + rr;
     if (row >= rows) break;
     const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
     const uint2* dyr = reinterpret_cast<const uint2*>(dy + row * cols);
+    const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
+    float4 xv[V], rv[V];
+    uint2 dv[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + 32 * i;
+      if (c < c4) {
+        xv[i] = xr[c];
+        dv[i] = dyr[c];
+        rv[i] = drr ? drr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     const float mean = mean_in[row], rstd = rstd_in[row];
-    // pass 1: row sums (x and dy stay in L1 for pass 2)
     float sg = 0.f, sgh = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int c = lane + 32 * i;
       if (c < c4) {
-        const float4 xv = xr[c];
-        const uint2 dv = dyr[c];
-        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+        const float2 d01 = unpack_bf16x2(dv[i].x), d23 = unpack_bf16x2(dv[i].y);
         const float4 gm = g4[c];
+        xv[i] = make_float4((xv[i].x - mean) * rstd, (xv[i].y - mean) * rstd,
+                            (xv[i].z - mean) * rstd, (xv[i].w - mean) * rstd);  // x_hat
         const float gx = d01.x * gm.x, gy = d01.y * gm.y, gz = d23.x * gm.z, gw = d23.y * gm.w;
         sg += (gx + gy) + (gz + gw);
-        sgh += (gx * ((xv.x - mean) * rstd) + gy * ((xv.y - mean) * rstd)) +
-               (gz * ((xv.z - mean) * rstd) + gw * ((xv.w - mean) * rstd));
+        sgh += (gx * xv[i].x + gy * xv[i].y) + (gz * xv[i].z + gw * xv[i].w);
       }
     }
     const float gmn = warp_sum(sg) * inv_n;
     const float ghm = warp_sum(sgh) * inv_n;
-    // pass 2: dx = dres + (g - mean(g) - x_hat mean(g x_hat)) rstd; column sums
-    const float4* drr = dres ? reinterpret_cast<const float4*>(dres + row * cols) : nullptr;
     float4* dxr = reinterpret_cast<float4*>(dx + row * cols);
     uint2* dxb = dx_bf16 ? reinterpret_cast<uint2*>(dx_bf16 + row * cols) : nullptr;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int c = lane + 32 * i;
       if (c < c4) {
-        const float4 xv = xr[c];
-        const uint2 dv = dyr[c];
-        const float4 rv = drr ? drr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float2 d01 = unpack_bf16x2(dv.x), d23 = unpack_bf16x2(dv.y);
+        const float2 d01 = unpack_bf16x2(dv[i].x), d23 = unpack_bf16x2(dv[i].y);
         const float4 gm = g4[c];
-        const float hx = (xv.x - mean) * rstd, hy = (xv.y - mean) * rstd,
-                    hz = (xv.z - mean) * rstd, hw = (xv.w - mean) * rstd;
+        const float4 h = xv[i];
         float4 o;
-        o.x = (d01.x * gm.x - gmn - hx * ghm) * rstd + rv.x;
-        o.y = (d01.y * gm.y - gmn - hy * ghm) * rstd + rv.y;
-        o.z = (d23.x * gm.z - gmn - hz * ghm) * rstd + rv.z;
-        o.w = (d23.y * gm.w - gmn - hw * ghm) * rstd + rv.w;
+        o.x = (d01.x * gm.x - gmn - h.x * ghm) * rstd + rv[i].x;
+        o.y = (d01.y * gm.y - gmn - h.y * ghm) * rstd + rv[i].y;
+        o.z = (d23.x * gm.z - gmn - h.z * ghm) * rstd + rv[i].z;
+        o.w = (d23.y * gm.w - gmn - h.w * ghm) * rstd + rv[i].w;
         dxr[c] = o;
         if (dxb) dxb[c] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
-        ag[i].x += d01.x * hx;
-        ag[i].y += d01.y * hy;
-        ag[i].z += d23.x * hz;
-        ag[i].w += d23.y * hw;
-        ab[i].x += d01.x;
-        ab[i].y += d01.y;
-        ab[i].z += d23.x;
-        ab[i].w += d23.y;
-      }
-    }
-  }
-  // combine the 8 warps in warp order through one [2][cols] buffer
-  for (int w = 0; w < kLnWarps; ++w) {
-    if (warp == w) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const int c = lane + 32 * i;
-        if (c < c4) {
-          float4* pg = reinterpret_cast<float4*>(acc) + c;
-          float4* pb = reinterpret_cast<float4*>(acc + cols) + c;
-          if (w == 0) {
-            *pg = ag[i];
-            *pb = ab[i];
-          } else {
-            float4 tg = *pg, tb = *pb;
-            tg.x += ag[i].x; tg.y += ag[i].y; tg.z += ag[i].z; tg.w += ag[i].w;
-            tb.x += ab[i].x; tb.y += ab[i].y; tb.z += ab[i].z; tb.w += ab[i].w;
-            *pg = tg;
-            *pb = tb;
-          }
+        float4 a = my[c];
+        a.x += d01.x * h.x; a.y += d01.y * h.y; a.z += d23.x * h.z; a.w += d23.y * h.w;
+        my[c] = a;
+        float4 bb = my[c4 + c];
+        bb.x += d01.x; bb.y += d01.y; bb.z += d23.x; bb.w += d23.y;
+        my[c4 + c] = bb;
+        if constexpr (NACC == 3) {
+          float4 cc = my[2 * c4 + c];
+          cc.x += o.x; cc.y += o.y; cc.z += o.z; cc.w += o.w;
+          my[2 * c4 + c] = cc;
         }
       }
     }
-    __syncthreads();
   }
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x)
-    part[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = acc[c];
+  __syncthreads();
+  // combine the warps' rows in warp order
+  float4* out = reinterpret_cast<float4*>(part + static_cast<int64_t>(blockIdx.x) * NACC * cols);
+  for (int i = threadIdx.x; i < NACC * c4; i += blockDim.x) {
+    float4 t = acc4[i];
+    for (int w = 1; w < kLnWarps; ++w) {
+      const float4 u = acc4[static_cast<int64_t>(w) * NACC * c4 + i];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    out[i] = t;
+  }
 }
 
 // Backward, column part (stage 1): CTA (rb, cb) sums dgamma = dy*x_hat and dbeta = dy
@@ -394,14 +386,29 @@ static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_
 }
 
 template <int V>
-static void launch_ln_bwd_fused(const float* x, const float* mean, const float* rstd,
+static void launch_ln_bwd_1pass(const float* x, const float* mean, const float* rstd,
                                 const float* gamma, const __nv_bfloat16* dy, const float* dres,
                                 int64_t rows, int cols, float* dx, __nv_bfloat16* dxb,
-                                float* part, cudaStream_t s) {
+                                float* part, int nacc, cudaStream_t s) {
   const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
-  const int smem = 2 * cols * static_cast<int>(sizeof(float));
-  launch_k(ln_bwd_fused_kernel<V>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32), smem, s, 
-      x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+  const int smem = kLnWarps * nacc * cols * static_cast<int>(sizeof(float));
+  if (nacc == 3) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kLnWarps * 3 * 2048 * 4);
+    });
+    launch_k(ln_bwd_1pass_kernel<V, 3>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32),
+             smem, s, x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+  } else {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kLnWarps * 2 * 2048 * 4);
+    });
+    launch_k(ln_bwd_1pass_kernel<V, 2>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32),
+             smem, s, x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
+  }
 }
 
 template <int V>
@@ -449,20 +456,49 @@ extern "C" int rp_layer_norm_fwd(const float* x, const float* gamma, const float
   return rp_check_launch("layer_norm_fwd");
 }
 
-extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float* rstd,
-                                 const float* gamma, const uint16_t* dy, const float* dres,
-                                 int64_t rows, int64_t cols, float* dx, uint16_t* dx_bf16,
-                                 float* dgamma, float* dbeta, float* workspace,
-                                 int accumulate, rp_stream_t stream) {
+static int g_ln_bwd_impl = 1;  // 1 = single pass (fused column sums), 0 = row kernel + column kernels
+
+extern "C" int rp_set_ln_bwd_impl(int impl) {
+  g_ln_bwd_impl = impl;
+  return RP_OK;
+}
+
+extern "C" int rp_layer_norm_bwd_ex(const float* x, const float* mean, const float* rstd,
+                                    const float* gamma, const uint16_t* dy, const float* dres,
+                                    int64_t rows, int64_t cols, float* dx, uint16_t* dx_bf16,
+                                    float* dgamma, float* dbeta, float* dx_colsum,
+                                    float* workspace, int accumulate, rp_stream_t stream) {
   if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* dyb = reinterpret_cast<const __nv_bfloat16*>(dy);
+  const int64_t nparts = rp_ln_bwd_num_parts(rows);
+  const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
+  if ((dgamma || dbeta || dx_colsum) && (g_ln_bwd_impl == 1 || dx_colsum) && cols <= 2048) {
+    const int nacc = dx_colsum ? 3 : 2;
+    RP_LN_DISPATCH(launch_ln_bwd_1pass, x, mean, rstd, gamma, dyb, dres, rows,
+                   static_cast<int>(cols), dx, reinterpret_cast<__nv_bfloat16*>(dx_bf16),
+                   workspace, nacc, s);
+    const int64_t ld = nacc * cols;
+    if (dgamma && dbeta == dgamma + cols) {
+      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
+               static_cast<int>(2 * cols), ld, dgamma, accumulate);
+    } else {
+      if (dgamma)
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
+                 static_cast<int>(cols), ld, dgamma, accumulate);
+      if (dbeta)
+        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols,
+                 nparts, static_cast<int>(cols), ld, dbeta, accumulate);
+    }
+    if (dx_colsum)
+      launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + 2 * cols,
+               nparts, static_cast<int>(cols), ld, dx_colsum, 0);
+    return rp_check_launch("layer_norm_bwd");
+  }
   if (dgamma || dbeta) {  // column partials first (reads x, dy before dx may alias dres)
-    const int64_t nparts = rp_ln_bwd_num_parts(rows);
     dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
     launch_k(ln_bwd_dgb_partial_kernel, grid, dim3(256), 0, s, x, mean, rstd, dyb, rows,
              static_cast<int>(cols), kLnBwdRows, workspace);
-    const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
       launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
                static_cast<int>(2 * cols), 2 * cols, dgamma, accumulate);
@@ -480,8 +516,17 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
   return rp_check_launch("layer_norm_bwd");
 }
 
+extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float* rstd,
+                                 const float* gamma, const uint16_t* dy, const float* dres,
+                                 int64_t rows, int64_t cols, float* dx, uint16_t* dx_bf16,
+                                 float* dgamma, float* dbeta, float* workspace,
+                                 int accumulate, rp_stream_t stream) {
+  return rp_layer_norm_bwd_ex(x, mean, rstd, gamma, dy, dres, rows, cols, dx, dx_bf16, dgamma,
+                              dbeta, nullptr, workspace, accumulate, stream);
+}
+
 extern "C" int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols) {
-  return rp_ln_bwd_num_parts(rows) * 2 * cols;
+  return rp_ln_bwd_num_parts(rows) * 3 * cols;
 }
 
 // column sum of a [rows, cols] matrix: out[c] (+)= sum_r in[r][c]

@@ -74,8 +74,9 @@ def layer_norm_fwd(x, gamma, beta, eps=1e-5, y=None, mean=None, rstd=None, strea
 
 
 def layer_norm_bwd(x, mean, rstd, gamma, dy, dres=None, dx=None, dx_bf16=None, dgamma=None,
-                   dbeta=None, accumulate=False, stream=None):
-    """ref:proj/core/src/ops.cpp:306-345 (+ fused residual cotangent add)."""
+                   dbeta=None, dx_colsum=None, accumulate=False, stream=None):
+    """ref:proj/core/src/ops.cpp:306-345 (+ fused residual cotangent add; optional column sum
+    of the produced dx, the next block's MLP output-bias gradient)."""
     rows, cols = x.numel() // x.shape[-1], x.shape[-1]
     dev = x.device
     if dx is None:
@@ -86,9 +87,10 @@ def layer_norm_bwd(x, mean, rstd, gamma, dy, dres=None, dx=None, dx_bf16=None, d
         dbeta = torch.zeros(cols, dtype=torch.float32, device=dev)
     ws = torch.empty(lib().rp_layer_norm_bwd_workspace_floats(rows, cols), dtype=torch.float32,
                      device=dev)
-    check(lib().rp_layer_norm_bwd(_p(x), _p(mean), _p(rstd), _p(gamma), _p(dy), _p(dres), rows,
-                                  cols, _p(dx), _p(dx_bf16), _p(dgamma), _p(dbeta), _p(ws),
-                                  int(accumulate), _stream(stream)), "layer_norm_vjp")
+    check(lib().rp_layer_norm_bwd_ex(_p(x), _p(mean), _p(rstd), _p(gamma), _p(dy), _p(dres), rows,
+                                     cols, _p(dx), _p(dx_bf16), _p(dgamma), _p(dbeta),
+                                     _p(dx_colsum), _p(ws), int(accumulate), _stream(stream)),
+          "layer_norm_vjp")
     return dx, dgamma, dbeta
 
 

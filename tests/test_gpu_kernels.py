@@ -181,6 +181,20 @@ def test_layer_norm_fwd_bwd(K, rows, cols):
     # bit-reproducible
     dx2, dg2, db2 = K.layer_norm_bwd(x, mean, rstd, gamma, dy, dres=dres)
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+    # fused column sum of the produced cotangent (the next block's output-bias grad)
+    cs = torch.empty(cols, device="cuda")
+    dx3, dg3, db3 = K.layer_norm_bwd(x, mean, rstd, gamma, dy, dres=dres, dx_colsum=cs)
+    assert torch.equal(dx, dx3) and torch.equal(dg, dg3) and torch.equal(db, db3)
+    assert rel(cs, dx_ref.sum(0)) < 1e-4
+    # the two-kernel path (row kernel + column pass) computes the same dx
+    from paper_2306_09342_b200 import _capi
+    _capi.lib().rp_set_ln_bwd_impl(0)
+    try:
+        dx4, dg4, db4 = K.layer_norm_bwd(x, mean, rstd, gamma, dy, dres=dres)
+    finally:
+        _capi.lib().rp_set_ln_bwd_impl(1)
+    assert rel(dx4, dx) < 1e-6
+    assert rel(dg4, dg) < 1e-5 and rel(db4, db) < 1e-5
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
