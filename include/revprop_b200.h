@@ -87,6 +87,9 @@ typedef struct RpGemmDesc {
   float* workspace; /* splits*M*N floats when splits > 1 */
   int max_ctas;     /* 0 = one CTA per SM */
   int bn;           /* tile N: 256 (default) or 128 */
+  float* colsum_part; /* optional (RP_EPI_MUL / RP_EPI_GELU_BWD): column sums of the fp32
+                         epilogue output per 32-row group, [ceil(M/32)][N]; reduce them with
+                         rp_colsum_parts (the MLP hidden-bias gradient, layers.cpp:38-52) */
 } RpGemmDesc;
 
 typedef struct RpGemmPlan RpGemmPlan;
@@ -124,6 +127,9 @@ int rp_set_ln_bwd_impl(int impl);
 int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols);
 int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t cols, float* out,
               float* workspace, int accumulate, rp_stream_t stream);
+/* out[c] (+)= sum_p part[p][c] in a fixed order (second stage of a column sum). */
+int rp_colsum_parts(const float* part, int64_t nparts, int64_t cols, float* out, int accumulate,
+                    rp_stream_t stream);
 int64_t rp_colsum_workspace_floats(int64_t rows, int64_t cols);
 
 /* ------------------------------------------------------------------ attention (head_dim 64)

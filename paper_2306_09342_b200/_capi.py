@@ -65,6 +65,7 @@ class GemmDesc(C.Structure):
         ("bias", C.c_void_p), ("sign", C.c_float),
         ("splits", C.c_int), ("workspace", C.c_void_p),
         ("max_ctas", C.c_int), ("bn", C.c_int),
+        ("colsum_part", C.c_void_p),
     ]
 
 
@@ -89,6 +90,7 @@ _SIGS = {
     "rp_layer_norm_bwd_workspace_floats": (_I64, [_I64, _I64]),
     "rp_colsum": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _P]),
     "rp_colsum_workspace_floats": (_I64, [_I64, _I64]),
+    "rp_colsum_parts": (_I, [_P, _I64, _I64, _P, _I, _P]),
     "rp_attention_fwd": (_I, [_P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "rp_attention_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "rp_attention_bwd_workspace_floats": (_I64, [_I64, _I64, _I64]),

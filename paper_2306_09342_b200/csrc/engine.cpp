@@ -186,6 +186,7 @@ struct GemmArgs {
   float sign = 1.f;
   int splits = 1;
   float* ws = nullptr;
+  float* colsum_part = nullptr;
 };
 
 int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
@@ -210,6 +211,7 @@ int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   d.sign = a.sign;
   d.splits = a.splits;
   d.workspace = a.ws;
+  d.colsum_part = a.colsum_part;
   d.max_ctas = 0;
   d.bn = kGemmBn;
   int rc = rp_gemm_plan_create(&d, out);
@@ -288,6 +290,7 @@ int build_plans(RpEngine* g) {
     {
       GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_MUL, g->du, h};
       a.aux = S.u;
+      a.colsum_part = g->col_ws;        // + per-32-row column sums of d_u (-> db1)
       RP_TRY(mk_plan(g, a, &p.g_dw2));  // d_u = gelu'(u) * (d_o1 . W2^T)
     }
     {
@@ -434,11 +437,13 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   const int64_t T = g->T, d = g->d, h = g->h;
   mark(g, 1, b, 0, s);
   // ---- G = MLP VJP with d_o1 (layers.cpp:241-259)
+  // (the own-b2 column sum runs first: the d_u GEMM below writes its partials to col_ws)
+  if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_dw2, s));
   RP_TRY(launch(p.g_ww2, s));
-  if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_ww1, s));
-  RP_TRY(rp_colsum(g->du, 1, T, h, gr(g, tix_block(b, kB1)), g->col_ws, 0, s));
+  // db1 = colsum(d_u): per-32-row partials come out of the d_u GEMM's epilogue (fp32)
+  RP_TRY(rp_colsum_parts(g->col_ws, (T + 31) / 32, h, gr(g, tix_block(b, kB1)), 0, s));
   RP_TRY(launch(p.g_dw1, s));
   // d_o2t = d_o2 + LN_G^T(d_hG)   (in place in d2 / d2b)
   RP_TRY(rp_layer_norm_bwd(X2(g, b + 1), S.meanG, S.rstdG, wf(g, tix_block(b, kLnGg)), g->dh,
@@ -681,7 +686,8 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
     const int s = pick_splits(mn.first, mn.second, T, kGemmBn);
     if (s > 1) split_ws = std::max<int64_t>(split_ws, s * mn.first * mn.second);
   }
-  const int64_t col_ws = rp_colsum_workspace_floats(T, h > d ? h : d);
+  int64_t col_ws = rp_colsum_workspace_floats(T, h > d ? h : d);
+  if (col_ws < ((T + 31) / 32) * h) col_ws = ((T + 31) / 32) * h;  // d_u epilogue partials
   if ((rc = dalloc(g, &g->d1, T * d)) || (rc = dalloc(g, &g->d2, T * d)) ||
       (rc = dalloc(g, &g->d1b, T * d)) || (rc = dalloc(g, &g->d2b, T * d)) ||
       (rc = dalloc(g, &g->du, T * h)) || (rc = dalloc(g, &g->dh, T * d)) ||

@@ -13,5 +13,7 @@ struct GemmEpi {
   const float* bias;
   float sign;
   int64_t split_stride;
+  float* colsum;  // optional: per-32-row column partials [ceil(M/32)][ldcs] of the fp32 output
+  int64_t ldcs;
 };
 }  // namespace rp

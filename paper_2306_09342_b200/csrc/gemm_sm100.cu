@@ -160,6 +160,37 @@ __device__ __forceinline__ void aux_rows(uint32_t st, int lane, const ChunkIn& i
   for (int c = 0; c < 8; ++c) row[c] = lds128(st + sw32(lane, c));
   __syncwarp();
 }
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// Column sums of a 32-row x 64-column chunk (this lane holds one row, v[64]): the fp32
+// values go through the swizzled staging tile 32 columns at a time, then lane j adds column
+// j down the 32 rows (conflict-free) -> ep.colsum[row0 / 32][col + j], coalesced.
+__device__ __forceinline__ void colsum_chunk64(const GemmEpi& ep, uint32_t st, int lane,
+                                               int64_t row0, int64_t col, const float* v) {
+  float* dst = ep.colsum + (row0 >> 5) * ep.ldcs + col;
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      sts128(st + sw32(lane, c),
+             make_uint4(__float_as_uint(v[32 * hf + 4 * c]), __float_as_uint(v[32 * hf + 4 * c + 1]),
+                        __float_as_uint(v[32 * hf + 4 * c + 2]),
+                        __float_as_uint(v[32 * hf + 4 * c + 3])));
+    __syncwarp();
+    const uint32_t a = st + static_cast<uint32_t>((lane & 3) * 4);
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int r = 0; r < 32; r += 2) {
+      s0 += lds32(a + sw32(r, lane >> 2));
+      s1 += lds32(a + sw32(r + 1, lane >> 2));
+    }
+    __syncwarp();
+    dst[32 * hf + lane] = s0 + s1;
+  }
+}
 // this lane's 64 bf16 values -> staging
 __device__ __forceinline__ void stage_row_bf16x64(uint32_t st, int lane, const float* v) {
 #pragma unroll
@@ -267,6 +298,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
         v[8 * c + 2 * k + 1] *= f.y;
       }
     }
+    if (ep.colsum) colsum_chunk64(ep, st, lane, row0, col, v);
     stage_row_bf16x64(st, lane, v);
     __syncwarp();
     store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
@@ -283,6 +315,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
         v[8 * c + 2 * k + 1] *= gelu_tanh_slope_fast(f.y);
       }
     }
+    if (ep.colsum) colsum_chunk64(ep, st, lane, row0, col, v);
     stage_row_bf16x64(st, lane, v);
     __syncwarp();
     store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
@@ -856,6 +889,12 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   p->ep.bias = d->bias;
   p->ep.sign = d->sign;
   p->ep.split_stride = M * d->ldo;
+  p->ep.colsum = d->colsum_part;
+  p->ep.ldcs = N;
+  if (d->colsum_part && d->epi != RP_EPI_MUL && d->epi != RP_EPI_GELU_BWD) {
+    delete p;
+    return rp_fail(RP_ERR_CONTRACT, "gemm: colsum_part needs the MUL or GELU_BWD epilogue");
+  }
   p->red_out = nullptr;
   p->red_n = 0;
   if (splits > 1) {

@@ -529,6 +529,15 @@ extern "C" int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols
   return rp_ln_bwd_num_parts(rows) * 3 * cols;
 }
 
+extern "C" int rp_colsum_parts(const float* part, int64_t nparts, int64_t cols, float* out,
+                               int accumulate, rp_stream_t stream) {
+  if (nparts <= 0 || cols <= 0) return rp_fail(RP_ERR_SHAPE, "colsum_parts: empty");
+  launch_k(colsum_final_kernel, dim3(static_cast<unsigned>((cols + 31) / 32)),
+           dim3(kFinWarps * 32), 0, static_cast<cudaStream_t>(stream), part, nparts,
+           static_cast<int>(cols), cols, out, accumulate);
+  return rp_check_launch("colsum_parts");
+}
+
 // column sum of a [rows, cols] matrix: out[c] (+)= sum_r in[r][c]
 // (ref:proj/core/src/layers.cpp:38-52 col_sum, used for the MLP bias grads)
 static const int kColRpb = 128;

@@ -32,7 +32,8 @@ def _req(t, dtype, name):
 
 def gemm(A, B, M, N, K, *, a_mn=False, b_mn=False, epi=_capi.RP_EPI_BF16, out=None,
          out2=None, aux=None, bias=None, sign=1.0, splits=1, workspace=None, max_ctas=0,
-         bn=256, lda=None, ldb=None, ldo=None, ldo2=None, ldaux=None, stream=None):
+         bn=256, lda=None, ldb=None, ldo=None, ldo2=None, ldaux=None, colsum_part=None,
+         stream=None):
     """C[M,N] = A.B on the tcgen05 path. A is [M,K] (a_mn=False) or [K,M] (a_mn=True);
     B is [N,K] (b_mn=False) or [K,N] (b_mn=True)."""
     d = GemmDesc()
@@ -54,7 +55,18 @@ def gemm(A, B, M, N, K, *, a_mn=False, b_mn=False, epi=_capi.RP_EPI_BF16, out=No
     d.workspace = workspace.data_ptr() if workspace is not None else None
     d.max_ctas = max_ctas
     d.bn = bn
+    d.colsum_part = colsum_part.data_ptr() if colsum_part is not None else None
     check(lib().rp_gemm(C.byref(d), _stream(stream)), "gemm")
+    return out
+
+
+def colsum_parts(part, out=None, accumulate=False, stream=None):
+    """Second stage of a column sum: out[c] (+)= sum_p part[p][c] (fixed order)."""
+    nparts, cols = part.shape
+    if out is None:
+        out = torch.zeros(cols, dtype=torch.float32, device=part.device)
+    check(lib().rp_colsum_parts(_p(part), nparts, cols, _p(out), int(accumulate),
+                                _stream(stream)), "colsum_parts")
     return out
 
 

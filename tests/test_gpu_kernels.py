@@ -139,8 +139,15 @@ def test_gemm_gelu_slope_then_mul(K, bn):
     dY = torch.randn(M, 512, device="cuda").bfloat16()
     W2 = (0.05 * torch.randn(N, 512, device="cuda")).bfloat16()
     du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    K.gemm(dY, W2, M, N, 512, a_mn=0, b_mn=0, epi=RP_EPI_MUL, out=du, aux=sl, bn=bn)
-    assert rel(du, (dY.float() @ W2.float().t()) * sl.float()) < 1e-2
+    part = torch.empty((M + 31) // 32, N, device="cuda")
+    K.gemm(dY, W2, M, N, 512, a_mn=0, b_mn=0, epi=RP_EPI_MUL, out=du, aux=sl, bn=bn,
+           colsum_part=part)
+    ref = (dY.float() @ W2.float().t()) * sl.float()
+    assert rel(du, ref) < 1e-2
+    # fused column sums of the fp32 product (the MLP hidden-bias gradient)
+    cs = K.colsum_parts(part)
+    assert rel(cs, ref.sum(0)) < 1e-4
+    assert torch.equal(cs, K.colsum_parts(part))
 
 
 @pytest.mark.parametrize("bn", [256, 512])
