@@ -204,6 +204,21 @@ __device__ __forceinline__ GeluParts gelu_parts(float x, float x2) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(1.0f + e));
   return {s, e * s};
 }
+#ifdef RP_GELU_TANH_APPROX  // A/B only: the MUFU.TANH forms (absolute error ~2^-11)
+__device__ __forceinline__ float gelu_tanh_fast(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float t = tanh_fast(c * (x + a * x * x * x));
+  return 0.5f * x * (1.0f + t);
+}
+__device__ __forceinline__ void gelu_and_slope_fast(float x, float& g, float& s) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float x2 = x * x;
+  const float t = tanh_fast(c * x * fmaf(a, x2, 1.0f));
+  const float hx = 0.5f * x;
+  g = fmaf(hx, t, hx);
+  s = fmaf(hx * (c * fmaf(3.0f * a, x2, 1.0f)), fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
+}
+#else
 __device__ __forceinline__ float gelu_tanh_fast(float x) {
   return x * gelu_parts(x, x * x).s;
 }
@@ -217,6 +232,7 @@ __device__ __forceinline__ void gelu_and_slope_fast(float x, float& g, float& sl
   g = x * p.s;
   sl = fmaf(x * (2.0f * c) * fmaf(3.0f * a, x2, 1.0f), p.s * p.om, p.s);
 }
+#endif
 __device__ __forceinline__ float gelu_tanh_slope_fast(float x) {
   float g, sl;
   gelu_and_slope_fast(x, g, sl);
