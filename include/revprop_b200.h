@@ -137,6 +137,8 @@ int64_t rp_colsum_workspace_floats(int64_t rows, int64_t cols);
  * (forward) and :185-208 (VJP). qkv [S*N, 3*H*64] bf16 (q | k | v, head i at column i*64,
  * layers.cpp:144-146), S independent sequences (batch x windows) of N tokens.
  * lse: [S][H][N] fp32 (log2 domain), kept instead of the probability tensor.
+ * N <= 768. tcgen05 kernels: forward N <= 512 (single pass N <= 224, two-pass above),
+ * backward N <= 768 (keys / queries streamed in 64-row chunks); mma.sync forward above 512.
  */
 int rp_attention_fwd(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64_t head_dim,
                      uint16_t* out, float* lse, rp_stream_t stream);
@@ -144,11 +146,8 @@ int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
                      const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
                      uint16_t* dqkv, float* workspace, rp_stream_t stream);
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
-/* 0 (default): tcgen05 kernels where they apply (N <= 256); 1: warp-level mma.sync only */
+/* 0 (default): tcgen05 kernels where they apply; 1: warp-level mma.sync only */
 int rp_set_attention_impl(int impl);
-/* Diagnostics: clock64 timeline of CTA 0 of the tcgen05 attention backward (tools/trace_attn.py);
- * on != 0 arms the trace, out1024 (may be NULL) receives the last one. */
-int rp_attn_trace(int on, long long* out1024);
 
 /* ------------------------------------------------------------------ training engine
  * Isotropic reversible model and its engines:

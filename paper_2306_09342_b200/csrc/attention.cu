@@ -442,10 +442,10 @@ static AttnGeom make_geom(int64_t B, int64_t N, int64_t H) {
 }
 
 static int set_smem_attr(const void* fn, int bytes) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-                 cudaSuccess
-             ? RP_OK
-             : RP_ERR_CUDA;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    return RP_OK;
+  cudaGetLastError();  // not sticky: do not leak it into the next launch check
+  return rp_fail(RP_ERR_SHAPE, "attention: sequence too long for the shared-memory tile");
 }
 
 }  // namespace rp
@@ -455,7 +455,8 @@ using namespace rp;
 static int attn_check(int64_t B, int64_t N, int64_t H, int64_t hd) {
   if (B <= 0 || N <= 0 || H <= 0) return rp_fail(RP_ERR_SHAPE, "attention: empty shape");
   if (hd != kHD) return rp_fail(RP_ERR_SHAPE, "attention: head_dim must be 64");
-  if (N > 1024) return rp_fail(RP_ERR_SHAPE, "attention: sequence (window) longer than 1024");
+  // tcgen05 forward up to 512 keys, mma.sync forward (K and V resident in smem) up to 768
+  if (N > 768) return rp_fail(RP_ERR_SHAPE, "attention: sequence (window) longer than 768");
   return RP_OK;
 }
 
@@ -478,7 +479,7 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
                                 rp_stream_t stream) {
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
-  if (g_attn_impl == 0 && N <= 256) {
+  if (g_attn_impl == 0 && N <= 512) {
     rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, static_cast<cudaStream_t>(stream));
     if (rc != RP_ERR_CONFIG) return rc;
   }
@@ -507,7 +508,7 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   if (rc) return rc;
   const AttnGeom g = make_geom(B, N, H);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (g_attn_impl == 0 && N <= 256) {  // tcgen05 path computes D itself
+  if (g_attn_impl == 0 && N <= 1024) {  // tcgen05 path computes D itself
     rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }

@@ -267,6 +267,257 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 16) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------- long-sequence forward
+// 224 < N <= 512 (the Rev-RoBERTa shape): the key row no longer fits next to its O in one
+// TMEM buffer, so each 128-query tile makes two passes over 128-key blocks:
+//   pass 1   S_j = Q K_j^T, row max only (FMNMX, no exponentials)
+//   pass 2   S_j again, p = exp2(s * scale * log2e - m), row sums, bf16 P packed over the
+//            block's own S columns, O += P V_j (one O accumulator, no rescaling needed)
+// An item is (sequence, head, group of up to kLongGroup query tiles); its K and V (<= 512
+// rows each) are resident in smem for the whole group, Q tiles are double-buffered. Sixteen
+// elementwise warps (TMEM lane quarter w%4, 32-key column quarter w/4 of a block) and one
+// TMA + MMA warp; S is double-buffered in TMEM so the next block's S is computed while the
+// current one is processed.
+constexpr int kLongGroup = 2;
+constexpr int kLongKV = 2 * 512 * 128;  // K | V, up to 512 rows each
+
+struct LongPlan {
+  int nitems, ntile, ngroup;  // items = S * H * ngroup; ntile query tiles per sequence
+  int nkb;                    // 128-key blocks
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_tc_long(const __grid_constant__ CUtensorMap tm_q,
+                     const __grid_constant__ CUtensorMap tm_kv,
+                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse, Geom g,
+                     LongPlan pl) {
+  pdl_trigger();
+
+  __shared__ float red_max[4][128];
+  __shared__ float red_sum[4][128];
+  __shared__ __align__(8) uint64_t bars[14];
+  __shared__ uint32_t tmem_slot;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sK = smem;                       // Nk rows
+  uint8_t* sV = smem + 512 * 128;           // Nk rows
+  uint8_t* sQ = smem + kLongKV;             // [2][128 rows]
+  uint64_t* kv_full = bars;                 // K, V of the item landed
+  uint64_t* kv_free = bars + 1;             // the item's last MMA retired
+  uint64_t* q_full = bars + 2;              // [2]
+  uint64_t* q_free = bars + 4;              // [2] the tile's last S MMA retired
+  uint64_t* bar_s = bars + 6;               // [2] per S buffer
+  uint64_t* bar_p = bars + 8;               // [2] per S buffer: consumed (16 warps)
+  uint64_t* bar_o = bars + 10;              // O of the tile complete
+  uint64_t* bar_e = bars + 11;              // O read out (16 warps)
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Nk = g.Nk, nkb = pl.nkb;
+  if (warp == 16) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_kv);
+      mbar_init(kv_full, 1);
+      mbar_init(kv_free, 1);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&q_full[i], 1);
+        mbar_init(&q_free[i], 1);
+        mbar_init(&bar_s[i], 1);
+        mbar_init(&bar_p[i], 16);
+      }
+      mbar_init(bar_o, 1);
+      mbar_init(bar_e, 16);
+      fence_barrier_init();
+    }
+    tmem_alloc(&tmem_slot, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  const int d = g.H * 64;
+  const int K = pl.nitems > static_cast<int>(blockIdx.x)
+                    ? (pl.nitems - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                          static_cast<int>(gridDim.x)
+                    : 0;
+  auto coords = [&](int k, int& b, int& h, int& t0, int& nt) {
+    const int item = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    const int grp = item % pl.ngroup, bh = item / pl.ngroup;
+    h = bh % g.H;
+    b = bh / g.H;
+    t0 = grp * kLongGroup;
+    nt = min(kLongGroup, pl.ntile - t0);
+  };
+  const uint32_t ocol = tmem + 256u;
+
+  if (warp == 16) {
+    if (lane == 0) {
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      // flat unit sequence: per item, per tile, pass 1 blocks then pass 2 blocks
+      int u = 0, tt = 0;  // unit and global tile counters
+      auto load_q = [&](int k, int t, int slot) {
+        int b, h, t0, nt;
+        coords(k, b, h, t0, nt);
+        mbar_arrive_expect_tx(&q_full[slot], 128 * 128);
+        tma_load_2d(sQ + slot * 16384, &tm_q, &q_full[slot], h * 64, b * g.N + (t0 + t) * 128);
+      };
+      auto load_kv = [&](int k) {
+        int b, h, t0, nt;
+        coords(k, b, h, t0, nt);
+        mbar_arrive_expect_tx(kv_full, 2 * nkb * 128 * 128);
+        for (int j = 0; j < nkb; ++j) {  // 128-row boxes (a TMA box is at most 256 rows)
+          tma_load_2d(sK + j * 16384, &tm_kv, kv_full, d + h * 64, b * g.N + 128 * j);
+          tma_load_2d(sV + j * 16384, &tm_kv, kv_full, 2 * d + h * 64, b * g.N + 128 * j);
+        }
+      };
+      if (K > 0) {
+        load_kv(0);
+        load_q(0, 0, 0);
+      }
+      for (int k = 0; k < K; ++k) {
+        int b, h, t0, nt;
+        coords(k, b, h, t0, nt);
+        if (k > 0) {
+          mbar_wait(kv_free, (k - 1) & 1);  // every MMA of item k-1 retired
+          load_kv(k);
+        }
+        mbar_wait(kv_full, k & 1);
+        for (int t = 0; t < nt; ++t, ++tt) {
+          // next tile's Q (this item's next tile or the next item's first one)
+          {
+            int nk = k, ntl = t + 1;
+            if (ntl >= nt) { nk = k + 1; ntl = 0; }
+            if (nk < K) {
+              if (tt >= 1) mbar_wait(&q_free[(tt + 1) & 1], ((tt - 1) >> 1) & 1);
+              load_q(nk, ntl, (tt + 1) & 1);
+            }
+          }
+          mbar_wait(&q_full[tt & 1], (tt >> 1) & 1);
+          const uint32_t aq = smem_u32(sQ + (tt & 1) * 16384);
+          for (int ps = 0; ps < 2; ++ps) {
+            for (int j = 0; j < nkb; ++j, ++u) {
+              const int w = min(128, Nk - 128 * j);
+              if (u >= 2) mbar_wait(&bar_p[u & 1], ((u - 2) >> 1) & 1);  // buffer consumed
+              tc_fence_after();
+              const uint32_t sb = tmem + static_cast<uint32_t>((u & 1) * 128);
+              const uint32_t bk = smem_u32(sK) + static_cast<uint32_t>(128 * j * 128);
+              const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(w), false, false);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(sb, make_sdesc_sw128(aq + kk * 32, 16, 1024),
+                          make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+              umma_commit(&bar_s[u & 1]);
+              if (ps == 1 && j == nkb - 1) umma_commit(&q_free[tt & 1]);
+              if (ps == 1) {
+                if (j == 0 && tt > 0) mbar_wait(bar_e, (tt - 1) & 1);  // previous O read out
+                mbar_wait(&bar_p[u & 1], (u >> 1) & 1);
+                tc_fence_after();
+                const uint32_t bv = smem_u32(sV) + static_cast<uint32_t>(128 * j * 128);
+                for (int ks = 0; ks < w / 16; ++ks)
+                  umma_ts_bf16(ocol, sb + static_cast<uint32_t>((ks >> 1) * 32 + (ks & 1) * 8),
+                               make_sdesc_sw128(bv + ks * 2048, 8192, 1024), idesc_o,
+                               (j > 0 || ks > 0) ? 1u : 0u);
+                if (j == nkb - 1) umma_commit(bar_o);
+              }
+            }
+          }
+        }
+        umma_commit(kv_free);
+      }
+    }
+  } else {
+    const int q = static_cast<int>(warp & 3u), cq = static_cast<int>(warp >> 2);
+    const uint32_t lq = (static_cast<uint32_t>(q) * 32u) << 16;
+    const int rloc = q * 32 + static_cast<int>(lane);
+    int u = 0, tt = 0;
+    for (int k = 0; k < K; ++k) {
+      int b, h, t0, nt;
+      coords(k, b, h, t0, nt);
+      for (int t = 0; t < nt; ++t, ++tt) {
+        const int tile = t0 + t;
+        const bool active = tile * 128 + q * 32 < g.N;
+        float mx = -INFINITY;
+        for (int j = 0; j < nkb; ++j, ++u) {  // ---- pass 1: row max
+          const int c0 = 128 * j + 32 * cq;
+          mbar_wait(&bar_s[u & 1], (u >> 1) & 1);
+          tc_fence_after();
+          if (active && c0 < Nk) {
+            float v[32];
+            tmem_ld32(tmem + static_cast<uint32_t>((u & 1) * 128 + 32 * cq) + lq, v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c0 + e < g.N) mx = fmaxf(mx, v[e]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_p[u & 1]);
+        }
+        red_max[cq][rloc] = mx;
+        named_bar(1, 512);
+        const float ms =
+            fmaxf(fmaxf(red_max[0][rloc], red_max[1][rloc]), fmaxf(red_max[2][rloc], red_max[3][rloc])) *
+            g.scale_log2;
+        float l = 0.f;
+        for (int j = 0; j < nkb; ++j, ++u) {  // ---- pass 2: exp, sums, P
+          const int c0 = 128 * j + 32 * cq;
+          mbar_wait(&bar_s[u & 1], (u >> 1) & 1);
+          tc_fence_after();
+          if (active && c0 < Nk) {
+            const uint32_t sb = tmem + static_cast<uint32_t>((u & 1) * 128 + 32 * cq) + lq;
+            float v[32];
+            tmem_ld32(sb, v);
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int key = c0 + 2 * e;
+              const float p0 = key < g.N ? ex2(fmaf(v[2 * e], g.scale_log2, -ms)) : 0.f;
+              const float p1 = key + 1 < g.N ? ex2(fmaf(v[2 * e + 1], g.scale_log2, -ms)) : 0.f;
+              l += p0 + p1;
+              pk[e] = pack_bf16x2(p0, p1);
+            }
+            tmem_st8(sb, pk);          // P over this warp's own, already-read S columns
+            tmem_st8(sb + 8, pk + 8);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_p[u & 1]);
+        }
+        red_sum[cq][rloc] = l;
+        named_bar(1, 512);
+        const float lt = (red_sum[0][rloc] + red_sum[1][rloc]) + (red_sum[2][rloc] + red_sum[3][rloc]);
+        // ---- epilogue: O / l (16 of the 64 head columns per warp), LSE
+        mbar_wait(bar_o, tt & 1);
+        tc_fence_after();
+        float o[16];
+        if (active) tmem_ld16(ocol + lq + static_cast<uint32_t>(cq * 16), o);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_e);
+        const int row = tile * 128 + rloc;
+        if (row < g.N) {
+          const float inv = 1.0f / lt;
+          uint4* dst = reinterpret_cast<uint4*>(
+              out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * 64 + cq * 16);
+          dst[0] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
+                              pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+          dst[1] = make_uint4(pack_bf16x2(o[8] * inv, o[9] * inv),
+                              pack_bf16x2(o[10] * inv, o[11] * inv),
+                              pack_bf16x2(o[12] * inv, o[13] * inv),
+                              pack_bf16x2(o[14] * inv, o[15] * inv));
+          if (cq == 0) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = ms + log2f(lt);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 16) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace attn_tc
 }  // namespace rp
 
@@ -277,7 +528,7 @@ using namespace rp;
 int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, uint16_t* out,
                         float* lse, cudaStream_t stream) {
   using namespace attn_tc;
-  if (N > 256 || N < 1) return RP_ERR_CONFIG;
+  if (N > 512 || N < 1) return RP_ERR_CONFIG;
   Geom g;
   g.B = static_cast<int>(S);
   g.N = static_cast<int>(N);
@@ -287,6 +538,28 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   g.scale_log2 = (1.0f / 8.0f) * 1.4426950408889634f;
   const int64_t T = S * N, cols = 3 * H * 64;
   CUtensorMap mq, mkv;
+  if (g.Nk > 224) {  // two-pass kernel with K / V resident per (sequence, head) group
+    if (make_map(&mq, qkv, T, cols, 128))
+      return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
+    const int smem = 1024 + kLongKV + 2 * 16384;
+    static std::once_flag once_l;
+    static int nsm_l = 148;
+    std::call_once(once_l, [smem] {
+      cudaFuncSetAttribute(attn_fwd_tc_long, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm_l, cudaDevAttrMultiProcessorCount, dev);
+    });
+    LongPlan pl;
+    pl.ntile = static_cast<int>((N + 127) / 128);
+    pl.ngroup = (pl.ntile + kLongGroup - 1) / kLongGroup;
+    pl.nitems = static_cast<int>(S * H) * pl.ngroup;
+    pl.nkb = static_cast<int>((N + 127) / 128);
+    const unsigned grid = static_cast<unsigned>(pl.nitems < nsm_l ? pl.nitems : nsm_l);
+    launch_k(attn_fwd_tc_long, dim3(grid), dim3(kFwdThreads), smem, stream, mq, mq,
+             reinterpret_cast<__nv_bfloat16*>(out), lse, g, pl);
+    return rp_check_launch("attention_fwd_tc_long");
+  }
   if (make_map(&mq, qkv, T, cols, 128) || make_map(&mkv, qkv, T, cols, static_cast<uint32_t>(g.Nk)))
     return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
   const int smem = 1024 + 2 * kFwdBuf;

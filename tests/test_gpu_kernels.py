@@ -221,7 +221,7 @@ def attn_ref(qkv, B, N, H, hd=64):
 
 
 @pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
-@pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3),
+@pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3), (2, 300, 2), (1, 480, 3), (3, 768, 1),
                                    (3, 256, 2), (2, 129, 1)])
 def test_attention_fwd_bwd(K, B, N, H, impl):
     from paper_2306_09342_b200 import _capi
