@@ -283,6 +283,12 @@ def main_ours(a, rank, world, local_rank):
     pk = peaks()
     gms, gflops, glaunch = eng.gemm_profile(REPROP)  # kernels serialised: clean durations
     ach = gflops / (gms / 1e3) / 1e12
+    traffic = None  # DRAM bytes per GEMM launch, from the committed ncu capture (profiles/)
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1_gemm_traffic_v5.json")) as f:
+            traffic = json.load(f)["avg_dram_bytes_per_launch"]
+    except Exception:
+        pass
     mf, hf = model_flops_per_img(dict(p, in_dim=cfg.in_dim, num_classes=cfg.num_classes))
     per_gpu = img_p / world
     launches = eng.graph_kernels(PAREPROP)
@@ -317,7 +323,9 @@ def main_ours(a, rank, world, local_rank):
                          "achieved": ach, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                          "frac": ach / pk["bf16_sustained"],
                          "peak_note": f"{pk['source']} sustained bf16 (kernel timed inside a step)",
-                         "launches_per_step": glaunch, "traffic": None},
+                         "launches_per_step": glaunch, "traffic": traffic,
+                         "traffic_note": "avg dram__bytes_read+write per GEMM launch, ncu, "
+                                         "profiles/round1_gemm_traffic_v5.json"},
             "gpu_launches": launches * a.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
