@@ -474,8 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = c_begin; c < c_end; c += CW) {
         float v[CW];
-        tmem_ld32(tbase + c, v);
-        if constexpr (CW == 64) tmem_ld32(tbase + c + 32, v + 32);
+        if constexpr (CW == 64)
+          tmem_ld64(tbase + c, v);
+        else
+          tmem_ld32(tbase + c, v);
         const ChunkIn cur = nxt;
         if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
           prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
@@ -673,8 +675,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = c_begin; c < c_end; c += CW) {
         float v[CW];
-        tmem_ld32(tbase + c, v);
-        if constexpr (CW == 64) tmem_ld32(tbase + c + 32, v + 32);
+        if constexpr (CW == 64)
+          tmem_ld64(tbase + c, v);
+        else
+          tmem_ld32(tbase + c, v);
         const ChunkIn cur = nxt;
         if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
           prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
