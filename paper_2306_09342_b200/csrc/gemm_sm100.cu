@@ -165,31 +165,28 @@ __device__ __forceinline__ float lds32(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
   return v;
 }
-// Column sums of a 32-row x 64-column chunk (this lane holds one row, v[64]): the fp32
-// values go through the swizzled staging tile 32 columns at a time, then lane j adds column
-// j down the 32 rows (conflict-free) -> ep.colsum[row0 / 32][col + j], coalesced.
-__device__ __forceinline__ void colsum_chunk64(const GemmEpi& ep, uint32_t st, int lane,
+// Column sums of a 32-row x 64-column chunk (this lane holds one row, v[64]) by a
+// register butterfly (reduce-scatter over the 32 lanes: 5 rounds of shfl.xor, halving the
+// live columns each round), so no shared-memory traffic competes with the tensor core's
+// operand reads. Afterwards lane j holds the sums of columns 2j and 2j+1 ->
+// ep.colsum[row0 / 32][col + 2j .. +1]. Fixed association order (deterministic).
+__device__ __forceinline__ void colsum_chunk64(const GemmEpi& ep, uint32_t /*st*/, int lane,
                                                int64_t row0, int64_t col, const float* v) {
-  float* dst = ep.colsum + (row0 >> 5) * ep.ldcs + col;
+  float a[64];
 #pragma unroll
-  for (int hf = 0; hf < 2; ++hf) {
+  for (int i = 0; i < 64; ++i) a[i] = v[i];
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      sts128(st + sw32(lane, c),
-             make_uint4(__float_as_uint(v[32 * hf + 4 * c]), __float_as_uint(v[32 * hf + 4 * c + 1]),
-                        __float_as_uint(v[32 * hf + 4 * c + 2]),
-                        __float_as_uint(v[32 * hf + 4 * c + 3])));
-    __syncwarp();
-    const uint32_t a = st + static_cast<uint32_t>((lane & 3) * 4);
-    float s0 = 0.f, s1 = 0.f;
+  for (int k = 16, n = 64; k >= 1; k >>= 1, n >>= 1) {
+    const bool up = (lane & k) != 0;  // keep the upper half of the live columns
 #pragma unroll
-    for (int r = 0; r < 32; r += 2) {
-      s0 += lds32(a + sw32(r, lane >> 2));
-      s1 += lds32(a + sw32(r + 1, lane >> 2));
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? a[i] : a[i + n / 2];
+      const float keep = up ? a[i + n / 2] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
     }
-    __syncwarp();
-    dst[32 * hf + lane] = s0 + s1;
   }
+  float2* dst = reinterpret_cast<float2*>(ep.colsum + (row0 >> 5) * ep.ldcs + col) + lane;
+  *dst = make_float2(a[0], a[1]);
 }
 // this lane's 64 bf16 values -> staging
 __device__ __forceinline__ void stage_row_bf16x64(uint32_t st, int lane, const float* v) {
