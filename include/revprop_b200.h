@@ -189,6 +189,14 @@ int rp_engine_set_batch(RpEngine* engine, const uint16_t* host_inputs_bf16,
                         const int32_t* host_labels);
 int rp_engine_set_batch_device(RpEngine* engine, const uint16_t* inputs_bf16,
                                const int32_t* labels);
+/* Pipelined input: H2D copy of the next step's batch on a copy stream, overlapping the
+ * current step; the next rp_engine_step consumes it. Host buffers pinned, valid until then. */
+int rp_engine_prefetch_batch(RpEngine* engine, const uint16_t* host_inputs_bf16,
+                             const int32_t* host_labels);
+/* Asynchronous D2H of the last enqueued step's loss into pinned `loss`; rp_engine_wait_loss
+ * blocks until it has landed. */
+int rp_engine_read_loss_async(RpEngine* engine, float* loss);
+int rp_engine_wait_loss(RpEngine* engine);
 int rp_engine_set_lr(RpEngine* engine, float lr);
 int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
 int rp_engine_invalidate_graphs(RpEngine* engine);

@@ -86,6 +86,12 @@ struct RpEngine {
   std::vector<int64_t> t_off, t_numel;  // flat tensor table
   int dev = 0;
   cudaStream_t sG = nullptr, sR = nullptr, sC = nullptr;
+  // input pipelining (rp_engine_prefetch_batch): copy stream, staging buffers, events
+  cudaStream_t sX = nullptr;
+  uint16_t* in_stage = nullptr;
+  int32_t* lab_stage = nullptr;
+  cudaEvent_t evStaged = nullptr, evStageFree = nullptr, evLoss = nullptr;
+  bool staged = false;
   std::vector<cudaEvent_t> evR, evG;
   cudaEvent_t evFwd = nullptr, evCommDone = nullptr, evRDone = nullptr, evEmbed = nullptr;
   std::vector<cudaEvent_t> ts;  // timing events for the slot log (eager, instrumented)
@@ -742,8 +748,10 @@ extern "C" void rp_engine_destroy(RpEngine* g) {
       if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed})
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {g->sG, g->sR, g->sC})
+  for (cudaStream_t s : {g->sG, g->sR, g->sC, g->sX})
     if (s) cudaStreamDestroy(s);
+  for (cudaEvent_t e : {g->evStaged, g->evStageFree, g->evLoss})
+    if (e) cudaEventDestroy(e);
   if (g->comm) ncclCommDestroy(g->comm);
   delete g;
 }
@@ -831,6 +839,48 @@ extern "C" int rp_engine_set_batch(RpEngine* g, const uint16_t* inputs, const in
                  "set_batch labels");
 }
 
+// Pipelined input: the host -> device copy of the NEXT step's batch runs on a copy stream
+// while the current step computes; the next rp_engine_step waits for it and moves it into
+// the step's input buffers (a device-to-device copy on the engine stream, outside the
+// captured graph). Host buffers should be pinned and stay valid until that step starts.
+extern "C" int rp_engine_prefetch_batch(RpEngine* g, const uint16_t* inputs, const int32_t* labels) {
+  if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  if (!g->sX) {
+    RP_TRY(cuda_ok(cudaStreamCreateWithFlags(&g->sX, cudaStreamNonBlocking), "stream"));
+    for (cudaEvent_t* e : {&g->evStaged, &g->evStageFree, &g->evLoss})
+      RP_TRY(cuda_ok(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event"));
+    RP_TRY(dalloc(g, &g->in_stage, g->T * g->in));
+    RP_TRY(dalloc(g, &g->lab_stage, g->B));
+  }
+  // the staging buffers are free once the previous staged batch has been moved out
+  RP_TRY(cuda_ok(cudaStreamWaitEvent(g->sX, g->evStageFree, 0), "wait"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->in_stage, inputs, static_cast<size_t>(g->T * g->in) * 2,
+                                 cudaMemcpyHostToDevice, g->sX),
+                 "prefetch inputs"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->lab_stage, labels, static_cast<size_t>(g->B) * 4,
+                                 cudaMemcpyHostToDevice, g->sX),
+                 "prefetch labels"));
+  RP_TRY(cuda_ok(cudaEventRecord(g->evStaged, g->sX), "record"));
+  g->staged = true;
+  return RP_OK;
+}
+
+// Asynchronous loss read-back: device -> host copy of the last enqueued step's loss into
+// `loss` (pinned) on the engine stream; rp_engine_wait_loss blocks until it has landed.
+extern "C" int rp_engine_read_loss_async(RpEngine* g, float* loss) {
+  if (!g || !loss) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  if (!g->evLoss) RP_TRY(cuda_ok(cudaEventCreateWithFlags(&g->evLoss, cudaEventDisableTiming), "event"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(loss, g->loss, sizeof(float), cudaMemcpyDeviceToHost, g->sG),
+                 "read_loss_async"));
+  return cuda_ok(cudaEventRecord(g->evLoss, g->sG), "record");
+}
+
+extern "C" int rp_engine_wait_loss(RpEngine* g) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  if (!g->evLoss) return RP_OK;
+  return cuda_ok(cudaEventSynchronize(g->evLoss), "wait_loss");
+}
+
 extern "C" int rp_engine_set_batch_device(RpEngine* g, const uint16_t* inputs,
                                           const int32_t* labels) {
   if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
@@ -914,6 +964,17 @@ extern "C" int rp_engine_step(RpEngine* g, int mode, int use_graph) {
   if (mode == 0 && !g->vanilla_ready)
     return rp_fail(RP_ERR_CONTRACT, "step: vanilla mode needs rp_engine_enable_vanilla()");
   set_partition(g, mode);
+  if (g->staged) {  // the batch prefetched by rp_engine_prefetch_batch becomes this step's
+    RP_TRY(cuda_ok(cudaStreamWaitEvent(g->sG, g->evStaged, 0), "wait staged batch"));
+    RP_TRY(cuda_ok(cudaMemcpyAsync(g->inputs, g->in_stage, static_cast<size_t>(g->T * g->in) * 2,
+                                   cudaMemcpyDeviceToDevice, g->sG),
+                   "stage -> inputs"));
+    RP_TRY(cuda_ok(cudaMemcpyAsync(g->labels, g->lab_stage, static_cast<size_t>(g->B) * 4,
+                                   cudaMemcpyDeviceToDevice, g->sG),
+                   "stage -> labels"));
+    RP_TRY(cuda_ok(cudaEventRecord(g->evStageFree, g->sG), "record"));
+    g->staged = false;
+  }
   if (!use_graph || g->instrument) return enqueue_step(g, mode);
   if (!g->graph[mode]) {
     cudaGraph_t graph = nullptr;

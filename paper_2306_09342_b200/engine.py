@@ -80,6 +80,9 @@ _API = {
     "rp_engine_get_params": (_I, [_P, _P]),
     "rp_engine_get_grads": (_I, [_P, _P]),
     "rp_engine_set_batch": (_I, [_P, _P, _P]),
+    "rp_engine_prefetch_batch": (_I, [_P, _P, _P]),
+    "rp_engine_read_loss_async": (_I, [_P, _P]),
+    "rp_engine_wait_loss": (_I, [_P]),
     "rp_engine_set_batch_device": (_I, [_P, _P, _P]),
     "rp_engine_set_lr": (_I, [_P, C.c_float]),
     "rp_engine_set_partition": (_I, [_P, _I, _I]),
@@ -188,6 +191,19 @@ class Engine:
         """Async H2D from caller-owned (pinned) host memory."""
         check(api("rp_engine_set_batch")(self._h, C.c_void_p(inputs_ptr), C.c_void_p(labels_ptr)),
               "set_batch")
+
+    def prefetch_batch(self, inputs_ptr: int, labels_ptr: int):
+        """Start the host -> device copy of the next step's batch (pinned host pointers);
+        it overlaps the current step and is consumed by the next step()."""
+        check(api("rp_engine_prefetch_batch")(self._h, C.c_void_p(inputs_ptr),
+                                                C.c_void_p(labels_ptr)), "prefetch_batch")
+
+    def read_loss_async(self, loss_ptr: int):
+        """Device -> host copy of the last enqueued step's loss into pinned memory."""
+        check(api("rp_engine_read_loss_async")(self._h, C.c_void_p(loss_ptr)), "read_loss_async")
+
+    def wait_loss(self):
+        check(api("rp_engine_wait_loss")(self._h), "wait_loss")
 
     def set_batch_device(self, inputs_ptr: int, labels_ptr: int):
         check(api("rp_engine_set_batch_device")(self._h, C.c_void_p(inputs_ptr),

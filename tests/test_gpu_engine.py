@@ -287,3 +287,27 @@ def test_two_class_sequence_head():
         off += n
     assert l2rel(g, r.grads) < TOL_L2
     eng.close()
+
+
+def test_prefetched_batch_matches_set_batch():
+    """rp_engine_prefetch_batch (copy stream, staged, consumed by the next step) trains on
+    exactly the same batch as rp_engine_set_batch; the async loss read-back matches."""
+    from paper_2306_09342_b200.engine import PAREPROP, bf16_bits
+    eng, mc, p32, pref = make(TI, batch=4)
+    x, lab = O.synthetic_batch(mc, 4, seed=5)
+    xb = bf16_bits(x)
+    eng.set_lr(0.0)
+    eng.set_batch(xb, lab)
+    eng.step(PAREPROP, graph=True)
+    g_ref, l_ref = eng.grads().copy(), eng.loss()
+    eng.set_batch(bf16_bits(np.zeros_like(x)), np.zeros_like(lab))  # clobber the inputs
+    h_in = torch.from_numpy(xb.view(np.int16).reshape(-1).copy()).pin_memory()
+    h_lab = torch.from_numpy(np.asarray(lab, np.int32)).pin_memory()
+    h_loss = torch.empty(1, dtype=torch.float32).pin_memory()
+    eng.prefetch_batch(h_in.data_ptr(), h_lab.data_ptr())
+    eng.step(PAREPROP, graph=True)
+    eng.read_loss_async(h_loss.data_ptr())
+    eng.wait_loss()
+    assert np.array_equal(eng.grads(), g_ref)
+    assert float(h_loss[0]) == l_ref
+    eng.close()
