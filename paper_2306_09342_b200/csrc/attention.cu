@@ -1,4 +1,5 @@
-// Fused multi-head self-attention forward / backward, head_dim 64.
+// Fused multi-head self-attention forward / backward on warp-level mma.sync, any head_dim
+// that is a multiple of 8 up to 128 (tiles padded to HDP = 64 or 128 columns, zero-filled).
 //
 // Replaces the per-(batch, head, window) loop of ref:proj/core/src/layers.cpp:150-166
 // (gather_block x3, matmul_nt, scale, row_softmax, probs_store, matmul, scatter_block)
@@ -25,12 +26,13 @@
 
 namespace rp {
 
-constexpr int kHD = 64;          // head dim
 constexpr int kTile = 64;        // query / key rows per CTA tile
-constexpr int kRowBytes = kHD * 2;
 
+// smem tiles hold HDP bf16 per row (HDP = padded head dim, 64 or 128): 16-byte chunk c of
+// row r at r*2*HDP + (c with its low 3 bits XOR r&7) -> ldmatrix is bank-conflict free
+template <int HDP>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
-  return static_cast<uint32_t>(r * kRowBytes + ((c ^ (r & 7)) << 4));
+  return static_cast<uint32_t>(r * HDP * 2 + (((c & ~7) | ((c ^ r) & 7)) << 4));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
@@ -41,15 +43,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-// Copy `rows` rows of one head (64 bf16) into a swizzled smem tile; rows >= valid are zero.
+// Copy `rows` rows of one head (hd bf16) into a swizzled smem tile of HDP columns; rows >=
+// valid and columns >= hd are zero.
+template <int HDP>
 __device__ __forceinline__ void load_rows(uint8_t* s, const __nv_bfloat16* g, int64_t ld, int rows,
-                                          int valid) {
+                                          int valid, int hd) {
   const uint32_t sb = smem_u32(s);
-  for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) {
-    const int r = i >> 3, c = i & 7;
-    const bool ok = r < valid;
+  constexpr int CH = HDP / 8;
+  for (int i = threadIdx.x; i < rows * CH; i += blockDim.x) {
+    const int r = i / CH, c = i % CH;
+    const bool ok = r < valid && c * 8 < hd;
     const __nv_bfloat16* src = ok ? g + static_cast<int64_t>(r) * ld + c * 8 : g;
-    cp_async16(sb + swz(r, c), src, ok ? 16 : 0);
+    cp_async16(sb + swz<HDP>(r, c), src, ok ? 16 : 0);
   }
 }
 
@@ -72,43 +77,48 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
 }
 
 // A fragment (16 rows x 16 k) from a row-major swizzled tile: rows r0.., k-chunk pair kc.
+template <int HDP>
 __device__ __forceinline__ void load_a(uint32_t base, int r0, int kc, uint32_t* a) {
   const int l = threadIdx.x & 31;
-  ldsm_x4(base + swz(r0 + (l & 15), kc + (l >> 4)), a);
+  ldsm_x4(base + swz<HDP>(r0 + (l & 15), kc + (l >> 4)), a);
 }
 // B fragments for two n8 tiles (n0..n0+15) x k16 from a tile stored [n][k] (no transpose).
+template <int HDP>
 __device__ __forceinline__ void load_b_nk(uint32_t base, int n0, int kc, uint32_t* b) {
   const int l = threadIdx.x & 31;
-  ldsm_x4(base + swz(n0 + (l & 7) + ((l >> 4) << 3), kc + ((l >> 3) & 1)), b);
+  ldsm_x4(base + swz<HDP>(n0 + (l & 7) + ((l >> 4) << 3), kc + ((l >> 3) & 1)), b);
 }
 // B fragments for two n8 tiles (column chunks nc, nc+1) x k16 (rows k0..) from [k][n].
+template <int HDP>
 __device__ __forceinline__ void load_b_kn(uint32_t base, int k0, int nc, uint32_t* b) {
   const int l = threadIdx.x & 31;
-  ldsm_x4_t(base + swz(k0 + (l & 15), nc + (l >> 4)), b);
+  ldsm_x4_t(base + swz<HDP>(k0 + (l & 15), nc + (l >> 4)), b);
 }
 
-// S(16 x 64) = A(16 x 64, regs) . B^T where B tile [64 n][64 k] in smem rows nb..nb+63;
+// S(16 x 64) = A(16 x HDP, regs) . B^T where B tile [64 n][HDP k] in smem rows nb..nb+63;
 // n16 blocks at or beyond `valid` rows of B are skipped (their S entries stay 0 and are
 // masked by the caller).
+template <int HDP>
 __device__ __forceinline__ void mm_abt(const uint32_t (*a)[4], uint32_t bbase, int nb,
                                        float (*s)[4], int valid = 64) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < HDP / 16; ++ks) {
 #pragma unroll
     for (int np = 0; np < 4; ++np) {
       if (16 * np >= valid) break;
       uint32_t b[4];
-      load_b_nk(bbase, nb + 16 * np, 2 * ks, b);
+      load_b_nk<HDP>(bbase, nb + 16 * np, 2 * ks, b);
       mma16816(s[2 * np], a[ks], b[0], b[1]);
       mma16816(s[2 * np + 1], a[ks], b[2], b[3]);
     }
   }
 }
 
-// acc(16 x 64) += P(16 x 64 k, C-fragment layout) . B where B tile [64 k][64 n] rows kb..;
+// acc(16 x HDP) += P(16 x 64 k, C-fragment layout) . B where B tile [64 k][HDP n] rows kb..;
 // k16 steps at or beyond `valid` are skipped (P is zero there).
+template <int HDP>
 __device__ __forceinline__ void mm_pb(const float (*p)[4], uint32_t bbase, int kb,
                                       float (*acc)[4], int valid = 64) {
 #pragma unroll
@@ -120,9 +130,9 @@ __device__ __forceinline__ void mm_pb(const float (*p)[4], uint32_t bbase, int k
     a[2] = pack_bf16x2(p[2 * ks + 1][0], p[2 * ks + 1][1]);
     a[3] = pack_bf16x2(p[2 * ks + 1][2], p[2 * ks + 1][3]);
 #pragma unroll
-    for (int np = 0; np < 4; ++np) {
+    for (int np = 0; np < HDP / 16; ++np) {
       uint32_t b[4];
-      load_b_kn(bbase, kb + 16 * ks, 2 * np, b);
+      load_b_kn<HDP>(bbase, kb + 16 * ks, 2 * np, b);
       mma16816(acc[2 * np], a, b[0], b[1]);
       mma16816(acc[2 * np + 1], a, b[2], b[3]);
     }
@@ -131,18 +141,26 @@ __device__ __forceinline__ void mm_pb(const float (*p)[4], uint32_t bbase, int k
 
 struct AttnGeom {
   int B, N, H;        // sequences, tokens per sequence, heads
-  int64_t ld_qkv;     // row pitch of qkv / d_qkv (3*H*64)
-  int64_t ld_o;       // row pitch of out / d_out (H*64)
+  int hd;             // head dim (multiple of 8, <= the kernel's HDP)
+  int64_t ld_qkv;     // row pitch of qkv / d_qkv (3*H*hd)
+  int64_t ld_o;       // row pitch of out / d_out (H*hd)
   float scale;        // 1/sqrt(hd)
   float scale_log2;   // scale * log2(e)
 };
 
+// bf16 pair store of a C-fragment column pair, only inside the real head columns
+__device__ __forceinline__ void store_pair(__nv_bfloat16* row, int col, int hd, float a, float b) {
+  if (col < hd) *reinterpret_cast<uint32_t*>(row + col) = pack_bf16x2(a, b);
+}
+
 // ------------------------------------------------------------------------ forward
 // grid (ceil(N/64), H, B); block 128 (4 warps x 16 query rows)
 // smem: Q tile [64][64] | K [Npad][64] | V [Npad][64]
+template <int HDP>
 __global__ void __launch_bounds__(128)
     attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, AttnGeom g) {
+  constexpr int kRowBytes = HDP * 2;
   pdl_trigger();
   pdl_wait();
 
@@ -152,10 +170,11 @@ __global__ void __launch_bounds__(128)
   uint8_t* sK = sQ + kTile * kRowBytes;
   uint8_t* sV = sK + npad * kRowBytes;
   const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
-  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
-  load_rows(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0);
-  load_rows(sK, base + g.H * kHD, g.ld_qkv, npad, g.N);
-  load_rows(sV, base + 2 * g.H * kHD, g.ld_qkv, npad, g.N);
+  const int hd = g.hd;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
+  load_rows<HDP>(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0, hd);
+  load_rows<HDP>(sK, base + g.H * hd, g.ld_qkv, npad, g.N, hd);
+  load_rows<HDP>(sV, base + 2 * g.H * hd, g.ld_qkv, npad, g.N, hd);
   cp_async_wait_all();
   __syncthreads();
 
@@ -163,19 +182,19 @@ __global__ void __launch_bounds__(128)
   if (q0 + warp * 16 >= g.N) return;  // all 16 rows are padding (no block syncs follow)
   const int gq = lane >> 2, tq = lane & 3;
   const uint32_t bQ = smem_u32(sQ), bK = smem_u32(sK), bV = smem_u32(sV);
-  uint32_t qa[4][4];
+  uint32_t qa[HDP / 16][4];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) load_a(bQ, warp * 16, 2 * ks, qa[ks]);
+  for (int ks = 0; ks < HDP / 16; ++ks) load_a<HDP>(bQ, warp * 16, 2 * ks, qa[ks]);
 
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-  float o[8][4];
+  float o[HDP / 8][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  for (int i = 0; i < HDP / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
   for (int kt = 0; kt < npad; kt += kTile) {
     float s[8][4];
     const int valid = g.N - kt;
-    mm_abt(qa, bK, kt, s, valid);
+    mm_abt<HDP>(qa, bK, kt, s, valid);
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
@@ -204,10 +223,13 @@ __global__ void __launch_bounds__(128)
         const float p = exp2f(s[nt][e] - m[e >> 1]);
         s[nt][e] = p;
         l[e >> 1] += p;
-        o[nt][e] *= corr[e >> 1];
       }
     }
-    mm_pb(s, bV, kt, o, valid);
+#pragma unroll
+    for (int nt = 0; nt < HDP / 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[nt][e] *= corr[e >> 1];
+    mm_pb<HDP>(s, bV, kt, o, valid);
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -220,11 +242,10 @@ __global__ void __launch_bounds__(128)
     const int row = rowa + 8 * r;
     if (row < g.N) {
       const float inv = 1.0f / l[r];
-      __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * kHD;
+      __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * hd;
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-        *reinterpret_cast<uint32_t*>(orow + nt * 8 + 2 * tq) =
-            pack_bf16x2(o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
+      for (int nt = 0; nt < HDP / 8; ++nt)
+        store_pair(orow, nt * 8 + 2 * tq, hd, o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
       if (tq == 0)
         lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = m[r] + log2f(l[r]);
     }
@@ -243,11 +264,10 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out,
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int h = static_cast<int>(i % g.H);
     const int64_t row = i / g.H;  // b*N + n
-    const uint4* o = reinterpret_cast<const uint4*>(out + row * g.ld_o + h * kHD);
-    const uint4* d = reinterpret_cast<const uint4*>(dout + row * g.ld_o + h * kHD);
+    const uint4* o = reinterpret_cast<const uint4*>(out + row * g.ld_o + h * g.hd);
+    const uint4* d = reinterpret_cast<const uint4*>(dout + row * g.ld_o + h * g.hd);
     float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < g.hd / 8; ++j) {
       const uint4 a = o[j], c = d[j];
       const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -264,6 +284,7 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out,
 // ------------------------------------------------------------------------ dK, dV
 // grid (ceil(N/64), H, B): CTA owns 64 keys; loops over all query tiles.
 // smem: K tile | V tile | Q [Npad] | dO [Npad] | lse [Npad] | D [Npad]
+template <int HDP>
 __global__ void __launch_bounds__(128)
     attn_bwd_dkdv_kernel(const __nv_bfloat16* __restrict__ qkv,
                          const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
@@ -272,6 +293,7 @@ __global__ void __launch_bounds__(128)
   pdl_trigger();
   pdl_wait();
 
+  constexpr int kRowBytes = HDP * 2;
   extern __shared__ __align__(128) uint8_t sm[];
   const int npad = (g.N + kTile - 1) / kTile * kTile;
   uint8_t* sK = sm;
@@ -281,12 +303,14 @@ __global__ void __launch_bounds__(128)
   float* sL = reinterpret_cast<float*>(sO + npad * kRowBytes);
   float* sD = sL + npad;
   const int k0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
-  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
-  load_rows(sK, base + static_cast<int64_t>(k0) * g.ld_qkv + g.H * kHD, g.ld_qkv, kTile, g.N - k0);
-  load_rows(sV, base + static_cast<int64_t>(k0) * g.ld_qkv + 2 * g.H * kHD, g.ld_qkv, kTile,
-            g.N - k0);
-  load_rows(sQ, base, g.ld_qkv, npad, g.N);
-  load_rows(sO, dout + static_cast<int64_t>(b) * g.N * g.ld_o + h * kHD, g.ld_o, npad, g.N);
+  const int hd = g.hd;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
+  load_rows<HDP>(sK, base + static_cast<int64_t>(k0) * g.ld_qkv + g.H * hd, g.ld_qkv, kTile,
+                 g.N - k0, hd);
+  load_rows<HDP>(sV, base + static_cast<int64_t>(k0) * g.ld_qkv + 2 * g.H * hd, g.ld_qkv, kTile,
+                 g.N - k0, hd);
+  load_rows<HDP>(sQ, base, g.ld_qkv, npad, g.N, hd);
+  load_rows<HDP>(sO, dout + static_cast<int64_t>(b) * g.N * g.ld_o + h * hd, g.ld_o, npad, g.N, hd);
   const float* lrow = lse + (static_cast<int64_t>(b) * g.H + h) * g.N;
   const float* drow = Dg + (static_cast<int64_t>(b) * g.H + h) * g.N;
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
@@ -300,23 +324,23 @@ __global__ void __launch_bounds__(128)
   if (k0 + warp * 16 >= g.N) return;  // padding keys only
   const int tq = lane & 3, gq = lane >> 2;
   const uint32_t bK = smem_u32(sK), bV = smem_u32(sV), bQ = smem_u32(sQ), bO = smem_u32(sO);
-  uint32_t ka[4][4], va[4][4];
+  uint32_t ka[HDP / 16][4], va[HDP / 16][4];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    load_a(bK, warp * 16, 2 * ks, ka[ks]);
-    load_a(bV, warp * 16, 2 * ks, va[ks]);
+  for (int ks = 0; ks < HDP / 16; ++ks) {
+    load_a<HDP>(bK, warp * 16, 2 * ks, ka[ks]);
+    load_a<HDP>(bV, warp * 16, 2 * ks, va[ks]);
   }
-  float dk[8][4], dv[8][4];
+  float dk[HDP / 8][4], dv[HDP / 8][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < HDP / 8; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
 
   for (int qt = 0; qt < npad; qt += kTile) {
     float st[8][4], dpt[8][4];
     const int valid = g.N - qt;
-    mm_abt(ka, bQ, qt, st, valid);   // S^T [16 keys][64 queries]
-    mm_abt(va, bO, qt, dpt, valid);  // dP^T = V . dO^T
+    mm_abt<HDP>(ka, bQ, qt, st, valid);   // S^T [16 keys][64 queries]
+    mm_abt<HDP>(va, bO, qt, dpt, valid);  // dP^T = V . dO^T
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
@@ -327,8 +351,8 @@ __global__ void __launch_bounds__(128)
         dpt[nt][e] = p * (dpt[nt][e] - sD[q]) * g.scale;
       }
     }
-    mm_pb(st, bO, qt, dv, valid);   // dV += P^T . dO
-    mm_pb(dpt, bQ, qt, dk, valid);  // dK += dS^T . Q
+    mm_pb<HDP>(st, bO, qt, dv, valid);   // dV += P^T . dO
+    mm_pb<HDP>(dpt, bQ, qt, dk, valid);  // dK += dS^T . Q
   }
   const int rowa = k0 + warp * 16 + gq;
 #pragma unroll
@@ -336,14 +360,12 @@ __global__ void __launch_bounds__(128)
     const int row = rowa + 8 * r;
     if (row < g.N) {
       __nv_bfloat16* drow_k =
-          dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + g.H * kHD + h * kHD;
-      __nv_bfloat16* drow_v = drow_k + g.H * kHD;
+          dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + g.H * hd + h * hd;
+      __nv_bfloat16* drow_v = drow_k + g.H * hd;
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        *reinterpret_cast<uint32_t*>(drow_k + nt * 8 + 2 * tq) =
-            pack_bf16x2(dk[nt][2 * r], dk[nt][2 * r + 1]);
-        *reinterpret_cast<uint32_t*>(drow_v + nt * 8 + 2 * tq) =
-            pack_bf16x2(dv[nt][2 * r], dv[nt][2 * r + 1]);
+      for (int nt = 0; nt < HDP / 8; ++nt) {
+        store_pair(drow_k, nt * 8 + 2 * tq, hd, dk[nt][2 * r], dk[nt][2 * r + 1]);
+        store_pair(drow_v, nt * 8 + 2 * tq, hd, dv[nt][2 * r], dv[nt][2 * r + 1]);
       }
     }
   }
@@ -353,6 +375,7 @@ __global__ void __launch_bounds__(128)
 // ------------------------------------------------------------------------ dQ
 // grid (ceil(N/64), H, B): CTA owns 64 queries; loops over all key tiles.
 // smem: Q tile | dO tile | K [Npad] | V [Npad]
+template <int HDP>
 __global__ void __launch_bounds__(128)
     attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ qkv,
                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
@@ -361,6 +384,7 @@ __global__ void __launch_bounds__(128)
   pdl_trigger();
   pdl_wait();
 
+  constexpr int kRowBytes = HDP * 2;
   extern __shared__ __align__(128) uint8_t sm[];
   const int npad = (g.N + kTile - 1) / kTile * kTile;
   uint8_t* sQ = sm;
@@ -368,12 +392,13 @@ __global__ void __launch_bounds__(128)
   uint8_t* sK = sO + kTile * kRowBytes;
   uint8_t* sV = sK + npad * kRowBytes;
   const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
-  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * kHD;
-  load_rows(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0);
-  load_rows(sO, dout + (static_cast<int64_t>(b) * g.N + q0) * g.ld_o + h * kHD, g.ld_o, kTile,
-            g.N - q0);
-  load_rows(sK, base + g.H * kHD, g.ld_qkv, npad, g.N);
-  load_rows(sV, base + 2 * g.H * kHD, g.ld_qkv, npad, g.N);
+  const int hd = g.hd;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
+  load_rows<HDP>(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0, hd);
+  load_rows<HDP>(sO, dout + (static_cast<int64_t>(b) * g.N + q0) * g.ld_o + h * hd, g.ld_o, kTile,
+                 g.N - q0, hd);
+  load_rows<HDP>(sK, base + g.H * hd, g.ld_qkv, npad, g.N, hd);
+  load_rows<HDP>(sV, base + 2 * g.H * hd, g.ld_qkv, npad, g.N, hd);
   cp_async_wait_all();
   __syncthreads();
 
@@ -381,11 +406,11 @@ __global__ void __launch_bounds__(128)
   if (q0 + warp * 16 >= g.N) return;  // padding queries only
   const int tq = lane & 3, gq = lane >> 2;
   const uint32_t bQ = smem_u32(sQ), bO = smem_u32(sO), bK = smem_u32(sK), bV = smem_u32(sV);
-  uint32_t qa[4][4], oa[4][4];
+  uint32_t qa[HDP / 16][4], oa[HDP / 16][4];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    load_a(bQ, warp * 16, 2 * ks, qa[ks]);
-    load_a(bO, warp * 16, 2 * ks, oa[ks]);
+  for (int ks = 0; ks < HDP / 16; ++ks) {
+    load_a<HDP>(bQ, warp * 16, 2 * ks, qa[ks]);
+    load_a<HDP>(bO, warp * 16, 2 * ks, oa[ks]);
   }
   const int rowa = q0 + warp * 16 + gq;
   float lr[2], dr[2];
@@ -396,15 +421,15 @@ __global__ void __launch_bounds__(128)
     lr[r] = row < g.N ? lse[hb + row] : 0.f;
     dr[r] = row < g.N ? Dg[hb + row] : 0.f;
   }
-  float dq[8][4];
+  float dq[HDP / 8][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+  for (int i = 0; i < HDP / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
 
   for (int kt = 0; kt < npad; kt += kTile) {
     float s[8][4], dp[8][4];
     const int valid = g.N - kt;
-    mm_abt(qa, bK, kt, s, valid);
-    mm_abt(oa, bV, kt, dp, valid);
+    mm_abt<HDP>(qa, bK, kt, s, valid);
+    mm_abt<HDP>(oa, bV, kt, dp, valid);
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
@@ -414,29 +439,29 @@ __global__ void __launch_bounds__(128)
         s[nt][e] = p * (dp[nt][e] - dr[e >> 1]) * g.scale;
       }
     }
-    mm_pb(s, bK, kt, dq, valid);  // dQ += dS . K
+    mm_pb<HDP>(s, bK, kt, dq, valid);  // dQ += dS . K
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int row = rowa + 8 * r;
     if (row < g.N) {
-      __nv_bfloat16* drow = dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + h * kHD;
+      __nv_bfloat16* drow = dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + h * hd;
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-        *reinterpret_cast<uint32_t*>(drow + nt * 8 + 2 * tq) =
-            pack_bf16x2(dq[nt][2 * r], dq[nt][2 * r + 1]);
+      for (int nt = 0; nt < HDP / 8; ++nt)
+        store_pair(drow, nt * 8 + 2 * tq, hd, dq[nt][2 * r], dq[nt][2 * r + 1]);
     }
   }
 }
 
-static AttnGeom make_geom(int64_t B, int64_t N, int64_t H) {
+static AttnGeom make_geom(int64_t B, int64_t N, int64_t H, int64_t hd) {
   AttnGeom g;
   g.B = static_cast<int>(B);
   g.N = static_cast<int>(N);
   g.H = static_cast<int>(H);
-  g.ld_qkv = 3 * H * kHD;
-  g.ld_o = H * kHD;
-  g.scale = 1.0f / sqrtf(static_cast<float>(kHD));
+  g.hd = static_cast<int>(hd);
+  g.ld_qkv = 3 * H * hd;
+  g.ld_o = H * hd;
+  g.scale = 1.0f / sqrtf(static_cast<float>(hd));
   g.scale_log2 = g.scale * 1.4426950408889634f;
   return g;
 }
@@ -454,24 +479,43 @@ using namespace rp;
 
 static int attn_check(int64_t B, int64_t N, int64_t H, int64_t hd) {
   if (B <= 0 || N <= 0 || H <= 0) return rp_fail(RP_ERR_SHAPE, "attention: empty shape");
-  if (hd != kHD) return rp_fail(RP_ERR_SHAPE, "attention: head_dim must be 64");
-  // tcgen05 forward up to 512 keys, mma.sync forward (K and V resident in smem) up to 768
-  if (N > 768) return rp_fail(RP_ERR_SHAPE, "attention: sequence (window) longer than 768");
+  if (hd < 8 || hd > 128 || hd % 8)
+    return rp_fail(RP_ERR_SHAPE, "attention: head_dim must be a multiple of 8 in [8, 128]");
+  // tcgen05 (head_dim 64): forward up to 512 keys, backward up to 768; mma.sync keeps K and
+  // V resident in smem: 768 keys at head_dim <= 64, 384 above
+  const int64_t nmax = hd <= 64 ? 768 : 384;
+  if (N > nmax) return rp_fail(RP_ERR_SHAPE, "attention: sequence (window) too long for head_dim");
   return RP_OK;
 }
 
-// qkv [B*N, 3*H*64] bf16 -> out [B*N, H*64] bf16, lse [B][H][N] (log2 domain).
+// qkv [B*N, 3*H*hd] bf16 -> out [B*N, H*hd] bf16, lse [B][H][N] (log2 domain).
 // B here is the number of independent sequences (batch x windows).
 int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, uint16_t* out,
                         float* lse, cudaStream_t stream);
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
                         uint16_t* dqkv, cudaStream_t stream);
-static int g_attn_impl = 0;  // 0 = tcgen05 where it applies (N <= 256), 1 = mma.sync only
+static int g_attn_impl = 0;  // 0 = tcgen05 where it applies (head_dim 64), 1 = mma.sync only
 
 extern "C" int rp_set_attention_impl(int impl) {
   g_attn_impl = impl;
   return RP_OK;
+}
+
+template <int HDP>
+static int attn_fwd_mma(const uint16_t* qkv, int64_t B, int64_t N, int64_t H, int64_t hd,
+                        uint16_t* out, float* lse, cudaStream_t stream) {
+  const AttnGeom g = make_geom(B, N, H, hd);
+  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
+  const int smem = (kTile + 2 * npad) * HDP * 2;
+  int rc;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel<HDP>), smem))) return rc;
+  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
+            static_cast<unsigned>(B));
+  launch_k(attn_fwd_kernel<HDP>, grid, dim3(128), smem, stream,
+           reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse,
+           g);
+  return rp_check_launch("attention_fwd");
 }
 
 extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64_t H,
@@ -479,58 +523,63 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
                                 rp_stream_t stream) {
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
-  if (g_attn_impl == 0 && N <= 512) {
-    rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (g_attn_impl == 0 && head_dim == 64 && N <= 512) {
+    rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
-  const AttnGeom g = make_geom(B, N, H);
-  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
-  const int smem = (kTile + 2 * npad) * kRowBytes;
-  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem))) return rc;
-  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
-            static_cast<unsigned>(B));
-  launch_k(attn_fwd_kernel, grid, dim3(128), smem, static_cast<cudaStream_t>(stream),
-           reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse,
-           g);
-  return rp_check_launch("attention_fwd");
+  return head_dim <= 64 ? attn_fwd_mma<64>(qkv, B, N, H, head_dim, out, lse, s)
+                        : attn_fwd_mma<128>(qkv, B, N, H, head_dim, out, lse, s);
 }
 
 extern "C" int64_t rp_attention_bwd_workspace_floats(int64_t B, int64_t N, int64_t H) {
   return B * N * H;
 }
 
-// d_out [B*N, H*64] -> d_qkv [B*N, 3*H*64]; workspace: B*N*H floats.
+template <int HDP>
+static int attn_bwd_mma(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                        const uint16_t* dout, int64_t B, int64_t N, int64_t H, int64_t hd,
+                        uint16_t* dqkv, float* workspace, cudaStream_t s) {
+  const AttnGeom g = make_geom(B, N, H, hd);
+  const int64_t total = B * N * H;
+  int blocks = static_cast<int>((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  launch_k(attn_bwd_dot_kernel, dim3(blocks), dim3(256), 0, s,
+           reinterpret_cast<const __nv_bfloat16*>(out),
+           reinterpret_cast<const __nv_bfloat16*>(dout), workspace, g);
+  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
+  const int rb = HDP * 2;
+  const int smem_kv = 2 * kTile * rb + 2 * npad * rb + 2 * npad * 4;
+  const int smem_q = 2 * kTile * rb + 2 * npad * rb;
+  int rc;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dkdv_kernel<HDP>), smem_kv)))
+    return rc;
+  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dq_kernel<HDP>), smem_q)))
+    return rc;
+  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
+            static_cast<unsigned>(B));
+  launch_k(attn_bwd_dkdv_kernel<HDP>, dim3(grid), dim3(128), smem_kv, s,
+           reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
+           lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  launch_k(attn_bwd_dq_kernel<HDP>, dim3(grid), dim3(128), smem_q, s,
+           reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
+           lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+  return rp_check_launch("attention_bwd");
+}
+
+// d_out [B*N, H*hd] -> d_qkv [B*N, 3*H*hd]; workspace: B*N*H floats.
 extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
                                 const uint16_t* dout, int64_t B, int64_t N, int64_t H,
                                 int64_t head_dim, uint16_t* dqkv, float* workspace,
                                 rp_stream_t stream) {
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
-  const AttnGeom g = make_geom(B, N, H);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (g_attn_impl == 0 && N <= 1024) {  // tcgen05 path computes D itself
+  if (g_attn_impl == 0 && head_dim == 64) {  // tcgen05 path computes D itself
     rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
-  const int64_t total = B * N * H;
-  int blocks = static_cast<int>((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  launch_k(attn_bwd_dot_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(out),
-                                             reinterpret_cast<const __nv_bfloat16*>(dout),
-                                             workspace, g);
-  const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
-  const int smem_kv = 2 * kTile * kRowBytes + 2 * npad * kRowBytes + 2 * npad * 4;
-  const int smem_q = 2 * kTile * kRowBytes + 2 * npad * kRowBytes;
-  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dkdv_kernel), smem_kv)))
-    return rc;
-  if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_dq_kernel), smem_q))) return rc;
-  dim3 grid(static_cast<unsigned>((N + kTile - 1) / kTile), static_cast<unsigned>(H),
-            static_cast<unsigned>(B));
-  launch_k(attn_bwd_dkdv_kernel, dim3(grid), dim3(128), smem_kv, s, 
-      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
-      lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
-  launch_k(attn_bwd_dq_kernel, dim3(grid), dim3(128), smem_q, s, 
-      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(dout),
-      lse, workspace, reinterpret_cast<__nv_bfloat16*>(dqkv), g);
-  return rp_check_launch("attention_bwd");
+  return head_dim <= 64
+             ? attn_bwd_mma<64>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s)
+             : attn_bwd_mma<128>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s);
 }

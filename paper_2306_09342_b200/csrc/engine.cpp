@@ -378,7 +378,7 @@ int ln_fwd(RpEngine* g, const float* x, int64_t tg, int64_t tb, uint16_t* y, flo
 }
 
 int attn_fwd(RpEngine* g, const uint16_t* qkv, uint16_t* att, float* lse, cudaStream_t s) {
-  return rp_attention_fwd(qkv, g->T / g->W, g->W, g->H, 64, att, lse, s);
+  return rp_attention_fwd(qkv, g->T / g->W, g->W, g->H, g->d / g->H, att, lse, s);
 }
 
 void mark(RpEngine* g, int lane, int64_t b, int which, cudaStream_t s) {
@@ -458,7 +458,7 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   // ---- F = attention VJP with d_o2t (layers.cpp:171-220)
   RP_TRY(launch(p.g_dproj, s));
   RP_TRY(launch(p.g_wproj, s));
-  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / g->W, g->W, g->H, 64, g->dqkv,
+  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / g->W, g->W, g->H, g->d / g->H, g->dqkv,
                           g->attn_ws, s));
   RP_TRY(launch(p.g_wqkv, s));
   RP_TRY(launch(p.g_dqkv, s));
@@ -597,9 +597,11 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   if (!c || !out) return rp_fail(RP_ERR_CONTRACT, "engine_create: null argument");
   *out = nullptr;
   if (c->depth < 1 || c->width < 16 || c->heads < 1 || c->width % c->heads ||
-      c->width / c->heads != 64 || c->hidden < 16 || c->seq_len < 1 || c->in_dim < 8 ||
-      c->num_classes < 1 || c->batch < 1)
-    return rp_fail(RP_ERR_CONFIG, "engine_create: invalid model config (head_dim must be 64)");
+      (c->width / c->heads) % 8 || c->width / c->heads > 128 || c->hidden < 16 ||
+      c->seq_len < 1 || c->in_dim < 8 || c->num_classes < 1 || c->batch < 1)
+    return rp_fail(RP_ERR_CONFIG,
+                   "engine_create: invalid model config (head_dim = width/heads must be a "
+                   "multiple of 8, at most 128)");
   if (c->width % 16 || c->hidden % 16 || c->in_dim % 16)
     return rp_fail(RP_ERR_CONFIG, "engine_create: width/hidden/in_dim must be multiples of 16");
   const int64_t W = c->window > 0 ? c->window : c->seq_len;

@@ -58,6 +58,8 @@ PRESETS = {
     "revvit-l": dict(depth=24, width=1024, heads=16, hidden=4096, seq_len=197, batch=256),
     "rev-roberta-base": dict(depth=12, width=768, heads=12, hidden=3072, seq_len=512,
                              batch=64, num_classes=2),
+    # BASELINE config 5: RevViT-G-style (depth 48, dim 1664, 16 heads of 104, MLP ratio 4)
+    "revvit-g48": dict(depth=48, width=1664, heads=16, hidden=6656, seq_len=197, batch=64),
 }
 
 

@@ -75,7 +75,9 @@ def test_layer_norm_and_attention_argument_errors(capi):
     with pytest.raises(capi.ShapeError, match="eps"):
         capi.check(L.rp_layer_norm_fwd(None, None, None, 4, 8, 0.0, None, None, None, None))
     with pytest.raises(capi.ShapeError, match="head_dim"):
-        capi.check(L.rp_attention_fwd(None, 2, 8, 2, 32, None, None, None))
+        capi.check(L.rp_attention_fwd(None, 2, 8, 2, 36, None, None, None))  # not a multiple of 8
+    with pytest.raises(capi.ShapeError, match="head_dim"):
+        capi.check(L.rp_attention_fwd(None, 2, 8, 2, 160, None, None, None))  # above 128
 
 
 def test_engine_config_errors(capi):
@@ -83,7 +85,7 @@ def test_engine_config_errors(capi):
     with pytest.raises(capi.ConfigError):
         Engine(ModelConfig(depth=0))
     with pytest.raises(capi.ConfigError, match="head_dim"):
-        Engine(ModelConfig(width=768, heads=8))
+        Engine(ModelConfig(width=768, heads=3))  # head_dim 256 > 128
 
 
 def test_activation_ledger_spec_invariants(capi):

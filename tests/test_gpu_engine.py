@@ -311,3 +311,23 @@ def test_prefetched_batch_matches_set_batch():
     assert np.array_equal(eng.grads(), g_ref)
     assert float(h_loss[0]) == l_ref
     eng.close()
+
+
+def test_general_head_dim_step():
+    """head_dim 104 (the G48 config's, here at width 832 with 8 heads) through the whole
+    Reprop / PaReprop step against the oracle; PaReprop bit-identical to Reprop."""
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits, bf16_round
+    cfg = dict(depth=2, width=832, heads=8, hidden=3328, seq_len=197, in_dim=768, num_classes=100)
+    eng, mc, p32, pref = make(cfg, batch=2)
+    x, lab = O.synthetic_batch(mc, 2, seed=12)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    eng.step(REPROP, graph=False)
+    g_r, loss = eng.grads().copy(), eng.loss()
+    eng.step(PAREPROP, graph=False)
+    assert np.array_equal(eng.grads(), g_r)
+    r = O.step(mc, pref, bf16_round(x).astype(np.float64), lab)
+    assert abs(loss - r.loss) < 1e-3 * abs(r.loss)
+    per_tensor(mc, g_r, r.grads, TOL_GRAD)
+    assert l2rel(g_r, r.grads) < TOL_L2
+    eng.close()

@@ -212,6 +212,27 @@ def test_colsum(K, dtype):
     assert torch.equal(out, K.colsum(x))
 
 
+@pytest.mark.parametrize("B,N,H,hd", [(2, 197, 2, 104), (3, 64, 3, 32), (1, 130, 2, 128),
+                                      (2, 50, 4, 96), (1, 300, 1, 104)])
+def test_attention_general_head_dim(K, B, N, H, hd):
+    """head_dim != 64 (e.g. the G48 config's 104) runs on the mma.sync kernels with the head
+    padded to 64 / 128 columns in smem."""
+    qkv = torch.randn(B * N, 3 * H * hd, device="cuda").bfloat16()
+    out, lse = K.attention_fwd(qkv, B, N, H, head_dim=hd)
+    qkv_r = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = attn_ref(qkv_r, B, N, H, hd)
+    assert rel(out, o_ref) < 1e-2
+    assert rel(lse / 1.4426950408889634, lse_ref) < 1e-4
+    dout = torch.randn(B * N, H * hd, device="cuda").bfloat16()
+    dqkv = K.attention_bwd(qkv, out, lse, dout, B, N, H, head_dim=hd)
+    o_ref.backward(dout.float())
+    g = qkv_r.grad
+    for i, name in enumerate("qkv"):
+        sl = slice(i * H * hd, (i + 1) * H * hd)
+        assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
+    assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H, head_dim=hd))
+
+
 def attn_ref(qkv, B, N, H, hd=64):
     q, k, v = qkv.float().view(B, N, 3, H, hd).permute(2, 0, 3, 1, 4)
     s = (q @ k.transpose(-1, -2)) / hd ** 0.5
