@@ -150,26 +150,49 @@ __global__ void pool_kernel(const float* __restrict__ o1, const float* __restric
 }
 
 // C[M,N] (+)= sum_k A(m,k) B(k,n), fp32 SIMT, 16x16 tiles; A(m,k) = A[m*sam + k*sak].
-__global__ void simt_gemm_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A,
-                                 int64_t sam, int64_t sak, const float* __restrict__ Bm,
-                                 int64_t sbk, int64_t sbn, float* __restrict__ Cm, int64_t ldc) {
+// fp32 GEMM for the small head products (C = 1000 is not a tensor-core tile multiple):
+// 32 x 32 output tile per CTA (enough CTAs to fill the GPU at M = 256), 256 threads, 2 x 2
+// outputs per thread in registers, 32-deep k slices staged through smem (any strides, so
+// transposed operands need no copy). Fixed k order: deterministic.
+__global__ void __launch_bounds__(256)
+    simt_gemm_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A, int64_t sam,
+                     int64_t sak, const float* __restrict__ Bm, int64_t sbk, int64_t sbn,
+                     float* __restrict__ Cm, int64_t ldc) {
   pdl_trigger();
   pdl_wait();
 
-  __shared__ float as[16][17], bs[16][17];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t m = blockIdx.y * 16 + ty, n = blockIdx.x * 16 + tx;
-  float acc = 0.f;
-  for (int64_t k0 = 0; k0 < K; k0 += 16) {
-    const int64_t ka = k0 + tx, kb = k0 + ty;
-    as[ty][tx] = (m < M && ka < K) ? A[m * sam + ka * sak] : 0.f;
-    bs[ty][tx] = (kb < K && n < N) ? Bm[kb * sbk + n * sbn] : 0.f;
+  __shared__ float as[32][32 + 1], bs[32][32 + 1];  // [k][m], [k][n]
+  const int tid = threadIdx.x;
+  const int tm = (tid >> 4) * 2, tn = (tid & 15) * 2;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 32, n0 = static_cast<int64_t>(blockIdx.x) * 32;
+  float acc[2][2] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+    for (int i = tid; i < 32 * 32; i += 256) {
+      const int kk = i & 31, mm = i >> 5;  // A: consecutive threads walk k
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      as[kk][mm] = (gm < M && gk < K) ? A[gm * sam + gk * sak] : 0.f;
+      const int nn = i & 31, kb = i >> 5;  // B: consecutive threads walk n
+      const int64_t gn = n0 + nn, gkb = k0 + kb;
+      bs[kb][nn] = (gkb < K && gn < N) ? Bm[gkb * sbk + gn * sbn] : 0.f;
+    }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc += as[ty][k] * bs[k][tx];
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const float a0 = as[k][tm], a1 = as[k][tm + 1], b0 = bs[k][tn], b1 = bs[k][tn + 1];
+      acc[0][0] = fmaf(a0, b0, acc[0][0]);
+      acc[0][1] = fmaf(a0, b1, acc[0][1]);
+      acc[1][0] = fmaf(a1, b0, acc[1][0]);
+      acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
     __syncthreads();
   }
-  if (m < M && n < N) Cm[m * ldc + n] = acc;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t m = m0 + tm + i, n = n0 + tn + j;
+      if (m < M && n < N) Cm[m * ldc + n] = acc[i][j];
+    }
 }
 
 // Mean cross-entropy, log-sum-exp stabilised. One warp per row:
@@ -306,8 +329,8 @@ int rpk_pool(const float* o1, const float* o2, int64_t B, int64_t N, int64_t d, 
 int rpk_simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t sam, int64_t sak,
                   const float* B, int64_t sbk, int64_t sbn, float* C, int64_t ldc,
                   cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((N + 15) / 16), static_cast<unsigned>((M + 15) / 16));
-  launch_k(simt_gemm_kernel, dim3(grid), dim3(16, 16), 0, s, M, N, K, A, sam, sak, B, sbk, sbn, C, ldc);
+  dim3 grid(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((M + 31) / 32));
+  launch_k(simt_gemm_kernel, dim3(grid), dim3(256), 0, s, M, N, K, A, sam, sak, B, sbk, sbn, C, ldc);
   return rp_check_launch("simt_gemm");
 }
 int rpk_cross_entropy(const float* logits, const int32_t* labels, int64_t B, int64_t C,
