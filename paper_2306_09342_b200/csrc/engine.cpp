@@ -93,7 +93,8 @@ struct RpEngine {
   cudaEvent_t evStaged = nullptr, evStageFree = nullptr, evLoss = nullptr;
   bool staged = false;
   std::vector<cudaEvent_t> evR, evG;
-  cudaEvent_t evFwd = nullptr, evCommDone = nullptr, evRDone = nullptr, evEmbed = nullptr;
+  cudaEvent_t evFwd = nullptr, evCommDone = nullptr, evRDone = nullptr, evEmbed = nullptr,
+              evLogits = nullptr;
   std::vector<cudaEvent_t> ts;  // timing events for the slot log (eager, instrumented)
   bool instrument = false;
   // parameters
@@ -409,8 +410,12 @@ int head(RpEngine* g, cudaStream_t s) {
   RP_TRY(rpk_pool(X1(g, g->L), X2(g, g->L), B, g->N, d, g->pooled, s));
   RP_TRY(rpk_simt_gemm(B, C, d, g->pooled, d, 1, hw, C, 1, g->logits, C, s));
   RP_TRY(rpk_cross_entropy(g->logits, g->labels, B, C, g->dlogits, g->row_loss, g->loss, s));
+  // the head weight gradient goes to the comm stream (ahead of the head bucket's optimizer
+  // step there), in parallel with d_pooled and the spread on the engine stream
+  RP_TRY(cuda_ok(cudaEventRecord(g->evLogits, s), "record"));
+  RP_TRY(cuda_ok(cudaStreamWaitEvent(g->sC, g->evLogits, 0), "wait"));
   RP_TRY(rpk_simt_gemm(d, C, B, g->pooled, 1, d, g->dlogits, C, 1, gr(g, 1 + kPerBlock * g->L),
-                       C, s));
+                       C, g->sC));
   RP_TRY(rpk_simt_gemm(B, d, C, g->dlogits, C, 1, hw, 1, C, g->dpooled, d, s));
   RP_TRY(rpk_spread(g->dpooled, B, g->N, d, g->d1, g->d2, g->d1b, g->d2b, s));
   return RP_OK;
@@ -668,7 +673,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   g->evG.resize(static_cast<size_t>(g->L));
   for (auto* v : {&g->evR, &g->evG})
     for (auto& e : *v) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed})
+  for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed, &g->evLogits})
     cudaEventCreateWithFlags(e, cudaEventDisableTiming);
   g->ts.resize(static_cast<size_t>(4 * g->L));
   for (auto& e : g->ts) cudaEventCreate(&e);
@@ -748,7 +753,7 @@ extern "C" void rp_engine_destroy(RpEngine* g) {
   for (auto* v : {&g->evR, &g->evG, &g->ts})
     for (auto& e : *v)
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed})
+  for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed, g->evLogits})
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {g->sG, g->sR, g->sC, g->sX})
     if (s) cudaStreamDestroy(s);

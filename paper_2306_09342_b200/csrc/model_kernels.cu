@@ -149,7 +149,7 @@ __global__ void pool_kernel(const float* __restrict__ o1, const float* __restric
   pooled[i] = s * (1.0f / static_cast<float>(N));
 }
 
-// C[M,N] (+)= sum_k A(m,k) B(k,n), fp32 SIMT, 16x16 tiles; A(m,k) = A[m*sam + k*sak].
+// C[M,N] = sum_k A(m,k) B(k,n); A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn].
 // fp32 GEMM for the small head products (C = 1000 is not a tensor-core tile multiple):
 // 32 x 32 output tile per CTA (enough CTAs to fill the GPU at M = 256), 256 threads, 2 x 2
 // outputs per thread in registers, 32-deep k slices staged through smem (any strides, so
@@ -251,17 +251,19 @@ __global__ void spread_kernel(const float* __restrict__ d_pooled, int64_t B, int
   pdl_trigger();
   pdl_wait();
 
-  const int64_t total = B * N * d;
-  const float invN = 1.0f / static_cast<float>(N);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+  // 4 consecutive columns per thread (d % 4 == 0): float4 / 2 x bf16x2 stores
+  const int64_t total4 = B * N * d / 4;
+  const float scale = 0.5f / static_cast<float>(N);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = i % d, b = i / (N * d);
-    const float v = (d_pooled[b * d + c] * invN) * 0.5f;
-    d1[i] = v;
-    d2[i] = v;
-    const __nv_bfloat16 vb = __float2bfloat16_rn(v);
-    d1b[i] = vb;
-    d2b[i] = vb;
+    const int64_t e = 4 * i, c = e % d, b = e / (N * d);
+    const float4 p = *reinterpret_cast<const float4*>(d_pooled + b * d + c);
+    const float4 v = make_float4(p.x * scale, p.y * scale, p.z * scale, p.w * scale);
+    reinterpret_cast<float4*>(d1)[i] = v;
+    reinterpret_cast<float4*>(d2)[i] = v;
+    const uint2 vb = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    reinterpret_cast<uint2*>(d1b)[i] = vb;
+    reinterpret_cast<uint2*>(d2b)[i] = vb;
   }
 }
 
@@ -342,7 +344,7 @@ int rpk_cross_entropy(const float* logits, const int32_t* labels, int64_t B, int
 }
 int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1, float* d2,
                uint16_t* d1b, uint16_t* d2b, cudaStream_t s) {
-  launch_k(spread_kernel, dim3(grid_for(B * N * d)), dim3(256), 0, s, d_pooled, B, N, d, d1, d2,
+  launch_k(spread_kernel, dim3(grid_for(B * N * d / 4)), dim3(256), 0, s, d_pooled, B, N, d, d1, d2,
                                                     reinterpret_cast<__nv_bfloat16*>(d1b),
                                                     reinterpret_cast<__nv_bfloat16*>(d2b));
   return rp_check_launch("spread");
