@@ -1,4 +1,4 @@
-// tcgen05 attention backward for short sequences (N <= 256, head_dim 64).
+// tcgen05 attention backward (head_dim 64, N <= 768: keys / queries streamed in 64-row chunks).
 //
 // ref:proj/core/src/layers.cpp:185-208 (per head: dA = dO V^T, dV = A^T dO,
 // dS = softmax_vjp(A, dA) / sqrt(hd), dQ = dS K, dK = dS^T Q; softmax VJP ops.cpp:206-225),
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 
 using namespace rp;
 
-// Backward on the tcgen05 path (N <= 256): dQ (and D = rowsum(dO * O) into `Dg`), then
+// Backward on the tcgen05 path (head_dim 64): dQ (and D = rowsum(dO * O) into `Dg`), then
 // dK / dV. Returns RP_ERR_CONFIG without launching when the shape is outside this path.
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,

@@ -1,4 +1,4 @@
-// tcgen05 attention for short sequences (N <= 256 keys, head_dim 64): forward and backward.
+// tcgen05 attention forward (head_dim 64): single-pass kernel for N <= 224, two-pass for N <= 512.
 //
 // Same contract as the mma.sync kernels in attention.cu (ref:proj/core/src/layers.cpp:150-166
 // forward: scores = (q k^T) * 1/sqrt(hd), row softmax, probs . v; layers.cpp:185-208

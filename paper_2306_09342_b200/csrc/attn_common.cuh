@@ -13,7 +13,7 @@ namespace attn_tc {
 
 
 struct Geom {
-  int B, N, H, Nk;  // sequences, tokens, heads, padded key count (multiple of 16, <= 256)
+  int B, N, H, Nk;  // sequences, tokens, heads, padded key count (multiple of 16)
   int64_t ld_o;
   float scale_log2;
 };
