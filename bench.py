@@ -301,6 +301,38 @@ def main_ours(a, rank, world, local_rank):
     per_gpu = img_p / world
     launches = eng.graph_kernels(PAREPROP)
 
+    # PaReprop vs Reprop at a small per-GPU batch, where a single stream leaves SMs idle
+    # (context for the headline gain; same kernels, same device-timed protocol)
+    small = None
+    if world == 1 and not a.no_small_batch:
+        eng.close()
+        ps = dict(p, batch=32)
+        es = Engine(ModelConfig(device=local_rank, seed=1234 + rank, **ps))
+        es.set_lr(1e-3)
+        for mode in (REPROP, PAREPROP):
+            for _ in range(max(a.warmup, 3)):
+                es.step(mode)
+        es.sync()
+        streams = torch.cuda.ExternalStream(es.stream_ptr)
+
+        def timed_small(mode, K):
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            e0 = torch.cuda.Event(enable_timing=True)
+            s0.record(streams)
+            for _ in range(K):
+                es.step(mode)
+            e0.record(streams)
+            e0.synchronize()
+            return s0.elapsed_time(e0)
+        k_small = max(a.steps, 10)
+        r_ms, p_ms = timed_small(REPROP, k_small), timed_small(PAREPROP, k_small)
+        small = {"per_gpu_batch": 32, "reprop_img_s": 32 * k_small / (r_ms / 1e3),
+                 "pareprop_img_s": 32 * k_small / (p_ms / 1e3),
+                 "gain_pct": 100.0 * (r_ms / p_ms - 1.0)}
+        es.close()
+        eng = None
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
@@ -321,6 +353,7 @@ def main_ours(a, rank, world, local_rank):
                        "l2": "per-step working set ~4.5 GB >> 126 MB L2 (no flush needed)"},
             "reprop": {"value": img_r, "ms_per_step": ms_r / a.steps},
             "pareprop_gain_pct": 100.0 * (img_p / img_r - 1.0),
+            "pareprop_gain_small_batch": small,
             "mfu": mf * per_gpu / (pk["bf16"] * 1e12),
             "hfu": hf * per_gpu / (pk["bf16"] * 1e12),
             "loss": loss,
@@ -339,7 +372,8 @@ def main_ours(a, rank, world, local_rank):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    eng.close()
+    if eng is not None:
+        eng.close()
     return 0
 
 
@@ -353,6 +387,7 @@ def main(argv=None):
     ap.add_argument("--r-ctas", type=int, default=0)
     ap.add_argument("--g-ctas", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-small-batch", action="store_true")
     a = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
