@@ -22,6 +22,12 @@ class RefCfg(C.Structure):
                                          "num_classes", "window")]
 
 
+class RefHierCfg(C.Structure):
+    _fields_ = [("stages", C.c_int64), ("depths", C.c_int64 * 8), ("widths", C.c_int64 * 8),
+                ("heads", C.c_int64 * 8)] + [(n, C.c_int64) for n in (
+                    "ratio", "seq_len", "in_dim", "num_classes", "window", "reduction", "fusion")]
+
+
 _lib = None
 
 
@@ -60,6 +66,9 @@ def lib():
                                            P]),
             "ref_step": (I, [I, C.POINTER(RefCfg), I, I64, P, P, P, P, P, P, P]),
             "ref_step_dp": (I, [I, C.POINTER(RefCfg), I, I64, I, P, P, P, P, P]),
+            "ref_hier_param_count": (I64, [C.POINTER(RefHierCfg)]),
+            "ref_hier_step": (I, [I, C.POINTER(RefHierCfg), I64, P, P, P, P, P]),
+            "ref_boundary": (I, [I, I64, I64, I64, I64, I64, I] + [P] * 10),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -195,3 +204,47 @@ def split_block(mc, pb):
     d = mc.width
     nf = 3 * d * d + d * d + 2 * d
     return pb[:nf], pb[nf:]
+
+
+def hier_cfg_of(mc) -> RefHierCfg:
+    S = len(mc.depths)
+    c = RefHierCfg()
+    c.stages = S
+    for s in range(S):
+        c.depths[s], c.widths[s], c.heads[s] = mc.depths[s], mc.widths[s], mc.stage_heads[s]
+    c.ratio = mc.hidden // mc.width
+    c.seq_len, c.in_dim, c.num_classes = mc.seq_len, mc.in_dim, mc.num_classes
+    c.window, c.reduction = mc.window or 0, mc.reduction
+    c.fusion = 1 if mc.fusion == "mlp" else 0
+    return c
+
+
+def hier_param_count(mc) -> int:
+    return int(lib().ref_hier_param_count(C.byref(hier_cfg_of(mc))))
+
+
+def hier_step(mc, params, x, labels):
+    """ref_hier_step (Reprop order): (loss, flat grads)."""
+    c = hier_cfg_of(mc)
+    f64 = params.dtype == np.float64
+    loss = C.c_double()
+    grads = np.empty_like(params)
+    lab = np.ascontiguousarray(labels, dtype=np.int64)
+    _chk(lib().ref_hier_step(int(f64), C.byref(c), x.shape[0], _p(params),
+                             _p(np.ascontiguousarray(x)), _p(lab), C.byref(loss), _p(grads)))
+    return loss.value, grads
+
+
+def boundary(i1, i2, merge_w, fusion_w, r, d_y):
+    """The reference's fuse -> patch_merge and its VJP: (y, d_i1, d_i2, d_merge_w, d_fusion_w)."""
+    B, N, d = i1.shape
+    dn = merge_w.shape[1]
+    dt = i1.dtype
+    y = np.empty((B, N // r, dn), dt)
+    d1, d2 = np.empty_like(i1), np.empty_like(i1)
+    dmw = np.empty_like(merge_w)
+    dfw = None if fusion_w is None else np.empty_like(fusion_w)
+    _chk(lib().ref_boundary(int(dt == np.float64), B, N, d, dn, r, int(fusion_w is not None),
+                            _p(i1), _p(i2), _p(merge_w), _p(fusion_w), _p(d_y), _p(y), _p(d1),
+                            _p(d2), _p(dmw), _p(dfw)))
+    return y, d1, d2, dmw, dfw

@@ -676,4 +676,174 @@ int ref_step_dp(int f64, const RefCfg* c, int engine, int64_t B, int threads,
   });
 }
 
+
+// ---------------------------------------------------------------- hierarchical model
+// Rev-Swin-style model: stages of RevBlocks joined by the
+// reference's own stage boundary (layers.cpp:261-303: fuse, then patch_merge, then the
+// fused-and-merged tensor duplicated into the next stage's pair). Stage s has width
+// widths[s], heads[s], MLP hidden ratio*widths[s], seq_len / r^s tokens and attention
+// windows of min(window, tokens). Only each stage's input and output pair are stored; the
+// backward recomputes the boundary's fuse from the stored stage output. Reprop order.
+// Flat parameter order: embed_w | stage 0 blocks | merge_w_0 [, fusion_w_0] | stage 1
+// blocks | ... | head_w (the numpy oracle's tensor_shapes and the GPU engine share it).
+typedef struct {
+  int64_t stages, depths[8], widths[8], heads[8], ratio, seq_len, in_dim, num_classes, window,
+      reduction, fusion;  // fusion: 0 average, 1 mlp
+} RefHierCfg;
+
+int64_t ref_hier_param_count(const RefHierCfg* c) {
+  int64_t n = c->in_dim * c->widths[0];
+  for (int64_t s = 0; s < c->stages; ++s) {
+    const int64_t d = c->widths[s], h = c->ratio * d;
+    n += c->depths[s] * (4 * d * d + 2 * d * h + h + 5 * d);
+    if (s + 1 < c->stages) n += c->reduction * d * c->widths[s + 1] + (c->fusion ? 2 * d * d : 0);
+  }
+  return n + c->widths[c->stages - 1] * c->num_classes;
+}
+
+int ref_hier_step(int f64, const RefHierCfg* c, int64_t B, const void* params,
+                  const void* inputs, const int64_t* labels, double* loss, void* grads) {
+  return guarded([&] {
+    if (c->stages < 2 || c->stages > 8) throw ConfigError("ref_hier_step: 2..8 stages");
+    const Dtype dt = dt_of(f64);
+    const std::size_t esz = dtype_size(dt);
+    const uint8_t* base = static_cast<const uint8_t*>(params);
+    View v{base, dt};
+    int64_t off = 0;
+    const std::size_t S = static_cast<std::size_t>(c->stages);
+    Tensor embed_w = v.take(off, {static_cast<std::size_t>(c->in_dim),
+                                  static_cast<std::size_t>(c->widths[0])});
+    std::vector<std::vector<RevBlock>> blocks(S);
+    std::vector<BoundaryParams> bnd(S - 1);
+    std::vector<int64_t> toks(S);
+    int64_t n = c->seq_len;
+    for (std::size_t s = 0; s < S; ++s) {
+      if (s) {
+        if (n % c->reduction) throw ShapeError("seq_len not divisible by r^(stages-1)");
+        n /= c->reduction;
+      }
+      toks[s] = n;
+      RefCfg sc{c->depths[s], c->widths[s], c->heads[s], c->ratio * c->widths[s], n, c->in_dim,
+                c->num_classes, c->window > 0 ? std::min(c->window, n) : 0};
+      const int64_t bs = layout_of(sc).block_size();
+      for (int64_t i = 0; i < c->depths[s]; ++i) {
+        blocks[s].push_back(block_from(sc, base + off * static_cast<int64_t>(esz), dt, i));
+        off += bs;
+      }
+      if (s + 1 < S) {
+        const std::size_t d = static_cast<std::size_t>(c->widths[s]);
+        bnd[s].reduction = static_cast<std::size_t>(c->reduction);
+        bnd[s].merge_w = v.take(off, {bnd[s].reduction * d, static_cast<std::size_t>(c->widths[s + 1])});
+        if (c->fusion) {
+          bnd[s].fusion_kind = FusionKind::mlp;
+          bnd[s].fusion_w = v.take(off, {2 * d, d});
+        }
+      }
+    }
+    Tensor head_w = v.take(off, {static_cast<std::size_t>(c->widths[S - 1]),
+                                 static_cast<std::size_t>(c->num_classes)});
+    Tensor x = from_raw(inputs,
+                        {static_cast<std::size_t>(B), static_cast<std::size_t>(c->seq_len),
+                         static_cast<std::size_t>(c->in_dim)},
+                        dt);
+    // forward_full
+    Tensor e = ops::matmul(x, embed_w);
+    std::vector<Coupled> s_in, s_out;
+    Coupled cur{e, e};
+    for (std::size_t s = 0; s < S; ++s) {
+      s_in.push_back(cur);
+      for (const RevBlock& b : blocks[s]) cur = rev_forward(b, cur);
+      s_out.push_back(cur);
+      if (s + 1 < S) {
+        FuseResult f = fuse(cur.i1, cur.i2, bnd[s]);
+        PatchMergeResult pm = patch_merge(f.y, bnd[s]);
+        cur = Coupled{pm.y, pm.y};
+      }
+    }
+    BoundaryParams avg;
+    FuseResult fused = fuse(cur.i1, cur.i2, avg);
+    Tensor pooled = ops::mean_tokens(fused.y);
+    Tensor logits = ops::matmul(pooled, head_w);
+    Tensor d_logits;
+    std::vector<int64_t> lab(labels, labels + B);
+    const double l = loss_and_grad_head(logits, lab, d_logits);
+    Tensor d_head_w = ops::matmul_tn(pooled, d_logits);
+    Tensor d_pooled = ops::matmul_nt(d_logits, head_w);
+    FuseVjp fv0 = fuse_vjp(fused, avg,
+                           ops::spread_tokens(d_pooled, static_cast<std::size_t>(toks[S - 1])));
+    Coupled d_out{std::move(fv0.d_i1), std::move(fv0.d_i2)};
+    std::vector<std::vector<RevBlockGrads>> bg(S);
+    std::vector<Tensor> d_merge(S - 1), d_fusion(S - 1);
+    for (std::size_t s = S; s-- > 0;) {
+      const std::size_t L = blocks[s].size();
+      bg[s].resize(L);
+      Coupled o = s_out[s];
+      for (std::size_t i = L; i-- > 0;) {
+        Recomputed r = i == 0 ? recompute_from_input(blocks[s][0], s_in[s])
+                              : recompute(blocks[s][i], o);
+        d_out = vjp_half(blocks[s][i], r, d_out, bg[s][i]);
+        o = std::move(r.inp);
+      }
+      if (s > 0) {
+        Tensor d_y = ops::add(d_out.i1, d_out.i2);
+        FuseResult f = fuse(s_out[s - 1].i1, s_out[s - 1].i2, bnd[s - 1]);
+        PatchMergeResult pm = patch_merge(f.y, bnd[s - 1]);
+        PatchMergeVjp pv = patch_merge_vjp(pm.grouped, bnd[s - 1], d_y);
+        d_merge[s - 1] = std::move(pv.d_merge_w);
+        FuseVjp fv = fuse_vjp(f, bnd[s - 1], pv.d_x);
+        if (fv.d_fusion_w) d_fusion[s - 1] = std::move(*fv.d_fusion_w);
+        d_out = Coupled{std::move(fv.d_i1), std::move(fv.d_i2)};
+      }
+    }
+    Tensor d_embed_w = ops::matmul_tn(x, ops::add(d_out.i1, d_out.i2));
+    if (loss) *loss = l;
+    if (!grads) return;
+    std::vector<Tensor> out;
+    out.push_back(std::move(d_embed_w));
+    for (std::size_t s = 0; s < S; ++s) {
+      for (auto& g : bg[s]) {
+        for (Tensor* t : {&g.f.d_w_qkv, &g.f.d_w_out, &g.f.d_ln_gamma, &g.f.d_ln_beta, &g.g.d_w1,
+                          &g.g.d_b1, &g.g.d_w2, &g.g.d_b2, &g.g.d_ln_gamma, &g.g.d_ln_beta})
+          out.push_back(std::move(*t));
+      }
+      if (s + 1 < S) {
+        out.push_back(std::move(d_merge[s]));
+        if (c->fusion) out.push_back(std::move(d_fusion[s]));
+      }
+    }
+    out.push_back(std::move(d_head_w));
+    flat_to_raw(out, grads);
+  });
+}
+
+// The reference's boundary layers on raw arrays (layers.cpp:261-303): y = patch_merge(
+// fuse(i1, i2)) and, given d_y, the cotangents d_i1, d_i2, d_merge_w, d_fusion_w.
+int ref_boundary(int f64, int64_t B, int64_t N, int64_t d, int64_t d_next, int64_t r, int fusion,
+                 const void* i1, const void* i2, const void* merge_w, const void* fusion_w,
+                 const void* d_y, void* y, void* d_i1, void* d_i2, void* d_merge_w,
+                 void* d_fusion_w) {
+  return guarded([&] {
+    const Dtype dt = dt_of(f64);
+    const std::size_t b = B, n = N, dd = d, dn = d_next, rr = r;
+    Tensor a = from_raw(i1, {b, n, dd}, dt), c = from_raw(i2, {b, n, dd}, dt);
+    BoundaryParams p;
+    p.reduction = rr;
+    p.merge_w = from_raw(merge_w, {rr * dd, dn}, dt);
+    if (fusion) {
+      p.fusion_kind = FusionKind::mlp;
+      p.fusion_w = from_raw(fusion_w, {2 * dd, dd}, dt);
+    }
+    FuseResult f = fuse(a, c, p);
+    PatchMergeResult pm = patch_merge(f.y, p);
+    to_raw(pm.y, y);
+    if (!d_y) return;
+    PatchMergeVjp pv = patch_merge_vjp(pm.grouped, p, from_raw(d_y, {b, n / rr, dn}, dt));
+    FuseVjp fv = fuse_vjp(f, p, pv.d_x);
+    to_raw(fv.d_i1, d_i1);
+    to_raw(fv.d_i2, d_i2);
+    to_raw(pv.d_merge_w, d_merge_w);
+    if (fv.d_fusion_w) to_raw(*fv.d_fusion_w, d_fusion_w);
+  });
+}
+
 }  // extern "C"

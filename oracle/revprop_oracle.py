@@ -258,6 +258,45 @@ def vjp_half(b: RevBlock, cf, cg, d_o1, d_o2):
     return (d_o1 + fx, d_o2t), (fg, gg)
 
 
+# ------------------------------------------------------------------ stage boundary
+# ref:proj/core/src/layers.cpp:261-303, ops.cpp:393-406 (group_tokens / ungroup_tokens)
+def fuse(i1, i2, fusion_w=None):
+    """layers.cpp:276-287: average -> (i1 + i2) * 0.5 (ops::scale(ops::add)); mlp ->
+    concat(i1, i2) . fusion_w. Returns (y, concat or None)."""
+    if fusion_w is None:
+        return (i1 + i2) * 0.5, None
+    concat = np.concatenate([i1, i2], -1)
+    return concat @ fusion_w, concat
+
+
+def fuse_vjp(concat, fusion_w, d_y):
+    """layers.cpp:289-303: (d_i1, d_i2, d_fusion_w or None)."""
+    if fusion_w is None:
+        half = d_y * 0.5
+        return half, half, None
+    d = d_y.shape[-1]
+    d_concat = d_y @ fusion_w.T
+    d_fw = concat.reshape(-1, 2 * d).T @ d_y.reshape(-1, d)
+    return d_concat[..., :d], d_concat[..., d:], d_fw
+
+
+def patch_merge(x, merge_w, r):
+    """layers.cpp:261-267: group r adjacent tokens ([B, N, d] -> [B, N/r, r*d], a reshape of
+    row-major data, ops.cpp:393-399) and project by merge_w [(r*d), d_next]."""
+    B, N, d = x.shape
+    assert N % r == 0, "group_tokens: token count not divisible by r"
+    grouped = x.reshape(B, N // r, r * d)
+    return grouped @ merge_w, grouped
+
+
+def patch_merge_vjp(grouped, merge_w, r, d_y):
+    """layers.cpp:269-274: (d_x [B, N, d], d_merge_w)."""
+    B, G, rd = grouped.shape
+    d_grouped = d_y @ merge_w.T
+    d_merge_w = grouped.reshape(-1, rd).T @ d_y.reshape(-1, d_y.shape[-1])
+    return d_grouped.reshape(B, G * r, rd // r), d_merge_w
+
+
 def rev_backward_local(b: RevBlock, o1, o2, d_o1, d_o2):
     """SPEC.md:231-239."""
     inp, cf, cg = recompute(b, o1, o2)
@@ -276,6 +315,43 @@ class ModelConfig:  # SPEC.md:275-278 (isotropic)
     in_dim: int
     num_classes: int
     window: int | None = None
+    # hierarchical (Rev-Swin): blocks / width / heads per stage; the MLP
+    # ratio hidden/width is kept in every stage; stage s has seq_len / r^s tokens and
+    # attends in windows of min(window, tokens) (full attention when window is None).
+    depths: tuple | None = None
+    widths: tuple | None = None
+    stage_heads: tuple | None = None
+    reduction: int = 2
+    fusion: str = "average"  # BoundaryParams.fusion_kind (layers.hpp:142-149)
+
+
+@dataclass
+class StageGeom:
+    depth: int
+    d: int
+    heads: int
+    hidden: int
+    tokens: int
+    window: int | None
+    first: int  # global index of the stage's first block
+
+
+def stages(cfg: ModelConfig):
+    """Per-stage geometry; an isotropic model is one stage."""
+    if not cfg.depths:
+        return [StageGeom(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.window, 0)]
+    assert len(cfg.depths) >= 2 and cfg.hidden % cfg.width == 0
+    ratio = cfg.hidden // cfg.width
+    out, first, n = [], 0, cfg.seq_len
+    for s, L in enumerate(cfg.depths):
+        if s:
+            assert n % cfg.reduction == 0, "seq_len not divisible by r^(stages-1)"
+            n //= cfg.reduction
+        d = cfg.widths[s]
+        w = None if cfg.window is None else min(cfg.window, n)
+        out.append(StageGeom(L, d, cfg.stage_heads[s], ratio * d, n, w, first))
+        first += L
+    return out
 
 
 BLOCK_TENSORS = ("w_qkv", "w_out", "lnF_g", "lnF_b", "w1", "b1", "w2", "b2", "lnG_g", "lnG_b")
@@ -283,13 +359,19 @@ BLOCK_TENSORS = ("w_qkv", "w_out", "lnF_g", "lnF_b", "w1", "b1", "w2", "b2", "ln
 
 def tensor_shapes(cfg: ModelConfig):
     """Flat parameter order shared with the GPU engine (include/revprop_b200.h)."""
-    d, h = cfg.width, cfg.hidden
-    shapes = [("embed_w", (cfg.in_dim, d))]
-    per = dict(w_qkv=(d, 3 * d), w_out=(d, d), lnF_g=(d,), lnF_b=(d,), w1=(d, h), b1=(h,),
-               w2=(h, d), b2=(d,), lnG_g=(d,), lnG_b=(d,))
-    for b in range(cfg.depth):
-        shapes += [(f"blocks.{b}.{n}", per[n]) for n in BLOCK_TENSORS]
-    shapes.append(("head_w", (d, cfg.num_classes)))
+    st = stages(cfg)
+    shapes = [("embed_w", (cfg.in_dim, st[0].d))]
+    for s, g in enumerate(st):
+        d, h = g.d, g.hidden
+        per = dict(w_qkv=(d, 3 * d), w_out=(d, d), lnF_g=(d,), lnF_b=(d,), w1=(d, h), b1=(h,),
+                   w2=(h, d), b2=(d,), lnG_g=(d,), lnG_b=(d,))
+        for b in range(g.first, g.first + g.depth):
+            shapes += [(f"blocks.{b}.{n}", per[n]) for n in BLOCK_TENSORS]
+        if s + 1 < len(st):  # BoundaryParams (layers.hpp:144-149): merge_w, fusion_w
+            shapes.append((f"boundary.{s}.merge_w", (cfg.reduction * d, st[s + 1].d)))
+            if cfg.fusion == "mlp":
+                shapes.append((f"boundary.{s}.fusion_w", (2 * d, d)))
+    shapes.append(("head_w", (st[-1].d, cfg.num_classes)))
     return shapes
 
 
@@ -340,12 +422,21 @@ def unflatten(cfg: ModelConfig, flat):
 def blocks_of(cfg: ModelConfig, flat):
     t = unflatten(cfg, flat)
     blocks = []
-    for b in range(cfg.depth):
-        g = lambda n: t[f"blocks.{b}.{n}"]
-        blocks.append(RevBlock(
-            AttentionParams(g("w_qkv"), g("w_out"), g("lnF_g"), g("lnF_b"), cfg.heads, cfg.window),
-            MlpParams(g("w1"), g("b1"), g("w2"), g("b2"), g("lnG_g"), g("lnG_b"))))
+    for st in stages(cfg):
+        for b in range(st.first, st.first + st.depth):
+            g = lambda n: t[f"blocks.{b}.{n}"]
+            blocks.append(RevBlock(
+                AttentionParams(g("w_qkv"), g("w_out"), g("lnF_g"), g("lnF_b"), st.heads,
+                                st.window),
+                MlpParams(g("w1"), g("b1"), g("w2"), g("b2"), g("lnG_g"), g("lnG_b"))))
     return t["embed_w"], blocks, t["head_w"]
+
+
+def boundaries_of(cfg: ModelConfig, flat):
+    """[(merge_w, fusion_w or None)] for the boundaries after stages 0..S-2."""
+    t = unflatten(cfg, flat)
+    return [(t[f"boundary.{s}.merge_w"], t.get(f"boundary.{s}.fusion_w"))
+            for s in range(len(stages(cfg)) - 1)]
 
 
 def loss_and_grad_head(logits, labels):
@@ -368,30 +459,13 @@ class StepResult:
     recomputed: list = field(default_factory=list)  # recomputed X_b (i1, i2), b = L-1..0
 
 
-def step(cfg: ModelConfig, flat, x, labels, engine="reprop", keep_recomputed=False):
-    """step_reprop (SPEC.md:369-377) / step_pareprop (SPEC.md:378-386).
-
-    pareprop runs lane R (recompute) on a second thread with a capacity-1 rendezvous
-    (SPEC.md:381, 415, 420); the arithmetic is identical, so the grads are identical."""
-    embed_w, blocks, head_w = blocks_of(cfg, flat)
-    # forward_full (SPEC.md:298-306)
-    e = x @ embed_w
-    stage_in = (e, e)  # duplication (SPEC.md:323)
-    o = stage_in
-    for b in blocks:
-        o = rev_forward(b, *o)
-    fused = (o[0] + o[1]) * 0.5  # fuse average (layers.cpp:276-280)
-    pooled = fused.mean(1)  # mean_tokens (ops.cpp:408-427)
-    logits = pooled @ head_w
-    loss, d_logits = loss_and_grad_head(logits, labels)
-    d_head_w = pooled.T @ d_logits
-    d_pooled = d_logits @ head_w.T
-    d_fused = np.repeat(d_pooled[:, None, :] * (1.0 / cfg.seq_len), cfg.seq_len, 1)  # spread
-    d_out = (d_fused * 0.5, d_fused * 0.5)  # fuse_vjp average (layers.cpp:289-293)
+def _backward_stage(blocks, first, stage_in, o, d_out, engine, bgrads, slots, recomputed,
+                    keep_recomputed):
+    """One stage's backward: blocks last -> first, lane R recomputing the
+    block input + caches from its output, lane G running the VJP. pareprop runs lane R on a
+    second thread with a capacity-1 rendezvous; the arithmetic is
+    identical, so the grads are identical. Returns the stage input's cotangent pair."""
     L = len(blocks)
-    bgrads = [None] * L
-    slots = []
-    recomputed = []
 
     def do_r(i, out):
         if i == 0:
@@ -402,11 +476,11 @@ def step(cfg: ModelConfig, flat, x, labels, engine="reprop", keep_recomputed=Fal
         out = o
         for i in range(L - 1, -1, -1):
             inp, cf, cg = do_r(i, out)
-            slots.append(("R", i + 1))
+            slots.append(("R", first + i + 1))
             if keep_recomputed:
                 recomputed.append(inp)
-            d_out, bgrads[i] = vjp_half(blocks[i], cf, cg, *d_out)
-            slots.append(("G", i + 1))
+            d_out, bgrads[first + i] = vjp_half(blocks[i], cf, cg, *d_out)
+            slots.append(("G", first + i + 1))
             out = inp
     elif engine == "pareprop":
         cv = threading.Condition()
@@ -421,7 +495,7 @@ def step(cfg: ModelConfig, flat, x, labels, engine="reprop", keep_recomputed=Fal
                         cv.wait_for(lambda: not box or err)
                     item = do_r(i, out)
                     with cv:
-                        slots.append(("R", i + 1))
+                        slots.append(("R", first + i + 1))
                         box.append((i, item))
                         cv.notify_all()
                     out = item[0]
@@ -442,23 +516,77 @@ def step(cfg: ModelConfig, flat, x, labels, engine="reprop", keep_recomputed=Fal
             assert j == i
             if keep_recomputed:
                 recomputed.append(inp)
-            d_out, bgrads[i] = vjp_half(blocks[i], cf, cg, *d_out)
+            d_out, bgrads[first + i] = vjp_half(blocks[i], cf, cg, *d_out)
             with cv:
-                slots.append(("G", i + 1))
+                slots.append(("G", first + i + 1))
         t.join()
         if err:
             raise RuntimeError(f"pipeline lane failed: {err[0]}")
     else:
         raise ValueError(engine)
+    return d_out
+
+
+def step(cfg: ModelConfig, flat, x, labels, engine="reprop", keep_recomputed=False):
+    """step_reprop / step_pareprop over the isotropic or
+    hierarchical model (forward_full: embed, duplicate, each stage's blocks,
+    at each boundary fuse -> patch_merge -> duplicate; head on fuse-average of the last
+    stage's output). Only each stage's input and output pairs are kept (SPEC.md:301, 325);
+    the backward recomputes the boundary's fuse from the stored stage output."""
+    embed_w, blocks, head_w = blocks_of(cfg, flat)
+    bnds = boundaries_of(cfg, flat)
+    st = stages(cfg)
+    e = x @ embed_w
+    stage_in, stage_out = [], []
+    o = (e, e)  # duplication (SPEC.md:323)
+    for s, g in enumerate(st):
+        stage_in.append(o)
+        for b in blocks[g.first:g.first + g.depth]:
+            o = rev_forward(b, *o)
+        stage_out.append(o)
+        if s + 1 < len(st):
+            f, _ = fuse(*o, bnds[s][1])
+            y, _ = patch_merge(f, bnds[s][0], cfg.reduction)
+            o = (y, y)
+    fused = (o[0] + o[1]) * 0.5  # fuse average (layers.cpp:276-280)
+    pooled = fused.mean(1)  # mean_tokens (ops.cpp:408-427)
+    logits = pooled @ head_w
+    loss, d_logits = loss_and_grad_head(logits, labels)
+    grads = {"head_w": pooled.T @ d_logits}
+    d_pooled = d_logits @ head_w.T
+    n_last = st[-1].tokens
+    d_fused = np.repeat(d_pooled[:, None, :] * (1.0 / n_last), n_last, 1)  # spread_tokens
+    d_out = (d_fused * 0.5, d_fused * 0.5)  # fuse_vjp average (layers.cpp:289-293)
+    bgrads = [None] * len(blocks)
+    slots, recomputed = [], []
+    for s in range(len(st) - 1, -1, -1):
+        g = st[s]
+        d_out = _backward_stage(blocks[g.first:g.first + g.depth], g.first, stage_in[s],
+                                stage_out[s], d_out, engine, bgrads, slots, recomputed,
+                                keep_recomputed)
+        if s > 0:
+            mw, fw = bnds[s - 1]
+            d_y = d_out[0] + d_out[1]  # both halves of the next stage's input are y
+            f, concat = fuse(*stage_out[s - 1], fw)
+            grouped = f.reshape(f.shape[0], -1, cfg.reduction * f.shape[-1])
+            d_f, grads[f"boundary.{s - 1}.merge_w"] = patch_merge_vjp(grouped, mw,
+                                                                       cfg.reduction, d_y)
+            d1, d2, d_fw = fuse_vjp(concat, fw, d_f)
+            if d_fw is not None:
+                grads[f"boundary.{s - 1}.fusion_w"] = d_fw
+            d_out = (d1, d2)
     d_e = d_out[0] + d_out[1]
-    d_embed = x.reshape(-1, x.shape[-1]).T @ d_e.reshape(-1, d_e.shape[-1])
-    parts = [d_embed.reshape(-1)]
-    for fg, gg in bgrads:
-        parts += [fg["d_w_qkv"], fg["d_w_out"], fg["d_ln_gamma"], fg["d_ln_beta"], gg["d_w1"],
-                  gg["d_b1"], gg["d_w2"], gg["d_b2"], gg["d_ln_gamma"], gg["d_ln_beta"]]
-    parts.append(d_head_w)
-    grads = np.concatenate([np.asarray(p).reshape(-1) for p in parts])
-    return StepResult(loss, grads, slots, recomputed)
+    grads["embed_w"] = x.reshape(-1, x.shape[-1]).T @ d_e.reshape(-1, d_e.shape[-1])
+    names = {"d_w_qkv": "w_qkv", "d_w_out": "w_out", "d_ln_gamma": "lnF_g", "d_ln_beta": "lnF_b"}
+    gnames = {"d_w1": "w1", "d_b1": "b1", "d_w2": "w2", "d_b2": "b2", "d_ln_gamma": "lnG_g",
+              "d_ln_beta": "lnG_b"}
+    for b, (fg, gg) in enumerate(bgrads):
+        for k, v in fg.items():
+            grads[f"blocks.{b}.{names[k]}"] = v
+        for k, v in gg.items():
+            grads[f"blocks.{b}.{gnames[k]}"] = v
+    flat_g = np.concatenate([np.asarray(grads[n]).reshape(-1) for n, _ in tensor_shapes(cfg)])
+    return StepResult(loss, flat_g, slots, recomputed)
 
 
 def sgd_update(flat, grads, lr):

@@ -25,6 +25,40 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 TINY = O.ModelConfig(depth=3, width=16, heads=2, hidden=32, seq_len=8, in_dim=16, num_classes=5)
 TINY_WIN = O.ModelConfig(depth=2, width=16, heads=2, hidden=64, seq_len=8, in_dim=16,
                          num_classes=5, window=4)
+# hierarchical (Rev-Swin-style): two stages / average fusion, three stages / mlp fusion, r=4
+HIER_AVG = O.ModelConfig(depth=4, width=16, heads=2, hidden=32, seq_len=16, in_dim=16,
+                         num_classes=5, window=4, depths=(2, 2), widths=(16, 32),
+                         stage_heads=(2, 4), reduction=2)
+HIER_MLP = O.ModelConfig(depth=4, width=16, heads=2, hidden=48, seq_len=32, in_dim=16,
+                         num_classes=5, window=4, depths=(1, 2, 1), widths=(16, 24, 32),
+                         stage_heads=(2, 3, 4), reduction=4, fusion="mlp")
+
+
+def main_hier():
+    """reference_golden_hier.npz: the reference's boundary layers (layers.cpp:261-303) on
+    random arrays, and hierarchical steps through ref_hier_step."""
+    rng = np.random.default_rng(20261017)
+    g = {}
+    for name, fusion, r in [("bavg", None, 2), ("bmlp", True, 4)]:
+        B, N, d, dn = 2, 8, 6, 10
+        i1, i2 = rng.standard_normal((B, N, d)), rng.standard_normal((B, N, d))
+        mw = rng.standard_normal((r * d, dn))
+        fw = rng.standard_normal((2 * d, d)) if fusion else None
+        dy = rng.standard_normal((B, N // r, dn))
+        y, d1, d2, dmw, dfw = R.boundary(i1, i2, mw, fw, r, dy)
+        g.update({f"{name}_{k}": v for k, v in dict(
+            i1=i1, i2=i2, merge_w=mw, d_y=dy, y=y, d_i1=d1, d_i2=d2, d_merge_w=dmw).items()})
+        if fusion:
+            g[f"{name}_fusion_w"], g[f"{name}_d_fusion_w"] = fw, dfw
+    for name, mc in [("havg", HIER_AVG), ("hmlp", HIER_MLP)]:
+        params = O.init_params(mc, 5)
+        assert params.size == R.hier_param_count(mc)
+        x, lab = O.synthetic_batch(mc, 2, seed=13)
+        loss, grads = R.hier_step(mc, params, x, lab)
+        g.update({f"{name}_params": params, f"{name}_x": x, f"{name}_labels": lab,
+                  f"{name}_loss": np.float64(loss), f"{name}_grads": grads})
+    np.savez_compressed(os.path.join(OUT, "reference_golden_hier.npz"), **g)
+    print("wrote", os.path.join(OUT, "reference_golden_hier.npz"), len(g), "arrays")
 
 
 def main():
@@ -68,4 +102,6 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--hier-only" not in sys.argv:
+        main()
+    main_hier()

@@ -327,3 +327,76 @@ def test_data_parallel_decomposition_gloo():
     for pr in ps:
         pr.join(timeout=60)
     assert rel(out[0], full) < 1e-12 and np.array_equal(out[0], out[1])
+
+
+# ---------------------------------------------------------------- hierarchical (Rev-Swin) path
+GOLD_H = np.load(os.path.join(HERE, "golden", "reference_golden_hier.npz"))
+HIER_AVG = O.ModelConfig(depth=4, width=16, heads=2, hidden=32, seq_len=16, in_dim=16,
+                         num_classes=5, window=4, depths=(2, 2), widths=(16, 32),
+                         stage_heads=(2, 4), reduction=2)
+HIER_MLP = O.ModelConfig(depth=4, width=16, heads=2, hidden=48, seq_len=32, in_dim=16,
+                         num_classes=5, window=4, depths=(1, 2, 1), widths=(16, 24, 32),
+                         stage_heads=(2, 3, 4), reduction=4, fusion="mlp")
+
+
+@pytest.mark.parametrize("name,r", [("bavg", 2), ("bmlp", 4)])
+def test_boundary_golden(name, r):
+    """fuse -> patch_merge and the VJPs vs the reference's layers.cpp:261-303."""
+    G = lambda k: GOLD_H[f"{name}_{k}"]
+    fw = G("fusion_w") if f"{name}_fusion_w" in GOLD_H.files else None
+    f, concat = O.fuse(G("i1"), G("i2"), fw)
+    y, grouped = O.patch_merge(f, G("merge_w"), r)
+    assert rel(y, G("y")) < 1e-13
+    d_f, d_mw = O.patch_merge_vjp(grouped, G("merge_w"), r, G("d_y"))
+    d1, d2, d_fw = O.fuse_vjp(concat, fw, d_f)
+    assert rel(d1, G("d_i1")) < 1e-13 and rel(d2, G("d_i2")) < 1e-13
+    assert rel(d_mw, G("d_merge_w")) < 1e-13
+    if fw is not None:
+        assert rel(d_fw, G("d_fusion_w")) < 1e-13
+
+
+def test_boundary_spec_known_answers():
+    """SPEC.md:155-172 examples."""
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((2, 6, 4))
+    sel = np.concatenate([np.eye(4), np.zeros((4, 4))])  # merge_w = [I; 0]
+    y, _ = O.patch_merge(x, sel, 2)
+    assert np.array_equal(y, x[:, 0::2])  # even-indexed tokens
+    assert y.shape == (2, 3, 4)
+    assert np.array_equal(O.fuse(x, x)[0], x)  # idempotent average
+    assert np.all(O.fuse(x, -x)[0] == 0)  # cancellation
+    eye2 = np.concatenate([np.eye(4), np.eye(4)])  # stacked identity -> i1 + i2
+    z = rng.standard_normal(x.shape)
+    assert np.allclose(O.fuse(x, z, eye2)[0], x + z, atol=1e-15)
+    with pytest.raises(AssertionError):
+        O.patch_merge(x[:, :5], sel, 2)
+
+
+@pytest.mark.parametrize("name,mc", [("havg", HIER_AVG), ("hmlp", HIER_MLP)])
+def test_hier_step_golden(name, mc):
+    G = lambda k: GOLD_H[f"{name}_{k}"]
+    params = G("params")
+    assert np.array_equal(params, O.init_params(mc, 5))
+    # shape chain (SPEC.md:297, 320): tokens after stage s = N / r^s, widths chain
+    st = O.stages(mc)
+    assert [g.tokens for g in st] == [mc.seq_len // mc.reduction ** s for s in range(len(st))]
+    r = O.step(mc, params, G("x"), G("labels"))
+    assert abs(r.loss - float(G("loss"))) < 1e-12
+    assert rel(r.grads, G("grads")) < 1e-10
+    p = O.step(mc, params, G("x"), G("labels"), engine="pareprop")
+    assert p.loss == r.loss and np.array_equal(p.grads, r.grads)
+    # slot order per stage: blocks last -> first within a stage, stages last -> first
+    gs = [b for lane, b in r.slots if lane == "G"]
+    assert gs == list(range(mc.depth, 0, -1))
+
+
+@needs_ref
+def test_hier_oracle_matches_compiled_reference():
+    from oracle import ref as R
+    for mc in (HIER_AVG, HIER_MLP):
+        params = O.init_params(mc, 21)
+        x, lab = O.synthetic_batch(mc, 3, seed=8)
+        loss, grads = R.hier_step(mc, params, x, lab)
+        r = O.step(mc, params, x, lab)
+        assert abs(r.loss - loss) < 1e-12
+        assert rel(r.grads, grads) < 1e-10
