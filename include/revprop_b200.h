@@ -167,6 +167,19 @@ typedef struct RpModelConfig {
   int lane_priority; /* 1: gradient lane high / recompute lane low stream priority */
   int optimizer;     /* 0: SGD, 1: AdamW */
   float beta1, beta2, adam_eps, weight_decay;
+  /* Hierarchical (Rev-Swin-style) model, SPEC.md:276-277 / 298-306 / 325: stages >= 2 stages
+   * of stage_depth[s] blocks, width stage_width[s], stage_heads[s] heads, MLP hidden
+   * stage_width[s] * hidden / width, seq_len / reduction^s tokens and attention windows of
+   * min(window, tokens). Stage s >= 1 starts from patch_merge(fuse(stage s-1 output))
+   * duplicated into both halves (ref:proj/core/src/layers.cpp:261-303). stages 0 or 1:
+   * isotropic (depth / width / heads / hidden). Requires depth = sum of stage_depth,
+   * width = stage_width[0], heads = stage_heads[0]. Parameters then follow the order
+   *   embed_w | stage 0 blocks | merge_w_0 [(r d_0), d_1] (, fusion_w_0 [2 d_0, d_0]) |
+   *   stage 1 blocks | ... | head_w [d_last, C]. */
+  int64_t stages;
+  int64_t stage_depth[8], stage_width[8], stage_heads[8];
+  int64_t reduction; /* r: tokens merged per boundary group (2 sequences, 4 2-D grids) */
+  int fusion;        /* BoundaryParams.fusion_kind: 0 average, 1 mlp */
 } RpModelConfig;
 
 /* Ledger-predicted peak activation bytes of an engine (mode 0 vanilla, 1 reprop,

@@ -1,6 +1,8 @@
 // The reversible training engine (host C++ over the sm_100a kernels).
 //
-// Implements the SPEC's engines module for the isotropic model on one B200:
+// Implements the SPEC's engines module on one B200, for the isotropic model and the
+// hierarchical (Rev-Swin-style) one -- stages of blocks joined by fuse + patch_merge
+// boundaries (ref:proj/core/src/layers.cpp:261-303):
 //   step_reprop  forward storing only the stage boundary, backward
 //                                     block L..1 with fused recompute + VJP, one lane
 //   step_pareprop  the same work split over two CUDA streams: lane R
@@ -13,11 +15,14 @@
 // "synchronous memory freeing" pitfall, §3.3, cannot occur). The coupled residual
 // stream and all cotangents are fp32; GEMM operands are bf16 shadows.
 //
-// Buffer rotation (block b maps X_b -> X_{b+1}, X_0 = (e, e) is the stored stage input):
-//   X_j.i1 lives in buf1[j % 2], X_j.i2 in buf2[j % 3] (j >= 1); block-b caches in slot[b % 2].
-//   R(b) writes buf1[b%2], buf2[b%3], slot[b%2]: exactly what VJP(b+2) reads, so R(b) waits
-//   on G_done[b+2] -- the capacity-1 rendezvous of SPEC.md:381/415/420 (R at most one
-//   block ahead, <= 2 blocks of caches live).
+// Buffer rotation, per stage (stage-local block j maps X_j -> X_{j+1}; X_0 = (e, e) is the
+// stored stage input): X_j.i1 lives in the stage's buf1[j % 2], X_j.i2 in buf2[j % 3]
+// (j >= 1), so the stage output X_L stays intact for the backward.
+// Block caches live in slot[b % 2] with b the GLOBAL block index (slots are shared by all
+// stages, sized for the largest). R(b) writes buf1[j%2], buf2[j%3], slot[b%2]: exactly what
+// VJP(b+2) reads, so R(b) waits on G_done[b+2] -- the capacity-1 rendezvous of
+// SPEC.md:381/415/420 (R at most one block ahead, <= 2 blocks of caches live), applied
+// across stage boundaries too.
 // Every kernel's arithmetic is independent of grid size and stream co-residency, so
 // PaReprop reproduces Reprop bit for bit.
 #include <cuda_runtime.h>
@@ -79,11 +84,36 @@ int pick_splits(int64_t M, int64_t N, int64_t K, int bn) {
 
 }  // namespace
 
+// One stage of blocks (an isotropic model has one). Geometry, the stored stage input e
+// (i1 = i2 = e), the rotating X buffers, and the boundary that follows it.
+struct RpStage {
+  int64_t L = 0, first = 0;                   // blocks, global index of the first block
+  int64_t N = 0, d = 0, h = 0, H = 0, W = 0;  // tokens, width, hidden, heads, window
+  int64_t T = 0, block_size = 0;              // rows (batch x tokens), params per block
+  float* e = nullptr;
+  float* buf1[2] = {nullptr, nullptr};
+  float* buf2[3] = {nullptr, nullptr, nullptr};
+  int64_t stash_off = 0;  // Vanilla stash offset of X_1 (floats)
+  // boundary after this stage (ref layers.hpp:144-149): merge_w [(r d), d_next] then
+  // fusion_w [2d, d] (mlp fusion); -1 for the last stage
+  int64_t bnd_tix = -1, bnd_size = 0;
+  RpGemmPlan *b_fuse = nullptr, *b_merge = nullptr, *b_dmerge = nullptr, *b_wmerge = nullptr,
+             *b_dfuse1 = nullptr, *b_dfuse2 = nullptr, *b_wfuse = nullptr;
+};
+
 struct RpEngine {
   RpModelConfig cfg{};
-  int64_t B = 0, N = 0, d = 0, h = 0, H = 0, in = 0, C = 0, L = 0, T = 0, W = 0;
-  int64_t P = 0, block_size = 0;
+  // B, in, C; L = total blocks; T = B * N input rows (stage 0)
+  int64_t B = 0, N = 0, in = 0, C = 0, L = 0, T = 0;
+  int64_t P = 0;
+  std::vector<RpStage> st;
+  std::vector<int> stage_of;        // global block -> stage
+  std::vector<int64_t> blk_tix;     // global block -> tensor index of its w_qkv
+  int64_t head_tix = 0;
+  int64_t r = 2;                    // tokens merged per boundary group
+  int fusion = 0;                   // 0 average, 1 mlp (BoundaryParams.fusion_kind)
   std::vector<int64_t> t_off, t_numel;  // flat tensor table
+  std::vector<int> t_kind;              // init kind: 0 weight, 1 zero (bias, beta), 2 one
   int dev = 0;
   cudaStream_t sG = nullptr, sR = nullptr, sC = nullptr;
   // input pipelining (rp_engine_prefetch_batch): copy stream, staging buffers, events
@@ -112,6 +142,9 @@ struct RpEngine {
   float *d1 = nullptr, *d2 = nullptr;
   uint16_t *d1b = nullptr, *d2b = nullptr, *du = nullptr, *dh = nullptr, *datt = nullptr,
            *dqkv = nullptr, *deb = nullptr;
+  // boundary recompute (fused stage output, bf16 [T, d]; mlp: concat [T, 2d]) and its events
+  uint16_t *fb = nullptr, *cb = nullptr;
+  std::vector<cudaEvent_t> evBnd, evFuse;
   float *ln_ws = nullptr, *col_ws = nullptr, *split_ws = nullptr, *attn_ws = nullptr;
   // head
   float *pooled = nullptr, *logits = nullptr, *dlogits = nullptr, *row_loss = nullptr,
@@ -133,7 +166,7 @@ struct RpEngine {
   size_t prof_used = 0;
   int64_t graph_kernels[3] = {0, 0, 0};
   // Vanilla engine: every block's input pair is stored in the forward
-  float *stash1 = nullptr, *stash2 = nullptr;  // X_1..X_L, [L][T*d] each
+  float *stash1 = nullptr, *stash2 = nullptr;  // per stage: X_1..X_L, [L][T*d] each
   bool vanilla_ready = false, vmode = false;
   std::vector<RpGemmPlan*> vf_proj, vf_w2;
   // optimizer: 0 SGD, 1 AdamW
@@ -173,7 +206,12 @@ int dalloc(RpEngine* g, T** p, int64_t count) {
 
 // tensor index helpers (flat order, SPEC.md:279-282 Model fields)
 enum BlockTensor { kWqkv = 0, kWout, kLnFg, kLnFb, kW1, kB1, kW2, kB2, kLnGg, kLnGb, kPerBlock };
-inline int64_t tix_block(int64_t b, int t) { return 1 + kPerBlock * b + t; }
+inline int64_t tix_block(const RpEngine* g, int64_t b, int t) {
+  return g->blk_tix[static_cast<size_t>(b)] + t;
+}
+inline RpStage& stage_of(RpEngine* g, int64_t b) {
+  return g->st[static_cast<size_t>(g->stage_of[static_cast<size_t>(b)])];
+}
 
 struct GemmArgs {
   const uint16_t* A;
@@ -231,111 +269,154 @@ const uint16_t* wb(const RpEngine* g, int64_t tix) { return g->pb + g->t_off[tix
 const float* wf(const RpEngine* g, int64_t tix) { return g->params + g->t_off[tix]; }
 float* gr(const RpEngine* g, int64_t tix) { return g->grads + g->t_off[tix]; }
 
-// X_j storage: rotating buffers for Reprop / PaReprop, the stash for Vanilla.
-float* X1(RpEngine* g, int64_t j) {
-  if (j == 0) return g->e;
-  return g->vmode ? g->stash1 + (j - 1) * g->T * g->d : g->buf1[j % 2];
+// X_j storage (stage-local j): rotating buffers for Reprop / PaReprop, the stash for Vanilla.
+float* X1(RpEngine* g, const RpStage& S, int64_t j) {
+  if (j == 0) return S.e;
+  return g->vmode ? g->stash1 + S.stash_off + (j - 1) * S.T * S.d : S.buf1[j % 2];
 }
-float* X2(RpEngine* g, int64_t j) {
-  if (j == 0) return g->e;
-  return g->vmode ? g->stash2 + (j - 1) * g->T * g->d : g->buf2[j % 3];
+float* X2(RpEngine* g, const RpStage& S, int64_t j) {
+  if (j == 0) return S.e;
+  return g->vmode ? g->stash2 + S.stash_off + (j - 1) * S.T * S.d : S.buf2[j % 3];
 }
 
 int build_plans(RpEngine* g) {
-  const int64_t T = g->T, d = g->d, h = g->h;
-  const int s_qkv = pick_splits(d, 3 * d, T, kGemmBn), s_proj = pick_splits(d, d, T, kGemmBn),
-            s_w1 = pick_splits(d, h, T, kGemmBn), s_w2 = pick_splits(h, d, T, kGemmBn),
-            s_emb = pick_splits(g->in, d, T, kGemmBn);
   g->plans.resize(static_cast<size_t>(g->L));
-  for (int64_t b = 0; b < g->L; ++b) {
-    BlockPlans& p = g->plans[static_cast<size_t>(b)];
-    Slot& S = g->slot[b % 2];
-    Slot& F = g->slot[0];  // forward temporaries
-    const uint16_t *Wqkv = wb(g, tix_block(b, kWqkv)), *Wout = wb(g, tix_block(b, kWout)),
-                   *W1 = wb(g, tix_block(b, kW1)), *W2 = wb(g, tix_block(b, kW2));
-    const float *b1 = wf(g, tix_block(b, kB1)), *b2 = wf(g, tix_block(b, kB2));
-    // ---- forward (stores nothing)
-    RP_TRY(mk_plan(g, {F.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, F.qkv, 3 * d},
-                   &p.f_qkv));
-    {
-      GemmArgs a{F.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, b + 1), d};
-      a.aux = X2(g, b);
-      RP_TRY(mk_plan(g, a, &p.f_proj));
+  for (size_t si = 0; si < g->st.size(); ++si) {
+    RpStage& St = g->st[si];
+    const int64_t T = St.T, d = St.d, h = St.h;
+    const int s_qkv = pick_splits(d, 3 * d, T, kGemmBn), s_proj = pick_splits(d, d, T, kGemmBn),
+              s_w1 = pick_splits(d, h, T, kGemmBn), s_w2 = pick_splits(h, d, T, kGemmBn);
+    for (int64_t j = 0; j < St.L; ++j) {
+      const int64_t b = St.first + j;
+      BlockPlans& p = g->plans[static_cast<size_t>(b)];
+      Slot& S = g->slot[b % 2];
+      Slot& F = g->slot[0];  // forward temporaries
+      const uint16_t *Wqkv = wb(g, tix_block(g, b, kWqkv)), *Wout = wb(g, tix_block(g, b, kWout)),
+                     *W1 = wb(g, tix_block(g, b, kW1)), *W2 = wb(g, tix_block(g, b, kW2));
+      const float *b1 = wf(g, tix_block(g, b, kB1)), *b2 = wf(g, tix_block(g, b, kB2));
+      // ---- forward (stores nothing)
+      RP_TRY(mk_plan(g, {F.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, F.qkv, 3 * d},
+                     &p.f_qkv));
+      {
+        GemmArgs a{F.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, St, j + 1), d};
+        a.aux = X2(g, St, j);
+        RP_TRY(mk_plan(g, a, &p.f_proj));
+      }
+      {
+        GemmArgs a{F.hF, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU, F.a, h};
+        a.bias = b1;
+        RP_TRY(mk_plan(g, a, &p.f_w1));
+      }
+      {
+        GemmArgs a{F.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, St, j + 1), d};
+        a.aux = X1(g, St, j);
+        a.bias = b2;
+        RP_TRY(mk_plan(g, a, &p.f_w2));
+      }
+      // ---- lane R: inverse with caches
+      {  // keeps gelu'(u) (not u) for the MLP dgrad: slot.u holds the slope
+        GemmArgs a{S.hG, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU_SLOPE, S.a, h};
+        a.out2 = S.u;
+        a.bias = b1;
+        RP_TRY(mk_plan(g, a, &p.r_w1));
+      }
+      RP_TRY(mk_plan(g, {S.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, S.qkv, 3 * d},
+                     &p.r_qkv));
+      if (j > 0) {
+        GemmArgs a{S.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, St, j), d};
+        a.aux = X1(g, St, j + 1);
+        a.bias = b2;
+        a.sign = -1.f;
+        RP_TRY(mk_plan(g, a, &p.r_w2));
+        GemmArgs c{S.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, St, j), d};
+        c.aux = X2(g, St, j + 1);
+        c.sign = -1.f;
+        RP_TRY(mk_plan(g, c, &p.r_proj));
+      }
+      // ---- lane G: VJPs (layers.cpp:171-220, 241-259)
+      {
+        GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_MUL, g->du, h};
+        a.aux = S.u;
+        a.colsum_part = g->col_ws;        // + per-32-row column sums of d_u (-> db1)
+        RP_TRY(mk_plan(g, a, &p.g_dw2));  // d_u = gelu'(u) * (d_o1 . W2^T)
+      }
+      {
+        GemmArgs a{S.a, h, 1, g->d1b, d, 1, h, d, T, RP_EPI_F32, gr(g, tix_block(g, b, kW2)), d};
+        a.splits = s_w2;
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &p.g_ww2));  // dW2 = a^T d_o1
+      }
+      {
+        GemmArgs a{S.hG, d, 1, g->du, h, 1, d, h, T, RP_EPI_F32, gr(g, tix_block(g, b, kW1)), h};
+        a.splits = s_w1;
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &p.g_ww1));  // dW1 = hG^T d_u
+      }
+      RP_TRY(mk_plan(g, {g->du, h, 0, W1, h, 0, T, d, h, RP_EPI_BF16, g->dh, d}, &p.g_dw1));
+      RP_TRY(mk_plan(g, {g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_BF16, g->datt, d}, &p.g_dproj));
+      {
+        GemmArgs a{S.att, d, 1, g->d2b, d, 1, d, d, T, RP_EPI_F32, gr(g, tix_block(g, b, kWout)), d};
+        a.splits = s_proj;
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &p.g_wproj));
+      }
+      {
+        GemmArgs a{S.hF, d, 1, g->dqkv, 3 * d, 1, d, 3 * d, T, RP_EPI_F32,
+                   gr(g, tix_block(g, b, kWqkv)), 3 * d};
+        a.splits = s_qkv;
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &p.g_wqkv));
+      }
+      RP_TRY(mk_plan(g, {g->dqkv, 3 * d, 0, Wqkv, 3 * d, 0, T, d, 3 * d, RP_EPI_BF16, g->dh, d},
+                     &p.g_dqkv));
     }
-    {
-      GemmArgs a{F.hF, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU, F.a, h};
-      a.bias = b1;
-      RP_TRY(mk_plan(g, a, &p.f_w1));
+    // ---- boundary after this stage (layers.cpp:261-303): f = fuse(o1, o2) (bf16, recomputed
+    // from the stored stage output in the backward), e_next = group_r(f) . merge_w (fp32)
+    if (St.bnd_tix >= 0) {
+      const RpStage& Nx = g->st[si + 1];
+      const int64_t rd = g->r * d, dn = Nx.d, Tn = Nx.T;
+      const uint16_t* Mw = wb(g, St.bnd_tix);
+      if (g->fusion == 1)  // f = concat(o1, o2) . fusion_w
+        RP_TRY(mk_plan(g, {g->cb, 2 * d, 0, wb(g, St.bnd_tix + 1), d, 1, T, d, 2 * d, RP_EPI_BF16,
+                           g->fb, d},
+                       &St.b_fuse));
+      RP_TRY(mk_plan(g, {g->fb, rd, 0, Mw, dn, 1, Tn, dn, rd, RP_EPI_F32, Nx.e, dn}, &St.b_merge));
+      // d_f = d_y . merge_w^T  ([Tn, r d] == [T, d] row-major): fp32 into d1 (average
+      // fusion: d_i1 = d_i2 = d_f / 2 next), bf16 into datt (mlp: the operand of two GEMMs)
+      if (g->fusion == 1)
+        RP_TRY(mk_plan(g, {g->deb, dn, 0, Mw, dn, 0, Tn, rd, dn, RP_EPI_BF16, g->datt, rd},
+                       &St.b_dmerge));
+      else
+        RP_TRY(mk_plan(g, {g->deb, dn, 0, Mw, dn, 0, Tn, rd, dn, RP_EPI_F32, g->d1, rd},
+                       &St.b_dmerge));
+      {  // d_merge_w = group_r(f)^T . d_y
+        GemmArgs a{g->fb, rd, 1, g->deb, dn, 1, rd, dn, Tn, RP_EPI_F32, gr(g, St.bnd_tix), dn};
+        a.splits = pick_splits(rd, dn, Tn, kGemmBn);
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &St.b_wmerge));
+      }
+      if (g->fusion == 1) {
+        // d_i1 = d_f . fusion_w[0:d]^T, d_i2 = d_f . fusion_w[d:2d]^T (fp32), d_f bf16 in datt
+        const uint16_t* Fw = wb(g, St.bnd_tix + 1);
+        RP_TRY(mk_plan(g, {g->datt, d, 0, Fw, d, 0, T, d, d, RP_EPI_F32, g->d1, d}, &St.b_dfuse1));
+        RP_TRY(mk_plan(g, {g->datt, d, 0, Fw + d * d, d, 0, T, d, d, RP_EPI_F32, g->d2, d},
+                       &St.b_dfuse2));
+        GemmArgs a{g->cb, 2 * d, 1, g->datt, d, 1, 2 * d, d, T, RP_EPI_F32,
+                   gr(g, St.bnd_tix + 1), d};
+        a.splits = pick_splits(2 * d, d, T, kGemmBn);
+        a.ws = g->split_ws;
+        RP_TRY(mk_plan(g, a, &St.b_wfuse));  // d_fusion_w = concat^T . d_f
+      }
     }
-    {
-      GemmArgs a{F.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, b + 1), d};
-      a.aux = X1(g, b);
-      a.bias = b2;
-      RP_TRY(mk_plan(g, a, &p.f_w2));
-    }
-    // ---- lane R: inverse with caches
-    {  // keeps gelu'(u) (not u) for the MLP dgrad: slot.u holds the slope
-      GemmArgs a{S.hG, d, 0, W1, h, 1, T, h, d, RP_EPI_BIAS_GELU_SLOPE, S.a, h};
-      a.out2 = S.u;
-      a.bias = b1;
-      RP_TRY(mk_plan(g, a, &p.r_w1));
-    }
-    RP_TRY(mk_plan(g, {S.hF, d, 0, Wqkv, 3 * d, 1, T, 3 * d, d, RP_EPI_BF16, S.qkv, 3 * d},
-                   &p.r_qkv));
-    if (b > 0) {
-      GemmArgs a{S.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, b), d};
-      a.aux = X1(g, b + 1);
-      a.bias = b2;
-      a.sign = -1.f;
-      RP_TRY(mk_plan(g, a, &p.r_w2));
-      GemmArgs c{S.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, b), d};
-      c.aux = X2(g, b + 1);
-      c.sign = -1.f;
-      RP_TRY(mk_plan(g, c, &p.r_proj));
-    }
-    // ---- lane G: VJPs (layers.cpp:171-220, 241-259)
-    {
-      GemmArgs a{g->d1b, d, 0, W2, d, 0, T, h, d, RP_EPI_MUL, g->du, h};
-      a.aux = S.u;
-      a.colsum_part = g->col_ws;        // + per-32-row column sums of d_u (-> db1)
-      RP_TRY(mk_plan(g, a, &p.g_dw2));  // d_u = gelu'(u) * (d_o1 . W2^T)
-    }
-    {
-      GemmArgs a{S.a, h, 1, g->d1b, d, 1, h, d, T, RP_EPI_F32, gr(g, tix_block(b, kW2)), d};
-      a.splits = s_w2;
-      a.ws = g->split_ws;
-      RP_TRY(mk_plan(g, a, &p.g_ww2));  // dW2 = a^T d_o1
-    }
-    {
-      GemmArgs a{S.hG, d, 1, g->du, h, 1, d, h, T, RP_EPI_F32, gr(g, tix_block(b, kW1)), h};
-      a.splits = s_w1;
-      a.ws = g->split_ws;
-      RP_TRY(mk_plan(g, a, &p.g_ww1));  // dW1 = hG^T d_u
-    }
-    RP_TRY(mk_plan(g, {g->du, h, 0, W1, h, 0, T, d, h, RP_EPI_BF16, g->dh, d}, &p.g_dw1));
-    RP_TRY(mk_plan(g, {g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_BF16, g->datt, d}, &p.g_dproj));
-    {
-      GemmArgs a{S.att, d, 1, g->d2b, d, 1, d, d, T, RP_EPI_F32, gr(g, tix_block(b, kWout)), d};
-      a.splits = s_proj;
-      a.ws = g->split_ws;
-      RP_TRY(mk_plan(g, a, &p.g_wproj));
-    }
-    {
-      GemmArgs a{S.hF, d, 1, g->dqkv, 3 * d, 1, d, 3 * d, T, RP_EPI_F32,
-                 gr(g, tix_block(b, kWqkv)), 3 * d};
-      a.splits = s_qkv;
-      a.ws = g->split_ws;
-      RP_TRY(mk_plan(g, a, &p.g_wqkv));
-    }
-    RP_TRY(mk_plan(g, {g->dqkv, 3 * d, 0, Wqkv, 3 * d, 0, T, d, 3 * d, RP_EPI_BF16, g->dh, d},
-                   &p.g_dqkv));
   }
   // embedding: e = x . embed_w ; d_embed_w = x^T . (d_i1 + d_i2)
-  RP_TRY(mk_plan(g, {g->inputs, g->in, 0, wb(g, 0), d, 1, T, d, g->in, RP_EPI_F32, g->e, d},
+  const RpStage& S0 = g->st[0];
+  RP_TRY(mk_plan(g, {g->inputs, g->in, 0, wb(g, 0), S0.d, 1, g->T, S0.d, g->in, RP_EPI_F32, S0.e,
+                     S0.d},
                  &g->p_embed));
   {
-    GemmArgs a{g->inputs, g->in, 1, g->deb, d, 1, g->in, d, T, RP_EPI_F32, gr(g, 0), d};
-    a.splits = s_emb;
+    GemmArgs a{g->inputs, g->in, 1, g->deb, S0.d, 1, g->in, S0.d, g->T, RP_EPI_F32, gr(g, 0), S0.d};
+    a.splits = pick_splits(g->in, S0.d, g->T, kGemmBn);
     a.ws = g->split_ws;
     RP_TRY(mk_plan(g, a, &g->p_embed_w));
   }
@@ -373,13 +454,13 @@ int launch(RpGemmPlan* p, cudaStream_t s) {
   return rc;
 }
 
-int ln_fwd(RpEngine* g, const float* x, int64_t tg, int64_t tb, uint16_t* y, float* mean,
-           float* rstd, cudaStream_t s) {
-  return rp_layer_norm_fwd(x, wf(g, tg), wf(g, tb), g->T, g->d, 1e-5, y, mean, rstd, s);
+int ln_fwd(RpEngine* g, const RpStage& St, const float* x, int64_t tg, int64_t tb, uint16_t* y,
+           float* mean, float* rstd, cudaStream_t s) {
+  return rp_layer_norm_fwd(x, wf(g, tg), wf(g, tb), St.T, St.d, 1e-5, y, mean, rstd, s);
 }
 
-int attn_fwd(RpEngine* g, const uint16_t* qkv, uint16_t* att, float* lse, cudaStream_t s) {
-  return rp_attention_fwd(qkv, g->T / g->W, g->W, g->H, g->d / g->H, att, lse, s);
+int attn_fwd(const RpStage& St, const uint16_t* qkv, uint16_t* att, float* lse, cudaStream_t s) {
+  return rp_attention_fwd(qkv, St.T / St.W, St.W, St.H, St.d / St.H, att, lse, s);
 }
 
 void mark(RpEngine* g, int lane, int64_t b, int which, cudaStream_t s) {
@@ -387,91 +468,116 @@ void mark(RpEngine* g, int lane, int64_t b, int which, cudaStream_t s) {
   cudaEventRecord(g->ts[static_cast<size_t>(((lane * g->L) + b) * 2 + which)], s);
 }
 
+// f = fuse(o1, o2) of stage St's output into g->fb (bf16): average (layers.cpp:277-279) or
+// concat . fusion_w (layers.cpp:283-286). Used by the forward and, from the stored stage
+// output, by the backward.
+int boundary_fuse(RpEngine* g, RpStage& St, cudaStream_t s) {
+  const float *o1 = X1(g, St, St.L), *o2 = X2(g, St, St.L);
+  if (g->fusion == 1) {
+    RP_TRY(rpk_concat_bf16(o1, o2, St.T, St.d, g->cb, s));
+    return launch(St.b_fuse, s);
+  }
+  return rpk_fuse_avg_bf16(o1, o2, St.T * St.d, g->fb, s);
+}
+
 int forward(RpEngine* g, cudaStream_t s) {
   RP_TRY(launch(g->p_embed, s));
   Slot& F = g->slot[0];
-  for (int64_t b = 0; b < g->L; ++b) {
-    BlockPlans& p = g->plans[static_cast<size_t>(b)];
-    RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), F.hF, F.meanF, F.rstdF, s));
-    RP_TRY(launch(p.f_qkv, s));
-    RP_TRY(attn_fwd(g, F.qkv, F.att, F.lse, s));
-    RP_TRY(launch(g->vmode ? g->vf_proj[static_cast<size_t>(b)] : p.f_proj, s));  // o2 = i2 + F(i1)
-    RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), F.hF, F.meanF,
-                  F.rstdF, s));
-    RP_TRY(launch(p.f_w1, s));
-    RP_TRY(launch(g->vmode ? g->vf_w2[static_cast<size_t>(b)] : p.f_w2, s));  // o1 = i1 + G(o2)
+  for (RpStage& St : g->st) {
+    for (int64_t j = 0; j < St.L; ++j) {
+      const int64_t b = St.first + j;
+      BlockPlans& p = g->plans[static_cast<size_t>(b)];
+      RP_TRY(ln_fwd(g, St, X1(g, St, j), tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), F.hF,
+                    F.meanF, F.rstdF, s));
+      RP_TRY(launch(p.f_qkv, s));
+      RP_TRY(attn_fwd(St, F.qkv, F.att, F.lse, s));
+      RP_TRY(launch(g->vmode ? g->vf_proj[static_cast<size_t>(b)] : p.f_proj, s));  // o2 = i2 + F(i1)
+      RP_TRY(ln_fwd(g, St, X2(g, St, j + 1), tix_block(g, b, kLnGg), tix_block(g, b, kLnGb), F.hF,
+                    F.meanF, F.rstdF, s));
+      RP_TRY(launch(p.f_w1, s));
+      RP_TRY(launch(g->vmode ? g->vf_w2[static_cast<size_t>(b)] : p.f_w2, s));  // o1 = i1 + G(o2)
+    }
+    if (St.bnd_tix >= 0) {  // fuse -> patch_merge -> duplicate
+      RP_TRY(boundary_fuse(g, St, s));
+      RP_TRY(launch(St.b_merge, s));
+    }
   }
   return RP_OK;
 }
 
 int head(RpEngine* g, cudaStream_t s) {
-  const int64_t B = g->B, d = g->d, C = g->C;
-  const float* hw = wf(g, 1 + kPerBlock * g->L);
-  RP_TRY(rpk_pool(X1(g, g->L), X2(g, g->L), B, g->N, d, g->pooled, s));
+  RpStage& Ls = g->st.back();
+  const int64_t B = g->B, d = Ls.d, C = g->C;
+  const float* hw = wf(g, g->head_tix);
+  RP_TRY(rpk_pool(X1(g, Ls, Ls.L), X2(g, Ls, Ls.L), B, Ls.N, d, g->pooled, s));
   RP_TRY(rpk_simt_gemm(B, C, d, g->pooled, d, 1, hw, C, 1, g->logits, C, s));
   RP_TRY(rpk_cross_entropy(g->logits, g->labels, B, C, g->dlogits, g->row_loss, g->loss, s));
   // the head weight gradient goes to the comm stream (ahead of the head bucket's optimizer
   // step there), in parallel with d_pooled and the spread on the engine stream
   RP_TRY(cuda_ok(cudaEventRecord(g->evLogits, s), "record"));
   RP_TRY(cuda_ok(cudaStreamWaitEvent(g->sC, g->evLogits, 0), "wait"));
-  RP_TRY(rpk_simt_gemm(d, C, B, g->pooled, 1, d, g->dlogits, C, 1, gr(g, 1 + kPerBlock * g->L),
-                       C, g->sC));
+  RP_TRY(rpk_simt_gemm(d, C, B, g->pooled, 1, d, g->dlogits, C, 1, gr(g, g->head_tix), C, g->sC));
   RP_TRY(rpk_simt_gemm(B, d, C, g->dlogits, C, 1, hw, 1, C, g->dpooled, d, s));
-  RP_TRY(rpk_spread(g->dpooled, B, g->N, d, g->d1, g->d2, g->d1b, g->d2b, s));
+  RP_TRY(rpk_spread(g->dpooled, B, Ls.N, d, g->d1, g->d2, g->d1b, g->d2b, s));
   return RP_OK;
 }
 
-// Lane R: recompute block b's input and caches from its output X_{b+1}.
+// Lane R: recompute block b's input and caches from its output X_{j+1}.
 int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
   Slot& S = g->slot[b % 2];
   mark(g, 0, b, 0, s);
-  RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), S.hG, S.meanG,
-                S.rstdG, s));
+  RP_TRY(ln_fwd(g, St, X2(g, St, j + 1), tix_block(g, b, kLnGg), tix_block(g, b, kLnGb), S.hG,
+                S.meanG, S.rstdG, s));
   RP_TRY(launch(p.r_w1, s));
-  if (b > 0 && !g->vmode) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
-  RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), S.hF, S.meanF, S.rstdF, s));
+  if (j > 0 && !g->vmode) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
+  RP_TRY(ln_fwd(g, St, X1(g, St, j), tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), S.hF, S.meanF,
+                S.rstdF, s));
   RP_TRY(launch(p.r_qkv, s));
-  RP_TRY(attn_fwd(g, S.qkv, S.att, S.lse, s));
-  if (b > 0 && !g->vmode) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
+  RP_TRY(attn_fwd(St, S.qkv, S.att, S.lse, s));
+  if (j > 0 && !g->vmode) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
   mark(g, 0, b, 1, s);
   return RP_OK;
 }
 
 // Lane G: the VJP half of rev_backward_local, G-path before F-path.
 // own_b2: this block's MLP output-bias grad from its incoming d_o1 (a column-sum pass);
-// in a step only the top block needs it, every other block's b2 grad is produced by the
+// in a stage only the top block needs it, every other block's b2 grad is produced by the
 // block above in the same pass that writes its d_o1 (next_b2, the F-path LN backward).
 int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
   Slot& S = g->slot[b % 2];
-  const int64_t T = g->T, d = g->d, h = g->h;
+  const int64_t T = St.T, d = St.d, h = St.h;
   mark(g, 1, b, 0, s);
   // ---- G = MLP VJP with d_o1 (layers.cpp:241-259)
   // (the own-b2 column sum runs first: the d_u GEMM below writes its partials to col_ws)
-  if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(b, kB2)), g->col_ws, 0, s));
+  if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(g, b, kB2)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_dw2, s));
   RP_TRY(launch(p.g_ww2, s));
   RP_TRY(launch(p.g_ww1, s));
   // db1 = colsum(d_u): per-32-row partials come out of the d_u GEMM's epilogue (fp32)
-  RP_TRY(rp_colsum_parts(g->col_ws, (T + 31) / 32, h, gr(g, tix_block(b, kB1)), 0, s));
+  RP_TRY(rp_colsum_parts(g->col_ws, (T + 31) / 32, h, gr(g, tix_block(g, b, kB1)), 0, s));
   RP_TRY(launch(p.g_dw1, s));
   // d_o2t = d_o2 + LN_G^T(d_hG)   (in place in d2 / d2b)
-  RP_TRY(rp_layer_norm_bwd(X2(g, b + 1), S.meanG, S.rstdG, wf(g, tix_block(b, kLnGg)), g->dh,
-                           g->d2, T, d, g->d2, g->d2b, gr(g, tix_block(b, kLnGg)),
-                           gr(g, tix_block(b, kLnGb)), g->ln_ws, 0, s));
+  RP_TRY(rp_layer_norm_bwd(X2(g, St, j + 1), S.meanG, S.rstdG, wf(g, tix_block(g, b, kLnGg)),
+                           g->dh, g->d2, T, d, g->d2, g->d2b, gr(g, tix_block(g, b, kLnGg)),
+                           gr(g, tix_block(g, b, kLnGb)), g->ln_ws, 0, s));
   // ---- F = attention VJP with d_o2t (layers.cpp:171-220)
   RP_TRY(launch(p.g_dproj, s));
   RP_TRY(launch(p.g_wproj, s));
-  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / g->W, g->W, g->H, g->d / g->H, g->dqkv,
+  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / St.W, St.W, St.H, d / St.H, g->dqkv,
                           g->attn_ws, s));
   RP_TRY(launch(p.g_wqkv, s));
   RP_TRY(launch(p.g_dqkv, s));
   // d_i1 = d_o1 + LN_F^T(d_hF)    (in place in d1 / d1b); d_i2 = d_o2t (already in d2)
-  RP_TRY(rp_layer_norm_bwd_ex(X1(g, b), S.meanF, S.rstdF, wf(g, tix_block(b, kLnFg)), g->dh,
-                              g->d1, T, d, g->d1, g->d1b, gr(g, tix_block(b, kLnFg)),
-                              gr(g, tix_block(b, kLnFb)),
-                              next_b2 ? gr(g, tix_block(b - 1, kB2)) : nullptr, g->ln_ws, 0, s));
+  RP_TRY(rp_layer_norm_bwd_ex(X1(g, St, j), S.meanF, S.rstdF, wf(g, tix_block(g, b, kLnFg)),
+                              g->dh, g->d1, T, d, g->d1, g->d1b, gr(g, tix_block(g, b, kLnFg)),
+                              gr(g, tix_block(g, b, kLnFb)),
+                              next_b2 ? gr(g, tix_block(g, b - 1, kB2)) : nullptr, g->ln_ws, 0, s));
   mark(g, 1, b, 1, s);
   return RP_OK;
 }
@@ -489,6 +595,27 @@ int bucket_update(RpEngine* g, int64_t off, int64_t n, cudaStream_t s) {
                      1.0f / static_cast<float>(g->world), s);
   return rpk_sgd(g->params + off, g->grads + off, g->pb + off, n, g->lr,
                  1.0f / static_cast<float>(g->world), s);
+}
+
+// Backward through the boundary after stage St (layers.cpp:269-303), on lane G, entered with
+// the next stage's input cotangents in d1/d2 (fp32): d_y = d_i1 + d_i2 (both halves of the
+// next stage's input are y), then patch_merge_vjp and fuse_vjp leave stage St's output
+// cotangents in d1/d2 (+ bf16 shadows). g->fb (and cb) hold fuse(St's output), recomputed
+// by boundary_fuse before this runs (evFuse[s] when it ran on lane R).
+int boundary_vjp(RpEngine* g, RpStage& St, cudaStream_t s) {
+  const RpStage& Nx = g->st[static_cast<size_t>(&St - g->st.data()) + 1];
+  RP_TRY(rpk_add_to_bf16(g->d1, g->d2, g->deb, Nx.T * Nx.d, s));
+  RP_TRY(launch(St.b_wmerge, s));
+  RP_TRY(launch(St.b_dmerge, s));
+  const int64_t n = St.T * St.d;
+  if (g->fusion == 1) {
+    RP_TRY(launch(St.b_wfuse, s));
+    RP_TRY(launch(St.b_dfuse1, s));
+    RP_TRY(launch(St.b_dfuse2, s));
+    RP_TRY(rpk_f32_to_bf16(g->d1, g->d1b, n, s));
+    return rpk_f32_to_bf16(g->d2, g->d2b, n, s);
+  }
+  return rpk_halve_dup(g->d1, n, g->d2, g->d1b, g->d2b, s);  // d_i1 = d_i2 = d_f / 2
 }
 
 int enqueue_step_impl(RpEngine* g, int mode);
@@ -510,37 +637,54 @@ int enqueue_step_impl(RpEngine* g, int mode) {
   RP_TRY(cuda_ok(cudaEventRecord(g->evFwd, sG), "record"));
   // the head bucket can go as soon as the head backward is done
   RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evFwd, 0), "wait"));
-  const int64_t head_off = g->t_off[1 + kPerBlock * g->L];
-  RP_TRY(bucket_update(g, head_off, g->d * g->C, sC));
-  if (mode == 2) {
-    RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evFwd, 0), "wait"));
-    for (int64_t b = g->L - 1; b >= 0; --b) {
-      if (b + 2 <= g->L - 1)
-        RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evG[static_cast<size_t>(b + 2)], 0), "wait"));
-      RP_TRY(lane_r(g, b, sR));
-      RP_TRY(cuda_ok(cudaEventRecord(g->evR[static_cast<size_t>(b)], sR), "record"));
-      RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
-      RP_TRY(lane_g(g, b, sG, b == g->L - 1, b > 0));
+  RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(g->head_tix)], g->st.back().d * g->C, sC));
+  if (mode == 2) RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evFwd, 0), "wait"));
+  for (size_t si = g->st.size(); si-- > 0;) {
+    RpStage& St = g->st[si];
+    for (int64_t j = St.L - 1; j >= 0; --j) {
+      const int64_t b = St.first + j;
+      const bool top = j == St.L - 1, next_b2 = j > 0;
+      if (mode == 2) {
+        if (b + 2 <= g->L - 1)
+          RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evG[static_cast<size_t>(b + 2)], 0), "wait"));
+        RP_TRY(lane_r(g, b, sR));
+        RP_TRY(cuda_ok(cudaEventRecord(g->evR[static_cast<size_t>(b)], sR), "record"));
+        RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
+      } else {
+        RP_TRY(lane_r(g, b, sG));
+      }
+      RP_TRY(lane_g(g, b, sG, top, next_b2));
       RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
-      RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
+      RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(tix_block(g, b, 0))], St.block_size, sC));
     }
-    RP_TRY(cuda_ok(cudaEventRecord(g->evRDone, sR), "record"));
-  } else {
-    for (int64_t b = g->L - 1; b >= 0; --b) {
-      RP_TRY(lane_r(g, b, sG));
-      RP_TRY(lane_g(g, b, sG, b == g->L - 1, b > 0));
-      RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
-      RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
-      RP_TRY(bucket_update(g, g->t_off[tix_block(b, 0)], g->block_size, sC));
+    if (si == 0) break;
+    // boundary between stage si-1 and si: recompute fuse(stage si-1 output) -- on lane R
+    // under PaReprop (after lane G has finished the previous boundary's use of fb / cb) --
+    // then the boundary VJP on lane G.
+    RpStage& Pv = g->st[si - 1];
+    if (mode == 2) {
+      if (si + 1 < g->st.size())
+        RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evBnd[si], 0), "wait"));
+      RP_TRY(boundary_fuse(g, Pv, sR));
+      RP_TRY(cuda_ok(cudaEventRecord(g->evFuse[si - 1], sR), "record"));
+      RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evFuse[si - 1], 0), "wait"));
+    } else {
+      RP_TRY(boundary_fuse(g, Pv, sG));
     }
+    RP_TRY(boundary_vjp(g, Pv, sG));
+    RP_TRY(cuda_ok(cudaEventRecord(g->evBnd[si - 1], sG), "record"));
+    RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evBnd[si - 1], 0), "wait"));
+    RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(Pv.bnd_tix)], Pv.bnd_size, sC));
   }
+  if (mode == 2) RP_TRY(cuda_ok(cudaEventRecord(g->evRDone, sR), "record"));
   // embedding backward: e fed both halves -> d_e = d_i1 + d_i2
-  RP_TRY(rpk_add_to_bf16(g->d1, g->d2, g->deb, g->T * g->d, sG));
+  const RpStage& S0 = g->st[0];
+  RP_TRY(rpk_add_to_bf16(g->d1, g->d2, g->deb, S0.T * S0.d, sG));
   RP_TRY(launch(g->p_embed_w, sG));
   RP_TRY(cuda_ok(cudaEventRecord(g->evEmbed, sG), "record"));
   RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evEmbed, 0), "wait"));
-  RP_TRY(bucket_update(g, 0, g->in * g->d, sC));
+  RP_TRY(bucket_update(g, 0, g->in * S0.d, sC));
   if (g->world > 1) {
     ncclResult_t r = ncclAllReduce(g->loss, g->loss, 1, ncclFloat32, ncclAvg, g->comm, sC);
     if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
@@ -565,34 +709,107 @@ void set_partition(RpEngine* g, int mode) {
 
 }  // namespace
 
+// Stage geometry from the config (validated); no allocation. An isotropic model is one stage.
+namespace {
+int stage_geoms(const RpModelConfig* c, std::vector<RpStage>* out) {
+  out->clear();
+  if (c->depth < 1 || c->width < 16 || c->heads < 1 || c->hidden < 16 || c->seq_len < 1 ||
+      c->in_dim < 8 || c->num_classes < 1 || c->batch < 1)
+    return rp_fail(RP_ERR_CONFIG, "engine_create: invalid model config");
+  if (c->in_dim % 16) return rp_fail(RP_ERR_CONFIG, "engine_create: in_dim must be a multiple of 16");
+  const bool hier = c->stages >= 2;
+  const int64_t S = hier ? c->stages : 1;
+  if (S > 8) return rp_fail(RP_ERR_CONFIG, "engine_create: at most 8 stages");
+  if (hier) {
+    int64_t tot = 0;
+    for (int64_t s = 0; s < S; ++s) tot += c->stage_depth[s];
+    if (tot != c->depth || c->stage_width[0] != c->width || c->stage_heads[0] != c->heads)
+      return rp_fail(RP_ERR_CONFIG,
+                     "engine_create: hierarchical config needs depth = sum(stage_depth), "
+                     "width = stage_width[0], heads = stage_heads[0]");
+    if (c->hidden % c->width)
+      return rp_fail(RP_ERR_CONFIG, "engine_create: hidden must be a multiple of width (MLP ratio)");
+    if (c->reduction < 1) return rp_fail(RP_ERR_CONFIG, "engine_create: reduction must be >= 1");
+    if (c->fusion != 0 && c->fusion != 1)
+      return rp_fail(RP_ERR_CONFIG, "engine_create: fusion must be 0 (average) or 1 (mlp)");
+  }
+  int64_t n = c->seq_len, first = 0;
+  for (int64_t s = 0; s < S; ++s) {
+    RpStage St;
+    if (s > 0) {
+      if (n % c->reduction)
+        return rp_fail(RP_ERR_SHAPE, "group_tokens: token count not divisible by r");
+      n /= c->reduction;
+    }
+    St.L = hier ? c->stage_depth[s] : c->depth;
+    St.d = hier ? c->stage_width[s] : c->width;
+    St.H = hier ? c->stage_heads[s] : c->heads;
+    St.h = hier ? St.d * (c->hidden / c->width) : c->hidden;
+    St.N = n;
+    St.first = first;
+    St.T = c->batch * n;
+    if (St.L < 1 || St.d < 16 || St.H < 1 || St.d % St.H || (St.d / St.H) % 8 || St.d / St.H > 128)
+      return rp_fail(RP_ERR_CONFIG,
+                     "engine_create: invalid stage (head_dim = width/heads must be a multiple of "
+                     "8, at most 128)");
+    if (St.d % 64 || St.h % 64)  // the GEMM epilogue works in 64-column chunks
+      return rp_fail(RP_ERR_CONFIG, "engine_create: width/hidden must be multiples of 64");
+    // hierarchical stages attend in windows of min(window, tokens) (the last stages of a
+    // Swin-style model are a single window); the isotropic model keeps the reference's
+    // rule that the window must divide the sequence (layers.cpp:118-120)
+    St.W = c->window > 0 ? (hier ? std::min(c->window, n) : c->window) : n;
+    if (n % St.W)
+      return rp_fail(RP_ERR_SHAPE, "attention: sequence length not divisible by window");
+    St.block_size = 4 * St.d * St.d + 2 * St.d * St.h + St.h + 5 * St.d;
+    first += St.L;
+    out->push_back(St);
+  }
+  return RP_OK;
+}
+}  // namespace
+
 // ---------------------------------------------------------------- activation ledger
 // Bytes of activation storage each engine keeps live at its peak (SPEC.md:346-349
 // MemoryLedger semantics, ref:proj/core/include/revprop/ledger.hpp:18-62), from the
-// arena plan of this engine: stored stage boundary, per-block recompute footprint,
+// arena plan of this engine: stored stage boundaries, per-block recompute footprint,
 // cotangents and lane-G temporaries. Parameters, gradients and split-K / reduction
 // workspaces are excluded (they do not scale with depth or batch in the same way).
 //   mode 0 vanilla   stores every block's input pair + one block's caches
-//   mode 1 reprop    stage input + stage output + one block footprint
+//   mode 1 reprop    every stage's input + output + one block footprint
 //   mode 2 pareprop  reprop + one more block footprint (rendezvous depth 1)
+// Per-block quantities are the largest over the stages (the slots are shared).
 extern "C" int rp_activation_bytes(const RpModelConfig* c, int mode, int64_t* out_peak,
                                    int64_t* out_block_footprint) {
   if (!c || !out_peak) return rp_fail(RP_ERR_CONTRACT, "null argument");
   if (mode < 0 || mode > 2) return rp_fail(RP_ERR_CONFIG, "mode must be 0, 1 or 2");
-  const int64_t T = c->batch * c->seq_len, d = c->width, h = c->hidden, H = c->heads;
-  const int64_t pair = 2 * T * d * 4;  // one coupled (i1, i2) fp32 pair
-  // block footprint: recomputed input pair + F caches (hF, qkv, att: bf16; lse, LN stats)
-  // + G caches (hG, slope, a: bf16; LN stats)
-  const int64_t cache_f = T * d * 2 + T * 3 * d * 2 + T * d * 2 + T * H * 4 + 2 * T * 4;
-  const int64_t cache_g = T * d * 2 + 2 * T * h * 2 + 2 * T * 4;
-  const int64_t block = pair + cache_f + cache_g;
-  const int64_t stage = T * d * 4 /* embedding e, shared by i1 = i2 */ + pair /* output */;
-  const int64_t cot = 2 * T * d * 4 + 2 * T * d * 2;                        // d_out pair
-  const int64_t temps = T * h * 2 + 2 * T * d * 2 + T * 3 * d * 2 + T * d * 2;  // du,dh,datt,dqkv,de
+  std::vector<RpStage> st;
+  RP_TRY(stage_geoms(c, &st));
+  int64_t block = 0, cache = 0, cot = 0, temps = 0, stages = 0, stash = 0;
+  for (const RpStage& S : st) {
+    const int64_t T = S.T, d = S.d, h = S.h, H = S.H;
+    const int64_t pair = 2 * T * d * 4;  // one coupled (i1, i2) fp32 pair
+    // block footprint: recomputed input pair + F caches (hF, qkv, att: bf16; lse, LN stats)
+    // + G caches (hG, slope, a: bf16; LN stats)
+    const int64_t cache_f = T * d * 2 + T * 3 * d * 2 + T * d * 2 + T * H * 4 + 2 * T * 4;
+    const int64_t cache_g = T * d * 2 + 2 * T * h * 2 + 2 * T * 4;
+    block = std::max(block, pair + cache_f + cache_g);
+    cache = std::max(cache, cache_f + cache_g);
+    cot = std::max(cot, 2 * T * d * 4 + 2 * T * d * 2);                               // d_out pair
+    temps = std::max(temps, T * h * 2 + 2 * T * d * 2 + T * 3 * d * 2 + T * d * 2);  // du,dh,datt,dqkv,de
+    stages += T * d * 4 /* stage input e, shared by i1 = i2 */ + pair /* stage output */;
+    stash += T * d * 4 + S.L * pair;
+  }
+  if (st.size() > 1) {  // boundary recompute buffers (fused output, mlp concat)
+    int64_t fb = 0;
+    for (size_t s = 0; s + 1 < st.size(); ++s)
+      fb = std::max(fb, st[s].T * st[s].d * 2 * (c->fusion == 1 ? 3 : 1));
+    temps += fb;
+  }
   int64_t peak = 0;
   if (mode == 0)
-    peak = T * d * 4 + c->depth * pair + (block - pair) + cot + temps;
+    peak = stash + cache + cot + temps;
   else
-    peak = stage + (mode == 2 ? 2 : 1) * block + cot + temps;
+    peak = stages + (mode == 2 ? 2 : 1) * block + cot + temps;
   *out_peak = peak;
   if (out_block_footprint) *out_block_footprint = block;
   return RP_OK;
@@ -601,57 +818,60 @@ extern "C" int rp_activation_bytes(const RpModelConfig* c, int mode, int64_t* ou
 extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   if (!c || !out) return rp_fail(RP_ERR_CONTRACT, "engine_create: null argument");
   *out = nullptr;
-  if (c->depth < 1 || c->width < 16 || c->heads < 1 || c->width % c->heads ||
-      (c->width / c->heads) % 8 || c->width / c->heads > 128 || c->hidden < 16 ||
-      c->seq_len < 1 || c->in_dim < 8 || c->num_classes < 1 || c->batch < 1)
-    return rp_fail(RP_ERR_CONFIG,
-                   "engine_create: invalid model config (head_dim = width/heads must be a "
-                   "multiple of 8, at most 128)");
-  if (c->width % 16 || c->hidden % 16 || c->in_dim % 16)
-    return rp_fail(RP_ERR_CONFIG, "engine_create: width/hidden/in_dim must be multiples of 16");
-  const int64_t W = c->window > 0 ? c->window : c->seq_len;
-  if (c->seq_len % W) return rp_fail(RP_ERR_SHAPE, "attention: sequence length not divisible by window");
+  std::vector<RpStage> geo;
+  RP_TRY(stage_geoms(c, &geo));
   RpEngine* g = new RpEngine();
   g->cfg = *c;
+  g->st = geo;
   g->B = c->batch;
   g->N = c->seq_len;
-  g->d = c->width;
-  g->h = c->hidden;
-  g->H = c->heads;
   g->in = c->in_dim;
   g->C = c->num_classes;
   g->L = c->depth;
-  g->W = W;
   g->T = g->B * g->N;
+  g->r = c->stages >= 2 ? c->reduction : 2;
+  g->fusion = c->stages >= 2 ? c->fusion : 0;
   g->dev = c->device;
-  const int64_t d = g->d, h = g->h, T = g->T;
   auto fail = [&](int rc) {
     rp_engine_destroy(g);
     return rc;
   };
   if (cudaSetDevice(g->dev) != cudaSuccess) return fail(rp_fail(RP_ERR_CUDA, "cudaSetDevice failed"));
-  // flat tensor table
-  auto add = [&](int64_t n) {
+  // flat tensor table: embed_w | stage blocks | boundary | ... | head_w
+  auto add = [&](int64_t n, int kind) {
     const int64_t off = g->t_off.empty() ? 0 : g->t_off.back() + g->t_numel.back();
     g->t_off.push_back(off);
     g->t_numel.push_back(n);
+    g->t_kind.push_back(kind);
   };
-  add(g->in * d);
-  for (int64_t b = 0; b < g->L; ++b) {
-    add(d * 3 * d);
-    add(d * d);
-    add(d);
-    add(d);
-    add(d * h);
-    add(h);
-    add(h * d);
-    add(d);
-    add(d);
-    add(d);
+  add(g->in * g->st[0].d, 0);
+  for (size_t s = 0; s < g->st.size(); ++s) {
+    RpStage& St = g->st[s];
+    const int64_t d = St.d, h = St.h;
+    for (int64_t j = 0; j < St.L; ++j) {
+      g->blk_tix.push_back(static_cast<int64_t>(g->t_off.size()));
+      g->stage_of.push_back(static_cast<int>(s));
+      add(d * 3 * d, 0);  // w_qkv
+      add(d * d, 0);      // w_out
+      add(d, 2);          // lnF gamma
+      add(d, 1);          // lnF beta
+      add(d * h, 0);      // w1
+      add(h, 1);          // b1
+      add(h * d, 0);      // w2
+      add(d, 1);          // b2
+      add(d, 2);          // lnG gamma
+      add(d, 1);          // lnG beta
+    }
+    if (s + 1 < g->st.size()) {
+      St.bnd_tix = static_cast<int64_t>(g->t_off.size());
+      add(g->r * d * g->st[s + 1].d, 0);    // merge_w
+      if (g->fusion == 1) add(2 * d * d, 0);  // fusion_w
+      St.bnd_size = g->r * d * g->st[s + 1].d + (g->fusion == 1 ? 2 * d * d : 0);
+    }
   }
-  add(d * g->C);
+  g->head_tix = static_cast<int64_t>(g->t_off.size());
+  add(g->st.back().d * g->C, 0);
   g->P = g->t_off.back() + g->t_numel.back();
-  g->block_size = 4 * d * d + 2 * d * h + h + 5 * d;
   int rc = RP_OK;
   // Lane G (the critical path) gets the highest stream priority, lane R and the comm /
   // SGD stream the lowest: the block scheduler then fills idle SMs and kernel tails with
@@ -671,47 +891,75 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
     return fail(rc);
   g->evR.resize(static_cast<size_t>(g->L));
   g->evG.resize(static_cast<size_t>(g->L));
-  for (auto* v : {&g->evR, &g->evG})
+  g->evBnd.resize(g->st.size());
+  g->evFuse.resize(g->st.size());
+  for (auto* v : {&g->evR, &g->evG, &g->evBnd, &g->evFuse})
     for (auto& e : *v) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed, &g->evLogits})
     cudaEventCreateWithFlags(e, cudaEventDisableTiming);
   g->ts.resize(static_cast<size_t>(4 * g->L));
   for (auto& e : g->ts) cudaEventCreate(&e);
-  // arena
+  // arena: per-block buffers sized for the largest stage (shared by all stages)
+  int64_t Td = 0, Th = 0, TH = 0, Tmax = 0, ln_ws = 0, attn_ws = 0, col_ws = 0, split_ws = 0;
+  int64_t fb = 0;
+  auto splits_ws = [&](int64_t m, int64_t n, int64_t k) {
+    const int sp = pick_splits(m, n, k, kGemmBn);
+    if (sp > 1) split_ws = std::max<int64_t>(split_ws, sp * m * n);
+  };
+  for (size_t s = 0; s < g->st.size(); ++s) {
+    const RpStage& St = g->st[s];
+    const int64_t T = St.T, d = St.d, h = St.h;
+    Td = std::max(Td, T * d);
+    Th = std::max(Th, T * h);
+    TH = std::max(TH, T * St.H);
+    Tmax = std::max(Tmax, T);
+    ln_ws = std::max(ln_ws, rp_layer_norm_bwd_workspace_floats(T, d));
+    attn_ws = std::max(attn_ws, rp_attention_bwd_workspace_floats(T / St.W, St.W, St.H));
+    col_ws = std::max(col_ws, rp_colsum_workspace_floats(T, h > d ? h : d));
+    col_ws = std::max(col_ws, ((T + 31) / 32) * h);  // d_u epilogue partials
+    for (auto mn : {std::pair<int64_t, int64_t>{d, 3 * d}, {d, d}, {d, h}, {h, d}}) splits_ws(mn.first, mn.second, T);
+    if (s + 1 < g->st.size()) {
+      const RpStage& Nx = g->st[s + 1];
+      splits_ws(g->r * d, Nx.d, Nx.T);
+      if (g->fusion == 1) splits_ws(2 * d, d, T);
+      fb = std::max(fb, T * d);
+    }
+  }
+  splits_ws(g->in, g->st[0].d, g->T);
   if ((rc = dalloc(g, &g->params, g->P)) || (rc = dalloc(g, &g->grads, g->P)) ||
       (rc = dalloc(g, &g->pb, g->P)) || (rc = dalloc(g, &g->lr, 1)) ||
-      (rc = dalloc(g, &g->inputs, T * g->in)) || (rc = dalloc(g, &g->labels, g->B)) ||
-      (rc = dalloc(g, &g->e, T * d)) || (rc = dalloc(g, &g->buf1[0], T * d)) ||
-      (rc = dalloc(g, &g->buf1[1], T * d)) || (rc = dalloc(g, &g->buf2[0], T * d)) ||
-      (rc = dalloc(g, &g->buf2[1], T * d)) || (rc = dalloc(g, &g->buf2[2], T * d)))
+      (rc = dalloc(g, &g->inputs, g->T * g->in)) || (rc = dalloc(g, &g->labels, g->B)))
     return fail(rc);
-  for (Slot& S : g->slot) {
-    if ((rc = dalloc(g, &S.hF, T * d)) || (rc = dalloc(g, &S.qkv, T * 3 * d)) ||
-        (rc = dalloc(g, &S.att, T * d)) || (rc = dalloc(g, &S.hG, T * d)) ||
-        (rc = dalloc(g, &S.u, T * h)) || (rc = dalloc(g, &S.a, T * h)) ||
-        (rc = dalloc(g, &S.lse, T * g->H)) || (rc = dalloc(g, &S.meanF, T)) ||
-        (rc = dalloc(g, &S.rstdF, T)) || (rc = dalloc(g, &S.meanG, T)) ||
-        (rc = dalloc(g, &S.rstdG, T)))
+  for (RpStage& St : g->st) {
+    const int64_t n = St.T * St.d;
+    if ((rc = dalloc(g, &St.e, n)) || (rc = dalloc(g, &St.buf1[0], n)) ||
+        (rc = dalloc(g, &St.buf1[1], n)) || (rc = dalloc(g, &St.buf2[0], n)) ||
+        (rc = dalloc(g, &St.buf2[1], n)) || (rc = dalloc(g, &St.buf2[2], n)))
       return fail(rc);
   }
-  int64_t split_ws = 0;
-  for (auto mn : {std::pair<int64_t, int64_t>{d, 3 * d}, {d, d}, {d, h}, {h, d}, {g->in, d}}) {
-    const int s = pick_splits(mn.first, mn.second, T, kGemmBn);
-    if (s > 1) split_ws = std::max<int64_t>(split_ws, s * mn.first * mn.second);
+  for (Slot& S : g->slot) {
+    if ((rc = dalloc(g, &S.hF, Td)) || (rc = dalloc(g, &S.qkv, 3 * Td)) ||
+        (rc = dalloc(g, &S.att, Td)) || (rc = dalloc(g, &S.hG, Td)) ||
+        (rc = dalloc(g, &S.u, Th)) || (rc = dalloc(g, &S.a, Th)) ||
+        (rc = dalloc(g, &S.lse, TH)) || (rc = dalloc(g, &S.meanF, Tmax)) ||
+        (rc = dalloc(g, &S.rstdF, Tmax)) || (rc = dalloc(g, &S.meanG, Tmax)) ||
+        (rc = dalloc(g, &S.rstdG, Tmax)))
+      return fail(rc);
   }
-  int64_t col_ws = rp_colsum_workspace_floats(T, h > d ? h : d);
-  if (col_ws < ((T + 31) / 32) * h) col_ws = ((T + 31) / 32) * h;  // d_u epilogue partials
-  if ((rc = dalloc(g, &g->d1, T * d)) || (rc = dalloc(g, &g->d2, T * d)) ||
-      (rc = dalloc(g, &g->d1b, T * d)) || (rc = dalloc(g, &g->d2b, T * d)) ||
-      (rc = dalloc(g, &g->du, T * h)) || (rc = dalloc(g, &g->dh, T * d)) ||
-      (rc = dalloc(g, &g->datt, T * d)) || (rc = dalloc(g, &g->dqkv, T * 3 * d)) ||
-      (rc = dalloc(g, &g->deb, T * d)) ||
-      (rc = dalloc(g, &g->ln_ws, rp_layer_norm_bwd_workspace_floats(T, d))) ||
+  if ((rc = dalloc(g, &g->d1, Td)) || (rc = dalloc(g, &g->d2, Td)) ||
+      (rc = dalloc(g, &g->d1b, Td)) || (rc = dalloc(g, &g->d2b, Td)) ||
+      (rc = dalloc(g, &g->du, Th)) || (rc = dalloc(g, &g->dh, Td)) ||
+      (rc = dalloc(g, &g->datt, Td)) || (rc = dalloc(g, &g->dqkv, 3 * Td)) ||
+      (rc = dalloc(g, &g->deb, Td)) || (rc = dalloc(g, &g->ln_ws, ln_ws)) ||
       (rc = dalloc(g, &g->col_ws, col_ws)) || (rc = dalloc(g, &g->split_ws, split_ws)) ||
-      (rc = dalloc(g, &g->attn_ws, rp_attention_bwd_workspace_floats(T / W, W, g->H))) ||
-      (rc = dalloc(g, &g->pooled, g->B * d)) || (rc = dalloc(g, &g->logits, g->B * g->C)) ||
-      (rc = dalloc(g, &g->dlogits, g->B * g->C)) || (rc = dalloc(g, &g->row_loss, g->B)) ||
-      (rc = dalloc(g, &g->loss, 1)) || (rc = dalloc(g, &g->dpooled, g->B * d)))
+      (rc = dalloc(g, &g->attn_ws, attn_ws)) ||
+      (rc = dalloc(g, &g->pooled, g->B * g->st.back().d)) ||
+      (rc = dalloc(g, &g->logits, g->B * g->C)) || (rc = dalloc(g, &g->dlogits, g->B * g->C)) ||
+      (rc = dalloc(g, &g->row_loss, g->B)) || (rc = dalloc(g, &g->loss, 1)) ||
+      (rc = dalloc(g, &g->dpooled, g->B * g->st.back().d)))
+    return fail(rc);
+  if (fb > 0 && ((rc = dalloc(g, &g->fb, fb)) ||
+                 (g->fusion == 1 && (rc = dalloc(g, &g->cb, 2 * fb)))))
     return fail(rc);
   if ((rc = build_plans(g))) return fail(rc);
   g->optimizer = c->optimizer;
@@ -750,7 +998,7 @@ extern "C" void rp_engine_destroy(RpEngine* g) {
     if (x) cudaGraphExecDestroy(x);
   for (RpGemmPlan* p : g->all_plans) rp_gemm_plan_destroy(p);
   for (void* p : g->allocs) cudaFree(p);
-  for (auto* v : {&g->evR, &g->evG, &g->ts})
+  for (auto* v : {&g->evR, &g->evG, &g->ts, &g->evBnd, &g->evFuse})
     for (auto& e : *v)
       if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed, g->evLogits})
@@ -781,12 +1029,7 @@ extern "C" int rp_engine_init_params(RpEngine* g, uint64_t seed) {
   if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
   // weights trunc-normal(0.02), biases zero; LayerNorm gamma = 1, beta = 0.
   for (size_t j = 0; j < g->t_off.size(); ++j) {
-    int kind = 0;
-    if (j >= 1 && j < 1 + static_cast<size_t>(kPerBlock * g->L)) {
-      const int t = static_cast<int>((j - 1) % kPerBlock);
-      if (t == kB1 || t == kB2 || t == kLnFb || t == kLnGb) kind = 1;
-      if (t == kLnFg || t == kLnGg) kind = 2;
-    }
+    const int kind = g->t_kind[j];
     RP_TRY(rpk_init_tensor(g->params + g->t_off[j], g->t_numel[j], seed, j, kind, 0.02, g->sG));
   }
   RP_TRY(rpk_f32_to_bf16(g->params, g->pb, g->P, g->sG));
@@ -910,23 +1153,29 @@ extern "C" int rp_engine_set_lr(RpEngine* g, float lr) {
 extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
   if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
   if (g->vanilla_ready) return RP_OK;
-  const int64_t n = g->L * g->T * g->d;
+  int64_t n = 0;
+  for (RpStage& St : g->st) {
+    St.stash_off = n;
+    n += St.L * St.T * St.d;
+  }
   RP_TRY(dalloc(g, &g->stash1, n));
   RP_TRY(dalloc(g, &g->stash2, n));
-  const int64_t T = g->T, d = g->d, h = g->h;
   Slot& F = g->slot[0];
   g->vmode = true;
   g->vf_proj.resize(static_cast<size_t>(g->L));
   g->vf_w2.resize(static_cast<size_t>(g->L));
   for (int64_t b = 0; b < g->L; ++b) {
-    GemmArgs a{F.att, d, 0, wb(g, tix_block(b, kWout)), d, 1, T, d, d, RP_EPI_RESID,
-               X2(g, b + 1), d};
-    a.aux = X2(g, b);
+    RpStage& St = stage_of(g, b);
+    const int64_t T = St.T, d = St.d, h = St.h, j = b - St.first;
+    GemmArgs a{F.att, d, 0, wb(g, tix_block(g, b, kWout)), d, 1, T, d, d, RP_EPI_RESID,
+               X2(g, St, j + 1), d};
+    a.aux = X2(g, St, j);
     int rc = mk_plan(g, a, &g->vf_proj[static_cast<size_t>(b)]);
     if (rc == RP_OK) {
-      GemmArgs c{F.a, h, 0, wb(g, tix_block(b, kW2)), d, 1, T, d, h, RP_EPI_RESID, X1(g, b + 1), d};
-      c.aux = X1(g, b);
-      c.bias = wf(g, tix_block(b, kB2));
+      GemmArgs c{F.a, h, 0, wb(g, tix_block(g, b, kW2)), d, 1, T, d, h, RP_EPI_RESID,
+                 X1(g, St, j + 1), d};
+      c.aux = X1(g, St, j);
+      c.bias = wf(g, tix_block(g, b, kB2));
       rc = mk_plan(g, c, &g->vf_w2[static_cast<size_t>(b)]);
     }
     if (rc != RP_OK) {
@@ -934,6 +1183,8 @@ extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
       return rc;
     }
   }
+  // the boundary merge GEMMs read fuse(stage output) computed from the stash in vmode and
+  // write the next stage's e, which is not stashed: the same plans serve both modes
   g->vmode = false;
   g->vanilla_ready = true;
   return RP_OK;
@@ -1107,42 +1358,49 @@ extern "C" int rp_engine_comm_init(RpEngine* g, const uint8_t* id128, int world,
 
 // ---------------------------------------------------------------- block-level entry points
 // (revcore on device pointers owned by the caller; params are the engine's block b)
-// rev_forward: (i1, i2) -> (o1, o2), fp32 [T, d]
+// rev_forward: (i1, i2) -> (o1, o2), fp32 [T_s, d_s] of block b's stage
 extern "C" int rp_engine_rev_forward(RpEngine* g, int64_t b, const float* i1, const float* i2,
                                      float* o1, float* o2) {
   if (!g || b < 0 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block");
   cudaStream_t s = g->sG;
-  const size_t bytes = static_cast<size_t>(g->T * g->d) * 4;
-  // stage the pair into X_b (b's input slots) so the forward plans can be reused
-  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, b), i1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
-  if (b > 0) RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, b), i2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
-  else if (i1 != i2) return rp_fail(RP_ERR_CONTRACT, "block 0 input is the duplicated embedding (i1 == i2)");
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
+  const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
+  // stage the pair into X_j (b's input slots) so the forward plans can be reused
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, j), i1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  if (j > 0) RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, j), i2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  else if (i1 != i2) return rp_fail(RP_ERR_CONTRACT, "a stage's first block input is the duplicated stage input (i1 == i2)");
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   Slot& F = g->slot[0];
-  RP_TRY(ln_fwd(g, X1(g, b), tix_block(b, kLnFg), tix_block(b, kLnFb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(ln_fwd(g, St, X1(g, St, j), tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), F.hF, F.meanF,
+                F.rstdF, s));
   RP_TRY(launch(p.f_qkv, s));
-  RP_TRY(attn_fwd(g, F.qkv, F.att, F.lse, s));
+  RP_TRY(attn_fwd(St, F.qkv, F.att, F.lse, s));
   RP_TRY(launch(p.f_proj, s));
-  RP_TRY(ln_fwd(g, X2(g, b + 1), tix_block(b, kLnGg), tix_block(b, kLnGb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(ln_fwd(g, St, X2(g, St, j + 1), tix_block(g, b, kLnGg), tix_block(g, b, kLnGb), F.hF,
+                F.meanF, F.rstdF, s));
   RP_TRY(launch(p.f_w1, s));
   RP_TRY(launch(p.f_w2, s));
-  RP_TRY(cuda_ok(cudaMemcpyAsync(o1, X1(g, b + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
-  RP_TRY(cuda_ok(cudaMemcpyAsync(o2, X2(g, b + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(o1, X1(g, St, j + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(o2, X2(g, St, j + 1), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   return rp_engine_sync(g);
 }
 
-// rev_backward_local for block b >= 1:
+// rev_backward_local for a block that is not its stage's first:
 // (o1, o2, d_o1, d_o2) -> (i1, i2, d_i1, d_i2) + the block's grads in the engine grad buffer.
 extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float* o1,
                                             const float* o2, const float* d_o1,
                                             const float* d_o2, float* i1, float* i2,
                                             float* d_i1, float* d_i2) {
   if (!g || b < 1 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block (b >= 1)");
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
+  if (j < 1) return rp_fail(RP_ERR_CONTRACT, "rev_backward_local: block is its stage's first");
   cudaStream_t s = g->sG;
-  const int64_t n = g->T * g->d;
+  const int64_t n = St.T * St.d;
   const size_t bytes = static_cast<size_t>(n) * 4;
-  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, b + 1), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
-  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, b + 1), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, j + 1), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, j + 1), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(g->d1, d_o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(g->d2, d_o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(rpk_f32_to_bf16(g->d1, g->d1b, n, s));
@@ -1150,8 +1408,8 @@ extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float*
   set_partition(g, 1);
   RP_TRY(lane_r(g, b, s));
   RP_TRY(lane_g(g, b, s, true, false));
-  RP_TRY(cuda_ok(cudaMemcpyAsync(i1, X1(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
-  RP_TRY(cuda_ok(cudaMemcpyAsync(i2, X2(g, b), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i1, X1(g, St, j), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i2, X2(g, St, j), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_i1, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_i2, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   return rp_engine_sync(g);

@@ -278,6 +278,58 @@ __global__ void add_to_bf16_kernel(const float* __restrict__ a, const float* __r
     out[i] = __float2bfloat16_rn(a[i] + b[i]);
 }
 
+// fuse(average) of a stage output (layers.cpp:277-279: ops::scale(ops::add(i1, i2), 0.5)),
+// written bf16 as the patch_merge GEMM operand
+__global__ void fuse_avg_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
+                                int64_t n4, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(o1)[i];
+    const float4 b = reinterpret_cast<const float4*>(o2)[i];
+    reinterpret_cast<uint2*>(out)[i] =
+        make_uint2(pack_bf16x2((a.x + b.x) * 0.5f, (a.y + b.y) * 0.5f),
+                   pack_bf16x2((a.z + b.z) * 0.5f, (a.w + b.w) * 0.5f));
+  }
+}
+
+// concat_last(o1, o2) (ops.cpp:366-391) for the mlp fusion: out [rows, 2d] bf16
+__global__ void concat_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
+                              int64_t rows, int64_t d, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+
+  const int64_t d4 = d / 4, total = rows * 2 * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (2 * d4), c = i % (2 * d4);
+    const float* src = c < d4 ? o1 : o2;
+    const float4 v = reinterpret_cast<const float4*>(src + r * d)[c < d4 ? c : c - d4];
+    reinterpret_cast<uint2*>(out)[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+  }
+}
+
+// fuse_vjp(average) (layers.cpp:289-292): d_i1 = d_i2 = d_y * 0.5; d1 holds d_y on entry
+__global__ void halve_dup_kernel(float* __restrict__ d1, int64_t n4, float* __restrict__ d2,
+                                 __nv_bfloat16* __restrict__ d1b,
+                                 __nv_bfloat16* __restrict__ d2b) {
+  pdl_trigger();
+  pdl_wait();
+
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 v = reinterpret_cast<float4*>(d1)[i];
+    v = make_float4(v.x * 0.5f, v.y * 0.5f, v.z * 0.5f, v.w * 0.5f);
+    reinterpret_cast<float4*>(d1)[i] = v;
+    reinterpret_cast<float4*>(d2)[i] = v;
+    const uint2 vb = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    reinterpret_cast<uint2*>(d1b)[i] = vb;
+    reinterpret_cast<uint2*>(d2b)[i] = vb;
+  }
+}
+
 static inline unsigned grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -352,4 +404,20 @@ int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1
 int rpk_add_to_bf16(const float* a, const float* b, uint16_t* out, int64_t n, cudaStream_t s) {
   launch_k(add_to_bf16_kernel, dim3(grid_for(n)), dim3(256), 0, s, a, b, reinterpret_cast<__nv_bfloat16*>(out), n);
   return rp_check_launch("add_to_bf16");
+}
+int rpk_fuse_avg_bf16(const float* o1, const float* o2, int64_t n, uint16_t* out, cudaStream_t s) {
+  launch_k(fuse_avg_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, o1, o2, n / 4,
+           reinterpret_cast<__nv_bfloat16*>(out));
+  return rp_check_launch("fuse_avg");
+}
+int rpk_concat_bf16(const float* o1, const float* o2, int64_t rows, int64_t d, uint16_t* out,
+                    cudaStream_t s) {
+  launch_k(concat_kernel, dim3(grid_for(rows * d / 2)), dim3(256), 0, s, o1, o2, rows, d,
+           reinterpret_cast<__nv_bfloat16*>(out));
+  return rp_check_launch("concat");
+}
+int rpk_halve_dup(float* d1, int64_t n, float* d2, uint16_t* d1b, uint16_t* d2b, cudaStream_t s) {
+  launch_k(halve_dup_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, d1, n / 4, d2,
+           reinterpret_cast<__nv_bfloat16*>(d1b), reinterpret_cast<__nv_bfloat16*>(d2b));
+  return rp_check_launch("halve_dup");
 }

@@ -24,3 +24,8 @@ int rpk_adamw(float* p, const float* g, uint16_t* pb, float* m, float* v, int64_
               const float* lr, const float* t, float b1, float b2, float eps, float wd,
               float scale, cudaStream_t s);
 int rpk_add_scalar(float* x, float a, cudaStream_t s);
+// stage boundary (layers.cpp:276-303)
+int rpk_fuse_avg_bf16(const float* o1, const float* o2, int64_t n, uint16_t* out, cudaStream_t s);
+int rpk_concat_bf16(const float* o1, const float* o2, int64_t rows, int64_t d, uint16_t* out,
+                    cudaStream_t s);
+int rpk_halve_dup(float* d1, int64_t n, float* d2, uint16_t* d1b, uint16_t* d2b, cudaStream_t s);

@@ -24,7 +24,9 @@ class ModelConfigC(C.Structure):
                 ("seed", C.c_uint64), ("device", C.c_int), ("r_ctas", C.c_int),
                 ("g_ctas", C.c_int), ("lane_priority", C.c_int), ("optimizer", C.c_int),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
-                ("weight_decay", C.c_float)]
+                ("weight_decay", C.c_float), ("stages", C.c_int64),
+                ("stage_depth", C.c_int64 * 8), ("stage_width", C.c_int64 * 8),
+                ("stage_heads", C.c_int64 * 8), ("reduction", C.c_int64), ("fusion", C.c_int)]
 
 
 @dataclass
@@ -49,6 +51,18 @@ class ModelConfig:
     beta2: float = 0.999
     adam_eps: float = 1e-8
     weight_decay: float = 0.0
+    # hierarchical (Rev-Swin-style): blocks / width / heads per stage,
+    # tokens merged per boundary group, fusion kind ("average" | "mlp", layers.hpp:142)
+    depths: tuple | None = None
+    widths: tuple | None = None
+    stage_heads: tuple | None = None
+    reduction: int = 2
+    fusion: str = "average"
+
+    def __post_init__(self):
+        if self.depths:
+            self.depth = int(sum(self.depths))
+            self.width, self.heads = int(self.widths[0]), int(self.stage_heads[0])
 
 
 PRESETS = {
@@ -60,6 +74,12 @@ PRESETS = {
                              batch=64, num_classes=2),
     # BASELINE config 5: RevViT-G-style (depth 48, dim 1664, 16 heads of 104, MLP ratio 4)
     "revvit-g48": dict(depth=48, width=1664, heads=16, hidden=6656, seq_len=197, batch=64),
+    # hierarchical Rev-Swin-B (Swin-B stages: C = 128, depths 2-2-18-2,
+    # heads 4-8-16-32, 7x7 windows over 56x56 tokens of 4x4x3 patches, 2x2 merges as r = 4
+    # adjacent tokens, ref ops.cpp:393-399), average fusion
+    "rev-swin-b": dict(depth=24, width=128, heads=4, hidden=512, seq_len=3136, in_dim=48,
+                       window=49, depths=(2, 2, 18, 2), widths=(128, 256, 512, 1024),
+                       stage_heads=(4, 8, 16, 32), reduction=4, batch=128),
 }
 
 
@@ -160,7 +180,7 @@ class Engine:
         return self._h
 
     def tensor_table(self):
-        cap = 1 + 10 * self.cfg.depth + 1
+        cap = 1 + 10 * self.cfg.depth + 2 * len(self.cfg.depths or ()) + 1
         off = np.zeros(cap, np.int64)
         num = np.zeros(cap, np.int64)
         n = api("rp_engine_tensor_table")(self._h, _np_ptr(off), _np_ptr(num), cap)
@@ -276,10 +296,21 @@ class Engine:
 
 
 def _cfg_c(cfg: "ModelConfig") -> ModelConfigC:
-    return ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
-                        cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
-                        cfg.g_ctas, cfg.lane_priority, cfg.optimizer, cfg.beta1, cfg.beta2,
-                        cfg.adam_eps, cfg.weight_decay)
+    c = ModelConfigC(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
+                     cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
+                     cfg.g_ctas, cfg.lane_priority, cfg.optimizer, cfg.beta1, cfg.beta2,
+                     cfg.adam_eps, cfg.weight_decay)
+    if cfg.depths:
+        if not (len(cfg.depths) == len(cfg.widths) == len(cfg.stage_heads) <= 8):
+            raise _capi.ConfigError("depths / widths / stage_heads: same length, at most 8")
+        c.stages = len(cfg.depths)
+        for s, (L, d, H) in enumerate(zip(cfg.depths, cfg.widths, cfg.stage_heads)):
+            c.stage_depth[s], c.stage_width[s], c.stage_heads[s] = L, d, H
+        c.reduction = cfg.reduction
+        if cfg.fusion not in ("average", "mlp"):
+            raise _capi.ConfigError("fusion must be 'average' or 'mlp'")
+        c.fusion = 1 if cfg.fusion == "mlp" else 0
+    return c
 
 
 VANILLA = 0
