@@ -30,6 +30,9 @@ DEFAULTS = {
     "model.window": "0", "bench.batch_sizes": "256", "bench.engines": "reprop,pareprop",
     "bench.steps": "10", "bench.warmup": "2", "bench.repeats": "3", "bench.out": "bench.csv",
     "optim.kind": "sgd", "optim.lr": "0.001", "seed": "0",
+    # hierarchical: model.kind = hierarchical plus comma lists per stage
+    "model.kind": "isotropic", "model.depths": "", "model.widths": "", "model.stage_heads": "",
+    "model.reduction": "2", "model.fusion": "average",
 }
 
 
@@ -51,11 +54,19 @@ def read_config(path: str | None) -> dict:
 def model_config(cfg: dict, batch: int):
     from .engine import ModelConfig
     w = int(cfg["model.width"])
+    hier = {}
+    if cfg["model.kind"] == "hierarchical":
+        ints = lambda k: tuple(int(v) for v in cfg[k].split(",") if v.strip())
+        hier = dict(depths=ints("model.depths"), widths=ints("model.widths"),
+                    stage_heads=ints("model.stage_heads"), reduction=int(cfg["model.reduction"]),
+                    fusion=cfg["model.fusion"])
+    elif cfg["model.kind"] != "isotropic":
+        raise SystemExit("model.kind must be isotropic or hierarchical")
     return ModelConfig(depth=int(cfg["model.depth"]), width=w, heads=int(cfg["model.heads"]),
                        hidden=int(cfg["model.mlp_ratio"]) * w, seq_len=int(cfg["model.seq_len"]),
                        in_dim=int(cfg["model.in_dim"]), num_classes=int(cfg["model.num_classes"]),
                        window=int(cfg["model.window"]), batch=batch, seed=int(cfg["seed"]),
-                       optimizer=1 if cfg["optim.kind"] == "adamw" else 0)
+                       optimizer=1 if cfg["optim.kind"] == "adamw" else 0, **hier)
 
 
 def cmd_bench(cfg: dict) -> int:
@@ -125,7 +136,8 @@ def cmd_verify(cfg: dict) -> int:
     B = int(cfg["bench.batch_sizes"].split(",")[0])
     mc = model_config(cfg, B)
     om = O.ModelConfig(mc.depth, mc.width, mc.heads, mc.hidden, mc.seq_len, mc.in_dim,
-                       mc.num_classes, mc.window or None)
+                       mc.num_classes, mc.window or None, depths=mc.depths, widths=mc.widths,
+                       stage_heads=mc.stage_heads, reduction=mc.reduction, fusion=mc.fusion)
     eng = Engine(mc)
     p32 = O.init_params(om, int(cfg["seed"]), np.float32)
     eng.set_params(p32)

@@ -1,5 +1,5 @@
 // Fused multi-head self-attention forward / backward on warp-level mma.sync, any head_dim
-// that is a multiple of 8 up to 128 (tiles padded to HDP = 64 or 128 columns, zero-filled).
+// that is a multiple of 8 up to 128 (tiles padded to HDP = 32, 64 or 128 columns, zero-filled).
 //
 // Replaces the per-(batch, head, window) loop of ref:proj/core/src/layers.cpp:150-166
 // (gather_block x3, matmul_nt, scale, row_softmax, probs_store, matmul, scatter_block)
@@ -28,10 +28,13 @@ namespace rp {
 
 constexpr int kTile = 64;        // query / key rows per CTA tile
 
-// smem tiles hold HDP bf16 per row (HDP = padded head dim, 64 or 128): 16-byte chunk c of
-// row r at r*2*HDP + (c with its low 3 bits XOR r&7) -> ldmatrix is bank-conflict free
+// smem tiles hold HDP bf16 per row (HDP = padded head dim, 32, 64 or 128): 16-byte chunk c
+// of row r at r*2*HDP + (c with its low 3 bits XOR r&7) -> ldmatrix is bank-conflict free.
+// 32-column rows (64 B) hold 4 chunks: XOR with (r/2)&3 keeps the 8 rows of one ldmatrix
+// phase on distinct bank groups (two rows share a 128-byte line).
 template <int HDP>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
+  if constexpr (HDP == 32) return static_cast<uint32_t>(r * 64 + (((c ^ (r >> 1)) & 3) << 4));
   return static_cast<uint32_t>(r * HDP * 2 + (((c & ~7) | ((c ^ r) & 7)) << 4));
 }
 
@@ -528,6 +531,7 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
     rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
+  if (head_dim <= 32) return attn_fwd_mma<32>(qkv, B, N, H, head_dim, out, lse, s);
   return head_dim <= 64 ? attn_fwd_mma<64>(qkv, B, N, H, head_dim, out, lse, s)
                         : attn_fwd_mma<128>(qkv, B, N, H, head_dim, out, lse, s);
 }
@@ -579,6 +583,8 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
     rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
+  if (head_dim <= 32)
+    return attn_bwd_mma<32>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s);
   return head_dim <= 64
              ? attn_bwd_mma<64>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s)
              : attn_bwd_mma<128>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s);
