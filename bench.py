@@ -203,8 +203,11 @@ def main_ours(a, rank, world, local_rank):
     p = dict(PRESETS[PRESET])
     if a.batch:
         p["batch"] = a.batch
-    cfg = ModelConfig(device=local_rank, seed=1234 + rank, r_ctas=a.r_ctas, g_ctas=a.g_ctas, **p)
+    # data parallel: every replica starts from the same weights (seed 1234) and draws its
+    # own synthetic shard of the batch (seed 1234 + rank)
+    cfg = ModelConfig(device=local_rank, seed=1234, r_ctas=a.r_ctas, g_ctas=a.g_ctas, **p)
     eng = Engine(cfg)
+    eng.synthetic_batch(1234 + rank)
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
