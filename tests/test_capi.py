@@ -120,3 +120,36 @@ def test_activation_ledger_spec_invariants(capi):
     assert probe_max_batch(replace(base, depth=16), VANILLA, budget) < 8
     with pytest.raises(capi.BudgetError):
         probe_max_batch(base, REPROP, 1000)
+
+
+def test_hierarchical_config_errors_and_ledger(capi):
+    """Hierarchical (Rev-Swin) configs: validation on the host (no device work) and the
+    ledger's storage contract -- Reprop / PaReprop peaks independent of the stages' depths
+    (only each stage's input + output pair is stored), Vanilla growing by
+    one stored pair of the stage a block is added to."""
+    from dataclasses import replace
+    from paper_2306_09342_b200.engine import (PAREPROP, REPROP, VANILLA, Engine, ModelConfig,
+                                              activation_bytes)
+    base = ModelConfig(width=128, heads=4, hidden=512, seq_len=3136, in_dim=48, window=49,
+                       depths=(2, 2, 6, 2), widths=(128, 256, 512, 1024),
+                       stage_heads=(4, 8, 16, 32), reduction=4, batch=8)
+    assert base.depth == 12
+    with pytest.raises(capi.ShapeError, match="divisible"):
+        Engine(replace(base, seq_len=3136 + 4))  # 3140 / 4 / 4 is not whole
+    with pytest.raises(capi.ConfigError):
+        Engine(replace(base, fusion="concat"))
+    with pytest.raises(capi.ConfigError, match="multiples of 64"):
+        Engine(replace(base, widths=(96, 192, 384, 768), width=96, hidden=384))
+    with pytest.raises(capi.ConfigError, match="head_dim"):
+        Engine(replace(base, stage_heads=(4, 8, 3, 32)))
+    T2 = base.batch * base.seq_len // 16  # stage-2 rows
+    pair2 = 2 * T2 * 512 * 4
+    for m in (REPROP, PAREPROP):
+        a = activation_bytes(base, m)[0]
+        b = activation_bytes(replace(base, depths=(2, 2, 18, 2)), m)[0]
+        assert a == b
+    va = activation_bytes(base, VANILLA)[0]
+    vb = activation_bytes(replace(base, depths=(2, 2, 18, 2)), VANILLA)[0]
+    assert vb - va == 12 * pair2
+    pr, blk = activation_bytes(base, REPROP)
+    assert activation_bytes(base, PAREPROP)[0] == pr + blk
