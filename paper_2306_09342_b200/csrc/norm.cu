@@ -361,12 +361,13 @@ __global__ void __launch_bounds__(kFinWarps * 32)
   const int c = blockIdx.x * 32 + lane;
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c < cols) {
-    int64_t p = warp;
-    for (; p + 7 * kFinWarps < nparts; p += 8 * kFinWarps) {
+    for (int64_t p = warp; p < nparts; p += 8 * kFinWarps) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] += part[(p + k * kFinWarps) * ld + c];
+      for (int k = 0; k < 8; ++k) {
+        const int64_t q = p + k * kFinWarps;
+        if (q < nparts) a[k] += part[q * ld + c];
+      }
     }
-    for (; p < nparts; p += kFinWarps) a[0] += part[p * ld + c];
   }
   red[warp][lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   __syncthreads();
