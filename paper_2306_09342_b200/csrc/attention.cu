@@ -22,6 +22,8 @@
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include <algorithm>
+
 #include "launch.h"
 
 namespace rp {
@@ -157,34 +159,16 @@ __device__ __forceinline__ void store_pair(__nv_bfloat16* row, int col, int hd, 
 }
 
 // ------------------------------------------------------------------------ forward
-// grid (ceil(N/64), H, B); block 128 (4 warps x 16 query rows)
-// smem: Q tile [64][64] | K [Npad][64] | V [Npad][64]
+// One 64-query tile of one (sequence b, head h) against all keys: Q tile, K and V
+// [npad rows] already in smem (swizzled); writes out rows and the log2-domain LSE.
 template <int HDP>
-__global__ void __launch_bounds__(128)
-    attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
-                    float* __restrict__ lse, AttnGeom g) {
-  constexpr int kRowBytes = HDP * 2;
-  pdl_trigger();
-  pdl_wait();
-
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int npad = (g.N + kTile - 1) / kTile * kTile;
-  uint8_t* sQ = sm;
-  uint8_t* sK = sQ + kTile * kRowBytes;
-  uint8_t* sV = sK + npad * kRowBytes;
-  const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
-  const int hd = g.hd;
-  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
-  load_rows<HDP>(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0, hd);
-  load_rows<HDP>(sK, base + g.H * hd, g.ld_qkv, npad, g.N, hd);
-  load_rows<HDP>(sV, base + 2 * g.H * hd, g.ld_qkv, npad, g.N, hd);
-  cp_async_wait_all();
-  __syncthreads();
-
+__device__ __forceinline__ void fwd_tile(uint32_t bQ, uint32_t bK, uint32_t bV, int npad, int q0,
+                                         int h, int b, int hd, const AttnGeom& g,
+                                         __nv_bfloat16* __restrict__ out,
+                                         float* __restrict__ lse) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (q0 + warp * 16 >= g.N) return;  // all 16 rows are padding (no block syncs follow)
+  if (q0 + warp * 16 >= g.N) return;  // all 16 rows of this warp are padding
   const int gq = lane >> 2, tq = lane & 3;
-  const uint32_t bQ = smem_u32(sQ), bK = smem_u32(sK), bV = smem_u32(sV);
   uint32_t qa[HDP / 16][4];
 #pragma unroll
   for (int ks = 0; ks < HDP / 16; ++ks) load_a<HDP>(bQ, warp * 16, 2 * ks, qa[ks]);
@@ -253,6 +237,71 @@ __global__ void __launch_bounds__(128)
         lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = m[r] + log2f(l[r]);
     }
   }
+}
+
+
+// grid (ceil(N/64), H, B); block 128 (4 warps x 16 query rows)
+// smem: Q tile [64][64] | K [Npad][64] | V [Npad][64]
+template <int HDP>
+__global__ void __launch_bounds__(128)
+    attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
+                    float* __restrict__ lse, AttnGeom g) {
+  constexpr int kRowBytes = HDP * 2;
+  pdl_trigger();
+  pdl_wait();
+
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int npad = (g.N + kTile - 1) / kTile * kTile;
+  uint8_t* sQ = sm;
+  uint8_t* sK = sQ + kTile * kRowBytes;
+  uint8_t* sV = sK + npad * kRowBytes;
+  const int q0 = blockIdx.x * kTile, h = blockIdx.y, b = blockIdx.z;
+  const int hd = g.hd;
+  const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
+  load_rows<HDP>(sQ, base + static_cast<int64_t>(q0) * g.ld_qkv, g.ld_qkv, kTile, g.N - q0, hd);
+  load_rows<HDP>(sK, base + g.H * hd, g.ld_qkv, npad, g.N, hd);
+  load_rows<HDP>(sV, base + 2 * g.H * hd, g.ld_qkv, npad, g.N, hd);
+  cp_async_wait_all();
+  __syncthreads();
+  fwd_tile<HDP>(smem_u32(sQ), smem_u32(sK), smem_u32(sV), npad, q0, h, b, hd, g, out, lse);
+}
+
+// Short sequences (windows of N <= 64 tokens, e.g. Swin's 49): a persistent CTA walks
+// (sequence, head) items with the next item's Q / K / V tiles streaming into the other
+// half of a double buffer (cp.async groups) while the current one computes -- one item's
+// loads alone cannot keep enough bytes in flight to cover HBM latency.
+template <int HDP>
+__global__ void __launch_bounds__(128)
+    attn_fwd_small_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
+                          float* __restrict__ lse, AttnGeom g) {
+  constexpr int kRowBytes = HDP * 2, kBuf = 3 * kTile * kRowBytes;
+  pdl_trigger();
+  pdl_wait();
+
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int total = g.B * g.H, hd = g.hd;
+  auto prefetch = [&](int item, int slot) {
+    const int h = item % g.H, b = item / g.H;
+    const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * g.N * g.ld_qkv + h * hd;
+    uint8_t* buf = sm + slot * kBuf;
+    load_rows<HDP>(buf, base, g.ld_qkv, kTile, g.N, hd);
+    load_rows<HDP>(buf + kTile * kRowBytes, base + g.H * hd, g.ld_qkv, kTile, g.N, hd);
+    load_rows<HDP>(buf + 2 * kTile * kRowBytes, base + 2 * g.H * hd, g.ld_qkv, kTile, g.N, hd);
+  };
+  int item = blockIdx.x;
+  if (item < total) prefetch(item, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int k = 0; item < total; ++k, item += gridDim.x) {
+    const int next = item + gridDim.x;
+    if (next < total) prefetch(next, (k + 1) & 1);
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const uint32_t b0 = smem_u32(sm + (k & 1) * kBuf);
+    fwd_tile<HDP>(b0, b0 + kTile * kRowBytes, b0 + 2 * kTile * kRowBytes, kTile, 0,
+                  item % g.H, item / g.H, hd, g, out, lse);
+    __syncthreads();  // this buffer is refilled by the prefetch two items ahead
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // D[b][h][n] = sum_c dO[row][h*64+c] * O[row][h*64+c]   (softmax VJP dot, ops.cpp:219-220)
@@ -509,6 +558,27 @@ template <int HDP>
 static int attn_fwd_mma(const uint16_t* qkv, int64_t B, int64_t N, int64_t H, int64_t hd,
                         uint16_t* out, float* lse, cudaStream_t stream) {
   const AttnGeom g = make_geom(B, N, H, hd);
+  if (N <= kTile && B * H >= 4 * 148) {  // many short windows: persistent, double-buffered
+    const int smem = 2 * 3 * kTile * HDP * 2;
+    int rc;
+    if ((rc = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_small_kernel<HDP>), smem)))
+      return rc;
+    static int per_sm[3] = {0, 0, 0};
+    int& occ = per_sm[HDP == 32 ? 0 : HDP == 64 ? 1 : 2];
+    if (!occ) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_fwd_small_kernel<HDP>, 128, smem);
+      if (occ < 1) occ = 1;
+    }
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = B * H;
+    const int64_t grid = std::min<int64_t>(items, static_cast<int64_t>(nsm) * occ);
+    launch_k(attn_fwd_small_kernel<HDP>, dim3(static_cast<unsigned>(grid)), dim3(128), smem,
+             stream, reinterpret_cast<const __nv_bfloat16*>(qkv),
+             reinterpret_cast<__nv_bfloat16*>(out), lse, g);
+    return rp_check_launch("attention_fwd");
+  }
   const int npad = static_cast<int>((N + kTile - 1) / kTile * kTile);
   const int smem = (kTile + 2 * npad) * HDP * 2;
   int rc;
