@@ -145,8 +145,12 @@ int rp_attention_fwd(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64
 int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
                      const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
                      uint16_t* dqkv, float* workspace, rp_stream_t stream);
+/* D = rowsum(dO * O) (S N H floats) and, for the tcgen05 backward, the bf16 dS^T of every
+ * (sequence, head) ([S H][Nk][Nk], Nk = N rounded up to 16) */
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
-/* 0 (default): tcgen05 kernels where they apply; 1: warp-level mma.sync only */
+/* 0 (default): tcgen05 kernels where they apply, backward = one dK/dV pass that also writes
+ * dS^T + a dQ = dS K pass over it; 1: warp-level mma.sync only; 2: tcgen05 with the
+ * two-pass backward (dQ pass, dK/dV pass, each recomputing S and dP; no dS stored) */
 int rp_set_attention_impl(int impl);
 
 /* ------------------------------------------------------------------ training engine

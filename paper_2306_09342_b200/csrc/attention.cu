@@ -546,8 +546,11 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
                         float* lse, cudaStream_t stream);
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream);
-static int g_attn_impl = 0;  // 0 = tcgen05 where it applies (head_dim 64), 1 = mma.sync only
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt);
+// 0 = tcgen05 where it applies (head_dim 64), backward as one dK/dV pass + dQ from the
+// stored dS^T; 1 = mma.sync only; 2 = tcgen05 with the two-pass (dQ pass, dK/dV pass)
+// backward that keeps no dS
+static int g_attn_impl = 0;
 
 extern "C" int rp_set_attention_impl(int impl) {
   g_attn_impl = impl;
@@ -597,7 +600,7 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (g_attn_impl == 0 && head_dim == 64 && N <= 512) {
+  if (g_attn_impl != 1 && head_dim == 64 && N <= 512) {
     rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
@@ -606,8 +609,12 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
                         : attn_fwd_mma<128>(qkv, B, N, H, head_dim, out, lse, s);
 }
 
+// D (B N H floats), then -- for the tcgen05 backward -- dS^T of every (sequence, head) as bf16
+// [B H][Nk][Nk] (Nk = N rounded up to 16), 64-float aligned
+static int64_t attn_ds_offset(int64_t B, int64_t N, int64_t H) { return (B * N * H + 63) / 64 * 64; }
 extern "C" int64_t rp_attention_bwd_workspace_floats(int64_t B, int64_t N, int64_t H) {
-  return B * N * H;
+  const int64_t nk = (N + 15) / 16 * 16;
+  return attn_ds_offset(B, N, H) + (B * H * nk * nk + 1) / 2;
 }
 
 template <int HDP>
@@ -649,8 +656,13 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (g_attn_impl == 0 && head_dim == 64) {  // tcgen05 path computes D itself
-    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s);
+  if (g_attn_impl != 1 && head_dim == 64) {  // tcgen05 path computes D itself
+    // dS^T storage pays off while it is small next to the dQ pass it replaces (measured:
+    // 495 -> 450 us at N = 197, a loss at N = 512)
+    uint16_t* dst = g_attn_impl == 0 && N <= 256
+                        ? reinterpret_cast<uint16_t*>(workspace + attn_ds_offset(B, N, H))
+                        : nullptr;
+    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst);
     if (rc != RP_ERR_CONFIG) return rc;
   }
   if (head_dim <= 32)

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     attn_bwd_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                 const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
                 const __nv_bfloat16* __restrict__ O, const float* __restrict__ lse,
-                float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdPlan pl) {
+                float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdPlan pl,
+                __nv_bfloat16* __restrict__ dSt) {
   pdl_trigger();
 
   __shared__ float red[2][128];                // DQ: D partials [column half][row]
@@ -312,6 +313,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               }
               tmem_st8(ts + 8 * hh, pp);       // P^T over own, already-read S^T columns
               tmem_st8(ts + 64 + 8 * hh, pd);  // dS^T over own dP^T columns
+              if (dSt != nullptr && row < Nk) {  // dS^T row (this key, 16 queries) for dQ
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+                const bool kv = row < g.N;
+                uint4* dst4 = reinterpret_cast<uint4*>(dSt + ((static_cast<int64_t>(b) * g.H + h) * Nk + row) * Nk + col0);
+                dst4[0] = kv ? make_uint4(pd[0], pd[1], pd[2], pd[3]) : z;
+                dst4[1] = kv ? make_uint4(pd[4], pd[5], pd[6], pd[7]) : z;
+              }
             }
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -348,16 +356,184 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   if (warp == 8) tmem_dealloc(tmem, 256);
 }
 
+// ------------------------------------------------------------------ D and dQ for the fused path
+// D[b][h][n] = rowsum(dO * O) (softmax VJP dot, ops.cpp:219-220): 8 threads per (row, head),
+// 16 B each, so a warp reads 4 heads' contiguous 512 B of a row; 3-step shuffle reduction.
+__global__ void __launch_bounds__(256)
+    attn_d_kernel(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ dO,
+                  float* __restrict__ Dg, int64_t rows, int N, int H) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t rh = i >> 3;  // (row, head) pair, head fastest
+  const bool ok = rh < rows * H;
+  float acc = 0.f;
+  if (ok) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(O) + i);
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(dO) + i);
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 fa = unpack_bf16x2(av[k]), fc = unpack_bf16x2(cv[k]);
+      acc = fmaf(fa.x, fc.x, acc);
+      acc = fmaf(fa.y, fc.y, acc);
+    }
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (ok && (i & 7) == 0) {
+    const int h = static_cast<int>(rh % H);
+    const int64_t row = rh / H, b = row / N, n = row % N;
+    Dg[(b * H + h) * N + n] = acc;
+  }
+}
+
+// dQ = dS K per (128-query tile, head, sequence) from the dS^T rows the dK/dV pass wrote
+// (dSt [S*H][Nk keys][Nk queries] bf16): D[M = queries][N = 64] += A . B over 64-key chunks
+// with A = dS (stored [keys][queries]: MN-major) and B = K_c ([keys][64]: MN-major), the
+// wgrad operand layout of the GEMM. Warp 0: TMA, warp 1: MMA (one thread), warps 2-5:
+// TMEM -> bf16 -> dqkv. Accumulators double-buffered in TMEM (2 x 64 columns).
+constexpr int kDqStages = 4;
+constexpr int kDqStage = 16384 + 8192;  // A (2 boxes of 64 keys x 64 queries) | B (64 x 64)
+__global__ void __launch_bounds__(192, 2)
+    attn_dq_tc(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
+               __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdPlan pl) {
+  pdl_trigger();
+  __shared__ __align__(8) uint64_t bars[2 * kDqStages + 4];
+  __shared__ uint32_t tmem_slot;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kDqStages;
+  uint64_t* tfull = bars + 2 * kDqStages;
+  uint64_t* tempty = bars + 2 * kDqStages + 2;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_ds);
+      tma_prefetch_desc(&tm_k);
+      for (int i = 0; i < kDqStages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&tfull[i], 1);
+        mbar_init(&tempty[i], 4);
+      }
+      fence_barrier_init();
+    }
+    tmem_alloc(&tmem_slot, 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  const int Nk = g.Nk, nch = (Nk + 63) / 64, d = g.H * 64;
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < pl.nitems; item += gridDim.x) {
+        int tile, h, b;
+        item_coords(item, pl.ntile, g.H, tile, h, b);
+        const int bh = b * g.H + h;
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = smem + stage * kDqStage;
+          const int krow = bh * Nk + 64 * c;  // dS^T rows of this chunk's keys
+          tma_load_2d(a, &tm_ds, &full[stage], tile * 128, krow);
+          tma_load_2d(a + 8192, &tm_ds, &full[stage], tile * 128 + 64, krow);
+          tma_load_2d(a + 16384, &tm_k, &full[stage], d + h * 64, b * g.N + 64 * c);
+          mbar_arrive_expect_tx(&full[stage], kDqStage);
+          if (++stage == kDqStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, 64, true, true);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int item = blockIdx.x; item < pl.nitems; item += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t td = tmem + static_cast<uint32_t>(acc * 64);
+        for (int c = 0; c < nch; ++c) {
+          const int w = min(64, Nk - 64 * c);  // keys of this chunk (multiple of 16)
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * kDqStage), b_addr = a_addr + 16384u;
+          for (int kk = 0; kk < w / 16; ++kk)
+            umma_bf16(td, make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024),
+                      make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024), idesc,
+                      (c > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == kDqStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = static_cast<int>(warp & 3u);  // TMEM lane quarter of warps 2..5
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int item = blockIdx.x; item < pl.nitems; item += gridDim.x) {
+      int tile, h, b;
+      item_coords(item, pl.ntile, g.H, tile, h, b);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      float o[64];
+      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 64);
+      tmem_ld32(ta, o);
+      tmem_ld32(ta + 32, o + 32);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const int row = tile * 128 + q * 32 + static_cast<int>(lane);
+      if (row < g.N) {
+        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * g.N + row) * g.ld_qkv + h * 64;
+        store_row32_bf16(dst, o);
+        store_row32_bf16(dst + 32, o + 32);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, 128);
+}
+
 }  // namespace attn_tc
 }  // namespace rp
 
 using namespace rp;
 
-// Backward on the tcgen05 path (head_dim 64): dQ (and D = rowsum(dO * O) into `Dg`), then
-// dK / dV. Returns RP_ERR_CONFIG without launching when the shape is outside this path.
+// Backward on the tcgen05 path (head_dim 64). Returns RP_ERR_CONFIG without launching when
+// the shape is outside this path.
+//   dSt == nullptr: two passes -- dQ (and D = rowsum(dO * O) into `Dg`), then dK / dV.
+//   dSt != nullptr: D first (attn_d_kernel), then ONE pass over (key tile, query chunk)
+//     computing dK / dV and writing dS^T (bf16, [S*H][Nk][Nk]) on the way, then dQ = dS K
+//     as a streamed MMA over dS^T (attn_dq_tc) -- S and dP are formed once instead of twice.
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream) {
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt) {
   using namespace attn_tc;
   if (N > 1024 || N < 1) return RP_ERR_CONFIG;
   BwdGeom g;
@@ -376,11 +552,13 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
       make_map(&do64, dout, T, H * 64, 64) || make_map(&k64, qkv, T, 3 * H * 64, 64))
     return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
   const int smem = 1024 + kBwdSmem;
+  const int smem_dq = 1024 + kDqStages * kDqStage;
   static std::once_flag once;
   static int nsm = 148;
-  std::call_once(once, [smem] {
+  std::call_once(once, [smem, smem_dq] {
     cudaFuncSetAttribute(attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -389,13 +567,28 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
   pl.ntile = static_cast<int>((N + 127) / 128);
   pl.nitems = static_cast<int>(S * H) * pl.ntile;
   const unsigned grid = static_cast<unsigned>(pl.nitems < 2 * nsm ? pl.nitems : 2 * nsm);
+  if (dSt != nullptr) {
+    CUtensorMap ds;
+    if (make_map(&ds, dSt, S * H * g.Nk, g.Nk, 64))
+      return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
+    const int64_t n = T * H * 8;
+    launch_k(attn_d_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
+             reinterpret_cast<const __nv_bfloat16*>(out),
+             reinterpret_cast<const __nv_bfloat16*>(dout), Dg, T, g.N, g.H);
+    launch_k(attn_bwd_tc<false>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64,
+             do64, reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
+             reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, reinterpret_cast<__nv_bfloat16*>(dSt));
+    launch_k(attn_dq_tc, dim3(grid), dim3(192), smem_dq, stream, ds, k64,
+             reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl);
+    return rp_check_launch("attention_bwd_tc");
+  }
   // dQ (+ D): tiles Q | dO, chunks K | V (qkv maps; the dO map for the dO tile)
   launch_k(attn_bwd_tc<true>, dim3(grid), dim3(kBwdThreads), smem, stream, q128, do128, k64, k64,
            reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
-           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl);
+           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
   // dK, dV: tiles K | V, chunks Q | dO
   launch_k(attn_bwd_tc<false>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64, do64,
            reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
-           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl);
+           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
   return rp_check_launch("attention_bwd_tc");
 }

@@ -133,7 +133,7 @@ def test_hier_vanilla_and_descent():
     for mode in (REPROP, PAREPROP):
         e2, _, _, _ = make(HM, batch=4)
         e2.set_batch(bf16_bits(x), lab)
-        e2.set_lr(0.2)
+        e2.set_lr(0.1)  # 0.2 overshoots on this 4-sample batch
         ls = []
         for _ in range(12):
             e2.step(mode)

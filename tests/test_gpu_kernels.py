@@ -243,7 +243,7 @@ def attn_ref(qkv, B, N, H, hd=64):
     return o.permute(0, 2, 1, 3).reshape(B * N, H * hd), torch.logsumexp(s, -1)
 
 
-@pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("impl", [0, 1, 2], ids=["tcgen05", "mma_sync", "tcgen05_2pass"])
 @pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3), (2, 300, 2), (1, 480, 3), (3, 768, 1),
                                    (3, 256, 2), (2, 129, 1)])
 def test_attention_fwd_bwd(K, B, N, H, impl):
