@@ -233,6 +233,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const bool active = tile * 128 + q * 32 < g.N;
       const int64_t hb = (static_cast<int64_t>(b) * g.H + h) * g.N;
       const int64_t grow = static_cast<int64_t>(b) * g.N + row;
+      // dS^T row of this lane's key (fused backward): written for keys < Nk, zero past N
+      __nv_bfloat16* ds_row =
+          (!DQ && dSt != nullptr && row < Nk)
+              ? dSt + ((static_cast<int64_t>(b) * g.H + h) * Nk + row) * Nk
+              : nullptr;
       float lr = 0.f, nds = 0.f;
       if constexpr (DQ) {
         // ---- D = rowsum(dO * O) for this lane's query (dO from the smem tile, O global)
@@ -313,12 +318,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               }
               tmem_st8(ts + 8 * hh, pp);       // P^T over own, already-read S^T columns
               tmem_st8(ts + 64 + 8 * hh, pd);  // dS^T over own dP^T columns
-              if (dSt != nullptr && row < Nk) {  // dS^T row (this key, 16 queries) for dQ
-                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+              if (ds_row != nullptr) {  // dS^T (this key, 16 queries) for the dQ pass
                 const bool kv = row < g.N;
-                uint4* dst4 = reinterpret_cast<uint4*>(dSt + ((static_cast<int64_t>(b) * g.H + h) * Nk + row) * Nk + col0);
-                dst4[0] = kv ? make_uint4(pd[0], pd[1], pd[2], pd[3]) : z;
-                dst4[1] = kv ? make_uint4(pd[4], pd[5], pd[6], pd[7]) : z;
+                uint4* dst4 = reinterpret_cast<uint4*>(ds_row + col0);
+                dst4[0] = kv ? make_uint4(pd[0], pd[1], pd[2], pd[3]) : make_uint4(0u, 0u, 0u, 0u);
+                dst4[1] = kv ? make_uint4(pd[4], pd[5], pd[6], pd[7]) : make_uint4(0u, 0u, 0u, 0u);
               }
             }
           }
