@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // Stage 2: out[c] (+)= sum_p part[p][c] in a fixed order. CTA = 32 warps x 32 columns;
-// warp w owns parts {w, w+32, ...} with 8 interleaved accumulators (8 loads in flight per
-// lane: the reduction is latency bound otherwise); combined in a fixed order.
+// warp w owns parts {w, w+32, ...} with 2 interleaved accumulators; combined in order.
+// (8 accumulators measured slower: the compiler reuses the load registers and serialises.)
 constexpr int kFinWarps = 32;
 __global__ void __launch_bounds__(kFinWarps * 32)
     colsum_final_kernel(const float* __restrict__ part, int64_t nparts, int cols, int64_t ld,
@@ -359,17 +359,16 @@ __global__ void __launch_bounds__(kFinWarps * 32)
   __shared__ float red[kFinWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float a0 = 0.f, a1 = 0.f;
   if (c < cols) {
-    for (int64_t p = warp; p < nparts; p += 8 * kFinWarps) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t q = p + k * kFinWarps;
-        if (q < nparts) a[k] += part[q * ld + c];
-      }
+    int64_t p = warp;
+    for (; p + kFinWarps < nparts; p += 2 * kFinWarps) {
+      a0 += part[p * ld + c];
+      a1 += part[(p + kFinWarps) * ld + c];
     }
+    for (; p < nparts; p += kFinWarps) a0 += part[p * ld + c];
   }
-  red[warp][lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  red[warp][lane] = a0 + a1;
   __syncthreads();
   if (warp == 0 && c < cols) {
     float s = red[0][lane];
