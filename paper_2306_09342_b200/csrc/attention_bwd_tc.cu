@@ -321,8 +321,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               if (ds_row != nullptr) {  // dS^T (this key, 16 queries) for the dQ pass
                 const bool kv = row < g.N;
                 uint4* dst4 = reinterpret_cast<uint4*>(ds_row + col0);
-                dst4[0] = kv ? make_uint4(pd[0], pd[1], pd[2], pd[3]) : make_uint4(0u, 0u, 0u, 0u);
-                dst4[1] = kv ? make_uint4(pd[4], pd[5], pd[6], pd[7]) : make_uint4(0u, 0u, 0u, 0u);
+                // streaming stores: dS^T is consumed by the next kernel, keep L2 for the
+                // operands this pass re-reads
+                __stcs(dst4, kv ? make_uint4(pd[0], pd[1], pd[2], pd[3]) : make_uint4(0u, 0u, 0u, 0u));
+                __stcs(dst4 + 1, kv ? make_uint4(pd[4], pd[5], pd[6], pd[7]) : make_uint4(0u, 0u, 0u, 0u));
               }
             }
           }
