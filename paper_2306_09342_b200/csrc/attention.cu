@@ -609,11 +609,13 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
                         : attn_fwd_mma<128>(qkv, B, N, H, head_dim, out, lse, s);
 }
 
-// D (B N H floats), then -- for the tcgen05 backward -- dS^T of every (sequence, head) as bf16
-// [B H][Nk][Nk] (Nk = N rounded up to 16), 64-float aligned
+// D (B N H floats), then -- for the tcgen05 backward at N <= kFusedBwdMaxN -- dS^T of every
+// (sequence, head) as bf16 [B H][Nk][Nk] (Nk = N rounded up to 16), 64-float aligned
+constexpr int64_t kFusedBwdMaxN = 256;
 static int64_t attn_ds_offset(int64_t B, int64_t N, int64_t H) { return (B * N * H + 63) / 64 * 64; }
 extern "C" int64_t rp_attention_bwd_workspace_floats(int64_t B, int64_t N, int64_t H) {
   const int64_t nk = (N + 15) / 16 * 16;
+  if (N > kFusedBwdMaxN) return B * N * H;
   return attn_ds_offset(B, N, H) + (B * H * nk * nk + 1) / 2;
 }
 
@@ -659,7 +661,7 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   if (g_attn_impl != 1 && head_dim == 64) {  // tcgen05 path computes D itself
     // dS^T storage pays off while it is small next to the dQ pass it replaces (measured:
     // 495 -> 450 us at N = 197, a loss at N = 512)
-    uint16_t* dst = g_attn_impl == 0 && N <= 256
+    uint16_t* dst = g_attn_impl == 0 && N <= kFusedBwdMaxN
                         ? reinterpret_cast<uint16_t*>(workspace + attn_ds_offset(B, N, H))
                         : nullptr;
     rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst);
