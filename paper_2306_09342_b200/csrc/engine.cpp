@@ -584,7 +584,7 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
 
 // bucket b (block params) -> allreduce (DP) -> SGD, on the comm stream
 int bucket_update(RpEngine* g, int64_t off, int64_t n, cudaStream_t s) {
-  if (g->world > 1) {
+  if (g->comm) {
     ncclResult_t r = ncclAllReduce(g->grads + off, g->grads + off, static_cast<size_t>(n),
                                    ncclFloat32, ncclSum, g->comm, s);
     if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
@@ -685,7 +685,7 @@ int enqueue_step_impl(RpEngine* g, int mode) {
   RP_TRY(cuda_ok(cudaEventRecord(g->evEmbed, sG), "record"));
   RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evEmbed, 0), "wait"));
   RP_TRY(bucket_update(g, 0, g->in * S0.d, sC));
-  if (g->world > 1) {
+  if (g->comm) {
     ncclResult_t r = ncclAllReduce(g->loss, g->loss, 1, ncclFloat32, ncclAvg, g->comm, sC);
     if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
   }
@@ -1340,7 +1340,10 @@ extern "C" int rp_nccl_unique_id(uint8_t* out128) {
 extern "C" int rp_engine_comm_init(RpEngine* g, const uint8_t* id128, int world, int rank) {
   if (!g || !id128) return rp_fail(RP_ERR_CONTRACT, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return rp_fail(RP_ERR_CONFIG, "bad world/rank");
-  if (world == 1) return RP_OK;
+  // world == 1 also builds a (single-rank) communicator: the NCCL path of the step --
+  // per-block bucket all-reduce on the comm stream inside the captured graph -- then runs
+  // and is testable on one GPU
+  if (g->comm) return rp_fail(RP_ERR_CONTRACT, "comm_init: communicator already initialised");
   ncclUniqueId id;
   std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
   cudaSetDevice(g->dev);

@@ -331,3 +331,31 @@ def test_general_head_dim_step():
     per_tensor(mc, g_r, r.grads, TOL_GRAD)
     assert l2rel(g_r, r.grads) < TOL_L2
     eng.close()
+
+
+def test_single_rank_nccl_path_matches_local():
+    """The data-parallel path on one GPU: a single-rank NCCL communicator makes the step
+    all-reduce every block bucket (and the loss) on the comm stream, inside the captured
+    graph. Sum over one rank and the 1/world scale are identities, so losses, gradients and
+    updated parameters must equal the local engine's bit for bit (eager and graph, Reprop
+    and PaReprop)."""
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits, nccl_unique_id
+    cfg = dict(TI, depth=3, num_classes=10)
+    runs = {}
+    for use_nccl in (False, True):
+        eng, mc, p32, _ = make(cfg, batch=8)
+        if use_nccl:
+            eng.comm_init(nccl_unique_id(), 1, 0)
+        x, lab = O.synthetic_batch(mc, 8, seed=21)
+        eng.set_batch(bf16_bits(x), lab)
+        eng.set_lr(0.05)
+        out = []
+        for mode, graph in [(REPROP, False), (PAREPROP, False), (REPROP, True), (PAREPROP, True)]:
+            eng.step(mode, graph=graph)
+            out.append((eng.loss(), eng.grads(), eng.params()))
+        runs[use_nccl] = out
+        eng.close()
+    for (la, ga, pa), (lb, gb, pb) in zip(runs[False], runs[True]):
+        assert la == lb
+        np.testing.assert_array_equal(ga, gb)
+        np.testing.assert_array_equal(pa, pb)
