@@ -128,7 +128,9 @@ int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols);
 int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t cols, float* out,
               float* workspace, int accumulate, rp_stream_t stream);
 /* out[c] (+)= sum_p part[p][c] in a fixed order (second stage of a column sum). */
-int rp_colsum_parts(const float* part, int64_t nparts, int64_t cols, float* out, int accumulate,
+/* out[c] (+)= sum_p part[p][c] in a fixed order; `part` is scratch afterwards (many parts
+ * are reduced in place in slices first) */
+int rp_colsum_parts(float* part, int64_t nparts, int64_t cols, float* out, int accumulate,
                     rp_stream_t stream);
 int64_t rp_colsum_workspace_floats(int64_t rows, int64_t cols);
 

@@ -377,6 +377,54 @@ __global__ void __launch_bounds__(kFinWarps * 32)
   }
 }
 
+// Column sums over many parts in two fixed-order stages: stage 1 (below) sums slices of
+// kSlice parts per CTA (8 warps x 32 columns, grid = column groups x slices) and writes the
+// slice sum IN PLACE over the slice's first part row (no other CTA reads that row); stage 2
+// is colsum_final_kernel over the slice rows (stride kSlice * ld). One CTA per 32 columns
+// walking all parts (the single-stage form) leaves most SMs idle when cols is small.
+constexpr int kSlice = 64;
+__global__ void __launch_bounds__(256)
+    colsum_slice_kernel(float* __restrict__ part, int64_t nparts, int cols, int64_t ld) {
+  pdl_trigger();
+  pdl_wait();
+
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.y) * kSlice;
+  float a0 = 0.f, a1 = 0.f;
+  if (c < cols) {
+#pragma unroll
+    for (int i = 0; i < kSlice / 8; i += 2) {
+      const int64_t p = p0 + warp + 8 * i, q = p + 8;
+      if (p < nparts) a0 += part[p * ld + c];
+      if (q < nparts) a1 += part[q * ld + c];
+    }
+  }
+  red[warp][lane] = a0 + a1;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    float t = red[0][lane];
+    for (int w = 1; w < 8; ++w) t += red[w][lane];
+    part[p0 * ld + c] = t;
+  }
+}
+
+static void colsum_final(cudaStream_t s, float* part, int64_t nparts, int cols, int64_t ld,
+                         float* out, int accumulate) {
+  const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
+  if (nparts > 2 * kSlice) {
+    const int64_t split = (nparts + kSlice - 1) / kSlice;
+    launch_k(colsum_slice_kernel, dim3(gb, static_cast<unsigned>(split)), dim3(256), 0, s, part,
+             nparts, cols, ld);
+    launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, part, split, cols,
+             ld * kSlice, out, accumulate);
+    return;
+  }
+  launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, part, nparts, cols, ld, out,
+           accumulate);
+}
+
 template <int V>
 static void launch_ln_fwd(const float* x, const float* g, const float* b, int64_t rows,
                           int cols, float eps, __nv_bfloat16* y, float* mean, float* rstd,
@@ -481,19 +529,15 @@ extern "C" int rp_layer_norm_bwd_ex(const float* x, const float* mean, const flo
                    workspace, nacc, s);
     const int64_t ld = nacc * cols;
     if (dgamma && dbeta == dgamma + cols) {
-      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
-               static_cast<int>(2 * cols), ld, dgamma, accumulate);
+      colsum_final(s, workspace, nparts, static_cast<int>(2 * cols), ld, dgamma, accumulate);
     } else {
       if (dgamma)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
-                 static_cast<int>(cols), ld, dgamma, accumulate);
+        colsum_final(s, workspace, nparts, static_cast<int>(cols), ld, dgamma, accumulate);
       if (dbeta)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols,
-                 nparts, static_cast<int>(cols), ld, dbeta, accumulate);
+        colsum_final(s, workspace + cols, nparts, static_cast<int>(cols), ld, dbeta, accumulate);
     }
     if (dx_colsum)
-      launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + 2 * cols,
-               nparts, static_cast<int>(cols), ld, dx_colsum, 0);
+      colsum_final(s, workspace + 2 * cols, nparts, static_cast<int>(cols), ld, dx_colsum, 0);
     return rp_check_launch("layer_norm_bwd");
   }
   if (dgamma || dbeta) {  // column partials first (reads x, dy before dx may alias dres)
@@ -501,15 +545,13 @@ extern "C" int rp_layer_norm_bwd_ex(const float* x, const float* mean, const flo
     launch_k(ln_bwd_dgb_partial_kernel, grid, dim3(256), 0, s, x, mean, rstd, dyb, rows,
              static_cast<int>(cols), kLnBwdRows, workspace);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
-      launch_k(colsum_final_kernel, dim3(2 * gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
-               static_cast<int>(2 * cols), 2 * cols, dgamma, accumulate);
+      colsum_final(s, workspace, nparts, static_cast<int>(2 * cols), 2 * cols, dgamma, accumulate);
     } else {
       if (dgamma)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace, nparts,
-                 static_cast<int>(cols), 2 * cols, dgamma, accumulate);
+        colsum_final(s, workspace, nparts, static_cast<int>(cols), 2 * cols, dgamma, accumulate);
       if (dbeta)
-        launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, workspace + cols,
-                 nparts, static_cast<int>(cols), 2 * cols, dbeta, accumulate);
+        colsum_final(s, workspace + cols, nparts, static_cast<int>(cols), 2 * cols, dbeta,
+                     accumulate);
     }
   }
   RP_LN_DISPATCH(launch_ln_bwd, x, mean, rstd, gamma, dyb, dres, rows, static_cast<int>(cols), dx,
@@ -530,12 +572,11 @@ extern "C" int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols
   return rp_ln_bwd_num_parts(rows) * 3 * cols;
 }
 
-extern "C" int rp_colsum_parts(const float* part, int64_t nparts, int64_t cols, float* out,
+extern "C" int rp_colsum_parts(float* part, int64_t nparts, int64_t cols, float* out,
                                int accumulate, rp_stream_t stream) {
   if (nparts <= 0 || cols <= 0) return rp_fail(RP_ERR_SHAPE, "colsum_parts: empty");
-  launch_k(colsum_final_kernel, dim3(static_cast<unsigned>((cols + 31) / 32)),
-           dim3(kFinWarps * 32), 0, static_cast<cudaStream_t>(stream), part, nparts,
-           static_cast<int>(cols), cols, out, accumulate);
+  colsum_final(static_cast<cudaStream_t>(stream), part, nparts, static_cast<int>(cols), cols, out,
+               accumulate);
   return rp_check_launch("colsum_parts");
 }
 
@@ -559,7 +600,6 @@ extern "C" int rp_colsum(const void* in, int in_is_bf16, int64_t rows, int64_t c
     launch_k(colsum_partial_kernel<float>, dim3(grid), dim3(256), 0, s, static_cast<const float*>(in), rows,
                                                       static_cast<int>(cols), kColRpb,
                                                       workspace);
-  launch_k(colsum_final_kernel, dim3(static_cast<unsigned>((cols + 31) / 32)), dim3(kFinWarps * 32), 0, s, 
-      workspace, nparts, static_cast<int>(cols), cols, out, accumulate);
+  colsum_final(s, workspace, nparts, static_cast<int>(cols), cols, out, accumulate);
   return rp_check_launch("col_sum");
 }
