@@ -359,3 +359,25 @@ def test_single_rank_nccl_path_matches_local():
         assert la == lb
         np.testing.assert_array_equal(ga, gb)
         np.testing.assert_array_equal(pa, pb)
+
+
+@pytest.mark.parametrize("kw", [dict(TI, depth=1), dict(TI, depth=2, seq_len=1),
+                                dict(TI, depth=3, seq_len=2)],
+                         ids=["depth1", "one-token", "two-tokens"])
+def test_degenerate_shapes_match_oracle(kw):
+    """A single block (no inverse at all: its input is the stored stage input), a single
+    token (softmax over one key is 1) and two tokens: grads vs the oracle and
+    PaReprop == Reprop."""
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits, bf16_round
+    eng, mc, p32, pref = make(kw, batch=4)
+    x, lab = O.synthetic_batch(mc, 4, seed=2)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    eng.step(REPROP, graph=False)
+    loss, g = eng.loss(), eng.grads()
+    r = O.step(mc, pref, bf16_round(x).astype(np.float64), lab)
+    assert abs(loss - r.loss) / abs(r.loss) < 1e-3
+    assert l2rel(g, r.grads) < TOL_L2
+    eng.step(PAREPROP, graph=True)
+    assert eng.loss() == loss
+    np.testing.assert_array_equal(eng.grads(), g)

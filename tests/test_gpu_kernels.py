@@ -245,7 +245,8 @@ def attn_ref(qkv, B, N, H, hd=64):
 
 @pytest.mark.parametrize("impl", [0, 1, 2], ids=["tcgen05", "mma_sync", "tcgen05_2pass"])
 @pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3), (2, 300, 2), (1, 480, 3), (3, 768, 1),
-                                   (3, 256, 2), (2, 129, 1)])
+                                   (3, 256, 2), (2, 129, 1), (3, 1, 2), (2, 2, 1), (1, 17, 1),
+                                   (4, 257, 1)])
 def test_attention_fwd_bwd(K, B, N, H, impl):
     from paper_2306_09342_b200 import _capi
     _capi.lib().rp_set_attention_impl(impl)
@@ -261,6 +262,11 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
     g = qkv_r.grad
     for i, name in enumerate("qkv"):
         sl = slice(i * H * 64, (i + 1) * H * 64)
-        assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
+        if g[:, sl].abs().max() < 1e-6 * g.abs().max():
+            # N = 1: softmax over one key has no gradient wrt q, k; ours is rounding noise
+            # of dP - D, bounded relative to the whole gradient
+            assert (dqkv[:, sl].float() - g[:, sl]).abs().max() < 1e-3 * g.abs().max(), name
+        else:
+            assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
     assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H))
     _capi.lib().rp_set_attention_impl(0)
