@@ -153,3 +153,25 @@ def test_hierarchical_config_errors_and_ledger(capi):
     assert vb - va == 12 * pair2
     pr, blk = activation_bytes(base, REPROP)
     assert activation_bytes(base, PAREPROP)[0] == pr + blk
+
+
+def test_cli_configs_parse(capi):
+    """bench-cli config files: every committed config builds a model config
+    the engine accepts (host-side validation only), incl. the hierarchical keys, and the
+    ledger-based probe runs on it without a device."""
+    import glob
+    import os
+    from paper_2306_09342_b200.cli import model_config, read_config
+    from paper_2306_09342_b200.engine import REPROP, activation_bytes, probe_max_batch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    seen_hier = False
+    for path in sorted(glob.glob(os.path.join(root, "configs", "*.cfg"))):
+        cfg = read_config(path)
+        mc = model_config(cfg, int(cfg["bench.batch_sizes"].split(",")[0]))
+        peak, blk = activation_bytes(mc, REPROP)
+        assert peak > blk > 0, path
+        assert probe_max_batch(mc, REPROP, 4 * peak) >= 1
+        if mc.depths:
+            seen_hier = True
+            assert mc.depth == sum(mc.depths) and mc.width == mc.widths[0]
+    assert seen_hier
