@@ -873,9 +873,10 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   add(g->st.back().d * g->C, 0);
   g->P = g->t_off.back() + g->t_numel.back();
   int rc = RP_OK;
-  // Lane G (the critical path) gets the highest stream priority, lane R and the comm /
-  // SGD stream the lowest: the block scheduler then fills idle SMs and kernel tails with
-  // recompute work instead of letting it compete with the gradient lane.
+  // Lane G (the critical path) and the comm / optimizer stream get the highest stream
+  // priority, lane R the lowest: the block scheduler then fills idle SMs and kernel tails
+  // with recompute work instead of letting it compete with the gradient lane, and a
+  // bucket's all-reduce (a few CTAs, latency-critical) is not queued behind the lanes' work.
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   const bool use_prio = c->lane_priority != 0;
@@ -886,7 +887,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
                                                  use_prio ? prio_lo : 0),
                     "stream")) ||
       (rc = cuda_ok(cudaStreamCreateWithPriority(&g->sC, cudaStreamNonBlocking,
-                                                 use_prio ? prio_lo : 0),
+                                                 use_prio ? prio_hi : 0),
                     "stream")))
     return fail(rc);
   g->evR.resize(static_cast<size_t>(g->L));
