@@ -219,6 +219,9 @@ int rp_engine_wait_loss(RpEngine* engine);
 int rp_engine_set_lr(RpEngine* engine, float lr);
 int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
 int rp_engine_invalidate_graphs(RpEngine* engine);
+/* Test hook of the verify command: kind 1 corrupts every block's F-path VJP
+ * (propagated cotangent x 1.5), kind 0 restores it. */
+int rp_engine_inject_fault(RpEngine* engine, int kind);
 int rp_engine_enable_vanilla(RpEngine* engine);
 /* mode: 0 vanilla (needs rp_engine_enable_vanilla), 1 reprop, 2 pareprop */
 int rp_engine_step(RpEngine* engine, int mode, int use_graph);

@@ -126,9 +126,11 @@ def cmd_bench(cfg: dict) -> int:
     return 0
 
 
-def cmd_verify(cfg: dict) -> int:
+def cmd_verify(cfg: dict, inject_fault: bool = False) -> int:
     """Engine vs oracle on a small model: step grads (stated tolerance), PaReprop == Reprop
-    bit-exact, Vanilla ~ Reprop, lr = 0 leaves the model unchanged."""
+    bit-exact, Vanilla ~ Reprop, lr = 0 leaves the model unchanged. inject_fault corrupts
+    every block's VJP first: the report must then flag the gradient checks
+    and the exit status be nonzero."""
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle import revprop_oracle as O
 
@@ -145,6 +147,8 @@ def cmd_verify(cfg: dict) -> int:
     eng.set_batch(bf16_bits(x), lab)
     eng.set_lr(0.0)
     eng.enable_vanilla()
+    if inject_fault:
+        eng.inject_fault(1)
     report = []
 
     def check(name, ok, value):
@@ -208,6 +212,8 @@ def main(argv=None) -> int:
     ap.add_argument("--batch-sizes")
     ap.add_argument("--budget-bytes", type=float, default=80e9)
     ap.add_argument("--dtype", default="bf16", choices=["bf16"])
+    ap.add_argument("--inject-fault", action="store_true",
+                    help="verify: corrupt the VJP first (the report must flag it)")
     a = ap.parse_args(argv)
     cfg = read_config(a.config)
     if a.seed is not None:
@@ -221,7 +227,7 @@ def main(argv=None) -> int:
     if a.command == "bench":
         return cmd_bench(cfg)
     if a.command == "verify":
-        return cmd_verify(cfg)
+        return cmd_verify(cfg, a.inject_fault)
     return cmd_probe(cfg, a.budget_bytes)
 
 

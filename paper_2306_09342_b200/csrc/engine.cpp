@@ -173,6 +173,7 @@ struct RpEngine {
   int optimizer = 0;
   float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f, wd = 0.f;
   float *adam_m = nullptr, *adam_v = nullptr, *step_t = nullptr;
+  int fault = 0;  // test hook: 1 = corrupt every block's F-path VJP
 };
 
 namespace {
@@ -578,6 +579,7 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
                               g->dh, g->d1, T, d, g->d1, g->d1b, gr(g, tix_block(g, b, kLnFg)),
                               gr(g, tix_block(g, b, kLnFb)),
                               next_b2 ? gr(g, tix_block(g, b - 1, kB2)) : nullptr, g->ln_ws, 0, s));
+  if (g->fault == 1) RP_TRY(rpk_scale_pair(g->d1, g->d1b, T * d, 1.5f, s));  // injected fault
   mark(g, 1, b, 1, s);
   return RP_OK;
 }
@@ -1189,6 +1191,15 @@ extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
   g->vmode = false;
   g->vanilla_ready = true;
   return RP_OK;
+}
+
+// Test hook for the verify command ("deliberately corrupted VJP"): kind 1
+// scales every block's propagated F-path cotangent by 1.5; kind 0 restores the true VJP.
+extern "C" int rp_engine_inject_fault(RpEngine* g, int kind) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  if (kind < 0 || kind > 1) return rp_fail(RP_ERR_CONFIG, "inject_fault: kind must be 0 or 1");
+  g->fault = kind;
+  return rp_engine_invalidate_graphs(g);
 }
 
 // Drop captured graphs (e.g. after toggling rp_set_pdl); the next step recaptures.

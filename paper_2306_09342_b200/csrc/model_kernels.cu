@@ -330,6 +330,20 @@ __global__ void halve_dup_kernel(float* __restrict__ d1, int64_t n4, float* __re
   }
 }
 
+// x *= s (fp32 and its bf16 shadow): the verify command's fault-injection hook
+__global__ void scale_pair_kernel(float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                  int64_t n, float s) {
+  pdl_trigger();
+  pdl_wait();
+
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i] * s;
+    x[i] = v;
+    xb[i] = __float2bfloat16_rn(v);
+  }
+}
+
 static inline unsigned grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -420,4 +434,9 @@ int rpk_halve_dup(float* d1, int64_t n, float* d2, uint16_t* d1b, uint16_t* d2b,
   launch_k(halve_dup_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, d1, n / 4, d2,
            reinterpret_cast<__nv_bfloat16*>(d1b), reinterpret_cast<__nv_bfloat16*>(d2b));
   return rp_check_launch("halve_dup");
+}
+int rpk_scale_pair(float* x, uint16_t* xb, int64_t n, float s, cudaStream_t st) {
+  launch_k(scale_pair_kernel, dim3(grid_for(n)), dim3(256), 0, st, x,
+           reinterpret_cast<__nv_bfloat16*>(xb), n, s);
+  return rp_check_launch("scale_pair");
 }

@@ -29,3 +29,4 @@ int rpk_fuse_avg_bf16(const float* o1, const float* o2, int64_t n, uint16_t* out
 int rpk_concat_bf16(const float* o1, const float* o2, int64_t rows, int64_t d, uint16_t* out,
                     cudaStream_t s);
 int rpk_halve_dup(float* d1, int64_t n, float* d2, uint16_t* d1b, uint16_t* d2b, cudaStream_t s);
+int rpk_scale_pair(float* x, uint16_t* xb, int64_t n, float s, cudaStream_t st);

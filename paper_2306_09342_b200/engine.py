@@ -109,6 +109,7 @@ _API = {
     "rp_engine_set_lr": (_I, [_P, C.c_float]),
     "rp_engine_set_partition": (_I, [_P, _I, _I]),
     "rp_engine_invalidate_graphs": (_I, [_P]),
+    "rp_engine_inject_fault": (_I, [_P, _I]),
     "rp_engine_enable_vanilla": (_I, [_P]),
     "rp_engine_step": (_I, [_P, _I, _I]),
     "rp_engine_sync": (_I, [_P]),
@@ -243,6 +244,10 @@ class Engine:
     def enable_vanilla(self):
         """Allocate the store-everything stash so step(VANILLA) works."""
         check(api("rp_engine_enable_vanilla")(self._h), "enable_vanilla")
+
+    def inject_fault(self, kind: int = 1):
+        """Verify's fault-injection hook: 1 corrupts the F-path VJP, 0 heals."""
+        check(api("rp_engine_inject_fault")(self._h, kind), "inject_fault")
 
     def invalidate_graphs(self):
         check(api("rp_engine_invalidate_graphs")(self._h), "invalidate_graphs")

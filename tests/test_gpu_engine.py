@@ -381,3 +381,14 @@ def test_degenerate_shapes_match_oracle(kw):
     eng.step(PAREPROP, graph=True)
     assert eng.loss() == loss
     np.testing.assert_array_equal(eng.grads(), g)
+
+
+def test_verify_command_and_fault_injection():
+    """bench-cli verify: the tiny config passes every check (exit 0); with
+    the corrupted-VJP hook the report flags the gradient checks and the exit status is 1."""
+    import os
+    from paper_2306_09342_b200.cli import main
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = os.path.join(root, "configs", "verify_tiny.cfg")
+    assert main(["verify", cfg]) == 0
+    assert main(["verify", cfg, "--inject-fault"]) == 1
