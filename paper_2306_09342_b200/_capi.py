@@ -109,6 +109,13 @@ def lib():
         if not _LIB_PATH.exists():
             raise ImportError(
                 f"{_LIB_PATH} is missing: build it with `python -m paper_2306_09342_b200.build`")
+        # torch first: its bundled libnccl.so.2 (newer than the system one) must be the one
+        # the dynamic loader binds for both torch and this library's ncclAllReduce -- loaded
+        # the other way round, torch's CUDA library fails on symbols the older NCCL lacks
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         L = C.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)

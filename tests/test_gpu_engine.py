@@ -93,7 +93,10 @@ def test_block_forward_and_backward_local(cfg):
         bf16_round(d1).astype(np.float64), bf16_round(d2).astype(np.float64))
     gi1, gi2, gd1, gd2 = (o.cpu().numpy().reshape(o1.shape) for o in outs)
     # recomputed inputs match the true inputs (round trip) and the oracle's recompute
-    assert maxrel(gi1, i1) < 1e-3 and maxrel(gi2, i2) < 1e-3
+    # round trip at the SPEC's f32 bound (<= 1e-4): F and G are recomputed by
+    # the same kernels, but i1 comes back with fp32 add / subtract rounding and its bf16
+    # LayerNorm output can then round the other way in a few elements
+    assert maxrel(gi1, i1) < 1e-4 and maxrel(gi2, i2) < 1e-4
     assert maxrel(gi1, ri1) < TOL_ACT and maxrel(gi2, ri2) < TOL_ACT
     assert maxrel(gd1, rd1) < TOL_ACT and maxrel(gd2, rd2) < TOL_ACT
     assert l2rel(gd1, rd1) < TOL_L2 and l2rel(gd2, rd2) < TOL_L2
