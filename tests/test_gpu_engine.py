@@ -395,3 +395,21 @@ def test_verify_command_and_fault_injection():
     cfg = os.path.join(root, "configs", "verify_tiny.cfg")
     assert main(["verify", cfg]) == 0
     assert main(["verify", cfg, "--inject-fault"]) == 1
+
+
+def test_pareprop_bit_identical_to_reprop_50_seeds():
+    """SPEC.md:499 acceptance 3 on the GPU: 50 seeded (weights, batch) trials, PaReprop's
+    loss and every gradient bit-identical to Reprop's (graph-captured steps)."""
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits
+    cfg = dict(TI, depth=3, seq_len=16)
+    eng, mc, _, _ = make(cfg, batch=2)
+    eng.set_lr(0.0)
+    for seed in range(50):
+        eng.set_params(O.init_params(mc, seed, np.float32))
+        x, lab = O.synthetic_batch(mc, 2, seed=100 + seed)
+        eng.set_batch(bf16_bits(x), lab)
+        eng.step(REPROP)
+        l1, g1 = eng.loss(), eng.grads()
+        eng.step(PAREPROP)
+        assert eng.loss() == l1, seed
+        np.testing.assert_array_equal(eng.grads(), g1, err_msg=f"seed {seed}")
