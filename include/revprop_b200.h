@@ -240,6 +240,18 @@ int rp_engine_rev_forward(RpEngine* engine, int64_t block, const float* i1, cons
 int rp_engine_rev_backward_local(RpEngine* engine, int64_t block, const float* o1,
                                  const float* o2, const float* d_o1, const float* d_o2,
                                  float* i1, float* i2, float* d_i1, float* d_i2);
+/* rev_inverse for a block that is not its stage's first: (o1, o2) ->
+ * (i1, i2) = (o1 - G(o2), o2 - F(i1)), fp32 [T_s, d_s] device pointers. */
+int rp_engine_rev_inverse(RpEngine* engine, int64_t block, const float* o1, const float* o2,
+                          float* i1, float* i2);
+/* Hierarchical models: the stage boundary after `stage` (ref:proj/core/src/layers.cpp:261-303).
+ * forward: y = patch_merge(fuse(o1, o2)), fp32 [T_{s+1}, d_{s+1}];
+ * vjp: from the next stage's input cotangents (d_i1, d_i2) to the stage output's (d_o1,
+ * d_o2); merge_w / fusion_w grads land in the engine's gradient buffer. */
+int rp_engine_boundary_forward(RpEngine* engine, int64_t stage, const float* o1,
+                               const float* o2, float* y);
+int rp_engine_boundary_vjp(RpEngine* engine, int64_t stage, const float* o1, const float* o2,
+                           const float* d_i1, const float* d_i2, float* d_o1, float* d_o2);
 
 #ifdef __cplusplus
 }

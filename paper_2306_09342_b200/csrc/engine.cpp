@@ -1429,3 +1429,66 @@ extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float*
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_i2, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   return rp_engine_sync(g);
 }
+
+// rev_inverse for a block that is not its stage's first:
+// (o1, o2) -> (i1, i2) = (o1 - G(o2), o2 - F(i1)); one F and one G evaluation.
+extern "C" int rp_engine_rev_inverse(RpEngine* g, int64_t b, const float* o1, const float* o2,
+                                     float* i1, float* i2) {
+  if (!g || b < 1 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block (b >= 1)");
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
+  if (j < 1) return rp_fail(RP_ERR_CONTRACT, "rev_inverse: block is its stage's first");
+  cudaStream_t s = g->sG;
+  const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, j + 1), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, j + 1), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  set_partition(g, 1);
+  RP_TRY(lane_r(g, b, s));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i1, X1(g, St, j), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(i2, X2(g, St, j), bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}
+
+// Stage boundary after stage `stage` (hierarchical models; ref:proj/core/src/layers.cpp:261-303):
+// forward  y = patch_merge(fuse(o1, o2)) -> fp32 [T_{s+1}, d_{s+1}] (the next stage's input);
+// backward given the next stage's input cotangents (d_i1, d_i2, fp32): the stage output's
+// cotangents (d_o1, d_o2) and the boundary's parameter grads in the engine grad buffer.
+extern "C" int rp_engine_boundary_forward(RpEngine* g, int64_t stage, const float* o1,
+                                          const float* o2, float* y) {
+  if (!g || stage < 0 || stage + 1 >= static_cast<int64_t>(g->st.size()))
+    return rp_fail(RP_ERR_CONTRACT, "boundary_forward: no boundary after this stage");
+  RpStage& St = g->st[static_cast<size_t>(stage)];
+  const RpStage& Nx = g->st[static_cast<size_t>(stage) + 1];
+  cudaStream_t s = g->sG;
+  const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, St.L), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, St.L), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(boundary_fuse(g, St, s));
+  RP_TRY(launch(St.b_merge, s));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(y, Nx.e, static_cast<size_t>(Nx.T * Nx.d) * 4,
+                                 cudaMemcpyDeviceToDevice, s),
+                 "copy"));
+  return rp_engine_sync(g);
+}
+
+extern "C" int rp_engine_boundary_vjp(RpEngine* g, int64_t stage, const float* o1,
+                                      const float* o2, const float* d_i1, const float* d_i2,
+                                      float* d_o1, float* d_o2) {
+  if (!g || stage < 0 || stage + 1 >= static_cast<int64_t>(g->st.size()))
+    return rp_fail(RP_ERR_CONTRACT, "boundary_vjp: no boundary after this stage");
+  RpStage& St = g->st[static_cast<size_t>(stage)];
+  const RpStage& Nx = g->st[static_cast<size_t>(stage) + 1];
+  cudaStream_t s = g->sG;
+  const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
+  const size_t nbytes = static_cast<size_t>(Nx.T * Nx.d) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, St.L), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, St.L), o2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d1, d_i1, nbytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d2, d_i2, nbytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  set_partition(g, 1);
+  RP_TRY(boundary_fuse(g, St, s));
+  RP_TRY(boundary_vjp(g, St, s));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_o1, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_o2, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}

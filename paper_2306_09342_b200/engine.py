@@ -124,6 +124,9 @@ _API = {
     "rp_engine_comm_init": (_I, [_P, _P, _I, _I]),
     "rp_engine_rev_forward": (_I, [_P, _I64, _P, _P, _P, _P]),
     "rp_engine_rev_backward_local": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "rp_engine_rev_inverse": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "rp_engine_boundary_forward": (_I, [_P, _I64, _P, _P, _P]),
+    "rp_engine_boundary_vjp": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P]),
 }
 _bound = {}
 
@@ -293,6 +296,22 @@ class Engine:
     def rev_forward(self, b, i1, i2, o1, o2):
         check(api("rp_engine_rev_forward")(self._h, b, i1.data_ptr(), i2.data_ptr(),
                                            o1.data_ptr(), o2.data_ptr()), "rev_forward")
+
+    def rev_inverse(self, b, o1, o2, i1, i2):
+        """SPEC.md:222-230 on device tensors (block b not first in its stage)."""
+        check(api("rp_engine_rev_inverse")(self._h, b, o1.data_ptr(), o2.data_ptr(),
+                                           i1.data_ptr(), i2.data_ptr()), "rev_inverse")
+
+    def boundary_forward(self, stage, o1, o2, y):
+        """patch_merge(fuse(o1, o2)) after `stage` (layers.cpp:261-287)."""
+        check(api("rp_engine_boundary_forward")(self._h, stage, o1.data_ptr(), o2.data_ptr(),
+                                                y.data_ptr()), "boundary_forward")
+
+    def boundary_vjp(self, stage, o1, o2, d_i1, d_i2, d_o1, d_o2):
+        """fuse_vjp(patch_merge_vjp(d_i1 + d_i2)) (layers.cpp:269-303); param grads in grads()."""
+        check(api("rp_engine_boundary_vjp")(self._h, stage, o1.data_ptr(), o2.data_ptr(),
+                                            d_i1.data_ptr(), d_i2.data_ptr(), d_o1.data_ptr(),
+                                            d_o2.data_ptr()), "boundary_vjp")
 
     def rev_backward_local(self, b, o1, o2, d_o1, d_o2, i1, i2, d_i1, d_i2):
         check(api("rp_engine_rev_backward_local")(

@@ -155,3 +155,75 @@ def test_hier_activation_ledger():
     pv, _ = activation_bytes(cfg, VANILLA)
     assert pp - pr == blk
     assert pv > pr
+
+
+@pytest.mark.parametrize("kw", [HA, HM], ids=["avg-r4", "mlp-r2"])
+def test_boundary_entry_points_match_oracle(kw):
+    """rp_engine_boundary_forward / _vjp (layers.cpp:261-303) vs the oracle's fuse +
+    patch_merge and their VJPs on the same bf16-rounded weights; inputs random."""
+    from paper_2306_09342_b200.engine import bf16_round
+    eng, mc, p32, pref = make(kw, batch=2)
+    st = O.stages(mc)
+    bnd = O.boundaries_of(mc, pref)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    rng = np.random.default_rng(3)
+    B = 2
+    mw_off = dict((n, None) for n, _ in O.tensor_shapes(mc))
+    for s in range(len(st) - 1):
+        g0, g1 = st[s], st[s + 1]
+        o1 = rng.standard_normal((B, g0.tokens, g0.d)).astype(np.float32)
+        o2 = rng.standard_normal((B, g0.tokens, g0.d)).astype(np.float32)
+        y = torch.empty(B * g1.tokens, g1.d, device="cuda")
+        eng.boundary_forward(s, t(o1), t(o2), y)
+        mw, fw = bnd[s]
+        # the GPU fuses in fp32, rounds the fused tensor to bf16 for the merge GEMM
+        f, _ = O.fuse(o1.astype(np.float64), o2.astype(np.float64), fw)
+        yr, grouped = O.patch_merge(bf16_round(f.astype(np.float32)).astype(np.float64), mw,
+                                    mc.reduction)
+        assert maxrel(y.cpu().numpy().reshape(yr.shape), yr) < 2e-2
+        d1 = rng.standard_normal((B, g1.tokens, g1.d)).astype(np.float32) * 1e-2
+        d2 = rng.standard_normal((B, g1.tokens, g1.d)).astype(np.float32) * 1e-2
+        do1 = torch.empty(B * g0.tokens, g0.d, device="cuda")
+        do2 = torch.empty_like(do1)
+        eng.boundary_vjp(s, t(o1), t(o2), t(d1), t(d2), do1, do2)
+        dy = bf16_round((d1 + d2).astype(np.float32)).astype(np.float64)
+        d_f, d_mw = O.patch_merge_vjp(grouped, mw, mc.reduction, dy)
+        _, concat = O.fuse(o1.astype(np.float64), o2.astype(np.float64), fw)
+        if concat is not None:
+            concat = bf16_round(concat.astype(np.float32)).astype(np.float64)
+        r1, r2, d_fw = O.fuse_vjp(concat, fw, d_f)
+        assert maxrel(do1.cpu().numpy().reshape(r1.shape), r1) < 2e-2
+        assert maxrel(do2.cpu().numpy().reshape(r2.shape), r2) < 2e-2
+        g = eng.grads()
+        off = 0
+        for name, shape in O.tensor_shapes(mc):
+            n = int(np.prod(shape))
+            if name == f"boundary.{s}.merge_w":
+                assert maxrel(g[off:off + n].reshape(shape), d_mw) < 5e-2, name
+            if name == f"boundary.{s}.fusion_w":
+                assert maxrel(g[off:off + n].reshape(shape), d_fw) < 5e-2, name
+            off += n
+
+
+def test_rev_inverse_round_trip():
+    """rp_engine_rev_inverse on a block inside a later stage: recovers the
+    block input at the SPEC's f32 round-trip bound and matches the oracle's inverse."""
+    eng, mc, p32, pref = make(HM, batch=2)
+    st = O.stages(mc)
+    g1 = st[1]  # depth 2: block g1.first + 1 is not the stage's first
+    b = g1.first + 1
+    _, blocks, _ = O.blocks_of(mc, pref)
+    rng = np.random.default_rng(5)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    i1 = rng.standard_normal((2, g1.tokens, g1.d)).astype(np.float32)
+    i2 = rng.standard_normal((2, g1.tokens, g1.d)).astype(np.float32)
+    rows = 2 * g1.tokens
+    o1, o2, r1, r2 = (torch.empty(rows, g1.d, device="cuda") for _ in range(4))
+    eng.rev_forward(b, t(i1), t(i2), o1, o2)
+    eng.rev_inverse(b, o1, o2, r1, r2)
+    assert maxrel(r1.cpu().numpy().reshape(i1.shape), i1) < 1e-4
+    assert maxrel(r2.cpu().numpy().reshape(i2.shape), i2) < 1e-4
+    ri1, ri2 = O.rev_inverse(blocks[b], o1.cpu().numpy().reshape(i1.shape).astype(np.float64),
+                             o2.cpu().numpy().reshape(i1.shape).astype(np.float64))
+    assert maxrel(r1.cpu().numpy().reshape(i1.shape), ri1) < 2e-2
+    assert maxrel(r2.cpu().numpy().reshape(i2.shape), ri2) < 2e-2
