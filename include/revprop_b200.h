@@ -252,6 +252,17 @@ int rp_engine_boundary_forward(RpEngine* engine, int64_t stage, const float* o1,
                                const float* o2, float* y);
 int rp_engine_boundary_vjp(RpEngine* engine, int64_t stage, const float* o1, const float* o2,
                            const float* d_i1, const float* d_i2, float* d_o1, float* d_o2);
+/* The reference's layer API on block `block`'s parameters (ref:proj/core/include/revprop/
+ * layers.hpp:82-138), fp32 [T_s, d_s] device pointers, no residual inside:
+ * attention_forward y = Proj(MHSA(LN_F(x))); mlp_forward y = W2 gelu(W1 LN_G(x) + b1) + b2;
+ * the VJPs recompute their caches from x, write d_x and the layer's parameter grads into
+ * the engine's gradient buffer. */
+int rp_engine_attention_forward(RpEngine* engine, int64_t block, const float* x, float* y);
+int rp_engine_mlp_forward(RpEngine* engine, int64_t block, const float* x, float* y);
+int rp_engine_attention_vjp(RpEngine* engine, int64_t block, const float* x, const float* d_y,
+                            float* d_x);
+int rp_engine_mlp_vjp(RpEngine* engine, int64_t block, const float* x, const float* d_y,
+                      float* d_x);
 
 #ifdef __cplusplus
 }

@@ -523,38 +523,54 @@ int head(RpEngine* g, cudaStream_t s) {
   return RP_OK;
 }
 
-// Lane R: recompute block b's input and caches from its output X_{j+1}.
-int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
+// Lane R halves: G recomputes the MLP caches from X2_{j+1} (= o2) and, unless j == 0, the
+// input i1 = o1 - G(o2); F recomputes the attention caches from X1_j (= i1) and, unless
+// j == 0, i2 = o2 - F(i1). `inverse` = false keeps only the caches (the layer VJP entries).
+int recompute_g(RpEngine* g, int64_t b, cudaStream_t s, bool inverse) {
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first;
   Slot& S = g->slot[b % 2];
-  mark(g, 0, b, 0, s);
   RP_TRY(ln_fwd(g, St, X2(g, St, j + 1), tix_block(g, b, kLnGg), tix_block(g, b, kLnGb), S.hG,
                 S.meanG, S.rstdG, s));
   RP_TRY(launch(p.r_w1, s));
-  if (j > 0 && !g->vmode) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
+  if (inverse && j > 0 && !g->vmode) RP_TRY(launch(p.r_w2, s));  // i1 = o1 - G(o2)
+  return RP_OK;
+}
+int recompute_f(RpEngine* g, int64_t b, cudaStream_t s, bool inverse) {
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
+  Slot& S = g->slot[b % 2];
   RP_TRY(ln_fwd(g, St, X1(g, St, j), tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), S.hF, S.meanF,
                 S.rstdF, s));
   RP_TRY(launch(p.r_qkv, s));
   RP_TRY(attn_fwd(St, S.qkv, S.att, S.lse, s));
-  if (j > 0 && !g->vmode) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
+  if (inverse && j > 0 && !g->vmode) RP_TRY(launch(p.r_proj, s));  // i2 = o2 - F(i1)
+  return RP_OK;
+}
+
+// Lane R: recompute block b's input and caches from its output X_{j+1}.
+int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
+  mark(g, 0, b, 0, s);
+  RP_TRY(recompute_g(g, b, s, true));
+  RP_TRY(recompute_f(g, b, s, true));
   mark(g, 0, b, 1, s);
   return RP_OK;
 }
 
-// Lane G: the VJP half of rev_backward_local (SPEC.md:234), G-path before F-path.
-// own_b2: this block's MLP output-bias grad from its incoming d_o1 (a column-sum pass);
-// in a stage only the top block needs it, every other block's b2 grad is produced by the
+// Lane G halves (layers.cpp:241-259 and 171-220). vjp_g: MLP VJP of d_o1 (d1 / d1b), adds
+// LN_G^T(d_hG) to d2 in place (d_o2t = d_o2 + VJP_G(d_o1)). vjp_f: attention VJP of d_o2t
+// (d2b), adds LN_F^T(d_hF) to d1 in place (d_i1 = d_o1 + VJP_F(d_o2t)).
+// own_b2: this block's MLP output-bias grad from its incoming d_o1 (a column-sum pass); in
+// a stage only the top block needs it, every other block's b2 grad is produced by the
 // block above in the same pass that writes its d_o1 (next_b2, the F-path LN backward).
-int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
+int vjp_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2) {
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first;
   Slot& S = g->slot[b % 2];
   const int64_t T = St.T, d = St.d, h = St.h;
-  mark(g, 1, b, 0, s);
-  // ---- G = MLP VJP with d_o1 (layers.cpp:241-259)
   // (the own-b2 column sum runs first: the d_u GEMM below writes its partials to col_ws)
   if (own_b2) RP_TRY(rp_colsum(g->d1, 0, T, d, gr(g, tix_block(g, b, kB2)), g->col_ws, 0, s));
   RP_TRY(launch(p.g_dw2, s));
@@ -564,10 +580,16 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   RP_TRY(rp_colsum_parts(g->col_ws, (T + 31) / 32, h, gr(g, tix_block(g, b, kB1)), 0, s));
   RP_TRY(launch(p.g_dw1, s));
   // d_o2t = d_o2 + LN_G^T(d_hG)   (in place in d2 / d2b)
-  RP_TRY(rp_layer_norm_bwd(X2(g, St, j + 1), S.meanG, S.rstdG, wf(g, tix_block(g, b, kLnGg)),
+  return rp_layer_norm_bwd(X2(g, St, j + 1), S.meanG, S.rstdG, wf(g, tix_block(g, b, kLnGg)),
                            g->dh, g->d2, T, d, g->d2, g->d2b, gr(g, tix_block(g, b, kLnGg)),
-                           gr(g, tix_block(g, b, kLnGb)), g->ln_ws, 0, s));
-  // ---- F = attention VJP with d_o2t (layers.cpp:171-220)
+                           gr(g, tix_block(g, b, kLnGb)), g->ln_ws, 0, s);
+}
+int vjp_f(RpEngine* g, int64_t b, cudaStream_t s, bool next_b2) {
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first;
+  Slot& S = g->slot[b % 2];
+  const int64_t T = St.T, d = St.d;
   RP_TRY(launch(p.g_dproj, s));
   RP_TRY(launch(p.g_wproj, s));
   RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / St.W, St.W, St.H, d / St.H, g->dqkv,
@@ -575,11 +597,19 @@ int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
   RP_TRY(launch(p.g_wqkv, s));
   RP_TRY(launch(p.g_dqkv, s));
   // d_i1 = d_o1 + LN_F^T(d_hF)    (in place in d1 / d1b); d_i2 = d_o2t (already in d2)
-  RP_TRY(rp_layer_norm_bwd_ex(X1(g, St, j), S.meanF, S.rstdF, wf(g, tix_block(g, b, kLnFg)),
+  return rp_layer_norm_bwd_ex(X1(g, St, j), S.meanF, S.rstdF, wf(g, tix_block(g, b, kLnFg)),
                               g->dh, g->d1, T, d, g->d1, g->d1b, gr(g, tix_block(g, b, kLnFg)),
                               gr(g, tix_block(g, b, kLnFb)),
-                              next_b2 ? gr(g, tix_block(g, b - 1, kB2)) : nullptr, g->ln_ws, 0, s));
-  if (g->fault == 1) RP_TRY(rpk_scale_pair(g->d1, g->d1b, T * d, 1.5f, s));  // injected fault
+                              next_b2 ? gr(g, tix_block(g, b - 1, kB2)) : nullptr, g->ln_ws, 0, s);
+}
+
+// Lane G: the VJP half of rev_backward_local (SPEC.md:234), G-path before F-path.
+int lane_g(RpEngine* g, int64_t b, cudaStream_t s, bool own_b2, bool next_b2) {
+  const RpStage& St = stage_of(g, b);
+  mark(g, 1, b, 0, s);
+  RP_TRY(vjp_g(g, b, s, own_b2));
+  RP_TRY(vjp_f(g, b, s, next_b2));
+  if (g->fault == 1) RP_TRY(rpk_scale_pair(g->d1, g->d1b, St.T * St.d, 1.5f, s));  // injected fault
   mark(g, 1, b, 1, s);
   return RP_OK;
 }
@@ -624,15 +654,19 @@ int enqueue_step_impl(RpEngine* g, int mode);
 
 int enqueue_step(RpEngine* g, int mode) {
   g->vmode = mode == 0;
+  // the live GEMM profiler looks its engine up through t_prof_engine while this step is
+  // enqueued -- and only then: outside a step (block / layer entry points, other engines)
+  // it must not point at an engine that may since have been destroyed
+  t_prof_engine = g;
+  g->prof_used = 0;
   const int rc = enqueue_step_impl(g, mode == 0 ? 1 : mode);
+  t_prof_engine = nullptr;
   g->vmode = false;
   return rc;
 }
 
 int enqueue_step_impl(RpEngine* g, int mode) {
   cudaStream_t sG = g->sG, sR = g->sR, sC = g->sC;
-  t_prof_engine = g;
-  g->prof_used = 0;
   if (g->optimizer == 1) RP_TRY(rpk_add_scalar(g->step_t, 1.0f, sG));
   RP_TRY(forward(g, sG));
   RP_TRY(head(g, sG));
@@ -1490,5 +1524,118 @@ extern "C" int rp_engine_boundary_vjp(RpEngine* g, int64_t stage, const float* o
   RP_TRY(boundary_vjp(g, St, s));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_o1, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_o2, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}
+
+// ---------------------------------------------------------------- layer-level entry points
+// The reference's F / G layer API (ref:proj/core/include/revprop/layers.hpp:82-138) on
+// block b's parameters, device pointers fp32 [T_s, d_s]; VJP parameter grads land in the
+// engine's gradient buffer (block b's slices), the input cotangent in d_x.
+namespace {
+int layer_check(RpEngine* g, int64_t b) {
+  if (!g || b < 0 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block");
+  return RP_OK;
+}
+}  // namespace
+
+// attention_forward (layers.cpp:134-169): y = Proj(MHSA(LN(x))), no residual
+extern "C" int rp_engine_attention_forward(RpEngine* g, int64_t b, const float* x, float* y) {
+  RP_TRY(layer_check(g, b));
+  RpStage& St = stage_of(g, b);
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  Slot& F = g->slot[0];
+  cudaStream_t s = g->sG;
+  set_partition(g, 1);
+  RP_TRY(ln_fwd(g, St, x, tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(launch(p.f_qkv, s));
+  RP_TRY(attn_fwd(St, F.qkv, F.att, F.lse, s));
+  RpGemmDesc dsc{};
+  dsc.A = F.att;
+  dsc.lda = St.d;
+  dsc.B = wb(g, tix_block(g, b, kWout));
+  dsc.ldb = St.d;
+  dsc.b_mn = 1;
+  dsc.M = St.T;
+  dsc.N = St.d;
+  dsc.K = St.d;
+  dsc.epi = RP_EPI_F32;
+  dsc.out = y;
+  dsc.ldo = St.d;
+  dsc.splits = 1;
+  dsc.bn = kGemmBn;
+  RP_TRY(rp_gemm(&dsc, s));
+  return rp_engine_sync(g);
+}
+
+// mlp_forward (layers.cpp:222-239): y = W2 gelu(W1 LN(x) + b1) + b2, no residual
+extern "C" int rp_engine_mlp_forward(RpEngine* g, int64_t b, const float* x, float* y) {
+  RP_TRY(layer_check(g, b));
+  RpStage& St = stage_of(g, b);
+  BlockPlans& p = g->plans[static_cast<size_t>(b)];
+  Slot& F = g->slot[0];
+  cudaStream_t s = g->sG;
+  set_partition(g, 1);
+  RP_TRY(ln_fwd(g, St, x, tix_block(g, b, kLnGg), tix_block(g, b, kLnGb), F.hF, F.meanF, F.rstdF, s));
+  RP_TRY(launch(p.f_w1, s));  // F.a = gelu(hG W1 + b1)
+  RP_TRY(cuda_ok(cudaMemsetAsync(y, 0, static_cast<size_t>(St.T * St.d) * 4, s), "memset"));
+  RpGemmDesc dsc{};
+  dsc.A = F.a;
+  dsc.lda = St.h;
+  dsc.B = wb(g, tix_block(g, b, kW2));
+  dsc.ldb = St.d;
+  dsc.b_mn = 1;
+  dsc.M = St.T;
+  dsc.N = St.d;
+  dsc.K = St.h;
+  dsc.epi = RP_EPI_RESID;  // y = 0 + (a W2 + b2)
+  dsc.out = y;
+  dsc.ldo = St.d;
+  dsc.aux = y;
+  dsc.ldaux = St.d;
+  dsc.bias = wf(g, tix_block(g, b, kB2));
+  dsc.sign = 1.f;
+  dsc.splits = 1;
+  dsc.bn = kGemmBn;
+  RP_TRY(rp_gemm(&dsc, s));
+  return rp_engine_sync(g);
+}
+
+// attention_vjp (layers.cpp:171-220): d_x and the F parameter grads of d_y, caches
+// recomputed from x
+extern "C" int rp_engine_attention_vjp(RpEngine* g, int64_t b, const float* x, const float* d_y,
+                                       float* d_x) {
+  RP_TRY(layer_check(g, b));
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first, n = St.T * St.d;
+  cudaStream_t s = g->sG;
+  set_partition(g, 1);
+  const size_t bytes = static_cast<size_t>(n) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, j), x, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d2, d_y, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(rpk_f32_to_bf16(g->d2, g->d2b, n, s));
+  RP_TRY(cuda_ok(cudaMemsetAsync(g->d1, 0, bytes, s), "memset"));  // no residual cotangent
+  RP_TRY(recompute_f(g, b, s, false));
+  RP_TRY(vjp_f(g, b, s, false));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_x, g->d1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  return rp_engine_sync(g);
+}
+
+// mlp_vjp (layers.cpp:241-259): d_x and the G parameter grads of d_y, caches recomputed
+// from x
+extern "C" int rp_engine_mlp_vjp(RpEngine* g, int64_t b, const float* x, const float* d_y,
+                                 float* d_x) {
+  RP_TRY(layer_check(g, b));
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first, n = St.T * St.d;
+  cudaStream_t s = g->sG;
+  set_partition(g, 1);
+  const size_t bytes = static_cast<size_t>(n) * 4;
+  RP_TRY(cuda_ok(cudaMemcpyAsync(X2(g, St, j + 1), x, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->d1, d_y, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
+  RP_TRY(rpk_f32_to_bf16(g->d1, g->d1b, n, s));
+  RP_TRY(cuda_ok(cudaMemsetAsync(g->d2, 0, bytes, s), "memset"));  // no residual cotangent
+  RP_TRY(recompute_g(g, b, s, false));
+  RP_TRY(vjp_g(g, b, s, true));
+  RP_TRY(cuda_ok(cudaMemcpyAsync(d_x, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   return rp_engine_sync(g);
 }

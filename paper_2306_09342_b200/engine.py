@@ -125,6 +125,10 @@ _API = {
     "rp_engine_rev_forward": (_I, [_P, _I64, _P, _P, _P, _P]),
     "rp_engine_rev_backward_local": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "rp_engine_rev_inverse": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "rp_engine_attention_forward": (_I, [_P, _I64, _P, _P]),
+    "rp_engine_mlp_forward": (_I, [_P, _I64, _P, _P]),
+    "rp_engine_attention_vjp": (_I, [_P, _I64, _P, _P, _P]),
+    "rp_engine_mlp_vjp": (_I, [_P, _I64, _P, _P, _P]),
     "rp_engine_boundary_forward": (_I, [_P, _I64, _P, _P, _P]),
     "rp_engine_boundary_vjp": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P]),
 }
@@ -296,6 +300,22 @@ class Engine:
     def rev_forward(self, b, i1, i2, o1, o2):
         check(api("rp_engine_rev_forward")(self._h, b, i1.data_ptr(), i2.data_ptr(),
                                            o1.data_ptr(), o2.data_ptr()), "rev_forward")
+
+    # layers API (ref layers.hpp:82-138) on block b's parameters, device tensors
+    def attention_forward(self, b, x, y):
+        check(api("rp_engine_attention_forward")(self._h, b, x.data_ptr(), y.data_ptr()),
+              "attention_forward")
+
+    def mlp_forward(self, b, x, y):
+        check(api("rp_engine_mlp_forward")(self._h, b, x.data_ptr(), y.data_ptr()), "mlp_forward")
+
+    def attention_vjp(self, b, x, d_y, d_x):
+        check(api("rp_engine_attention_vjp")(self._h, b, x.data_ptr(), d_y.data_ptr(),
+                                             d_x.data_ptr()), "attention_vjp")
+
+    def mlp_vjp(self, b, x, d_y, d_x):
+        check(api("rp_engine_mlp_vjp")(self._h, b, x.data_ptr(), d_y.data_ptr(), d_x.data_ptr()),
+              "mlp_vjp")
 
     def rev_inverse(self, b, o1, o2, i1, i2):
         """SPEC.md:222-230 on device tensors (block b not first in its stage)."""

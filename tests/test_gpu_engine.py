@@ -413,3 +413,51 @@ def test_pareprop_bit_identical_to_reprop_50_seeds():
         eng.step(PAREPROP)
         assert eng.loss() == l1, seed
         np.testing.assert_array_equal(eng.grads(), g1, err_msg=f"seed {seed}")
+
+
+@pytest.mark.parametrize("cfg", [TI, BW], ids=["ti", "b-width"])
+@pytest.mark.parametrize("b", [0, 1])
+def test_layer_api_matches_oracle(cfg, b):
+    """attention_forward / attention_vjp / mlp_forward / mlp_vjp entry points (ref
+    layers.hpp:82-138) on block b's parameters vs the oracle's layers (layers.cpp:134-259)."""
+    from paper_2306_09342_b200.engine import bf16_round
+    eng, mc, p32, pref = make(cfg, batch=2)
+    _, blocks, _ = O.blocks_of(mc, pref)
+    blk = blocks[b]
+    T, d = 2 * mc.seq_len, mc.width
+    rng = np.random.default_rng(9 + b)
+    x = rng.standard_normal((2, mc.seq_len, d)).astype(np.float32)
+    dy = (rng.standard_normal((2, mc.seq_len, d)) * 1e-2).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    y, dx = torch.empty(T, d, device="cuda"), torch.empty(T, d, device="cuda")
+    x64, dy64 = x.astype(np.float64), bf16_round(dy).astype(np.float64)
+    names = [n for n, _ in O.tensor_shapes(mc)]
+    shapes = dict(O.tensor_shapes(mc))
+
+    def grad(name):
+        off = 0
+        g = eng.grads()
+        for n in names:
+            k = int(np.prod(shapes[n]))
+            if n == name:
+                return g[off:off + k].reshape(shapes[n])
+            off += k
+
+    eng.attention_forward(b, t(x), y)
+    yr, cache = O.attention_forward(x64, blk.f)
+    assert maxrel(y.cpu().numpy().reshape(yr.shape), yr) < TOL_ACT
+    eng.attention_vjp(b, t(x), t(dy), dx)
+    dxr, gr = O.attention_vjp(cache, blk.f, dy64)
+    assert maxrel(dx.cpu().numpy().reshape(dxr.shape), dxr) < TOL_ACT
+    for k, n in [("d_w_qkv", "w_qkv"), ("d_w_out", "w_out"), ("d_ln_gamma", "lnF_g"),
+                 ("d_ln_beta", "lnF_b")]:
+        assert maxrel(grad(f"blocks.{b}.{n}"), gr[k]) < TOL_GRAD, n
+    eng.mlp_forward(b, t(x), y)
+    yr, cache = O.mlp_forward(x64, blk.g)
+    assert maxrel(y.cpu().numpy().reshape(yr.shape), yr) < TOL_ACT
+    eng.mlp_vjp(b, t(x), t(dy), dx)
+    dxr, gr = O.mlp_vjp(cache, blk.g, dy64)
+    assert maxrel(dx.cpu().numpy().reshape(dxr.shape), dxr) < TOL_ACT
+    for k, n in [("d_w1", "w1"), ("d_b1", "b1"), ("d_w2", "w2"), ("d_b2", "b2"),
+                 ("d_ln_gamma", "lnG_g"), ("d_ln_beta", "lnG_b")]:
+        assert maxrel(grad(f"blocks.{b}.{n}"), gr[k]) < TOL_GRAD, n
