@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   const int c4 = cols >> 2;
   float4* my = acc4 + static_cast<int64_t>(warp) * NACC * c4;
   for (int i = lane; i < NACC * c4; i += 32) my[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();  // when cols/4 is not a multiple of 32, another lane zeroed this lane's slots
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
   const float inv_n = 1.0f / static_cast<float>(cols);
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
