@@ -1,0 +1,55 @@
+"""Small-shape driver of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck): GEMM epilogue kinds (1-CTA and CTA-pair), LayerNorm forward / backward, column
+sums, attention forward / backward on all paths (tcgen05 fused and two-pass, mma.sync at
+head_dim 32 / 64 / 104 incl. the short-window kernel).
+
+    compute-sanitizer --tool racecheck python tools/sanitize_kernels.py
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2306_09342_b200 import _capi, kernels as K  # noqa: E402
+from paper_2306_09342_b200._capi import (RP_EPI_BF16, RP_EPI_BIAS_GELU, RP_EPI_F32,  # noqa: E402
+                                         RP_EPI_GELU_BWD, RP_EPI_RESID)
+
+dev = "cuda"
+bf = torch.bfloat16
+M, N, Kd = 300, 256, 192
+a = torch.randn(M, Kd, device=dev).to(bf)
+w = (0.05 * torch.randn(Kd, N, device=dev)).to(bf)
+for bn in (256, 512):
+    K.gemm(a, w, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BF16,
+           out=torch.empty(M, N, device=dev, dtype=bf), bn=bn)
+    K.gemm(a, w, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_BIAS_GELU,
+           out=torch.empty(M, N, device=dev, dtype=bf), out2=torch.empty(M, N, device=dev, dtype=bf),
+           bias=torch.zeros(N, device=dev), bn=bn)
+    res = torch.randn(M, N, device=dev)
+    K.gemm(a, w, M, N, Kd, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=torch.empty(M, N, device=dev),
+           aux=res, bn=bn)
+    u = torch.randn(M, N, device=dev).to(bf)
+    K.gemm(a, w.t().contiguous(), M, N, Kd, a_mn=0, b_mn=0, epi=RP_EPI_GELU_BWD,
+           out=torch.empty(M, N, device=dev, dtype=bf), aux=u, bn=bn)
+    ws = torch.empty(4 * Kd * N, device=dev)
+    K.gemm(a, torch.randn(M, N, device=dev).to(bf), Kd, N, M, a_mn=1, b_mn=1, epi=RP_EPI_F32,
+           out=torch.empty(Kd, N, device=dev), splits=2, workspace=ws, bn=bn)
+for cols in (64, 192, 768):
+    x = torch.randn(130, cols, device=dev)
+    g, b = torch.ones(cols, device=dev), torch.zeros(cols, device=dev)
+    y = torch.empty(130, cols, device=dev, dtype=bf)
+    mean, rstd = torch.empty(130, device=dev), torch.empty(130, device=dev)
+    K.layer_norm_fwd(x, g, b, 1e-5, y=y, mean=mean, rstd=rstd)
+    K.layer_norm_bwd(x, mean, rstd, g, y, dres=torch.randn_like(x), dx=torch.empty_like(x),
+                     dx_bf16=torch.empty_like(y))
+    K.colsum(y)
+for impl in (0, 1, 2):
+    _capi.lib().rp_set_attention_impl(impl)
+    for (B, Nn, H, hd) in [(2, 197, 2, 64), (1, 300, 1, 64), (700, 49, 1, 32), (2, 70, 2, 104)]:
+        qkv = torch.randn(B * Nn, 3 * H * hd, device=dev).to(bf)
+        out, lse = K.attention_fwd(qkv, B, Nn, H, head_dim=hd)
+        K.attention_bwd(qkv, out, lse, torch.randn(B * Nn, H * hd, device=dev).to(bf), B, Nn, H,
+                        head_dim=hd)
+_capi.lib().rp_set_attention_impl(0)
+torch.cuda.synchronize()
+print("kernels ok")
