@@ -273,16 +273,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 //   pass 1   S_j = Q K_j^T, row max only (FMNMX, no exponentials)
 //   pass 2   S_j again, p = exp2(s * scale * log2e - m), row sums, bf16 P packed over the
 //            block's own S columns, O += P V_j (one O accumulator, no rescaling needed)
-// An item is (sequence, head, group of up to kLongGroup query tiles); its K and V (<= 512
+// An item is (sequence, head, group of up to pl.group query tiles); its K and V (<= 512
 // rows each) are resident in smem for the whole group, Q tiles are double-buffered. Sixteen
 // elementwise warps (TMEM lane quarter w%4, 32-key column quarter w/4 of a block) and one
 // TMA + MMA warp; S is double-buffered in TMEM so the next block's S is computed while the
 // current one is processed.
-constexpr int kLongGroup = 2;
 constexpr int kLongKV = 2 * 512 * 128;  // K | V, up to 512 rows each
 
 struct LongPlan {
   int nitems, ntile, ngroup;  // items = S * H * ngroup; ntile query tiles per sequence
+  int group;                  // query tiles per item (K, V loaded once per item)
   int nkb;                    // 128-key blocks
 };
 
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int grp = item % pl.ngroup, bh = item / pl.ngroup;
     h = bh % g.H;
     b = bh / g.H;
-    t0 = grp * kLongGroup;
-    nt = min(kLongGroup, pl.ntile - t0);
+    t0 = grp * pl.group;
+    nt = min(pl.group, pl.ntile - t0);
   };
   const uint32_t ocol = tmem + 256u;
 
@@ -552,7 +552,12 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
     });
     LongPlan pl;
     pl.ntile = static_cast<int>((N + 127) / 128);
-    pl.ngroup = (pl.ntile + kLongGroup - 1) / kLongGroup;
+    // all of a sequence's query tiles per item (K, V loaded once), except at N = 512 with
+    // too few (sequence, head) pairs to balance 148 SMs, where pairs of tiles do better
+    // (measured, tools/attn_fwd_ab.py: 64 x 512 x 12 heads 234 us vs 243 us; 256 x 512:
+    // 819 vs 873 us; 64 x 300: 132 vs 163 us)
+    pl.group = (pl.ntile == 4 && S * H < 8 * nsm_l) ? 2 : pl.ntile;
+    pl.ngroup = (pl.ntile + pl.group - 1) / pl.group;
     pl.nitems = static_cast<int>(S * H) * pl.ngroup;
     pl.nkb = static_cast<int>((N + 127) / 128);
     const unsigned grid = static_cast<unsigned>(pl.nitems < nsm_l ? pl.nitems : nsm_l);
