@@ -175,3 +175,22 @@ def test_cli_configs_parse(capi):
             seen_hier = True
             assert mc.depth == sum(mc.depths) and mc.width == mc.widths[0]
     assert seen_hier
+
+
+def _build_example(tmp_path):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2306_09342_b200", "_lib")
+    exe = os.path.join(str(tmp_path), "train_revvit")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "train_revvit.cpp"), "-L", lib,
+                    "-lrevprop_b200", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_example_builds_against_the_c_abi(capi, tmp_path):
+    """The reference-side C++ call site (examples/train_revvit.cpp) compiles and links
+    against include/revprop_b200.h and the library with g++ alone."""
+    import os
+    assert os.path.exists(_build_example(tmp_path))

@@ -461,3 +461,14 @@ def test_layer_api_matches_oracle(cfg, b):
     for k, n in [("d_w1", "w1"), ("d_b1", "b1"), ("d_w2", "w2"), ("d_b2", "b2"),
                  ("d_ln_gamma", "lnG_g"), ("d_ln_beta", "lnG_b")]:
         assert maxrel(grad(f"blocks.{b}.{n}"), gr[k]) < TOL_GRAD, n
+
+
+def test_cpp_example_trains(tmp_path):
+    """examples/train_revvit.cpp through the C ABI only: PaReprop == Reprop bit for bit and
+    the loss falls over 10 SGD steps."""
+    import subprocess
+    from test_capi import _build_example
+    r = subprocess.run([_build_example(tmp_path), "10"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "pareprop == reprop (bit-exact grads): yes" in r.stdout
