@@ -61,6 +61,10 @@ struct BlockPlans {
 // GEMM tiling used by the engine: CTA-pair (cta_group::2) 256 x 256 tiles.
 constexpr int kGemmBn = 512;
 
+// Narrow outputs (the Rev-Swin stages of width 128 / 384) waste a large part of a 256-wide
+// CTA-pair tile; they run on single-CTA 128 x 128 tiles instead.
+int gemm_bn(int64_t N) { return (N % 256 != 0 && N < 512) ? 128 : kGemmBn; }
+
 int pick_splits(int64_t M, int64_t N, int64_t K, int bn) {
   const bool pair = bn == 512;
   const int tm = pair ? 256 : 128, tn = pair ? 256 : bn;
@@ -259,7 +263,7 @@ int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   d.workspace = a.ws;
   d.colsum_part = a.colsum_part;
   d.max_ctas = 0;
-  d.bn = kGemmBn;
+  d.bn = gemm_bn(a.N);
   int rc = rp_gemm_plan_create(&d, out);
   if (rc != RP_OK) return rp_fail(rc, "engine: gemm plan creation failed");
   g->all_plans.push_back(*out);
@@ -285,8 +289,9 @@ int build_plans(RpEngine* g) {
   for (size_t si = 0; si < g->st.size(); ++si) {
     RpStage& St = g->st[si];
     const int64_t T = St.T, d = St.d, h = St.h;
-    const int s_qkv = pick_splits(d, 3 * d, T, kGemmBn), s_proj = pick_splits(d, d, T, kGemmBn),
-              s_w1 = pick_splits(d, h, T, kGemmBn), s_w2 = pick_splits(h, d, T, kGemmBn);
+    const int s_qkv = pick_splits(d, 3 * d, T, gemm_bn(3 * d)),
+              s_proj = pick_splits(d, d, T, gemm_bn(d)), s_w1 = pick_splits(d, h, T, gemm_bn(h)),
+              s_w2 = pick_splits(h, d, T, gemm_bn(d));
     for (int64_t j = 0; j < St.L; ++j) {
       const int64_t b = St.first + j;
       BlockPlans& p = g->plans[static_cast<size_t>(b)];
@@ -392,7 +397,7 @@ int build_plans(RpEngine* g) {
                        &St.b_dmerge));
       {  // d_merge_w = group_r(f)^T . d_y
         GemmArgs a{g->fb, rd, 1, g->deb, dn, 1, rd, dn, Tn, RP_EPI_F32, gr(g, St.bnd_tix), dn};
-        a.splits = pick_splits(rd, dn, Tn, kGemmBn);
+        a.splits = pick_splits(rd, dn, Tn, gemm_bn(dn));
         a.ws = g->split_ws;
         RP_TRY(mk_plan(g, a, &St.b_wmerge));
       }
@@ -404,7 +409,7 @@ int build_plans(RpEngine* g) {
                        &St.b_dfuse2));
         GemmArgs a{g->cb, 2 * d, 1, g->datt, d, 1, 2 * d, d, T, RP_EPI_F32,
                    gr(g, St.bnd_tix + 1), d};
-        a.splits = pick_splits(2 * d, d, T, kGemmBn);
+        a.splits = pick_splits(2 * d, d, T, gemm_bn(d));
         a.ws = g->split_ws;
         RP_TRY(mk_plan(g, a, &St.b_wfuse));  // d_fusion_w = concat^T . d_f
       }
@@ -417,7 +422,7 @@ int build_plans(RpEngine* g) {
                  &g->p_embed));
   {
     GemmArgs a{g->inputs, g->in, 1, g->deb, S0.d, 1, g->in, S0.d, g->T, RP_EPI_F32, gr(g, 0), S0.d};
-    a.splits = pick_splits(g->in, S0.d, g->T, kGemmBn);
+    a.splits = pick_splits(g->in, S0.d, g->T, gemm_bn(S0.d));
     a.ws = g->split_ws;
     RP_TRY(mk_plan(g, a, &g->p_embed_w));
   }
@@ -940,7 +945,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   int64_t Td = 0, Th = 0, TH = 0, Tmax = 0, ln_ws = 0, attn_ws = 0, col_ws = 0, split_ws = 0;
   int64_t fb = 0;
   auto splits_ws = [&](int64_t m, int64_t n, int64_t k) {
-    const int sp = pick_splits(m, n, k, kGemmBn);
+    const int sp = pick_splits(m, n, k, gemm_bn(n));
     if (sp > 1) split_ws = std::max<int64_t>(split_ws, sp * m * n);
   };
   for (size_t s = 0; s < g->st.size(); ++s) {
@@ -1562,7 +1567,7 @@ extern "C" int rp_engine_attention_forward(RpEngine* g, int64_t b, const float* 
   dsc.out = y;
   dsc.ldo = St.d;
   dsc.splits = 1;
-  dsc.bn = kGemmBn;
+  dsc.bn = gemm_bn(dsc.N);
   RP_TRY(rp_gemm(&dsc, s));
   return rp_engine_sync(g);
 }
@@ -1595,7 +1600,7 @@ extern "C" int rp_engine_mlp_forward(RpEngine* g, int64_t b, const float* x, flo
   dsc.bias = wf(g, tix_block(g, b, kB2));
   dsc.sign = 1.f;
   dsc.splits = 1;
-  dsc.bn = kGemmBn;
+  dsc.bn = gemm_bn(dsc.N);
   RP_TRY(rp_gemm(&dsc, s));
   return rp_engine_sync(g);
 }
