@@ -116,6 +116,12 @@ __device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bflo
     if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 8 * c) = x;
   }
 }
+// Internal epilogue kind (not in the C ABI): RP_EPI_RESID stored through TMA, chosen for
+// CTA-pair tiles with a short K loop (the attention projection), where the epilogue's
+// stores, not the MMA, bound the tile.
+constexpr int kEpiResidTma = 100;
+constexpr bool is_resid(int epi) { return epi == RP_EPI_RESID || epi == kEpiResidTma; }
+
 // Epilogue inputs of one chunk, fetched one chunk ahead (software pipelining) so the
 // global-load latency of the residual / saved pre-activation overlaps the previous chunk.
 // A chunk is 32 rows x 128 B: 32 fp32 columns (fp32 outputs) or 64 bf16 columns (bf16
@@ -127,8 +133,8 @@ struct ChunkIn {
 template <int EPI>
 __device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
                                                int64_t rows_left, int64_t col, ChunkIn& in) {
-  if constexpr (EPI == RP_EPI_RESID || EPI == RP_EPI_GELU_BWD || EPI == RP_EPI_MUL) {
-    const int esz = EPI == RP_EPI_RESID ? 4 : 2;
+  if constexpr (is_resid(EPI) || EPI == RP_EPI_GELU_BWD || EPI == RP_EPI_MUL) {
+    const int esz = is_resid(EPI) ? 4 : 2;
     const uint8_t* g = static_cast<const uint8_t*>(ep.aux) + col * esz;
     const int64_t ldb = ep.ldaux * esz;
 #pragma unroll
@@ -200,7 +206,7 @@ __device__ __forceinline__ void stage_row_bf16x64(uint32_t st, int lane, const f
 
 template <int EPI>
 struct EpiTraits {
-  static constexpr int kCW = (EPI == RP_EPI_F32 || EPI == RP_EPI_RESID) ? 32 : 64;
+  static constexpr int kCW = (EPI == RP_EPI_F32 || is_resid(EPI)) ? 32 : 64;
 };
 
 // One chunk: rows [row0, row0+32), cols [col, col+CW); v = this lane's row (CW values).
@@ -323,7 +329,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, const GemmShape sh,
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap /*tmO: 2-SM residual only*/,
+                      const GemmShape sh,
                       const GemmEpi ep) {
   pdl_trigger();
 
@@ -504,20 +512,58 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (r = 0) issues tcgen05.mma.cta_group::2 (M = 256, N = 256) which reads both CTAs'
 // halves; each CTA's TMEM receives its 128 accumulator rows. Per SM this moves 32 KB of
 // operands per 128x256x64 step instead of 48 KB, which is what the L2 can sustain.
+// The TMA-store residual epilogue (fp32 in, fp32 out) stores from two staging buffers per
+// warp (the store of one chunk drains while the next is computed), paid for with one
+// pipeline stage -- a win for short K loops (K = 768: 95.7 -> 87.1 us), a loss for long
+// ones (K = 3072: 182 -> 187 us), so plans pick it by K.
 template <int EPI>
 struct Gemm2Cfg {
-  static constexpr int kStages = 6;
+  static constexpr bool kTmaStore = EPI == kEpiResidTma;
+  static constexpr int kStages = kTmaStore ? 5 : 6;
   static constexpr int kHalfBytes = 128 * kBK * 2;         // 16 KB: one A or B half stage
   static constexpr int kStageBytes = 2 * kHalfBytes;       // per CTA
   static constexpr int kTmemCols = 512;                    // 2 x 256 accumulator columns
-  static constexpr int kEpiBytes = 8 * 4096;
+  static constexpr int kEpiBytes = 8 * 4096 * (kTmaStore ? 2 : 1);
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
 };
+
+// Residual epilogue chunk (32 rows x 32 fp32 columns) with a TMA store: out = aux + sign *
+// (acc + bias) staged in the 128-byte-swizzled layout the output map expects, then one
+// cp.async.bulk.tensor store issued by lane 0 (rows / columns past M / N are clipped).
+__device__ __forceinline__ void resid_chunk_tma(const GemmEpi& ep, const CUtensorMap* tmO,
+                                                uint32_t st, int lane, int64_t row0, int64_t col,
+                                                float* v, const ChunkIn& in) {
+  uint4 rr[8];
+  aux_rows(st, lane, in, rr);
+  const float s = ep.sign;
+  const float4* b4 = ep.bias ? reinterpret_cast<const float4*>(ep.bias + col) : nullptr;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 b = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + b.x);
+    v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + b.y);
+    v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + b.z);
+    v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + b.w);
+  }
+  stage_rows_f32(st, lane, v);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(tmO)),
+        "r"(static_cast<int32_t>(col)), "r"(static_cast<int32_t>(row0)), "r"(st)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  __syncwarp();
+}
 
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_sm100_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, const GemmShape sh,
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmO, const GemmShape sh,
                           const GemmEpi ep) {
   pdl_trigger();
 
@@ -651,8 +697,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ---------------- epilogue warps 2..9 (both CTAs; this CTA's 128 rows of the tile)
     const uint32_t q = warp & 3u;
     const int half = (static_cast<int>(warp) - 2) >> 2;
-    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage);
+    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage * (Cfg::kTmaStore ? 2 : 1));
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int sbuf = 0;  // TMA-store staging buffer toggle (kTmaStore)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster_id; u < units; u += nclusters) {
@@ -679,8 +726,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const ChunkIn cur = nxt;
         if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
           prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
-        if (rows_ok && n0 + c < sh.N)
+        if constexpr (Cfg::kTmaStore) {
+          if (rows_ok && n0 + c < sh.N) {
+            const uint32_t sb = st + static_cast<uint32_t>(sbuf * kEpiStage);
+            // this buffer's previous store (two chunks ago) has finished reading smem
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            resid_chunk_tma(ep, &tmO, sb, static_cast<int>(lane), row0, n0 + c, v, cur);
+            sbuf ^= 1;
+          }
+        } else if (rows_ok && n0 + c < sh.N) {
           epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -692,6 +749,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
 
+  if constexpr (Cfg::kTmaStore) {
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
   __syncwarp();
   tc_fence_before();
   cluster_sync_all();
@@ -755,7 +815,22 @@ static int encode_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
   return r == CUDA_SUCCESS ? RP_OK : RP_ERR_CUDA;
 }
 
-typedef void (*GemmKernelPtr)(CUtensorMap, CUtensorMap, GemmShape, GemmEpi);
+// fp32 row-major [rows][cols], pitch ld elements; box = {32 cols, 32 rows} = one epilogue
+// chunk, 128-byte swizzle (the staging layout sw32).
+static int encode_map_f32(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+  PFN_encodeTiled_t fn = get_encode_fn();
+  if (!fn) return RP_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? RP_OK : RP_ERR_CUDA;
+}
+
+typedef void (*GemmKernelPtr)(CUtensorMap, CUtensorMap, CUtensorMap, GemmShape, GemmEpi);
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static GemmKernelPtr kernel_ptr() {
@@ -803,6 +878,7 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
     case RP_EPI_GELU_BWD: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_GELU_BWD>();
     case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
     case RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_MUL>();
+    case kEpiResidTma: return kernel_ptr_2sm<A_MN, B_MN, kEpiResidTma>();
   }
   return nullptr;
 }
@@ -838,7 +914,7 @@ static int num_sms() {
 using namespace rp;
 
 struct RpGemmPlan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmO;  // tmO: fp32 output map of the TMA-store (residual) epilogue
   GemmShape sh;
   GemmEpi ep;
   GemmKernelPtr kern;
@@ -919,18 +995,21 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
     else
       rc = encode_map(&p->tmB, d->B, N, K, d->ldb, two_sm ? 128u : static_cast<uint32_t>(bn));
   }
+  const bool tma_store = two_sm && d->epi == RP_EPI_RESID && K <= 1024;
+  if (rc == RP_OK && tma_store) rc = encode_map_f32(&p->tmO, d->out, M, N, d->ldo);
   if (rc != RP_OK) {
     delete p;
     return rp_fail(rc, "gemm: cuTensorMapEncodeTiled failed");
   }
-  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, d->epi)
+  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, tma_store ? kEpiResidTma : d->epi)
                    : (bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi)
                                 : pick<128>(d->a_mn, d->b_mn, d->epi));
   if (!p->kern) {
     delete p;
     return rp_fail(RP_ERR_CONFIG, "gemm: unknown epilogue");
   }
-  p->smem = two_sm ? Gemm2Cfg<RP_EPI_F32>::kSmemBytes
+  p->smem = two_sm ? (tma_store ? Gemm2Cfg<kEpiResidTma>::kSmemBytes
+                              : Gemm2Cfg<RP_EPI_F32>::kSmemBytes)
                    : (bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes);
   rp_gemm_plan_set_max_ctas(p, d->max_ctas);
   *out = p;
@@ -940,7 +1019,8 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
 extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!p) return RP_ERR_CONTRACT;
-  launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->sh, p->ep);
+  launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->tmO, p->sh,
+           p->ep);
   if (cudaPeekAtLastError() != cudaSuccess) return rp_check_launch("gemm");
   if (p->sh.splits > 1) {
     const int64_t n4 = p->red_n / 4;

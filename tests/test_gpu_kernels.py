@@ -102,9 +102,11 @@ def test_gemm_bias_gelu(K, bn):
 
 @pytest.mark.parametrize("bn", [256, 512])
 @pytest.mark.parametrize("sign", [1.0, -1.0])
-def test_gemm_residual(K, sign, bn):
+@pytest.mark.parametrize("Kd,N", [(3072, 768), (768, 768), (512, 320)])
+def test_gemm_residual(K, sign, bn, Kd, N):
+    """Residual epilogue; CTA-pair tiles with K <= 1024 store through TMA (ragged N too)."""
     from paper_2306_09342_b200._capi import RP_EPI_RESID
-    M, N, Kd = 700, 768, 3072
+    M = 700
     A = torch.randn(M, Kd, device="cuda").bfloat16()
     W = (0.05 * torch.randn(Kd, N, device="cuda")).bfloat16()
     bias = torch.randn(N, device="cuda")
