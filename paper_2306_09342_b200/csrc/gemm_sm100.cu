@@ -116,11 +116,12 @@ __device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bflo
     if (r < rows_left) *reinterpret_cast<uint4*>(g + (row0 + r) * ld + 8 * c) = x;
   }
 }
-// Internal epilogue kind (not in the C ABI): RP_EPI_RESID stored through TMA, chosen for
-// CTA-pair tiles with a short K loop (the attention projection), where the epilogue's
+// Internal epilogue kinds (not in the C ABI): kEpiTma + k is epilogue k with its outputs
+// stored through TMA, chosen for CTA-pair tiles with a short K loop, where the epilogue's
 // stores, not the MMA, bound the tile.
-constexpr int kEpiResidTma = 100;
-constexpr bool is_resid(int epi) { return epi == RP_EPI_RESID || epi == kEpiResidTma; }
+constexpr int kEpiTma = 100;
+constexpr int base_epi(int epi) { return epi >= kEpiTma ? epi - kEpiTma : epi; }
+constexpr bool is_resid(int epi) { return base_epi(epi) == RP_EPI_RESID; }
 
 // Epilogue inputs of one chunk, fetched one chunk ahead (software pipelining) so the
 // global-load latency of the residual / saved pre-activation overlaps the previous chunk.
@@ -133,7 +134,7 @@ struct ChunkIn {
 template <int EPI>
 __device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
                                                int64_t rows_left, int64_t col, ChunkIn& in) {
-  if constexpr (is_resid(EPI) || EPI == RP_EPI_GELU_BWD || EPI == RP_EPI_MUL) {
+  if constexpr (is_resid(EPI) || base_epi(EPI) == RP_EPI_GELU_BWD || base_epi(EPI) == RP_EPI_MUL) {
     const int esz = is_resid(EPI) ? 4 : 2;
     const uint8_t* g = static_cast<const uint8_t*>(ep.aux) + col * esz;
     const int64_t ldb = ep.ldaux * esz;
@@ -206,20 +207,66 @@ __device__ __forceinline__ void stage_row_bf16x64(uint32_t st, int lane, const f
 
 template <int EPI>
 struct EpiTraits {
-  static constexpr int kCW = (EPI == RP_EPI_F32 || is_resid(EPI)) ? 32 : 64;
+  static constexpr int kCW = (base_epi(EPI) == RP_EPI_F32 || is_resid(EPI)) ? 32 : 64;
 };
 
+// Output staging. Register path (TMA = false): one staging buffer per warp, staged chunk ->
+// global by coalesced 16-byte stores. TMA path: two buffers per warp used in turn; a chunk is
+// staged into a buffer whose previous bulk store has finished reading it, then lane 0
+// issues one cp.async.bulk.tensor store (its own bulk group; rows / columns past M / N are
+// clipped by the tensor map).
+struct StageRing {
+  uint32_t base;
+  int idx;
+};
+template <bool TMA>
+__device__ __forceinline__ uint32_t stage_acquire(uint32_t st, StageRing& ring, int lane) {
+  if constexpr (!TMA) {
+    return st;
+  } else {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    return ring.base + static_cast<uint32_t>(ring.idx * kEpiStage);
+  }
+}
+template <bool TMA>
+__device__ __forceinline__ void stage_emit(uint32_t buf, StageRing& ring, int lane, void* g,
+                                           int64_t ldb, int64_t row0, int64_t rows_left,
+                                           const CUtensorMap* tm, int64_t col) {
+  if constexpr (TMA) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+              reinterpret_cast<uint64_t>(tm)),
+          "r"(static_cast<int32_t>(col)), "r"(static_cast<int32_t>(row0)), "r"(buf)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    __syncwarp();
+    ring.idx ^= 1;
+  } else {
+    __syncwarp();
+    store_tile(buf, lane, g, ldb, row0, rows_left);
+    __syncwarp();
+  }
+}
+
 // One chunk: rows [row0, row0+32), cols [col, col+CW); v = this lane's row (CW values).
-template <int EPI>
+// EPI is a base kind (< kEpiTma); TMA selects the output path (see StageRing).
+template <int EPI, bool TMA>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShape& sh,
-                                               uint32_t st, int lane, int64_t row0,
-                                               int64_t col, int split, float* v,
-                                               const ChunkIn& in) {
+                                               uint32_t st, StageRing& ring,
+                                               const CUtensorMap* tmO, const CUtensorMap* tmO2,
+                                               int lane, int64_t row0, int64_t col, int split,
+                                               float* v, const ChunkIn& in) {
   const int64_t rows_left = sh.M - row0;
   if constexpr (EPI == RP_EPI_BF16) {
-    stage_row_bf16x64(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
+    const uint32_t b = stage_acquire<TMA>(st, ring, lane);
+    stage_row_bf16x64(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
+                    rows_left, tmO, col);
   } else if constexpr (EPI == RP_EPI_F32) {
     stage_rows_f32(st, lane, v);
     __syncwarp();
@@ -239,33 +286,34 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
       }
     }
     if (ep.out2) {  // pre-activation u (kept for the backward's gelu')
-      stage_row_bf16x64(st, lane, v);
-      __syncwarp();
-      store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0,
-                 rows_left);
-      __syncwarp();
+      const uint32_t b = stage_acquire<TMA>(st, ring, lane);
+      stage_row_bf16x64(b, lane, v);
+      stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2,
+                      row0, rows_left, tmO2, col);
     }
 #pragma unroll
     for (int i = 0; i < 64; ++i) v[i] = gelu_tanh_fast(v[i]);
-    stage_row_bf16x64(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
+    const uint32_t b = stage_acquire<TMA>(st, ring, lane);
+    stage_row_bf16x64(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
+                    rows_left, tmO, col);
   } else if constexpr (EPI == RP_EPI_RESID) {
+    const uint32_t b = stage_acquire<TMA>(st, ring, lane);
     uint4 rr[8];
-    aux_rows(st, lane, in, rr);
+    aux_rows(b, lane, in, rr);
     const float s = ep.sign;
     const float4* b4 = ep.bias ? reinterpret_cast<const float4*>(ep.bias + col) : nullptr;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const float4 b = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + b.x);
-      v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + b.y);
-      v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + b.z);
-      v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + b.w);
+      const float4 bb = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + bb.x);
+      v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + bb.y);
+      v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + bb.z);
+      v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + bb.w);
     }
-    stage_rows_f32(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<float*>(ep.out) + col, ep.ldo * 4, row0, rows_left);
+    stage_rows_f32(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<float*>(ep.out) + col, ep.ldo * 4, row0,
+                    rows_left, tmO, col);
   } else if constexpr (EPI == RP_EPI_BIAS_GELU_SLOPE) {
     if (ep.bias) {
       const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col);
@@ -281,47 +329,37 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
     float sl[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) gelu_and_slope_fast(v[i], v[i], sl[i]);
-    stage_row_bf16x64(st, lane, sl);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0, rows_left);
-    __syncwarp();
-    stage_row_bf16x64(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
-  } else if constexpr (EPI == RP_EPI_MUL) {
+    uint32_t b = stage_acquire<TMA>(st, ring, lane);
+    stage_row_bf16x64(b, lane, sl);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0,
+                    rows_left, tmO2, col);
+    b = stage_acquire<TMA>(st, ring, lane);
+    stage_row_bf16x64(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
+                    rows_left, tmO, col);
+  } else if constexpr (EPI == RP_EPI_MUL || EPI == RP_EPI_GELU_BWD) {
+    const uint32_t b = stage_acquire<TMA>(st, ring, lane);
     uint4 uu[8];
-    aux_rows(st, lane, in, uu);
+    aux_rows(b, lane, in, uu);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t w[4] = {uu[c].x, uu[c].y, uu[c].z, uu[c].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = unpack_bf16x2(w[k]);
-        v[8 * c + 2 * k] *= f.x;
-        v[8 * c + 2 * k + 1] *= f.y;
+        if constexpr (EPI == RP_EPI_MUL) {
+          v[8 * c + 2 * k] *= f.x;
+          v[8 * c + 2 * k + 1] *= f.y;
+        } else {
+          v[8 * c + 2 * k] *= gelu_tanh_slope_fast(f.x);
+          v[8 * c + 2 * k + 1] *= gelu_tanh_slope_fast(f.y);
+        }
       }
     }
-    if (ep.colsum) colsum_chunk64(ep, st, lane, row0, col, v);
-    stage_row_bf16x64(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
-  } else if constexpr (EPI == RP_EPI_GELU_BWD) {
-    uint4 uu[8];
-    aux_rows(st, lane, in, uu);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t w[4] = {uu[c].x, uu[c].y, uu[c].z, uu[c].w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = unpack_bf16x2(w[k]);
-        v[8 * c + 2 * k] *= gelu_tanh_slope_fast(f.x);
-        v[8 * c + 2 * k + 1] *= gelu_tanh_slope_fast(f.y);
-      }
-    }
-    if (ep.colsum) colsum_chunk64(ep, st, lane, row0, col, v);
-    stage_row_bf16x64(st, lane, v);
-    __syncwarp();
-    store_tile(st, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0, rows_left);
+    if (ep.colsum) colsum_chunk64(ep, b, lane, row0, col, v);
+    stage_row_bf16x64(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
+                    rows_left, tmO, col);
   }
   __syncwarp();
 }
@@ -330,7 +368,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
-                      const __grid_constant__ CUtensorMap /*tmO: 2-SM residual only*/,
+                      const __grid_constant__ CUtensorMap /*tmO: 2-SM TMA store only*/,
+                      const __grid_constant__ CUtensorMap /*tmO2*/,
                       const GemmShape sh,
                       const GemmEpi ep) {
   pdl_trigger();
@@ -460,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3u;
     const int half = (static_cast<int>(warp) - 2) >> 2;
     const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage);
+    StageRing ring{st, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -487,7 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
           prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
         if (rows_ok && n0 + c < sh.N)
-          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
+          epilogue_chunk<EPI, false>(ep, sh, st, ring, nullptr, nullptr, static_cast<int>(lane),
+                                     row0, n0 + c, split, v, cur);
       }
       tc_fence_before();
       __syncwarp();
@@ -512,13 +553,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (r = 0) issues tcgen05.mma.cta_group::2 (M = 256, N = 256) which reads both CTAs'
 // halves; each CTA's TMEM receives its 128 accumulator rows. Per SM this moves 32 KB of
 // operands per 128x256x64 step instead of 48 KB, which is what the L2 can sustain.
-// The TMA-store residual epilogue (fp32 in, fp32 out) stores from two staging buffers per
-// warp (the store of one chunk drains while the next is computed), paid for with one
-// pipeline stage -- a win for short K loops (K = 768: 95.7 -> 87.1 us), a loss for long
-// ones (K = 3072: 182 -> 187 us), so plans pick it by K.
+// The TMA-store epilogues (kEpiTma + k) store from two staging buffers per warp (the store
+// of one chunk drains while the next is computed), paid for with one pipeline stage -- a
+// win for short K loops (residual, K = 768: 95.7 -> 87.1 us), a loss for long ones
+// (K = 3072: 182 -> 187 us), so plans pick them by K.
 template <int EPI>
 struct Gemm2Cfg {
-  static constexpr bool kTmaStore = EPI == kEpiResidTma;
+  static constexpr bool kTmaStore = EPI >= kEpiTma;
   static constexpr int kStages = kTmaStore ? 5 : 6;
   static constexpr int kHalfBytes = 128 * kBK * 2;         // 16 KB: one A or B half stage
   static constexpr int kStageBytes = 2 * kHalfBytes;       // per CTA
@@ -527,43 +568,12 @@ struct Gemm2Cfg {
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
 };
 
-// Residual epilogue chunk (32 rows x 32 fp32 columns) with a TMA store: out = aux + sign *
-// (acc + bias) staged in the 128-byte-swizzled layout the output map expects, then one
-// cp.async.bulk.tensor store issued by lane 0 (rows / columns past M / N are clipped).
-__device__ __forceinline__ void resid_chunk_tma(const GemmEpi& ep, const CUtensorMap* tmO,
-                                                uint32_t st, int lane, int64_t row0, int64_t col,
-                                                float* v, const ChunkIn& in) {
-  uint4 rr[8];
-  aux_rows(st, lane, in, rr);
-  const float s = ep.sign;
-  const float4* b4 = ep.bias ? reinterpret_cast<const float4*>(ep.bias + col) : nullptr;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float4 b = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + b.x);
-    v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + b.y);
-    v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + b.z);
-    v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + b.w);
-  }
-  stage_rows_f32(st, lane, v);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncwarp();
-  if (lane == 0) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-            reinterpret_cast<uint64_t>(tmO)),
-        "r"(static_cast<int32_t>(col)), "r"(static_cast<int32_t>(row0)), "r"(st)
-        : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-  __syncwarp();
-}
-
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_sm100_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmO, const GemmShape sh,
+                          const __grid_constant__ CUtensorMap tmO,
+                          const __grid_constant__ CUtensorMap tmO2, const GemmShape sh,
                           const GemmEpi ep) {
   pdl_trigger();
 
@@ -699,7 +709,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = (static_cast<int>(warp) - 2) >> 2;
     const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage * (Cfg::kTmaStore ? 2 : 1));
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
-    int sbuf = 0;  // TMA-store staging buffer toggle (kTmaStore)
+    StageRing ring{st, 0};  // TMA-store staging buffers (kTmaStore)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster_id; u < units; u += nclusters) {
@@ -726,18 +736,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const ChunkIn cur = nxt;
         if (rows_ok && c + CW < c_end && n0 + c + CW < sh.N)
           prefetch_chunk<EPI>(ep, static_cast<int>(lane), row0, sh.M - row0, n0 + c + CW, nxt);
-        if constexpr (Cfg::kTmaStore) {
-          if (rows_ok && n0 + c < sh.N) {
-            const uint32_t sb = st + static_cast<uint32_t>(sbuf * kEpiStage);
-            // this buffer's previous store (two chunks ago) has finished reading smem
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            __syncwarp();
-            resid_chunk_tma(ep, &tmO, sb, static_cast<int>(lane), row0, n0 + c, v, cur);
-            sbuf ^= 1;
-          }
-        } else if (rows_ok && n0 + c < sh.N) {
-          epilogue_chunk<EPI>(ep, sh, st, static_cast<int>(lane), row0, n0 + c, split, v, cur);
-        }
+        if (rows_ok && n0 + c < sh.N)
+          epilogue_chunk<base_epi(EPI), Cfg::kTmaStore>(ep, sh, st, ring, &tmO, &tmO2,
+                                                        static_cast<int>(lane), row0, n0 + c,
+                                                        split, v, cur);
       }
       tc_fence_before();
       __syncwarp();
@@ -815,6 +817,13 @@ static int encode_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
   return r == CUDA_SUCCESS ? RP_OK : RP_ERR_CUDA;
 }
 
+static int encode_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                      uint32_t box_rows);
+// bf16 output [rows][cols]: box = {64 cols, box_rows rows} (one 32-row epilogue chunk)
+static int encode_map_rows(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
+                           int64_t ld, uint32_t box_rows) {
+  return encode_map(m, ptr, rows, cols, ld, box_rows);
+}
 // fp32 row-major [rows][cols], pitch ld elements; box = {32 cols, 32 rows} = one epilogue
 // chunk, 128-byte swizzle (the staging layout sw32).
 static int encode_map_f32(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
@@ -830,7 +839,8 @@ static int encode_map_f32(CUtensorMap* m, const void* ptr, int64_t rows, int64_t
   return r == CUDA_SUCCESS ? RP_OK : RP_ERR_CUDA;
 }
 
-typedef void (*GemmKernelPtr)(CUtensorMap, CUtensorMap, CUtensorMap, GemmShape, GemmEpi);
+typedef void (*GemmKernelPtr)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmShape,
+                              GemmEpi);
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static GemmKernelPtr kernel_ptr() {
@@ -878,7 +888,15 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
     case RP_EPI_GELU_BWD: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_GELU_BWD>();
     case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
     case RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_MUL>();
-    case kEpiResidTma: return kernel_ptr_2sm<A_MN, B_MN, kEpiResidTma>();
+    case kEpiTma + RP_EPI_BF16: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BF16>();
+    case kEpiTma + RP_EPI_BIAS_GELU:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BIAS_GELU>();
+    case kEpiTma + RP_EPI_RESID: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_RESID>();
+    case kEpiTma + RP_EPI_GELU_BWD:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_GELU_BWD>();
+    case kEpiTma + RP_EPI_BIAS_GELU_SLOPE:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BIAS_GELU_SLOPE>();
+    case kEpiTma + RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_MUL>();
   }
   return nullptr;
 }
@@ -914,7 +932,7 @@ static int num_sms() {
 using namespace rp;
 
 struct RpGemmPlan {
-  CUtensorMap tmA, tmB, tmO;  // tmO: fp32 output map of the TMA-store (residual) epilogue
+  CUtensorMap tmA, tmB, tmO, tmO2;  // tmO / tmO2: output maps of the TMA-store epilogues
   GemmShape sh;
   GemmEpi ep;
   GemmKernelPtr kern;
@@ -995,20 +1013,36 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
     else
       rc = encode_map(&p->tmB, d->B, N, K, d->ldb, two_sm ? 128u : static_cast<uint32_t>(bn));
   }
-  const bool tma_store = two_sm && d->epi == RP_EPI_RESID && K <= 1024;
-  if (rc == RP_OK && tma_store) rc = encode_map_f32(&p->tmO, d->out, M, N, d->ldo);
+  // TMA stores pay off for epilogues that also read an input (residual, saved slope / u)
+  // or write two outputs; a plain single bf16 output is a little faster on the register
+  // path (same-box A/B, K = 768: bf16 134.5 -> 137.4 us; gelu' multiply 286 -> 240-256;
+  // bias + GELU + u 226.5 -> 219.4; residual 95.7 -> 87.1)
+  const bool tma_store =
+      two_sm && K <= 1024 &&
+      (d->epi == RP_EPI_RESID || d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
+       d->epi == RP_EPI_BIAS_GELU_SLOPE || (d->epi == RP_EPI_BIAS_GELU && d->out2 != nullptr));
+  if (rc == RP_OK && tma_store) {
+    if (d->epi == RP_EPI_RESID) {
+      rc = encode_map_f32(&p->tmO, d->out, M, N, d->ldo);
+    } else {
+      rc = encode_map_rows(&p->tmO, d->out, M, N, d->ldo, 32);
+      if (rc == RP_OK && d->out2 &&
+          (d->epi == RP_EPI_BIAS_GELU || d->epi == RP_EPI_BIAS_GELU_SLOPE))
+        rc = encode_map_rows(&p->tmO2, d->out2, M, N, d->ldo2, 32);
+    }
+  }
   if (rc != RP_OK) {
     delete p;
     return rp_fail(rc, "gemm: cuTensorMapEncodeTiled failed");
   }
-  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, tma_store ? kEpiResidTma : d->epi)
+  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, tma_store ? kEpiTma + d->epi : d->epi)
                    : (bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi)
                                 : pick<128>(d->a_mn, d->b_mn, d->epi));
   if (!p->kern) {
     delete p;
     return rp_fail(RP_ERR_CONFIG, "gemm: unknown epilogue");
   }
-  p->smem = two_sm ? (tma_store ? Gemm2Cfg<kEpiResidTma>::kSmemBytes
+  p->smem = two_sm ? (tma_store ? Gemm2Cfg<kEpiTma + RP_EPI_BF16>::kSmemBytes
                               : Gemm2Cfg<RP_EPI_F32>::kSmemBytes)
                    : (bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes);
   rp_gemm_plan_set_max_ctas(p, d->max_ctas);
@@ -1019,8 +1053,8 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
 extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!p) return RP_ERR_CONTRACT;
-  launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->tmO, p->sh,
-           p->ep);
+  launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->tmO,
+           p->tmO2, p->sh, p->ep);
   if (cudaPeekAtLastError() != cudaSuccess) return rp_check_launch("gemm");
   if (p->sh.splits > 1) {
     const int64_t n4 = p->red_n / 4;
