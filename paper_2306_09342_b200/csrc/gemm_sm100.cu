@@ -119,8 +119,11 @@ __device__ __forceinline__ void store_tile_bf16(uint32_t st, int lane, __nv_bflo
 // Internal epilogue kinds (not in the C ABI): kEpiTma + k is epilogue k with its outputs
 // stored through TMA, chosen for CTA-pair tiles with a short K loop, where the epilogue's
 // stores, not the MMA, bound the tile.
-constexpr int kEpiTma = 100;
-constexpr int base_epi(int epi) { return epi >= kEpiTma ? epi - kEpiTma : epi; }
+constexpr int kEpiTma = 100;   // two staging buffers per warp, one pipeline stage fewer
+constexpr int kEpiTma1 = 200;  // one staging buffer per warp, full pipeline (long K)
+constexpr int base_epi(int epi) {
+  return epi >= kEpiTma1 ? epi - kEpiTma1 : (epi >= kEpiTma ? epi - kEpiTma : epi);
+}
 constexpr bool is_resid(int epi) { return base_epi(epi) == RP_EPI_RESID; }
 
 // Epilogue inputs of one chunk, fetched one chunk ahead (software pipelining) so the
@@ -218,13 +221,19 @@ struct EpiTraits {
 struct StageRing {
   uint32_t base;
   int idx;
+  int nbuf;  // 1 or 2 staging buffers
 };
 template <bool TMA>
 __device__ __forceinline__ uint32_t stage_acquire(uint32_t st, StageRing& ring, int lane) {
   if constexpr (!TMA) {
     return st;
   } else {
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    if (lane == 0) {
+      if (ring.nbuf == 2)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
     __syncwarp();
     return ring.base + static_cast<uint32_t>(ring.idx * kEpiStage);
   }
@@ -245,7 +254,7 @@ __device__ __forceinline__ void stage_emit(uint32_t buf, StageRing& ring, int la
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     __syncwarp();
-    ring.idx ^= 1;
+    ring.idx = ring.nbuf == 2 ? ring.idx ^ 1 : 0;
   } else {
     __syncwarp();
     store_tile(buf, lane, g, ldb, row0, rows_left);
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3u;
     const int half = (static_cast<int>(warp) - 2) >> 2;
     const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage);
-    StageRing ring{st, 0};
+    StageRing ring{st, 0, 1};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -560,11 +569,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int EPI>
 struct Gemm2Cfg {
   static constexpr bool kTmaStore = EPI >= kEpiTma;
-  static constexpr int kStages = kTmaStore ? 5 : 6;
+  static constexpr int kTmaBufs = (kTmaStore && EPI < kEpiTma1) ? 2 : 1;
+  static constexpr int kStages = kTmaBufs == 2 ? 5 : 6;
   static constexpr int kHalfBytes = 128 * kBK * 2;         // 16 KB: one A or B half stage
   static constexpr int kStageBytes = 2 * kHalfBytes;       // per CTA
   static constexpr int kTmemCols = 512;                    // 2 x 256 accumulator columns
-  static constexpr int kEpiBytes = 8 * 4096 * (kTmaStore ? 2 : 1);
+  static constexpr int kEpiBytes = 8 * 4096 * kTmaBufs;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
 };
 
@@ -707,9 +717,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ---------------- epilogue warps 2..9 (both CTAs; this CTA's 128 rows of the tile)
     const uint32_t q = warp & 3u;
     const int half = (static_cast<int>(warp) - 2) >> 2;
-    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage * (Cfg::kTmaStore ? 2 : 1));
+    const uint32_t st = smem_u32(sEpi + (warp - 2) * kEpiStage * Cfg::kTmaBufs);
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
-    StageRing ring{st, 0};  // TMA-store staging buffers (kTmaStore)
+    StageRing ring{st, 0, Cfg::kTmaBufs};  // TMA-store staging buffers (kTmaStore)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster_id; u < units; u += nclusters) {
@@ -897,6 +907,7 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
     case kEpiTma + RP_EPI_BIAS_GELU_SLOPE:
       return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BIAS_GELU_SLOPE>();
     case kEpiTma + RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_MUL>();
+    case kEpiTma1 + RP_EPI_RESID: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_RESID>();
   }
   return nullptr;
 }
@@ -1017,10 +1028,17 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   // or write two outputs; a plain single bf16 output is a little faster on the register
   // path (same-box A/B, K = 768: bf16 134.5 -> 137.4 us; gelu' multiply 286 -> 240-256;
   // bias + GELU + u 226.5 -> 219.4; residual 95.7 -> 87.1)
-  const bool tma_store =
-      two_sm && K <= 1024 &&
-      (d->epi == RP_EPI_RESID || d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
-       d->epi == RP_EPI_BIAS_GELU_SLOPE || (d->epi == RP_EPI_BIAS_GELU && d->out2 != nullptr));
+  const bool aux_or_two =
+      d->epi == RP_EPI_RESID || d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
+      d->epi == RP_EPI_BIAS_GELU_SLOPE || (d->epi == RP_EPI_BIAS_GELU && d->out2 != nullptr);
+  int tma_kind = 0;  // 0: register stores; kEpiTma: two buffers; kEpiTma1: one buffer
+  if (two_sm && aux_or_two) {
+    if (K <= 1024)
+      tma_kind = kEpiTma;
+    else if (d->epi == RP_EPI_RESID)
+      tma_kind = kEpiTma1;
+  }
+  const bool tma_store = tma_kind != 0;
   if (rc == RP_OK && tma_store) {
     if (d->epi == RP_EPI_RESID) {
       rc = encode_map_f32(&p->tmO, d->out, M, N, d->ldo);
@@ -1035,14 +1053,14 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
     delete p;
     return rp_fail(rc, "gemm: cuTensorMapEncodeTiled failed");
   }
-  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, tma_store ? kEpiTma + d->epi : d->epi)
+  p->kern = two_sm ? pick_2sm(d->a_mn, d->b_mn, tma_store ? tma_kind + d->epi : d->epi)
                    : (bn == 256 ? pick<256>(d->a_mn, d->b_mn, d->epi)
                                 : pick<128>(d->a_mn, d->b_mn, d->epi));
   if (!p->kern) {
     delete p;
     return rp_fail(RP_ERR_CONFIG, "gemm: unknown epilogue");
   }
-  p->smem = two_sm ? (tma_store ? Gemm2Cfg<kEpiTma + RP_EPI_BF16>::kSmemBytes
+  p->smem = two_sm ? (tma_kind == kEpiTma ? Gemm2Cfg<kEpiTma + RP_EPI_BF16>::kSmemBytes
                               : Gemm2Cfg<RP_EPI_F32>::kSmemBytes)
                    : (bn == 256 ? GemmCfg<256>::kSmemBytes : GemmCfg<128>::kSmemBytes);
   rp_gemm_plan_set_max_ctas(p, d->max_ctas);

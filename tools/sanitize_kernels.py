@@ -34,6 +34,11 @@ for bn in (256, 512):
     ws = torch.empty(4 * Kd * N, device=dev)
     K.gemm(a, torch.randn(M, N, device=dev).to(bf), Kd, N, M, a_mn=1, b_mn=1, epi=RP_EPI_F32,
            out=torch.empty(Kd, N, device=dev), splits=2, workspace=ws, bn=bn)
+# long K: the residual epilogue's single-buffer TMA-store path
+a2 = torch.randn(M, 2048, device=dev).to(bf)
+w2 = (0.02 * torch.randn(2048, N, device=dev)).to(bf)
+K.gemm(a2, w2, M, N, 2048, a_mn=0, b_mn=1, epi=RP_EPI_RESID, out=torch.empty(M, N, device=dev),
+       aux=torch.randn(M, N, device=dev), bn=512)
 for cols in (64, 192, 768):
     x = torch.randn(130, cols, device=dev)
     g, b = torch.ones(cols, device=dev), torch.zeros(cols, device=dev)
