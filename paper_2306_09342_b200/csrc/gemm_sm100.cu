@@ -908,6 +908,14 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
       return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BIAS_GELU_SLOPE>();
     case kEpiTma + RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_MUL>();
     case kEpiTma1 + RP_EPI_RESID: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_RESID>();
+    case kEpiTma1 + RP_EPI_BF16: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_BF16>();
+    case kEpiTma1 + RP_EPI_BIAS_GELU:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_BIAS_GELU>();
+    case kEpiTma1 + RP_EPI_GELU_BWD:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_GELU_BWD>();
+    case kEpiTma1 + RP_EPI_BIAS_GELU_SLOPE:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_BIAS_GELU_SLOPE>();
+    case kEpiTma1 + RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_MUL>();
   }
   return nullptr;
 }
@@ -1028,16 +1036,15 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   // or write two outputs; a plain single bf16 output is a little faster on the register
   // path (same-box A/B, K = 768: bf16 134.5 -> 137.4 us; gelu' multiply 286 -> 240-256;
   // bias + GELU + u 226.5 -> 219.4; residual 95.7 -> 87.1)
-  const bool aux_or_two =
-      d->epi == RP_EPI_RESID || d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
-      d->epi == RP_EPI_BIAS_GELU_SLOPE || (d->epi == RP_EPI_BIAS_GELU && d->out2 != nullptr);
   int tma_kind = 0;  // 0: register stores; kEpiTma: two buffers; kEpiTma1: one buffer
-  if (two_sm && aux_or_two) {
-    if (K <= 1024)
-      tma_kind = kEpiTma;
-    else if (d->epi == RP_EPI_RESID)
-      tma_kind = kEpiTma1;
-  }
+  // Interleaved same-box A/B (µs, K = 768 unless noted): two staging buffers (one pipeline
+  // stage fewer) win for the epilogues that read a bf16 input (gelu' multiply 250 vs 258);
+  // one buffer with the full pipeline wins or ties everywhere else (bias + GELU + u 216 vs
+  // 221, residual 87.4 vs 88.7 and K = 3072 180.6 vs 187, plain bf16 132.5 vs 135.2 on
+  // register stores). The split-K fp32 partials keep register stores.
+  if (two_sm && d->epi != RP_EPI_F32)
+    tma_kind = (K <= 1024 && (d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL)) ? kEpiTma
+                                                                                : kEpiTma1;
   const bool tma_store = tma_kind != 0;
   if (rc == RP_OK && tma_store) {
     if (d->epi == RP_EPI_RESID) {
