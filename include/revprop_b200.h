@@ -63,7 +63,10 @@ enum {
   RP_EPI_RESID = 3,     /* out(f32) = aux(f32) + sign * (acc + bias)              */
   RP_EPI_GELU_BWD = 4,  /* out(bf16) = acc * gelu'(aux(bf16) u)                   */
   RP_EPI_BIAS_GELU_SLOPE = 5, /* u = acc + bias; out(bf16) = gelu(u); out2(bf16) = gelu'(u) */
-  RP_EPI_MUL = 6        /* out(bf16) = acc * aux(bf16)  (MLP dgrad with the saved slope) */
+  RP_EPI_MUL = 6,       /* out(bf16) = acc * aux(bf16)  (MLP dgrad with the saved slope) */
+  RP_EPI_ROWDOT = 7     /* out(bf16) = acc; and per 64-column head h of row r = s*rd_seq + t:
+                           rowdot[(s*H + h)*rd_seq + t] = sum_c bf16(acc) aux(bf16), H = N/64
+                           (the attention-backward D = rowsum(dO * O) from the d_att GEMM) */
 };
 
 typedef struct RpGemmDesc {
@@ -90,6 +93,8 @@ typedef struct RpGemmDesc {
   float* colsum_part; /* optional (RP_EPI_MUL / RP_EPI_GELU_BWD): column sums of the fp32
                          epilogue output per 32-row group, [ceil(M/32)][N]; reduce them with
                          rp_colsum_parts (the MLP hidden-bias gradient, layers.cpp:38-52) */
+  float* rowdot;    /* RP_EPI_ROWDOT output */
+  int64_t rd_seq;   /* RP_EPI_ROWDOT: rows per sequence (tokens per attention window) */
 } RpGemmDesc;
 
 typedef struct RpGemmPlan RpGemmPlan;
@@ -147,6 +152,11 @@ int rp_attention_fwd(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64
 int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
                      const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
                      uint16_t* dqkv, float* workspace, rp_stream_t stream);
+/* as rp_attention_bwd; d_ready = 1: D = rowsum(dO * O) is already in workspace[0, S N H)
+ * (e.g. from an RP_EPI_ROWDOT d_att GEMM) and the tcgen05 path does not recompute it */
+int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                        const uint16_t* dout, int64_t S, int64_t N, int64_t H, int64_t head_dim,
+                        uint16_t* dqkv, float* workspace, int d_ready, rp_stream_t stream);
 /* D = rowsum(dO * O) (S N H floats) and, for the tcgen05 backward, the bf16 dS^T of every
  * (sequence, head) ([S H][Nk][Nk], Nk = N rounded up to 16) */
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);

@@ -50,7 +50,7 @@ _CODE_TO_EXC = {1: ShapeError, 2: ContractError, 3: ConfigError, 4: BudgetError,
                 5: SchedulerError, 6: AccountingError, 7: DeviceError}
 
 (RP_EPI_BF16, RP_EPI_F32, RP_EPI_BIAS_GELU, RP_EPI_RESID, RP_EPI_GELU_BWD,
- RP_EPI_BIAS_GELU_SLOPE, RP_EPI_MUL) = range(7)
+ RP_EPI_BIAS_GELU_SLOPE, RP_EPI_MUL, RP_EPI_ROWDOT) = range(8)
 
 
 class GemmDesc(C.Structure):
@@ -66,6 +66,7 @@ class GemmDesc(C.Structure):
         ("splits", C.c_int), ("workspace", C.c_void_p),
         ("max_ctas", C.c_int), ("bn", C.c_int),
         ("colsum_part", C.c_void_p),
+        ("rowdot", C.c_void_p), ("rd_seq", C.c_int64),
     ]
 
 
@@ -93,6 +94,7 @@ _SIGS = {
     "rp_colsum_parts": (_I, [_P, _I64, _I64, _P, _I, _P]),
     "rp_attention_fwd": (_I, [_P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "rp_attention_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
+    "rp_attention_bwd_ex": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I, _P]),
     "rp_attention_bwd_workspace_floats": (_I64, [_I64, _I64, _I64]),
     "rp_set_attention_impl": (_I, [_I]),
 }

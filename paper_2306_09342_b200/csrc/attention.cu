@@ -546,7 +546,7 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
                         float* lse, cudaStream_t stream);
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt);
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready);
 // 0 = tcgen05 where it applies (head_dim 64), backward as one dK/dV pass + dQ from the
 // stored dS^T; 1 = mma.sync only; 2 = tcgen05 with the two-pass (dQ pass, dK/dV pass)
 // backward that keeps no dS
@@ -651,10 +651,10 @@ static int attn_bwd_mma(const uint16_t* qkv, const uint16_t* out, const float* l
 }
 
 // d_out [B*N, H*hd] -> d_qkv [B*N, 3*H*hd]; workspace: B*N*H floats.
-extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
-                                const uint16_t* dout, int64_t B, int64_t N, int64_t H,
-                                int64_t head_dim, uint16_t* dqkv, float* workspace,
-                                rp_stream_t stream) {
+extern "C" int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                                   const uint16_t* dout, int64_t B, int64_t N, int64_t H,
+                                   int64_t head_dim, uint16_t* dqkv, float* workspace,
+                                   int d_ready, rp_stream_t stream) {
   int rc = attn_check(B, N, H, head_dim);
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -664,7 +664,7 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
     uint16_t* dst = g_attn_impl == 0 && N <= kFusedBwdMaxN
                         ? reinterpret_cast<uint16_t*>(workspace + attn_ds_offset(B, N, H))
                         : nullptr;
-    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst);
+    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst, d_ready);
     if (rc != RP_ERR_CONFIG) return rc;
   }
   if (head_dim <= 32)
@@ -672,4 +672,12 @@ extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const 
   return head_dim <= 64
              ? attn_bwd_mma<64>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s)
              : attn_bwd_mma<128>(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, s);
+}
+
+// d_out [B*N, H*hd] -> d_qkv [B*N, 3*H*hd]; workspace: rp_attention_bwd_workspace_floats.
+extern "C" int rp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const float* lse,
+                                const uint16_t* dout, int64_t B, int64_t N, int64_t H,
+                                int64_t head_dim, uint16_t* dqkv, float* workspace,
+                                rp_stream_t stream) {
+  return rp_attention_bwd_ex(qkv, out, lse, dout, B, N, H, head_dim, dqkv, workspace, 0, stream);
 }

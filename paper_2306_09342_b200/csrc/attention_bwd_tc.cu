@@ -539,7 +539,7 @@ using namespace rp;
 //     as a streamed MMA over dS^T (attn_dq_tc) -- S and dP are formed once instead of twice.
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt) {
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready) {
   using namespace attn_tc;
   if (N > 1024 || N < 1) return RP_ERR_CONFIG;
   BwdGeom g;
@@ -577,10 +577,12 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
     CUtensorMap ds;
     if (make_map(&ds, dSt, S * H * g.Nk, g.Nk, 64))
       return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
-    const int64_t n = T * H * 8;
-    launch_k(attn_d_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
-             reinterpret_cast<const __nv_bfloat16*>(out),
-             reinterpret_cast<const __nv_bfloat16*>(dout), Dg, T, g.N, g.H);
+    if (!d_ready) {  // D = rowsum(dO * O), unless the d_att GEMM already produced it
+      const int64_t n = T * H * 8;
+      launch_k(attn_d_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
+               reinterpret_cast<const __nv_bfloat16*>(out),
+               reinterpret_cast<const __nv_bfloat16*>(dout), Dg, T, g.N, g.H);
+    }
     launch_k(attn_bwd_tc<false>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64,
              do64, reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
              reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, reinterpret_cast<__nv_bfloat16*>(dSt));

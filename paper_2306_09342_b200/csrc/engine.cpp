@@ -237,7 +237,13 @@ struct GemmArgs {
   int splits = 1;
   float* ws = nullptr;
   float* colsum_part = nullptr;
+  float* rowdot = nullptr;
+  int64_t rd_seq = 0;
 };
+
+// the tcgen05 attention backward with the stored dS^T (head_dim 64, <= 256 tokens per
+// window) takes D = rowsum(dO * O) from the d_att GEMM's ROWDOT epilogue
+inline bool fused_attn_bwd(const RpStage& St) { return St.d / St.H == 64 && St.W <= 256; }
 
 int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   RpGemmDesc d{};
@@ -262,6 +268,8 @@ int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   d.splits = a.splits;
   d.workspace = a.ws;
   d.colsum_part = a.colsum_part;
+  d.rowdot = a.rowdot;
+  d.rd_seq = a.rd_seq;
   d.max_ctas = 0;
   d.bn = gemm_bn(a.N);
   int rc = rp_gemm_plan_create(&d, out);
@@ -359,7 +367,15 @@ int build_plans(RpEngine* g) {
         RP_TRY(mk_plan(g, a, &p.g_ww1));  // dW1 = hG^T d_u
       }
       RP_TRY(mk_plan(g, {g->du, h, 0, W1, h, 0, T, d, h, RP_EPI_BF16, g->dh, d}, &p.g_dw1));
-      RP_TRY(mk_plan(g, {g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_BF16, g->datt, d}, &p.g_dproj));
+      if (fused_attn_bwd(St)) {  // d_att GEMM also emits D = rowsum(d_att * att) per head
+        GemmArgs a{g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_ROWDOT, g->datt, d};
+        a.aux = S.att;
+        a.rowdot = g->attn_ws;
+        a.rd_seq = St.W;
+        RP_TRY(mk_plan(g, a, &p.g_dproj));
+      } else {
+        RP_TRY(mk_plan(g, {g->d2b, d, 0, Wout, d, 0, T, d, d, RP_EPI_BF16, g->datt, d}, &p.g_dproj));
+      }
       {
         GemmArgs a{S.att, d, 1, g->d2b, d, 1, d, d, T, RP_EPI_F32, gr(g, tix_block(g, b, kWout)), d};
         a.splits = s_proj;
@@ -597,8 +613,8 @@ int vjp_f(RpEngine* g, int64_t b, cudaStream_t s, bool next_b2) {
   const int64_t T = St.T, d = St.d;
   RP_TRY(launch(p.g_dproj, s));
   RP_TRY(launch(p.g_wproj, s));
-  RP_TRY(rp_attention_bwd(S.qkv, S.att, S.lse, g->datt, T / St.W, St.W, St.H, d / St.H, g->dqkv,
-                          g->attn_ws, s));
+  RP_TRY(rp_attention_bwd_ex(S.qkv, S.att, S.lse, g->datt, T / St.W, St.W, St.H, d / St.H,
+                             g->dqkv, g->attn_ws, fused_attn_bwd(St) ? 1 : 0, s));
   RP_TRY(launch(p.g_wqkv, s));
   RP_TRY(launch(p.g_dqkv, s));
   // d_i1 = d_o1 + LN_F^T(d_hF)    (in place in d1 / d1b); d_i2 = d_o2t (already in d2)

@@ -15,5 +15,8 @@ struct GemmEpi {
   int64_t split_stride;
   float* colsum;  // optional: per-32-row column partials [ceil(M/32)][ldcs] of the fp32 output
   int64_t ldcs;
+  float* rowdot;   // RP_EPI_ROWDOT: per-(row, 64-column head) dot of the bf16 output with aux
+  int64_t rd_seq;  // rows per sequence
+  int64_t rd_heads;
 };
 }  // namespace rp

@@ -137,7 +137,8 @@ struct ChunkIn {
 template <int EPI>
 __device__ __forceinline__ void prefetch_chunk(const GemmEpi& ep, int lane, int64_t row0,
                                                int64_t rows_left, int64_t col, ChunkIn& in) {
-  if constexpr (is_resid(EPI) || base_epi(EPI) == RP_EPI_GELU_BWD || base_epi(EPI) == RP_EPI_MUL) {
+  if constexpr (is_resid(EPI) || base_epi(EPI) == RP_EPI_GELU_BWD || base_epi(EPI) == RP_EPI_MUL ||
+                base_epi(EPI) == RP_EPI_ROWDOT) {
     const int esz = is_resid(EPI) ? 4 : 2;
     const uint8_t* g = static_cast<const uint8_t*>(ep.aux) + col * esz;
     const int64_t ldb = ep.ldaux * esz;
@@ -343,6 +344,32 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
     stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out2) + col, ep.ldo2 * 2, row0,
                     rows_left, tmO2, col);
     b = stage_acquire<TMA>(st, ring, lane);
+    stage_row_bf16x64(b, lane, v);
+    stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
+                    rows_left, tmO, col);
+  } else if constexpr (EPI == RP_EPI_ROWDOT) {
+    // bf16 output unchanged; D of this lane's row for head col / 64, from the bf16-rounded
+    // output (what the attention backward reads as dO) and aux = O
+    const uint32_t b = stage_acquire<TMA>(st, ring, lane);
+    uint4 uu[8];
+    aux_rows(b, lane, in, uu);
+    float dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t w[4] = {uu[c].x, uu[c].y, uu[c].z, uu[c].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 o = unpack_bf16x2(w[k]);
+        const float2 g = unpack_bf16x2(pack_bf16x2(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]));
+        dot = fmaf(g.x, o.x, dot);
+        dot = fmaf(g.y, o.y, dot);
+      }
+    }
+    const int64_t row = row0 + lane;
+    if (lane < rows_left) {
+      const int64_t sq = row / ep.rd_seq, t = row % ep.rd_seq, h = col >> 6;
+      ep.rowdot[(sq * ep.rd_heads + h) * ep.rd_seq + t] = dot;
+    }
     stage_row_bf16x64(b, lane, v);
     stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
                     rows_left, tmO, col);
@@ -873,6 +900,7 @@ static GemmKernelPtr pick_epi(int epi) {
     case RP_EPI_GELU_BWD: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_GELU_BWD>();
     case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
     case RP_EPI_MUL: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_MUL>();
+    case RP_EPI_ROWDOT: return kernel_ptr<BN, A_MN, B_MN, RP_EPI_ROWDOT>();
   }
   return nullptr;
 }
@@ -898,6 +926,10 @@ static GemmKernelPtr pick_epi_2sm(int epi) {
     case RP_EPI_GELU_BWD: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_GELU_BWD>();
     case RP_EPI_BIAS_GELU_SLOPE: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_BIAS_GELU_SLOPE>();
     case RP_EPI_MUL: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_MUL>();
+    case RP_EPI_ROWDOT: return kernel_ptr_2sm<A_MN, B_MN, RP_EPI_ROWDOT>();
+    case kEpiTma + RP_EPI_ROWDOT: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_ROWDOT>();
+    case kEpiTma1 + RP_EPI_ROWDOT:
+      return kernel_ptr_2sm<A_MN, B_MN, kEpiTma1 + RP_EPI_ROWDOT>();
     case kEpiTma + RP_EPI_BF16: return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BF16>();
     case kEpiTma + RP_EPI_BIAS_GELU:
       return kernel_ptr_2sm<A_MN, B_MN, kEpiTma + RP_EPI_BIAS_GELU>();
@@ -1005,6 +1037,13 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   p->ep.split_stride = M * d->ldo;
   p->ep.colsum = d->colsum_part;
   p->ep.ldcs = N;
+  p->ep.rowdot = d->rowdot;
+  p->ep.rd_seq = d->rd_seq;
+  p->ep.rd_heads = N / 64;
+  if (d->epi == RP_EPI_ROWDOT && (!d->rowdot || !d->aux || d->rd_seq < 1 || N % 64)) {
+    delete p;
+    return rp_fail(RP_ERR_CONTRACT, "gemm: ROWDOT needs rowdot, aux, rd_seq >= 1, N % 64 == 0");
+  }
   if (d->colsum_part && d->epi != RP_EPI_MUL && d->epi != RP_EPI_GELU_BWD) {
     delete p;
     return rp_fail(RP_ERR_CONTRACT, "gemm: colsum_part needs the MUL or GELU_BWD epilogue");
@@ -1043,8 +1082,10 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   // 221, residual 87.4 vs 88.7 and K = 3072 180.6 vs 187, plain bf16 132.5 vs 135.2 on
   // register stores). The split-K fp32 partials keep register stores.
   if (two_sm && d->epi != RP_EPI_F32)
-    tma_kind = (K <= 1024 && (d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL)) ? kEpiTma
-                                                                                : kEpiTma1;
+    tma_kind = (K <= 1024 && (d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
+                              d->epi == RP_EPI_ROWDOT))
+                   ? kEpiTma
+                   : kEpiTma1;
   const bool tma_store = tma_kind != 0;
   if (rc == RP_OK && tma_store) {
     if (d->epi == RP_EPI_RESID) {

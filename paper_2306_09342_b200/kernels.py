@@ -33,7 +33,7 @@ def _req(t, dtype, name):
 def gemm(A, B, M, N, K, *, a_mn=False, b_mn=False, epi=_capi.RP_EPI_BF16, out=None,
          out2=None, aux=None, bias=None, sign=1.0, splits=1, workspace=None, max_ctas=0,
          bn=256, lda=None, ldb=None, ldo=None, ldo2=None, ldaux=None, colsum_part=None,
-         stream=None):
+         rowdot=None, rd_seq=0, stream=None):
     """C[M,N] = A.B on the tcgen05 path. A is [M,K] (a_mn=False) or [K,M] (a_mn=True);
     B is [N,K] (b_mn=False) or [K,N] (b_mn=True)."""
     d = GemmDesc()
@@ -53,6 +53,8 @@ def gemm(A, B, M, N, K, *, a_mn=False, b_mn=False, epi=_capi.RP_EPI_BF16, out=No
     d.sign = sign
     d.splits = splits
     d.workspace = workspace.data_ptr() if workspace is not None else None
+    d.rowdot = rowdot.data_ptr() if rowdot is not None else None
+    d.rd_seq = rd_seq
     d.max_ctas = max_ctas
     d.bn = bn
     d.colsum_part = colsum_part.data_ptr() if colsum_part is not None else None

@@ -272,3 +272,23 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
             assert rel(dqkv[:, sl], g[:, sl]) < 2e-2, name
     assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H))
     _capi.lib().rp_set_attention_impl(0)
+
+
+@pytest.mark.parametrize("bn", [256, 128, 512])
+def test_gemm_rowdot(K, bn):
+    """RP_EPI_ROWDOT: bf16 output plus, per (row, 64-column head), the dot of the bf16 output
+    with aux -- the attention backward's D = rowsum(dO * O) laid out [(seq, head), token]."""
+    from paper_2306_09342_b200._capi import RP_EPI_ROWDOT
+    S_, Ntok, H, Kd = 5, 197, 4, 768
+    M, N = S_ * Ntok, H * 64
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    W = (0.05 * torch.randn(N, Kd, device="cuda")).bfloat16()
+    O = torch.randn(M, N, device="cuda").bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    D = torch.full((S_ * H * Ntok,), float("nan"), device="cuda")
+    K.gemm(A, W, M, N, Kd, a_mn=0, b_mn=0, epi=RP_EPI_ROWDOT, out=out, aux=O, rowdot=D,
+           rd_seq=Ntok, bn=bn)
+    ref = A.float() @ W.float().t()
+    assert rel(out, ref) < 1e-2
+    dref = (out.float() * O.float()).view(S_, Ntok, H, 64).sum(-1).permute(0, 2, 1).reshape(-1)
+    assert rel(D, dref) < 1e-5
