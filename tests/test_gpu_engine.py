@@ -472,3 +472,16 @@ def test_cpp_example_trains(tmp_path):
                        timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "pareprop == reprop (bit-exact grads): yes" in r.stdout
+
+
+def test_out_of_memory_is_a_budget_error():
+    """An arena that does not fit in HBM fails engine creation with the reference's
+    BudgetError (no crash, nothing leaked: a normal engine still works afterwards)."""
+    from paper_2306_09342_b200 import _capi
+    from paper_2306_09342_b200.engine import PRESETS, REPROP, Engine, ModelConfig
+    with pytest.raises(_capi.BudgetError):
+        Engine(ModelConfig(**dict(PRESETS["revvit-b"], batch=200000)))
+    eng = Engine(ModelConfig(**dict(TI, depth=2, batch=2)))
+    eng.step(REPROP, graph=False)
+    assert np.isfinite(eng.loss())
+    eng.close()
