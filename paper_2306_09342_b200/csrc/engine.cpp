@@ -200,6 +200,7 @@ int dalloc(RpEngine* g, T** p, int64_t count) {
   const size_t bytes = static_cast<size_t>(count > 0 ? count : 1) * sizeof(T);
   cudaError_t e = cudaMalloc(&q, bytes);
   if (e != cudaSuccess) {
+    cudaGetLastError();  // not sticky: do not leak it into the next launch check
     std::string m = "device allocation of " + std::to_string(bytes) + " bytes failed: " +
                     cudaGetErrorString(e);
     return rp_fail(RP_ERR_BUDGET, m.c_str());

@@ -19,7 +19,8 @@ int rp_check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) return RP_OK;
   g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
-  return RP_ERR_CUDA;
+  // device memory exhausted is the reference's BudgetError (errors.hpp), not a fault
+  return e == cudaErrorMemoryAllocation ? RP_ERR_BUDGET : RP_ERR_CUDA;
 }
 
 extern "C" const char* rp_last_error(void) { return g_last_error.c_str(); }
