@@ -166,16 +166,30 @@ __global__ void __launch_bounds__(256)
   const int tm = (tid >> 4) * 2, tn = (tid & 15) * 2;
   const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 32, n0 = static_cast<int64_t>(blockIdx.x) * 32;
   float acc[2][2] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += 32) {
-    for (int i = tid; i < 32 * 32; i += 256) {
+  // the next k slice is fetched into registers while the current one is multiplied
+  float ra[4], rb[4];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = tid + 256 * j;
       const int kk = i & 31, mm = i >> 5;  // A: consecutive threads walk k
       const int64_t gm = m0 + mm, gk = k0 + kk;
-      as[kk][mm] = (gm < M && gk < K) ? A[gm * sam + gk * sak] : 0.f;
+      ra[j] = (gm < M && gk < K) ? A[gm * sam + gk * sak] : 0.f;
       const int nn = i & 31, kb = i >> 5;  // B: consecutive threads walk n
       const int64_t gn = n0 + nn, gkb = k0 + kb;
-      bs[kb][nn] = (gkb < K && gn < N) ? Bm[gkb * sbk + gn * sbn] : 0.f;
+      rb[j] = (gkb < K && gn < N) ? Bm[gkb * sbk + gn * sbn] : 0.f;
+    }
+  };
+  fetch(0);
+  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = tid + 256 * j;
+      as[i & 31][i >> 5] = ra[j];
+      bs[i >> 5][i & 31] = rb[j];
     }
     __syncthreads();
+    if (k0 + 32 < K) fetch(k0 + 32);
 #pragma unroll 8
     for (int k = 0; k < 32; ++k) {
       const float a0 = as[k][tm], a1 = as[k][tm + 1], b0 = bs[k][tn], b1 = bs[k][tn + 1];
