@@ -215,7 +215,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       red_max[j & 1][cq][rloc] = mx;
-      named_bar(1, 512);  // every warp has read its S quarter: P may now overwrite [0, Nk/2)
+      // the four warps of this lane quarter have read their S columns: P may now overwrite
+      // [0, Nk/2) of these lanes (only they exchange maxima and sums for these rows)
+      named_bar(1 + q, 128);
       const float* rm = &red_max[j & 1][0][rloc];
       const float ms = fmaxf(fmaxf(rm[0], rm[128]), fmaxf(rm[256], rm[384])) * g.scale_log2;
       float l = 0.f;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       ms_prev = ms;
     }
     if (J > 0) {
-      named_bar(1, 512);  // last tile's sums
+      named_bar(1 + q, 128);  // last tile's sums
       epilogue(J - 1, ms_prev);
     }
   }
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (lane == 0) mbar_arrive(&bar_p[u & 1]);
         }
         red_max[cq][rloc] = mx;
-        named_bar(1, 512);
+        named_bar(1 + q, 128);  // only the four warps of a lane quarter share rows
         const float ms =
             fmaxf(fmaxf(red_max[0][rloc], red_max[1][rloc]), fmaxf(red_max[2][rloc], red_max[3][rloc])) *
             g.scale_log2;
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (lane == 0) mbar_arrive(&bar_p[u & 1]);
         }
         red_sum[cq][rloc] = l;
-        named_bar(1, 512);
+        named_bar(1 + q, 128);
         const float lt = (red_sum[0][rloc] + red_sum[1][rloc]) + (red_sum[2][rloc] + red_sum[3][rloc]);
         // ---- epilogue: O / l (16 of the 64 head columns per warp), LSE
         mbar_wait(bar_o, tt & 1);
