@@ -1080,7 +1080,8 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   // stage fewer) win for the epilogues that read a bf16 input (gelu' multiply 250 vs 258);
   // one buffer with the full pipeline wins or ties everywhere else (bias + GELU + u 216 vs
   // 221, residual 87.4 vs 88.7 and K = 3072 180.6 vs 187, plain bf16 132.5 vs 135.2 on
-  // register stores). The split-K fp32 partials keep register stores.
+  // register stores; bias + GELU + slope 271.4 vs 271.8, tools/gemm_epi_ab.py). The split-K
+  // fp32 partials keep register stores.
   if (two_sm && d->epi != RP_EPI_F32)
     tma_kind = (K <= 1024 && (d->epi == RP_EPI_GELU_BWD || d->epi == RP_EPI_MUL ||
                               d->epi == RP_EPI_ROWDOT))
