@@ -153,6 +153,30 @@ def test_pareprop_bit_identical_to_reprop():
         np.testing.assert_array_equal(g, g0)
 
 
+def test_pdl_bit_identical():
+    """Programmatic dependent launch (rp_set_pdl, off by default) only changes when kernels
+    may start, never what they compute: same loss and gradients bit for bit, eager and graph."""
+    from paper_2306_09342_b200 import _capi
+    from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits
+    cfg = dict(TI, depth=3)
+    eng, mc, _, _ = make(cfg, batch=8)
+    x, lab = O.synthetic_batch(mc, 8, seed=4)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    eng.step(REPROP, graph=False)
+    l0, g0 = eng.loss(), eng.grads()
+    try:
+        _capi.lib().rp_set_pdl(1)
+        eng.invalidate_graphs()
+        for mode, graph in [(REPROP, False), (PAREPROP, False), (PAREPROP, True)]:
+            eng.step(mode, graph=graph)
+            assert eng.loss() == l0
+            np.testing.assert_array_equal(eng.grads(), g0)
+    finally:
+        _capi.lib().rp_set_pdl(0)
+        eng.invalidate_graphs()
+
+
 def test_sgd_descent():
     """SPEC.md:395 / acceptance 9: loss falls over 20 SGD steps on one fixed batch."""
     from paper_2306_09342_b200.engine import PAREPROP, REPROP, bf16_bits
