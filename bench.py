@@ -160,6 +160,17 @@ def cpu_reference_sample(threads: int, steps: int = 1, warmup: int = 0):
                         f"img/s scaled to depth {depth}")), ts
 
 
+WORKLOAD = ("RevViT-B/16 train step (depth 12, dim 768, 12 heads, 197 tokens, 1000 classes), "
+            "PaReprop, SGD")
+
+
+def workload_config(world, per_gpu, engine="pareprop"):
+    """The `config` object both arms print (same workload, batch and geometry)."""
+    return {"workload": WORKLOAD, "global_batch": per_gpu * world, "per_gpu_batch": per_gpu,
+            "seq_len": 197, "parallelism": f"dp{world}", "engine": engine,
+            "l2": "per-step working set ~4.5 GB >> 126 MB L2 (no flush needed)"}
+
+
 def host_threads():
     try:
         n = len(os.sched_getaffinity(0))
@@ -173,15 +184,17 @@ def main_reference(a, rank):
         return 0
     thr = host_threads()
     base, ts = cpu_reference_sample(thr, steps=a.steps, warmup=a.warmup)
-    model = PRESET
+    cfg = workload_config(a.gpus, a.batch or 256,
+                          engine="reference CPU code (Reprop, one sample per host thread)")
+    cfg.pop("l2")
+    cfg["sample"] = base["sample"]
     line = {
         "impl": "reference", "metric": "train img/s (RevViT-B PaReprop step)",
         "value": base["value"], "unit": "img/s", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1000.0 * float(np.mean(ts)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "RevViT-B/16 train step (depth 12, dim 768, 12 heads, 197 tokens)",
-                   "model": model, "sample": base["sample"]},
+        "config": cfg,
         "cpu_baseline": {"value": base["value"], "unit": "img/s", "cores": base["cores"],
                          "kind": base["kind"], "sample": base["sample"]},
         "e2e": {"value": base["value"], "unit": "img/s", "h2d_bytes_per_step": 0,
@@ -349,11 +362,7 @@ def main_ours(a, rank, world, local_rank):
             "value": img_p, "unit": "img/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_p / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "RevViT-B/16 train step (depth 12, dim 768, 12 heads, "
-                                   "197 tokens, 1000 classes), PaReprop, SGD",
-                       "global_batch": B * world, "per_gpu_batch": B, "seq_len": cfg.seq_len,
-                       "parallelism": f"dp{world}", "engine": "pareprop",
-                       "l2": "per-step working set ~4.5 GB >> 126 MB L2 (no flush needed)"},
+            "config": workload_config(world, B),
             "reprop": {"value": img_r, "ms_per_step": ms_r / a.steps},
             "pareprop_gain_pct": 100.0 * (img_p / img_r - 1.0),
             "pareprop_gain_small_batch": small,
