@@ -28,3 +28,15 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _seed_torch_per_test(request):
+    """GPU tests draw their inputs from torch's global RNG: seed it from the test id so every
+    case sees the same inputs whatever runs before it (-k subsets, reordering)."""
+    if "gpu" not in request.keywords:
+        return
+    import zlib
+
+    import torch
+    torch.manual_seed(zlib.crc32(request.node.nodeid.encode()))
