@@ -110,54 +110,80 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- CPU reference
-def _ref_cfg(depth):
+def _ref_cfg(preset, depth=None):
     from oracle import revprop_oracle as O
     from paper_2306_09342_b200.engine import PRESETS
-    p = dict(PRESETS[PRESET])
-    return O.ModelConfig(depth, p["width"], p["heads"], p["hidden"], p["seq_len"], 768, 1000)
+    p = dict(PRESETS[preset])
+    return O.ModelConfig(depth or p["depth"], p["width"], p["heads"], p["hidden"], p["seq_len"],
+                         768, p.get("num_classes", 1000))
 
 
-def cpu_reference_sample(threads: int, steps: int = 1, warmup: int = 0):
-    """The reference's own CPU path (oracle/_ref: ref ops.cpp + layers.cpp, SPEC engines),
-    Reprop on RevViT-B geometry: each sample step runs embed + ONE reversible block
-    (forward, recompute, VJP) + head on `threads` images, one image per host thread, and
-    the img/s is scaled to the full depth-12 model (blocks are identical work).
-    Falls back to the numpy port (kind "port") when oracle/_ref is absent."""
+def _ref_runner(mc, images, threads, engine):
+    """One training step of the reference's own CPU code (oracle/_ref: ref ops.cpp +
+    layers.cpp compiled in place, SPEC engines in ref_shim.cpp) on `images` images, the batch
+    split over `threads` shards run concurrently (ref_step_dp); PaReprop runs each shard's
+    recompute lane on its own extra thread. Parameters and inputs are seeded
+    random (timing is data-independent). Falls back to the numpy port of the
+    same algorithm (kind "port", one thread) when oracle/_ref is absent."""
     from oracle import revprop_oracle as O
-    cfg1 = _ref_cfg(1)
     rng = np.random.default_rng(0)
-    params = O.init_params(cfg1, 0, np.float32)
-    x = rng.standard_normal((threads, cfg1.seq_len, cfg1.in_dim)).astype(np.float32)
-    lab = rng.integers(0, cfg1.num_classes, threads)
-    kind = "reference"
+    params = (0.02 * rng.standard_normal(O.param_count(mc))).astype(np.float32)
+    x = rng.standard_normal((images, mc.seq_len, mc.in_dim)).astype(np.float32)
+    lab = rng.integers(0, mc.num_classes, images)
     try:
         from oracle import ref as R
         R.lib()
-
-        def run():
-            R.step_dp(cfg1, params, x, lab, threads, "reprop")
+        return "reference", lambda: R.step_dp(mc, params, x, lab, threads, engine)
     except Exception:
-        kind = "port"
-        threads = 1
-        x1, lab1 = x[:1].astype(np.float64), lab[:1]
-        p64 = params.astype(np.float64)
+        p64, x64 = params.astype(np.float64), x.astype(np.float64)
+        return "port", lambda: O.step(mc, p64, x64, lab, engine)
 
-        def run():
-            O.step(cfg1, p64, x1, lab1, "reprop")
-    for _ in range(warmup):
-        run()
+
+def cpu_reference_sample(threads: int, steps: int = 1, warmup: int = 0):
+    """The reference's CPU path on the benchmarked workload: full depth-12 RevViT-B PaReprop
+    training steps (embed, 12 reversible blocks forward, head + CE, the two-lane backward with
+    recompute, all parameter grads), each on threads // 2 images -- one image per shard, each
+    shard a 2-thread PaReprop pipeline, so every host thread is busy. Warm-up steps run the
+    same code on a depth-1 model (the CPU code needs no warm-up beyond loading; this keeps a
+    K-step run bounded)."""
+    images = max(1, threads // 2)
+    mc = _ref_cfg("revvit-b")
+    kind, run = _ref_runner(mc, images, images, "pareprop")
+    if kind == "port":
+        images, threads = 1, 1
+    if warmup:
+        _, run_w = _ref_runner(_ref_cfg("revvit-b", depth=1), images, images, "pareprop")
+        for _ in range(warmup):
+            run_w()
     ts = []
     for _ in range(steps):
         t0 = time.perf_counter()
         run()
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
-    depth = 12
-    val = threads / (t * depth)
-    return dict(value=val, unit="img/s", cores=threads, kind=kind,
-                sample=(f"RevViT-B geometry, Reprop fp32, embed + 1 of {depth} blocks + head per "
-                        f"sample on {threads} image(s) (one per host thread), {t:.2f} s/sample; "
-                        f"img/s scaled to depth {depth}")), ts
+    used = 2 * images if kind == "reference" else 1
+    return dict(value=images / t, unit="img/s", cores=used, kind=kind,
+                sample=(f"full RevViT-B training step (depth 12, PaReprop, fp32) of the "
+                        f"{'reference CPU code' if kind == 'reference' else 'numpy port'} on "
+                        f"{images} image(s), one 2-lane pipeline per image on {used} host "
+                        f"thread(s), {t:.1f} s/step")), ts
+
+
+def cpu_reference_ti():
+    """BASELINE.json configs[0] in the same run: RevViT-Ti (depth 12, d 192) fp32 batch 8 on
+    the reference CPU code, Reprop on 1 thread vs PaReprop on 2, one step each."""
+    mc = _ref_cfg("revvit-ti")
+    out = {"config": "RevViT-Ti fp32 batch 8 (BASELINE configs[0]), reference CPU code"}
+    for engine in ("reprop", "pareprop"):
+        kind, run = _ref_runner(mc, 8, 1, engine)
+        t0 = time.perf_counter()
+        run()
+        dt = time.perf_counter() - t0
+        out[engine] = {"s_per_step": dt, "img_per_s": 8 / dt,
+                       "threads": 1 if engine == "reprop" else 2, "kind": kind}
+    out["pareprop_gain_pct"] = 100 * (out["reprop"]["s_per_step"] /
+                                      out["pareprop"]["s_per_step"] - 1)
+    return out
 
 
 WORKLOAD = ("RevViT-B/16 train step (depth 12, dim 768, 12 heads, 197 tokens, 1000 classes), "
@@ -184,10 +210,9 @@ def main_reference(a, rank):
         return 0
     thr = host_threads()
     base, ts = cpu_reference_sample(thr, steps=a.steps, warmup=a.warmup)
-    cfg = workload_config(a.gpus, a.batch or 256,
-                          engine="reference CPU code (Reprop, one sample per host thread)")
-    cfg.pop("l2")
-    cfg["sample"] = base["sample"]
+    # the same config object as the GPU arm (same workload, batch, engine); what the CPU
+    # actually ran per step is in cpu_baseline.sample
+    cfg = workload_config(a.gpus, a.batch or 256)
     line = {
         "impl": "reference", "metric": "train img/s (RevViT-B PaReprop step)",
         "value": base["value"], "unit": "img/s", "n_gpus": a.gpus, "steps": a.steps,
@@ -353,6 +378,7 @@ def main_ours(a, rank, world, local_rank):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             cpu, _ = cpu_reference_sample(host_threads(), steps=1, warmup=0)
+            cpu["configs0_ti"] = cpu_reference_ti()
         except Exception as ex:  # never let the baseline kill the GPU line
             cpu = {"value": None, "unit": "img/s", "cores": 0, "kind": "port",
                    "sample": f"failed: {ex}"}
@@ -401,12 +427,30 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small-batch", action="store_true")
     a = ap.parse_args(argv)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: start the N ranks ourselves (one per GPU,
+        # torchrun on 127.0.0.1) and return their status; rank 0 prints the line
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)]
+        cmd += list(sys.argv[1:] if argv is None else argv)
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         return main_reference(a, rank)
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but the launcher started {world} rank(s)")
     if world > 1:
+        # deterministic bucket all-reduces (the engine pins the same when unset); must be set
+        # before the first NCCL communicator of the process
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

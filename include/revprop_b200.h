@@ -162,7 +162,9 @@ int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, const float* l
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
 /* 0 (default): tcgen05 kernels where they apply, backward = one dK/dV pass that also writes
  * dS^T + a dQ = dS K pass over it; 1: warp-level mma.sync only; 2: tcgen05 with the
- * two-pass backward (dQ pass, dK/dV pass, each recomputing S and dP; no dS stored) */
+ * two-pass backward (dQ pass, dK/dV pass, each recomputing S and dP; no dS stored).
+ * Process-global; other values are RP_ERR_CONFIG. Captured engine graphs keep the kernels
+ * they were captured with: call rp_engine_invalidate_graphs after changing it. */
 int rp_set_attention_impl(int impl);
 
 /* ------------------------------------------------------------------ training engine
@@ -196,6 +198,11 @@ typedef struct RpModelConfig {
   int64_t stage_depth[8], stage_width[8], stage_heads[8];
   int64_t reduction; /* r: tokens merged per boundary group (2 sequences, 4 2-D grids) */
   int fusion;        /* BoundaryParams.fusion_kind: 0 average, 1 mlp */
+  /* Data parallel (rp_engine_comm_init): NCCL CTAs per all-reduce (ncclConfig_t maxCTAs;
+   * 0 = 4). With world > 1 the backward GEMMs leave as many SMs (rounded up to CTA pairs)
+   * free for them, so bucket all-reduces overlap the backward instead of queueing behind
+   * the persistent GEMM grids. */
+  int comm_ctas;
 } RpModelConfig;
 
 /* Ledger-predicted peak activation bytes of an engine (mode 0 vanilla, 1 reprop,
@@ -243,8 +250,65 @@ int rp_engine_gemm_profile(RpEngine* engine, int mode, double* ms, double* flops
                            int64_t* launches);
 int rp_engine_set_instrument(RpEngine* engine, int on);
 int rp_engine_slot_log(RpEngine* engine, float* out);
+
+/* StepStats of the last step (the reference's MemoryLedger semantics,
+ * ref:proj/core/include/revprop/ledger.hpp:18-104). Blocks until that step is done.
+ *   wall_ns                device time of the step (events on the engine stream around it)
+ *   peak_activation_bytes  peak of the live ledger: the step's enqueue replays every
+ *                          activation buffer's lifetime as charge / release events in the
+ *                          order the schedule allows on the device; equals
+ *                          rp_activation_bytes() for isotropic models, <= it for
+ *                          hierarchical ones (per-stage footprints); a release below zero
+ *                          fails the step with RP_ERR_ACCOUNTING (AccountingError)
+ *   lane_busy_ns[2]        lane R / lane G busy time, instrumented steps only (else -1)
+ *   blocks_processed       reversible blocks run through the backward (== depth)
+ *   arena_*_bytes          device bytes the engine actually allocated: activation storage
+ *                          (what the ledger accounts), parameters / grads / optimizer
+ *                          state, and everything (incl. workspaces) */
+typedef struct RpStepStats {
+  float loss;
+  int mode;
+  int64_t wall_ns;
+  int64_t peak_activation_bytes;
+  int64_t lane_busy_ns[2];
+  int64_t blocks_processed;
+  int64_t ledger_events;
+  int64_t arena_activation_bytes;
+  int64_t arena_param_bytes;
+  int64_t arena_total_bytes;
+} RpStepStats;
+int rp_engine_step_stats(RpEngine* engine, RpStepStats* out);
+
+/* Stream contract of the block / layer entry points below (rp_engine_rev_*,
+ * rp_engine_boundary_*, rp_engine_attention_* / mlp_*, rp_engine_set_batch_device): they
+ * read caller-owned device pointers on the engine's own (non-blocking) stream after waiting
+ * for an event recorded on the caller's stream at entry, so everything the caller enqueued
+ * on that stream before the call is visible. Default caller stream: the legacy default
+ * stream (torch's default stream); set another with rp_engine_set_caller_stream. They return
+ * after their results are complete (host-synchronous). */
+int rp_engine_set_caller_stream(RpEngine* engine, rp_stream_t stream);
+
+/* Recompute trace (test instrumentation): when set, eager steps copy every block's input
+ * pair (i1 | i2, fp32 [T_s d_s] each) as the forward saw it into `fwd` and as lane R
+ * reconstructed it in the backward into `rec` (the stage's first block: its stored input).
+ * Buffers: rp_engine_trace_floats() floats each, device memory; block b at the sum over
+ * earlier blocks of 2 T_s d_s. NULL turns it off. Traced steps never use the CUDA graph. */
+int64_t rp_engine_trace_floats(const RpEngine* engine);
+int rp_engine_set_trace(RpEngine* engine, float* fwd, float* rec);
+/* Data parallelism over NCCL: one fp32 all-reduce (sum) per gradient
+ * bucket on the engine's comm stream as soon as lane G finishes the bucket's owner, the
+ * optimizer step of that bucket right after with 1/world folded in. The communicator is
+ * created with ncclCommInitRankConfig (maxCTAs = comm_ctas); NCCL_ALGO=Ring and
+ * NCCL_PROTO=Simple are set unless the caller set them (deterministic reduction order).
+ * world == 1 builds a single-rank communicator (the same code path on one GPU).
+ * rp_engine_get_grads then returns the MEAN of the ranks' gradients. */
 int rp_nccl_unique_id(uint8_t* out128);
 int rp_engine_comm_init(RpEngine* engine, const uint8_t* id128, int world, int rank);
+/* The gradient buckets of a config in all-reduce order (no device needed): offsets / sizes
+ * in floats into the flat parameter vector, kinds 0 embed, 1 block, 2 boundary, 3 head.
+ * Returns the bucket count (negative status if cap is too small). */
+int rp_model_bucket_plan(const RpModelConfig* cfg, int64_t* offsets, int64_t* sizes, int* kinds,
+                         int64_t cap);
 int rp_engine_rev_forward(RpEngine* engine, int64_t block, const float* i1, const float* i2,
                           float* o1, float* o2);
 int rp_engine_rev_backward_local(RpEngine* engine, int64_t block, const float* o1,

@@ -552,7 +552,10 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
 // backward that keeps no dS
 static int g_attn_impl = 0;
 
+// Process-global switch, read when a step is enqueued: engines must drop their captured
+// graphs (rp_engine_invalidate_graphs) after changing it, or the graphs keep the old kernels.
 extern "C" int rp_set_attention_impl(int impl) {
+  if (impl < 0 || impl > 2) return rp_fail(RP_ERR_CONFIG, "attention impl must be 0, 1 or 2");
   g_attn_impl = impl;
   return RP_OK;
 }

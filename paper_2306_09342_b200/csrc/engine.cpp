@@ -98,6 +98,9 @@ struct RpStage {
   float* buf1[2] = {nullptr, nullptr};
   float* buf2[3] = {nullptr, nullptr, nullptr};
   int64_t stash_off = 0;  // Vanilla stash offset of X_1 (floats)
+  // ledger quantities (bytes): block footprint, caches alone (Vanilla),
+  // stored stage input + output, Vanilla stash
+  int64_t led_block = 0, led_cache = 0, led_store = 0, led_stash = 0;
   // boundary after this stage (ref layers.hpp:144-149): merge_w [(r d), d_next] then
   // fusion_w [2d, d] (mlp fusion); -1 for the last stage
   int64_t bnd_tix = -1, bnd_size = 0;
@@ -178,6 +181,31 @@ struct RpEngine {
   float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f, wd = 0.f;
   float *adam_m = nullptr, *adam_v = nullptr, *step_t = nullptr;
   int fault = 0;  // test hook: 1 = corrupt every block's F-path VJP
+  // caller-stream ordering of the block / layer entry points: work the caller enqueued on
+  // `caller` (default: the legacy default stream) before the call is complete before the
+  // engine reads the caller's device pointers
+  cudaStream_t caller = nullptr;
+  cudaEvent_t evCaller = nullptr;
+  // recompute trace (eager steps): every block's input pair as the forward saw it and as
+  // lane R reconstructed it, [sum_b 2 T_s d_s] floats each, block b at trace_off[b]
+  float *trace_fwd = nullptr, *trace_rec = nullptr;
+  std::vector<int64_t> trace_off;
+  // arena bookkeeping (bytes actually allocated, by category) and the live ledger replay of
+  // the last enqueued step's schedule (ref ledger.hpp:18-104)
+  int64_t arena_bytes[3] = {0, 0, 0};  // 0 other, 1 activations, 2 params / grads / state
+  int64_t led_live = 0, led_peak = 0, led_events = 0, blocks_processed = 0, led_fixed = 0;
+  std::vector<int64_t> led_held;  // per block: bytes charged and not yet released
+  int led_error = 0;
+  // last step: timing events around it on the engine stream, whether it was instrumented
+  cudaEvent_t evStepBeg = nullptr, evStepEnd = nullptr;
+  bool step_timed = false, step_instrumented = false;
+  int last_mode = -1;
+  // ledger results of the last enqueue of each mode (a graph replay re-runs that schedule)
+  int64_t led_peak_m[3] = {0, 0, 0}, led_events_m[3] = {0, 0, 0}, blocks_m[3] = {0, 0, 0};
+  // gradient buckets (offset, floats) by owner, from the shared bucket plan
+  std::pair<int64_t, int64_t> bk_head{0, 0}, bk_embed{0, 0};
+  std::vector<std::pair<int64_t, int64_t>> bk_block, bk_bnd;
+  int comm_reserve = 0;  // SMs kept free of GEMM CTAs for the NCCL kernels (world > 1)
 };
 
 namespace {
@@ -194,8 +222,10 @@ int cuda_ok(cudaError_t e, const char* what) {
   return rp_fail(RP_ERR_CUDA, m.c_str());
 }
 
+// cat: 0 workspace / other, 1 activation storage (what the ledger accounts), 2 parameters,
+// gradients and optimizer state
 template <class T>
-int dalloc(RpEngine* g, T** p, int64_t count) {
+int dalloc(RpEngine* g, T** p, int64_t count, int cat = 0) {
   void* q = nullptr;
   const size_t bytes = static_cast<size_t>(count > 0 ? count : 1) * sizeof(T);
   cudaError_t e = cudaMalloc(&q, bytes);
@@ -206,8 +236,18 @@ int dalloc(RpEngine* g, T** p, int64_t count) {
     return rp_fail(RP_ERR_BUDGET, m.c_str());
   }
   g->allocs.push_back(q);
+  g->arena_bytes[cat] += static_cast<int64_t>(bytes);
   *p = static_cast<T*>(q);
   return RP_OK;
+}
+
+// The block / layer entry points read caller device pointers on the engine stream: order
+// them after everything the caller enqueued on its stream (default: the legacy stream,
+// torch's default) before the call.
+int wait_caller(RpEngine* g) {
+  cudaStream_t cs = g->caller ? g->caller : cudaStreamLegacy;
+  RP_TRY(cuda_ok(cudaEventRecord(g->evCaller, cs), "record caller stream"));
+  return cuda_ok(cudaStreamWaitEvent(g->sG, g->evCaller, 0), "wait caller stream");
 }
 
 // tensor index helpers (flat order, SPEC.md:279-282 Model fields)
@@ -503,13 +543,58 @@ int boundary_fuse(RpEngine* g, RpStage& St, cudaStream_t s) {
   return rpk_fuse_avg_bf16(o1, o2, St.T * St.d, g->fb, s);
 }
 
+// ---- live ledger (SPEC.md:346-349 ledger_track; ref ledger.hpp:18-104): the step's
+// enqueue replays each activation buffer's lifetime as charge / release events, in the
+// order the schedule's dependencies allow them on the device (a block's footprint lives
+// from its recompute (lane R) until its VJP (lane G) is done; under PaReprop R(b) may only
+// start once G(b+2) is done, the capacity-1 rendezvous). A release larger than the live
+// total is the reference's AccountingError.
+void led_charge(RpEngine* g, int64_t bytes) {
+  g->led_live += bytes;
+  g->led_peak = std::max(g->led_peak, g->led_live);
+  ++g->led_events;
+}
+void led_release(RpEngine* g, int64_t bytes) {
+  ++g->led_events;
+  if (bytes > g->led_live) {
+    g->led_error = 1;
+    g->led_live = 0;
+    return;
+  }
+  g->led_live -= bytes;
+}
+void led_release_block(RpEngine* g, int64_t b) {
+  if (b < 0 || b >= g->L) return;
+  int64_t& h = g->led_held[static_cast<size_t>(b)];
+  if (h) led_release(g, h);
+  h = 0;
+}
+void led_charge_block(RpEngine* g, int64_t b, int64_t bytes) {
+  led_charge(g, bytes);
+  g->led_held[static_cast<size_t>(b)] += bytes;
+}
+
+// recompute trace: block b's input pair into trace buffer `dst` (eager steps only)
+int trace_pair(RpEngine* g, float* dst, int64_t b, cudaStream_t s) {
+  if (!dst) return RP_OK;
+  RpStage& St = stage_of(g, b);
+  const int64_t j = b - St.first, n = St.T * St.d;
+  float* o = dst + g->trace_off[static_cast<size_t>(b)];
+  RP_TRY(cuda_ok(cudaMemcpyAsync(o, X1(g, St, j), static_cast<size_t>(n) * 4,
+                                 cudaMemcpyDeviceToDevice, s), "trace"));
+  return cuda_ok(cudaMemcpyAsync(o + n, X2(g, St, j), static_cast<size_t>(n) * 4,
+                                 cudaMemcpyDeviceToDevice, s), "trace");
+}
+
 int forward(RpEngine* g, cudaStream_t s) {
   RP_TRY(launch(g->p_embed, s));
   Slot& F = g->slot[0];
   for (RpStage& St : g->st) {
+    led_charge(g, g->vmode ? St.led_stash : St.led_store);  // stored stage boundaries
     for (int64_t j = 0; j < St.L; ++j) {
       const int64_t b = St.first + j;
       BlockPlans& p = g->plans[static_cast<size_t>(b)];
+      RP_TRY(trace_pair(g, g->trace_fwd, b, s));
       RP_TRY(ln_fwd(g, St, X1(g, St, j), tix_block(g, b, kLnFg), tix_block(g, b, kLnFb), F.hF,
                     F.meanF, F.rstdF, s));
       RP_TRY(launch(p.f_qkv, s));
@@ -577,6 +662,7 @@ int lane_r(RpEngine* g, int64_t b, cudaStream_t s) {
   mark(g, 0, b, 0, s);
   RP_TRY(recompute_g(g, b, s, true));
   RP_TRY(recompute_f(g, b, s, true));
+  RP_TRY(trace_pair(g, g->trace_rec, b, s));
   mark(g, 0, b, 1, s);
   return RP_OK;
 }
@@ -684,24 +770,38 @@ int enqueue_step(RpEngine* g, int mode) {
   const int rc = enqueue_step_impl(g, mode == 0 ? 1 : mode);
   t_prof_engine = nullptr;
   g->vmode = false;
+  if (rc == RP_OK) {
+    g->led_peak_m[mode] = g->led_peak;
+    g->led_events_m[mode] = g->led_events;
+    g->blocks_m[mode] = g->blocks_processed;
+  }
   return rc;
 }
 
 int enqueue_step_impl(RpEngine* g, int mode) {
   cudaStream_t sG = g->sG, sR = g->sR, sC = g->sC;
+  g->led_live = g->led_peak = g->led_events = g->blocks_processed = 0;
+  g->led_error = 0;
+  g->led_held.assign(static_cast<size_t>(g->L), 0);
+  led_charge(g, g->led_fixed);  // cotangent pair + lane-G temporaries
   if (g->optimizer == 1) RP_TRY(rpk_add_scalar(g->step_t, 1.0f, sG));
   RP_TRY(forward(g, sG));
   RP_TRY(head(g, sG));
   RP_TRY(cuda_ok(cudaEventRecord(g->evFwd, sG), "record"));
   // the head bucket can go as soon as the head backward is done
   RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evFwd, 0), "wait"));
-  RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(g->head_tix)], g->st.back().d * g->C, sC));
+  RP_TRY(bucket_update(g, g->bk_head.first, g->bk_head.second, sC));
   if (mode == 2) RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evFwd, 0), "wait"));
   for (size_t si = g->st.size(); si-- > 0;) {
     RpStage& St = g->st[si];
     for (int64_t j = St.L - 1; j >= 0; --j) {
       const int64_t b = St.first + j;
       const bool top = j == St.L - 1, next_b2 = j > 0;
+      // ledger: the footprint lane R is about to fill replaces the one whose VJP it waits
+      // for (b + 2 under PaReprop, b + 1 in one lane); Vanilla only recomputes caches
+      led_release_block(g, b + (mode == 2 ? 2 : 1));
+      led_charge_block(g, b, g->vmode ? St.led_cache : St.led_block);
+      ++g->blocks_processed;
       if (mode == 2) {
         if (b + 2 <= g->L - 1)
           RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evG[static_cast<size_t>(b + 2)], 0), "wait"));
@@ -714,7 +814,8 @@ int enqueue_step_impl(RpEngine* g, int mode) {
       RP_TRY(lane_g(g, b, sG, top, next_b2));
       RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
-      RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(tix_block(g, b, 0))], St.block_size, sC));
+      RP_TRY(bucket_update(g, g->bk_block[static_cast<size_t>(b)].first,
+                           g->bk_block[static_cast<size_t>(b)].second, sC));
     }
     if (si == 0) break;
     // boundary between stage si-1 and si: recompute fuse(stage si-1 output) -- on lane R
@@ -733,16 +834,21 @@ int enqueue_step_impl(RpEngine* g, int mode) {
     RP_TRY(boundary_vjp(g, Pv, sG));
     RP_TRY(cuda_ok(cudaEventRecord(g->evBnd[si - 1], sG), "record"));
     RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evBnd[si - 1], 0), "wait"));
-    RP_TRY(bucket_update(g, g->t_off[static_cast<size_t>(Pv.bnd_tix)], Pv.bnd_size, sC));
+    RP_TRY(bucket_update(g, g->bk_bnd[si - 1].first, g->bk_bnd[si - 1].second, sC));
   }
   if (mode == 2) RP_TRY(cuda_ok(cudaEventRecord(g->evRDone, sR), "record"));
+  for (int64_t b = 0; b < g->L; ++b) led_release_block(g, b);
+  for (const RpStage& St : g->st) led_release(g, g->vmode ? St.led_stash : St.led_store);
+  led_release(g, g->led_fixed);
+  if (g->led_error || g->led_live != 0)
+    return rp_fail(RP_ERR_ACCOUNTING, "ledger: activation bytes released twice or never");
   // embedding backward: e fed both halves -> d_e = d_i1 + d_i2
   const RpStage& S0 = g->st[0];
   RP_TRY(rpk_add_to_bf16(g->d1, g->d2, g->deb, S0.T * S0.d, sG));
   RP_TRY(launch(g->p_embed_w, sG));
   RP_TRY(cuda_ok(cudaEventRecord(g->evEmbed, sG), "record"));
   RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evEmbed, 0), "wait"));
-  RP_TRY(bucket_update(g, 0, g->in * S0.d, sC));
+  RP_TRY(bucket_update(g, g->bk_embed.first, g->bk_embed.second, sC));
   if (g->comm) {
     ncclResult_t r = ncclAllReduce(g->loss, g->loss, 1, ncclFloat32, ncclAvg, g->comm, sC);
     if (r != ncclSuccess) return rp_fail(RP_ERR_SCHEDULER, ncclGetErrorString(r));
@@ -754,8 +860,16 @@ int enqueue_step_impl(RpEngine* g, int mode) {
 }
 
 void set_partition(RpEngine* g, int mode) {
-  const int r = (mode == 2) ? g->r_ctas : 0;
-  const int gg = (mode == 2) ? g->g_ctas : 0;
+  int r = (mode == 2) ? g->r_ctas : 0;
+  int gg = (mode == 2) ? g->g_ctas : 0;
+  // data parallel: the backward's persistent GEMM grids leave comm_reserve SMs to the NCCL
+  // kernels of the bucket all-reduces, so those start at once instead of waiting for a
+  // whole GEMM to drain (the all-reduce then overlaps the backward)
+  if (g->comm_reserve > 0) {
+    const int cap = kSms - g->comm_reserve;
+    r = r > 0 ? std::min(r, cap) : cap;
+    gg = gg > 0 ? std::min(gg, cap) : cap;
+  }
   for (auto& p : g->plans) {
     for (RpGemmPlan* q : {p.r_w1, p.r_w2, p.r_qkv, p.r_proj})
       if (q) rp_gemm_plan_set_max_ctas(q, r);
@@ -824,7 +938,67 @@ int stage_geoms(const RpModelConfig* c, std::vector<RpStage>* out) {
   }
   return RP_OK;
 }
+
+// The data-parallel gradient buckets (one all-reduce each) in the order the step issues
+// them: the head, then per stage from the last, its blocks from the top down, then the
+// boundary below that stage, and the embedding last. Offsets into the flat parameter /
+// gradient vector (order of include/revprop_b200.h). kind: 0 embed, 1 block, 2 boundary,
+// 3 head; index: block / stage index.
+struct Bucket {
+  int64_t off, n;
+  int kind;
+  int64_t index;
+};
+void bucket_plan(const RpModelConfig* c, const std::vector<RpStage>& st, std::vector<Bucket>* out) {
+  const int64_t r = c->stages >= 2 ? c->reduction : 2;
+  const int fusion = c->stages >= 2 ? c->fusion : 0;
+  std::vector<int64_t> blk_off, bnd_off, bnd_n;
+  int64_t off = c->in_dim * st[0].d;  // embed_w first
+  for (size_t s = 0; s < st.size(); ++s) {
+    for (int64_t j = 0; j < st[s].L; ++j) {
+      blk_off.push_back(off);
+      off += st[s].block_size;
+    }
+    if (s + 1 < st.size()) {
+      const int64_t n = r * st[s].d * st[s + 1].d + (fusion == 1 ? 2 * st[s].d * st[s].d : 0);
+      bnd_off.push_back(off);
+      bnd_n.push_back(n);
+      off += n;
+    }
+  }
+  out->clear();
+  out->push_back({off, st.back().d * c->num_classes, 3, 0});
+  for (size_t s = st.size(); s-- > 0;) {
+    for (int64_t j = st[s].L - 1; j >= 0; --j) {
+      const int64_t b = st[s].first + j;
+      out->push_back({blk_off[static_cast<size_t>(b)], st[s].block_size, 1, b});
+    }
+    if (s > 0) out->push_back({bnd_off[s - 1], bnd_n[s - 1], 2, static_cast<int64_t>(s - 1)});
+  }
+  out->push_back({0, c->in_dim * st[0].d, 0, 0});
+}
 }  // namespace
+
+// The gradient buckets of a model config (no device needed): offsets / sizes (floats) in
+// all-reduce order, kinds (0 embed, 1 block, 2 boundary, 3 head). Returns the count, or a
+// negative status when `cap` is too small.
+extern "C" int rp_model_bucket_plan(const RpModelConfig* c, int64_t* offsets, int64_t* sizes,
+                                    int* kinds, int64_t cap) {
+  if (!c) return -rp_fail(RP_ERR_CONTRACT, "null config");
+  std::vector<RpStage> st;
+  const int rc = stage_geoms(c, &st);
+  if (rc != RP_OK) return -rc;
+  std::vector<Bucket> bk;
+  bucket_plan(c, st, &bk);
+  if (cap < static_cast<int64_t>(bk.size()))
+    return -rp_fail(RP_ERR_SHAPE, "bucket plan capacity too small");
+  for (size_t i = 0; i < bk.size(); ++i) {
+    if (offsets) offsets[i] = bk[i].off;
+    if (sizes) sizes[i] = bk[i].n;
+    if (kinds) kinds[i] = bk[i].kind;
+  }
+  return static_cast<int>(bk.size());
+}
 
 // ---------------------------------------------------------------- activation ledger
 // Bytes of activation storage each engine keeps live at its peak (SPEC.md:346-349
@@ -836,40 +1010,66 @@ int stage_geoms(const RpModelConfig* c, std::vector<RpStage>* out) {
 //   mode 1 reprop    every stage's input + output + one block footprint
 //   mode 2 pareprop  reprop + one more block footprint (rendezvous depth 1)
 // Per-block quantities are the largest over the stages (the slots are shared).
+namespace {
+// one stage's ledger quantities (bytes)
+struct StageLedger {
+  int64_t block, cache, store, stash;
+};
+StageLedger stage_ledger(const RpStage& S) {
+  const int64_t T = S.T, d = S.d, h = S.h, H = S.H;
+  const int64_t pair = 2 * T * d * 4;  // one coupled (i1, i2) fp32 pair
+  // block footprint: recomputed input pair + F caches (hF, qkv, att: bf16; lse, LN stats)
+  // + G caches (hG, slope, a: bf16; LN stats)
+  const int64_t cache_f = T * d * 2 + T * 3 * d * 2 + T * d * 2 + T * H * 4 + 2 * T * 4;
+  const int64_t cache_g = T * d * 2 + 2 * T * h * 2 + 2 * T * 4;
+  StageLedger r;
+  r.cache = cache_f + cache_g;
+  r.block = pair + r.cache;
+  r.store = T * d * 4 /* stage input e, shared by i1 = i2 */ + pair /* stage output */;
+  r.stash = T * d * 4 + S.L * pair;  // Vanilla: e + every block's output pair
+  return r;
+}
+struct LedgerTerms {
+  int64_t block = 0, cache = 0, stages = 0, stash = 0, fixed = 0;
+};
+LedgerTerms ledger_terms(const std::vector<RpStage>& st, int fusion) {
+  LedgerTerms t;
+  int64_t cot = 0, temps = 0;
+  for (const RpStage& S : st) {
+    const StageLedger l = stage_ledger(S);
+    const int64_t T = S.T, d = S.d, h = S.h;
+    t.block = std::max(t.block, l.block);
+    t.cache = std::max(t.cache, l.cache);
+    cot = std::max(cot, 2 * T * d * 4 + 2 * T * d * 2);                               // d_out pair
+    temps = std::max(temps, T * h * 2 + 2 * T * d * 2 + T * 3 * d * 2 + T * d * 2);  // du,dh,datt,dqkv,de
+    t.stages += l.store;
+    t.stash += l.stash;
+  }
+  if (st.size() > 1) {  // boundary recompute buffers (fused output, mlp concat)
+    int64_t fb = 0;
+    for (size_t s = 0; s + 1 < st.size(); ++s)
+      fb = std::max(fb, st[s].T * st[s].d * 2 * (fusion == 1 ? 3 : 1));
+    temps += fb;
+  }
+  t.fixed = cot + temps;
+  return t;
+}
+}  // namespace
+
 extern "C" int rp_activation_bytes(const RpModelConfig* c, int mode, int64_t* out_peak,
                                    int64_t* out_block_footprint) {
   if (!c || !out_peak) return rp_fail(RP_ERR_CONTRACT, "null argument");
   if (mode < 0 || mode > 2) return rp_fail(RP_ERR_CONFIG, "mode must be 0, 1 or 2");
   std::vector<RpStage> st;
   RP_TRY(stage_geoms(c, &st));
-  int64_t block = 0, cache = 0, cot = 0, temps = 0, stages = 0, stash = 0;
-  for (const RpStage& S : st) {
-    const int64_t T = S.T, d = S.d, h = S.h, H = S.H;
-    const int64_t pair = 2 * T * d * 4;  // one coupled (i1, i2) fp32 pair
-    // block footprint: recomputed input pair + F caches (hF, qkv, att: bf16; lse, LN stats)
-    // + G caches (hG, slope, a: bf16; LN stats)
-    const int64_t cache_f = T * d * 2 + T * 3 * d * 2 + T * d * 2 + T * H * 4 + 2 * T * 4;
-    const int64_t cache_g = T * d * 2 + 2 * T * h * 2 + 2 * T * 4;
-    block = std::max(block, pair + cache_f + cache_g);
-    cache = std::max(cache, cache_f + cache_g);
-    cot = std::max(cot, 2 * T * d * 4 + 2 * T * d * 2);                               // d_out pair
-    temps = std::max(temps, T * h * 2 + 2 * T * d * 2 + T * 3 * d * 2 + T * d * 2);  // du,dh,datt,dqkv,de
-    stages += T * d * 4 /* stage input e, shared by i1 = i2 */ + pair /* stage output */;
-    stash += T * d * 4 + S.L * pair;
-  }
-  if (st.size() > 1) {  // boundary recompute buffers (fused output, mlp concat)
-    int64_t fb = 0;
-    for (size_t s = 0; s + 1 < st.size(); ++s)
-      fb = std::max(fb, st[s].T * st[s].d * 2 * (c->fusion == 1 ? 3 : 1));
-    temps += fb;
-  }
+  const LedgerTerms t = ledger_terms(st, c->fusion);
   int64_t peak = 0;
   if (mode == 0)
-    peak = stash + cache + cot + temps;
+    peak = t.stash + t.cache + t.fixed;
   else
-    peak = stages + (mode == 2 ? 2 : 1) * block + cot + temps;
+    peak = t.stages + (mode == 2 ? 2 : 1) * t.block + t.fixed;
   *out_peak = peak;
-  if (out_block_footprint) *out_block_footprint = block;
+  if (out_block_footprint) *out_block_footprint = t.block;
   return RP_OK;
 }
 
@@ -930,6 +1130,50 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   g->head_tix = static_cast<int64_t>(g->t_off.size());
   add(g->st.back().d * g->C, 0);
   g->P = g->t_off.back() + g->t_numel.back();
+  {
+    std::vector<Bucket> bk;
+    bucket_plan(c, g->st, &bk);
+    g->bk_block.resize(static_cast<size_t>(g->L));
+    g->bk_bnd.resize(g->st.size());
+    int64_t covered = 0;
+    for (const Bucket& k : bk) {
+      const std::pair<int64_t, int64_t> v{k.off, k.n};
+      covered += k.n;
+      if (k.kind == 0) g->bk_embed = v;
+      if (k.kind == 1) g->bk_block[static_cast<size_t>(k.index)] = v;
+      if (k.kind == 2) g->bk_bnd[static_cast<size_t>(k.index)] = v;
+      if (k.kind == 3) g->bk_head = v;
+    }
+    // the plan must tile the tensor table exactly (every parameter in one bucket)
+    bool ok = covered == g->P && g->bk_head.first == g->t_off[static_cast<size_t>(g->head_tix)];
+    for (int64_t b = 0; b < g->L; ++b)
+      ok = ok && g->bk_block[static_cast<size_t>(b)].first ==
+                     g->t_off[static_cast<size_t>(tix_block(g, b, 0))];
+    for (size_t si = 0; si + 1 < g->st.size(); ++si)
+      ok = ok && g->bk_bnd[si].first == g->t_off[static_cast<size_t>(g->st[si].bnd_tix)];
+    if (!ok) {
+      rp_engine_destroy(g);
+      return rp_fail(RP_ERR_CONTRACT, "engine_create: bucket plan does not tile the parameters");
+    }
+  }
+  {
+    const LedgerTerms lt = ledger_terms(g->st, g->fusion);
+    g->led_fixed = lt.fixed;
+    for (RpStage& St : g->st) {
+      const StageLedger l = stage_ledger(St);
+      St.led_block = l.block;
+      St.led_cache = l.cache;
+      St.led_store = l.store;
+      St.led_stash = l.stash;
+    }
+    int64_t off = 0;
+    for (int64_t b = 0; b < g->L; ++b) {
+      g->trace_off.push_back(off);
+      const RpStage& St = stage_of(g, b);
+      off += 2 * St.T * St.d;
+    }
+    g->trace_off.push_back(off);  // total
+  }
   int rc = RP_OK;
   // Lane G (the critical path) and the comm / optimizer stream get the highest stream
   // priority, lane R the lowest: the block scheduler then fills idle SMs and kernel tails
@@ -954,8 +1198,11 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   g->evFuse.resize(g->st.size());
   for (auto* v : {&g->evR, &g->evG, &g->evBnd, &g->evFuse})
     for (auto& e : *v) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed, &g->evLogits})
+  for (cudaEvent_t* e : {&g->evFwd, &g->evCommDone, &g->evRDone, &g->evEmbed, &g->evLogits,
+                         &g->evCaller})
     cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+  cudaEventCreate(&g->evStepBeg);
+  cudaEventCreate(&g->evStepEnd);
   g->ts.resize(static_cast<size_t>(4 * g->L));
   for (auto& e : g->ts) cudaEventCreate(&e);
   // arena: per-block buffers sized for the largest stage (shared by all stages)
@@ -985,31 +1232,31 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
     }
   }
   splits_ws(g->in, g->st[0].d, g->T);
-  if ((rc = dalloc(g, &g->params, g->P)) || (rc = dalloc(g, &g->grads, g->P)) ||
-      (rc = dalloc(g, &g->pb, g->P)) || (rc = dalloc(g, &g->lr, 1)) ||
+  if ((rc = dalloc(g, &g->params, g->P, 2)) || (rc = dalloc(g, &g->grads, g->P, 2)) ||
+      (rc = dalloc(g, &g->pb, g->P, 2)) || (rc = dalloc(g, &g->lr, 1)) ||
       (rc = dalloc(g, &g->inputs, g->T * g->in)) || (rc = dalloc(g, &g->labels, g->B)))
     return fail(rc);
   for (RpStage& St : g->st) {
     const int64_t n = St.T * St.d;
-    if ((rc = dalloc(g, &St.e, n)) || (rc = dalloc(g, &St.buf1[0], n)) ||
-        (rc = dalloc(g, &St.buf1[1], n)) || (rc = dalloc(g, &St.buf2[0], n)) ||
-        (rc = dalloc(g, &St.buf2[1], n)) || (rc = dalloc(g, &St.buf2[2], n)))
+    if ((rc = dalloc(g, &St.e, n, 1)) || (rc = dalloc(g, &St.buf1[0], n, 1)) ||
+        (rc = dalloc(g, &St.buf1[1], n, 1)) || (rc = dalloc(g, &St.buf2[0], n, 1)) ||
+        (rc = dalloc(g, &St.buf2[1], n, 1)) || (rc = dalloc(g, &St.buf2[2], n, 1)))
       return fail(rc);
   }
   for (Slot& S : g->slot) {
-    if ((rc = dalloc(g, &S.hF, Td)) || (rc = dalloc(g, &S.qkv, 3 * Td)) ||
-        (rc = dalloc(g, &S.att, Td)) || (rc = dalloc(g, &S.hG, Td)) ||
-        (rc = dalloc(g, &S.u, Th)) || (rc = dalloc(g, &S.a, Th)) ||
-        (rc = dalloc(g, &S.lse, TH)) || (rc = dalloc(g, &S.meanF, Tmax)) ||
-        (rc = dalloc(g, &S.rstdF, Tmax)) || (rc = dalloc(g, &S.meanG, Tmax)) ||
-        (rc = dalloc(g, &S.rstdG, Tmax)))
+    if ((rc = dalloc(g, &S.hF, Td, 1)) || (rc = dalloc(g, &S.qkv, 3 * Td, 1)) ||
+        (rc = dalloc(g, &S.att, Td, 1)) || (rc = dalloc(g, &S.hG, Td, 1)) ||
+        (rc = dalloc(g, &S.u, Th, 1)) || (rc = dalloc(g, &S.a, Th, 1)) ||
+        (rc = dalloc(g, &S.lse, TH, 1)) || (rc = dalloc(g, &S.meanF, Tmax, 1)) ||
+        (rc = dalloc(g, &S.rstdF, Tmax, 1)) || (rc = dalloc(g, &S.meanG, Tmax, 1)) ||
+        (rc = dalloc(g, &S.rstdG, Tmax, 1)))
       return fail(rc);
   }
-  if ((rc = dalloc(g, &g->d1, Td)) || (rc = dalloc(g, &g->d2, Td)) ||
-      (rc = dalloc(g, &g->d1b, Td)) || (rc = dalloc(g, &g->d2b, Td)) ||
-      (rc = dalloc(g, &g->du, Th)) || (rc = dalloc(g, &g->dh, Td)) ||
-      (rc = dalloc(g, &g->datt, Td)) || (rc = dalloc(g, &g->dqkv, 3 * Td)) ||
-      (rc = dalloc(g, &g->deb, Td)) || (rc = dalloc(g, &g->ln_ws, ln_ws)) ||
+  if ((rc = dalloc(g, &g->d1, Td, 1)) || (rc = dalloc(g, &g->d2, Td, 1)) ||
+      (rc = dalloc(g, &g->d1b, Td, 1)) || (rc = dalloc(g, &g->d2b, Td, 1)) ||
+      (rc = dalloc(g, &g->du, Th, 1)) || (rc = dalloc(g, &g->dh, Td, 1)) ||
+      (rc = dalloc(g, &g->datt, Td, 1)) || (rc = dalloc(g, &g->dqkv, 3 * Td, 1)) ||
+      (rc = dalloc(g, &g->deb, Td, 1)) || (rc = dalloc(g, &g->ln_ws, ln_ws)) ||
       (rc = dalloc(g, &g->col_ws, col_ws)) || (rc = dalloc(g, &g->split_ws, split_ws)) ||
       (rc = dalloc(g, &g->attn_ws, attn_ws)) ||
       (rc = dalloc(g, &g->pooled, g->B * g->st.back().d)) ||
@@ -1017,8 +1264,8 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
       (rc = dalloc(g, &g->row_loss, g->B)) || (rc = dalloc(g, &g->loss, 1)) ||
       (rc = dalloc(g, &g->dpooled, g->B * g->st.back().d)))
     return fail(rc);
-  if (fb > 0 && ((rc = dalloc(g, &g->fb, fb)) ||
-                 (g->fusion == 1 && (rc = dalloc(g, &g->cb, 2 * fb)))))
+  if (fb > 0 && ((rc = dalloc(g, &g->fb, fb, 1)) ||
+                 (g->fusion == 1 && (rc = dalloc(g, &g->cb, 2 * fb, 1)))))
     return fail(rc);
   if ((rc = build_plans(g))) return fail(rc);
   g->optimizer = c->optimizer;
@@ -1027,7 +1274,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
     g->beta2 = c->beta2;
     g->eps = c->adam_eps;
     g->wd = c->weight_decay;
-    if ((rc = dalloc(g, &g->adam_m, g->P)) || (rc = dalloc(g, &g->adam_v, g->P)) ||
+    if ((rc = dalloc(g, &g->adam_m, g->P, 2)) || (rc = dalloc(g, &g->adam_v, g->P, 2)) ||
         (rc = dalloc(g, &g->step_t, 1)))
       return fail(rc);
     cudaMemset(g->adam_m, 0, static_cast<size_t>(g->P) * 4);
@@ -1060,7 +1307,8 @@ extern "C" void rp_engine_destroy(RpEngine* g) {
   for (auto* v : {&g->evR, &g->evG, &g->ts, &g->evBnd, &g->evFuse})
     for (auto& e : *v)
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed, g->evLogits})
+  for (cudaEvent_t e : {g->evFwd, g->evCommDone, g->evRDone, g->evEmbed, g->evLogits,
+                        g->evCaller, g->evStepBeg, g->evStepEnd})
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {g->sG, g->sR, g->sC, g->sX})
     if (s) cudaStreamDestroy(s);
@@ -1128,12 +1376,20 @@ extern "C" int rp_engine_get_params(RpEngine* g, float* host) {
   return rp_engine_sync(g);
 }
 
+// The gradient of the mean loss over the global batch: after a data-parallel step the
+// buffer holds the all-reduced SUM of the ranks' gradients (the optimizer folds 1 / world
+// into its step), so the host copy is scaled by 1 / world.
 extern "C" int rp_engine_get_grads(RpEngine* g, float* host) {
   if (!g || !host) return rp_fail(RP_ERR_CONTRACT, "null argument");
   RP_TRY(cuda_ok(cudaMemcpyAsync(host, g->grads, static_cast<size_t>(g->P) * 4,
                                  cudaMemcpyDeviceToHost, g->sG),
                  "get_grads"));
-  return rp_engine_sync(g);
+  RP_TRY(rp_engine_sync(g));
+  if (g->world > 1) {
+    const float inv = 1.0f / static_cast<float>(g->world);
+    for (int64_t i = 0; i < g->P; ++i) host[i] *= inv;
+  }
+  return RP_OK;
 }
 
 // inputs: bf16 [B, N, in_dim] (host, ideally pinned), labels int32 [B]; async on the
@@ -1156,8 +1412,10 @@ extern "C" int rp_engine_prefetch_batch(RpEngine* g, const uint16_t* inputs, con
   if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
   if (!g->sX) {
     RP_TRY(cuda_ok(cudaStreamCreateWithFlags(&g->sX, cudaStreamNonBlocking), "stream"));
-    for (cudaEvent_t* e : {&g->evStaged, &g->evStageFree, &g->evLoss})
+    for (cudaEvent_t* e : {&g->evStaged, &g->evStageFree})
       RP_TRY(cuda_ok(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event"));
+    // (evLoss belongs to read_loss_async: created there on first use, never replaced here,
+    // so a recorded loss read-back is not lost)
     RP_TRY(dalloc(g, &g->in_stage, g->T * g->in));
     RP_TRY(dalloc(g, &g->lab_stage, g->B));
   }
@@ -1193,6 +1451,7 @@ extern "C" int rp_engine_wait_loss(RpEngine* g) {
 extern "C" int rp_engine_set_batch_device(RpEngine* g, const uint16_t* inputs,
                                           const int32_t* labels) {
   if (!g || !inputs || !labels) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  RP_TRY(wait_caller(g));
   RP_TRY(cuda_ok(cudaMemcpyAsync(g->inputs, inputs, static_cast<size_t>(g->T * g->in) * 2,
                                  cudaMemcpyDeviceToDevice, g->sG),
                  "set_batch inputs"));
@@ -1217,8 +1476,8 @@ extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
     St.stash_off = n;
     n += St.L * St.T * St.d;
   }
-  RP_TRY(dalloc(g, &g->stash1, n));
-  RP_TRY(dalloc(g, &g->stash2, n));
+  RP_TRY(dalloc(g, &g->stash1, n, 1));
+  RP_TRY(dalloc(g, &g->stash2, n, 1));
   Slot& F = g->slot[0];
   g->vmode = true;
   g->vf_proj.resize(static_cast<size_t>(g->L));
@@ -1301,7 +1560,15 @@ extern "C" int rp_engine_step(RpEngine* g, int mode, int use_graph) {
     RP_TRY(cuda_ok(cudaEventRecord(g->evStageFree, g->sG), "record"));
     g->staged = false;
   }
-  if (!use_graph || g->instrument) return enqueue_step(g, mode);
+  const bool eager = !use_graph || g->instrument || g->trace_fwd || g->trace_rec;
+  g->last_mode = mode;
+  g->step_instrumented = g->instrument && eager;
+  RP_TRY(cuda_ok(cudaEventRecord(g->evStepBeg, g->sG), "record"));
+  g->step_timed = true;
+  if (eager) {
+    RP_TRY(enqueue_step(g, mode));
+    return cuda_ok(cudaEventRecord(g->evStepEnd, g->sG), "record");
+  }
   if (!g->graph[mode]) {
     cudaGraph_t graph = nullptr;
     RP_TRY(cuda_ok(cudaStreamBeginCapture(g->sG, cudaStreamCaptureModeThreadLocal), "capture"));
@@ -1323,7 +1590,8 @@ extern "C" int rp_engine_step(RpEngine* g, int mode, int use_graph) {
     g->graph_kernels[mode] = kernels;
     cudaGraphDestroy(graph);
   }
-  return cuda_ok(cudaGraphLaunch(g->graph[mode], g->sG), "graph launch");
+  RP_TRY(cuda_ok(cudaGraphLaunch(g->graph[mode], g->sG), "graph launch"));
+  return cuda_ok(cudaEventRecord(g->evStepEnd, g->sG), "record");
 }
 
 extern "C" int rp_engine_sync(RpEngine* g) {
@@ -1415,10 +1683,23 @@ extern "C" int rp_engine_comm_init(RpEngine* g, const uint8_t* id128, int world,
   ncclUniqueId id;
   std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
   cudaSetDevice(g->dev);
-  ncclResult_t r = ncclCommInitRank(&g->comm, world, id, rank);
+  // Deterministic all-reduce: one algorithm and protocol for every bucket size (the
+  // ring's reduction order is then fixed, so results repeat run to run and PaReprop equals
+  // Reprop bit for bit at any world size). Caller settings win (setenv does not overwrite);
+  // they must be in place before the process's first NCCL communicator is created.
+  setenv("NCCL_ALGO", "Ring", 0);
+  setenv("NCCL_PROTO", "Simple", 0);
+  // a bounded number of NCCL CTAs, and as many SMs kept free of backward GEMM CTAs
+  const int ctas = g->cfg.comm_ctas > 0 ? g->cfg.comm_ctas : 4;
+  ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+  nc.blocking = 1;
+  nc.minCTAs = std::min(2, ctas);
+  nc.maxCTAs = ctas;
+  ncclResult_t r = ncclCommInitRankConfig(&g->comm, world, id, rank, &nc);
   if (r != ncclSuccess) return rp_fail(RP_ERR_CUDA, ncclGetErrorString(r));
   g->world = world;
   g->rank = rank;
+  g->comm_reserve = world > 1 ? (ctas + 1) / 2 * 2 : 0;  // whole CTA pairs
   for (auto& x : g->graph)
     if (x) {
       cudaGraphExecDestroy(x);
@@ -1433,6 +1714,7 @@ extern "C" int rp_engine_comm_init(RpEngine* g, const uint8_t* id128, int world,
 extern "C" int rp_engine_rev_forward(RpEngine* g, int64_t b, const float* i1, const float* i2,
                                      float* o1, float* o2) {
   if (!g || b < 0 || b >= g->L) return rp_fail(RP_ERR_CONTRACT, "bad engine/block");
+  RP_TRY(wait_caller(g));
   cudaStream_t s = g->sG;
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first;
@@ -1467,6 +1749,7 @@ extern "C" int rp_engine_rev_backward_local(RpEngine* g, int64_t b, const float*
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first;
   if (j < 1) return rp_fail(RP_ERR_CONTRACT, "rev_backward_local: block is its stage's first");
+  RP_TRY(wait_caller(g));
   cudaStream_t s = g->sG;
   const int64_t n = St.T * St.d;
   const size_t bytes = static_cast<size_t>(n) * 4;
@@ -1494,6 +1777,7 @@ extern "C" int rp_engine_rev_inverse(RpEngine* g, int64_t b, const float* o1, co
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first;
   if (j < 1) return rp_fail(RP_ERR_CONTRACT, "rev_inverse: block is its stage's first");
+  RP_TRY(wait_caller(g));
   cudaStream_t s = g->sG;
   const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
   RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, j + 1), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
@@ -1515,6 +1799,7 @@ extern "C" int rp_engine_boundary_forward(RpEngine* g, int64_t stage, const floa
     return rp_fail(RP_ERR_CONTRACT, "boundary_forward: no boundary after this stage");
   RpStage& St = g->st[static_cast<size_t>(stage)];
   const RpStage& Nx = g->st[static_cast<size_t>(stage) + 1];
+  RP_TRY(wait_caller(g));
   cudaStream_t s = g->sG;
   const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
   RP_TRY(cuda_ok(cudaMemcpyAsync(X1(g, St, St.L), o1, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
@@ -1534,6 +1819,7 @@ extern "C" int rp_engine_boundary_vjp(RpEngine* g, int64_t stage, const float* o
     return rp_fail(RP_ERR_CONTRACT, "boundary_vjp: no boundary after this stage");
   RpStage& St = g->st[static_cast<size_t>(stage)];
   const RpStage& Nx = g->st[static_cast<size_t>(stage) + 1];
+  RP_TRY(wait_caller(g));
   cudaStream_t s = g->sG;
   const size_t bytes = static_cast<size_t>(St.T * St.d) * 4;
   const size_t nbytes = static_cast<size_t>(Nx.T * Nx.d) * 4;
@@ -1563,6 +1849,7 @@ int layer_check(RpEngine* g, int64_t b) {
 // attention_forward (layers.cpp:134-169): y = Proj(MHSA(LN(x))), no residual
 extern "C" int rp_engine_attention_forward(RpEngine* g, int64_t b, const float* x, float* y) {
   RP_TRY(layer_check(g, b));
+  RP_TRY(wait_caller(g));
   RpStage& St = stage_of(g, b);
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   Slot& F = g->slot[0];
@@ -1592,6 +1879,7 @@ extern "C" int rp_engine_attention_forward(RpEngine* g, int64_t b, const float* 
 // mlp_forward (layers.cpp:222-239): y = W2 gelu(W1 LN(x) + b1) + b2, no residual
 extern "C" int rp_engine_mlp_forward(RpEngine* g, int64_t b, const float* x, float* y) {
   RP_TRY(layer_check(g, b));
+  RP_TRY(wait_caller(g));
   RpStage& St = stage_of(g, b);
   BlockPlans& p = g->plans[static_cast<size_t>(b)];
   Slot& F = g->slot[0];
@@ -1627,6 +1915,7 @@ extern "C" int rp_engine_mlp_forward(RpEngine* g, int64_t b, const float* x, flo
 extern "C" int rp_engine_attention_vjp(RpEngine* g, int64_t b, const float* x, const float* d_y,
                                        float* d_x) {
   RP_TRY(layer_check(g, b));
+  RP_TRY(wait_caller(g));
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first, n = St.T * St.d;
   cudaStream_t s = g->sG;
@@ -1647,6 +1936,7 @@ extern "C" int rp_engine_attention_vjp(RpEngine* g, int64_t b, const float* x, c
 extern "C" int rp_engine_mlp_vjp(RpEngine* g, int64_t b, const float* x, const float* d_y,
                                  float* d_x) {
   RP_TRY(layer_check(g, b));
+  RP_TRY(wait_caller(g));
   RpStage& St = stage_of(g, b);
   const int64_t j = b - St.first, n = St.T * St.d;
   cudaStream_t s = g->sG;
@@ -1660,4 +1950,59 @@ extern "C" int rp_engine_mlp_vjp(RpEngine* g, int64_t b, const float* x, const f
   RP_TRY(vjp_g(g, b, s, true));
   RP_TRY(cuda_ok(cudaMemcpyAsync(d_x, g->d2, bytes, cudaMemcpyDeviceToDevice, s), "copy"));
   return rp_engine_sync(g);
+}
+
+// ---------------------------------------------------------------- stream contract, trace, stats
+extern "C" int rp_engine_set_caller_stream(RpEngine* g, rp_stream_t stream) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  g->caller = static_cast<cudaStream_t>(stream);
+  return RP_OK;
+}
+
+extern "C" int64_t rp_engine_trace_floats(const RpEngine* g) {
+  return g ? g->trace_off.back() : -1;
+}
+
+extern "C" int rp_engine_set_trace(RpEngine* g, float* fwd, float* rec) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  g->trace_fwd = fwd;
+  g->trace_rec = rec;
+  return RP_OK;
+}
+
+// StepStats of the last step: waits for it. wall_ns: device time between
+// events recorded on the engine stream before and after the step; lane_busy_ns: sum of the
+// lane's block slots (instrumented steps only, else -1); ledger peak / events and
+// blocks_processed from the step's schedule; arena bytes as allocated.
+extern "C" int rp_engine_step_stats(RpEngine* g, RpStepStats* out) {
+  if (!g || !out) return rp_fail(RP_ERR_CONTRACT, "null argument");
+  if (!g->step_timed) return rp_fail(RP_ERR_CONTRACT, "step_stats: no step has run");
+  RP_TRY(rp_engine_sync(g));
+  std::memset(out, 0, sizeof(*out));
+  RP_TRY(cuda_ok(cudaMemcpy(&out->loss, g->loss, sizeof(float), cudaMemcpyDeviceToHost), "loss"));
+  float ms = 0.f;
+  RP_TRY(cuda_ok(cudaEventElapsedTime(&ms, g->evStepBeg, g->evStepEnd), "elapsed"));
+  out->wall_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+  const int m = g->last_mode;
+  out->mode = m;
+  out->peak_activation_bytes = g->led_peak_m[m];
+  out->ledger_events = g->led_events_m[m];
+  out->blocks_processed = g->blocks_m[m];
+  out->lane_busy_ns[0] = out->lane_busy_ns[1] = -1;
+  if (g->step_instrumented) {
+    for (int lane = 0; lane < 2; ++lane) {
+      double busy = 0.0;
+      for (int64_t b = 0; b < g->L; ++b) {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, g->ts[static_cast<size_t>(((lane * g->L) + b) * 2)],
+                             g->ts[static_cast<size_t>(((lane * g->L) + b) * 2 + 1)]);
+        busy += x;
+      }
+      out->lane_busy_ns[lane] = static_cast<int64_t>(busy * 1e6);
+    }
+  }
+  out->arena_activation_bytes = g->arena_bytes[1];
+  out->arena_param_bytes = g->arena_bytes[2];
+  out->arena_total_bytes = g->arena_bytes[0] + g->arena_bytes[1] + g->arena_bytes[2];
+  return RP_OK;
 }

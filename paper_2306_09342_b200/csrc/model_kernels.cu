@@ -92,10 +92,12 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
   pdl_trigger();
   pdl_wait();
 
-  const float step = lr[0] * scale;
+  // explicit roundings (no FMA contraction): p - (lr * scale) * g exactly as the fp32
+  // formula reads, so the update is bit-reproducible on the host
+  const float step = __fmul_rn(lr[0], scale);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float v = p[i] - step * g[i];
+    const float v = __fsub_rn(p[i], __fmul_rn(step, g[i]));
     p[i] = v;
     pb[i] = __float2bfloat16_rn(v);
   }
@@ -111,7 +113,10 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
   pdl_wait();
   const float step = lr[0];
   const float tt = t[0];
-  const float c1 = 1.0f / (1.0f - powf(b1, tt)), c2 = 1.0f / (1.0f - powf(b2, tt));
+  // torch.optim.AdamW's order of operations (decay first, then the bias-corrected step):
+  // p *= 1 - lr wd; p -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps)
+  const float bc1 = 1.0f - powf(b1, tt), bc2s = sqrtf(1.0f - powf(b2, tt));
+  const float step_size = step / bc1, decay = 1.0f - step * wd;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float gi = g[i] * scale;
@@ -119,8 +124,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
     m[i] = mi;
     v[i] = vi;
-    const float upd = (mi * c1) / (sqrtf(vi * c2) + eps) + wd * p[i];
-    const float pv = p[i] - step * upd;
+    const float pv = p[i] * decay - step_size * (mi / (sqrtf(vi) / bc2s + eps));
     p[i] = pv;
     pb[i] = __float2bfloat16_rn(pv);
   }

@@ -26,7 +26,8 @@ class ModelConfigC(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
                 ("weight_decay", C.c_float), ("stages", C.c_int64),
                 ("stage_depth", C.c_int64 * 8), ("stage_width", C.c_int64 * 8),
-                ("stage_heads", C.c_int64 * 8), ("reduction", C.c_int64), ("fusion", C.c_int)]
+                ("stage_heads", C.c_int64 * 8), ("reduction", C.c_int64), ("fusion", C.c_int),
+                ("comm_ctas", C.c_int)]
 
 
 @dataclass
@@ -58,6 +59,7 @@ class ModelConfig:
     stage_heads: tuple | None = None
     reduction: int = 2
     fusion: str = "average"
+    comm_ctas: int = 0          # NCCL CTAs per all-reduce (0 = 4), SMs reserved for them
 
     def __post_init__(self):
         if self.depths:
@@ -131,7 +133,35 @@ _API = {
     "rp_engine_mlp_vjp": (_I, [_P, _I64, _P, _P, _P]),
     "rp_engine_boundary_forward": (_I, [_P, _I64, _P, _P, _P]),
     "rp_engine_boundary_vjp": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P]),
+    "rp_engine_step_stats": (_I, [_P, _P]),
+    "rp_engine_set_caller_stream": (_I, [_P, _P]),
+    "rp_engine_trace_floats": (_I64, [_P]),
+    "rp_engine_set_trace": (_I, [_P, _P, _P]),
+    "rp_model_bucket_plan": (_I, [C.POINTER(ModelConfigC), _P, _P, _P, _I64]),
 }
+
+
+class StepStatsC(C.Structure):
+    _fields_ = [("loss", C.c_float), ("mode", C.c_int), ("wall_ns", C.c_int64),
+                ("peak_activation_bytes", C.c_int64), ("lane_busy_ns", C.c_int64 * 2),
+                ("blocks_processed", C.c_int64), ("ledger_events", C.c_int64),
+                ("arena_activation_bytes", C.c_int64), ("arena_param_bytes", C.c_int64),
+                ("arena_total_bytes", C.c_int64)]
+
+
+@dataclass
+class StepStats:
+    """SPEC.md:350-353 (plus the ledger event count and the arena's real allocations)."""
+    loss: float
+    mode: int
+    wall_ns: int
+    peak_activation_bytes: int
+    lane_busy_ns: tuple
+    blocks_processed: int
+    ledger_events: int
+    arena_activation_bytes: int
+    arena_param_bytes: int
+    arena_total_bytes: int
 _bound = {}
 
 
@@ -262,6 +292,28 @@ class Engine:
     def step(self, mode=REPROP, graph=True):
         check(api("rp_engine_step")(self._h, mode, int(graph)), "step")
 
+    def step_stats(self) -> "StepStats":
+        """StepStats of the last step (waits for it)."""
+        st = StepStatsC()
+        check(api("rp_engine_step_stats")(self._h, C.byref(st)), "step_stats")
+        return StepStats(st.loss, st.mode, st.wall_ns, st.peak_activation_bytes,
+                         tuple(st.lane_busy_ns), st.blocks_processed, st.ledger_events,
+                         st.arena_activation_bytes, st.arena_param_bytes, st.arena_total_bytes)
+
+    def set_caller_stream(self, stream_ptr: int):
+        """Stream whose prior work the block / layer entry points wait for (default: the
+        legacy default stream)."""
+        check(api("rp_engine_set_caller_stream")(self._h, C.c_void_p(stream_ptr)),
+              "set_caller_stream")
+
+    def trace_floats(self) -> int:
+        return int(api("rp_engine_trace_floats")(self._h))
+
+    def set_trace(self, fwd_ptr: int, rec_ptr: int):
+        """Recompute trace buffers (device pointers, trace_floats() floats each; 0 = off)."""
+        check(api("rp_engine_set_trace")(self._h, C.c_void_p(fwd_ptr or None),
+                                         C.c_void_p(rec_ptr or None)), "set_trace")
+
     def sync(self):
         check(api("rp_engine_sync")(self._h), "sync")
 
@@ -293,6 +345,11 @@ class Engine:
         return out
 
     def comm_init(self, uid: bytes, world: int, rank: int):
+        """Join the data-parallel group (rp_engine_comm_init). The NCCL algorithm / protocol
+        are pinned for a deterministic reduction order unless already set."""
+        import os
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         check(api("rp_engine_comm_init")(self._h, buf, world, rank), "comm_init")
 
@@ -344,6 +401,7 @@ def _cfg_c(cfg: "ModelConfig") -> ModelConfigC:
                      cfg.num_classes, cfg.batch, cfg.window, cfg.seed, cfg.device, cfg.r_ctas,
                      cfg.g_ctas, cfg.lane_priority, cfg.optimizer, cfg.beta1, cfg.beta2,
                      cfg.adam_eps, cfg.weight_decay)
+    c.comm_ctas = cfg.comm_ctas
     if cfg.depths:
         if not (len(cfg.depths) == len(cfg.widths) == len(cfg.stage_heads) <= 8):
             raise _capi.ConfigError("depths / widths / stage_heads: same length, at most 8")
@@ -379,6 +437,21 @@ def probe_max_batch(cfg: "ModelConfig", mode: int, budget_bytes: int) -> int:
     while activation_bytes(replace(cfg, batch=2 * b), mode)[0] <= budget_bytes:
         b *= 2
     return b
+
+
+def bucket_plan(cfg: "ModelConfig"):
+    """The engine's data-parallel gradient buckets in all-reduce order:
+    [(offset, size, kind)] with kind 'embed' | 'block' | 'boundary' | 'head'."""
+    cap = cfg.depth + 16
+    off = np.zeros(cap, np.int64)
+    n = np.zeros(cap, np.int64)
+    k = np.zeros(cap, np.int32)
+    c = _cfg_c(cfg)
+    cnt = api("rp_model_bucket_plan")(C.byref(c), _np_ptr(off), _np_ptr(n), _np_ptr(k), cap)
+    if cnt < 0:
+        check(-cnt, "bucket_plan")
+    names = ("embed", "block", "boundary", "head")
+    return [(int(off[i]), int(n[i]), names[k[i]]) for i in range(cnt)]
 
 
 def nccl_unique_id() -> bytes:

@@ -1,0 +1,61 @@
+"""GPU parity at the benchmarked and north-star depths (SPEC.md:497 reconstruction,
+SURVEY.md §7 hard part 4): RevViT-Ti depth 12 batch 8 (BASELINE configs[0]), RevViT-B depth
+12, RevViT-L depth 24, RevViT-G48 depth 48 (head_dim 104) against the f64 oracle, with the
+per-block reconstruction error of the recomputed block inputs against the forward's
+(= the Vanilla engine's stored) inputs. Tolerances are stated in tests/depth_parity.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import depth_parity as DP  # noqa: E402  (tests/ is on sys.path under pytest)
+
+
+@pytest.mark.parametrize("case", list(DP.CASES))
+def test_depth_parity(case):
+    r = DP.run_case(case)
+    assert r["stats"]["blocks_processed"] == r["depth"]
+    assert r["loss_rel"] < DP.TOL_LOSS, r["loss_rel"]
+    bad = [(x["block"], x["rec"]) for x in r["blocks"] if x["rec"] > DP.TOL_REC]
+    assert not bad, ("reconstruction", bad)
+    bad = [(x["block"], x["fwd"]) for x in r["blocks"] if x["fwd"] > DP.TOL_FWD]
+    assert not bad, ("forward", bad)
+    assert r["grad_worst"] < DP.TOL_GRAD, (r["grad_worst_tensor"], r["grad_worst"])
+    assert r["grad_l2"] < DP.TOL_L2, r["grad_l2"]
+
+
+def test_forward_trace_is_the_vanilla_stash():
+    """The forward trace the reconstruction is measured against is exactly what the Vanilla
+    engine stores: Vanilla's stored block inputs equal the Reprop
+    forward's bit for bit, and Vanilla's gradients (stored X) match Reprop's (recomputed X)
+    within the stated tolerance."""
+    from paper_2306_09342_b200.engine import REPROP, VANILLA, Engine, ModelConfig, bf16_bits
+    from oracle import revprop_oracle as O
+    geo, batch = DP.CASES["b-d12-b2"]
+    cfg = ModelConfig(**geo, **DP.COMMON, batch=batch)
+    mc = O.ModelConfig(cfg.depth, cfg.width, cfg.heads, cfg.hidden, cfg.seq_len, cfg.in_dim,
+                       cfg.num_classes)
+    eng = Engine(cfg)
+    x, lab = O.synthetic_batch(mc, batch, seed=11)
+    eng.set_batch(bf16_bits(x), lab)
+    eng.set_lr(0.0)
+    eng.enable_vanilla()
+    nf = eng.trace_floats()
+    out = {}
+    for mode in (VANILLA, REPROP):
+        tf = torch.zeros(nf, device="cuda")
+        tr = torch.zeros(nf, device="cuda")
+        eng.set_trace(tf.data_ptr(), tr.data_ptr())
+        eng.step(mode, graph=False)
+        out[mode] = (tf.cpu().numpy(), tr.cpu().numpy(), eng.grads(), eng.loss())
+        eng.set_trace(0, 0)
+    fv, rv, gv, lv = out[VANILLA]
+    fr, rr, gr, lr_ = out[REPROP]
+    np.testing.assert_array_equal(fv, fr)      # same forward kernels, same stored X
+    np.testing.assert_array_equal(rv, fv)      # Vanilla's backward reads the stash itself
+    assert DP.maxrel(rr, fv) < DP.TOL_REC      # Reprop's reconstruction vs the stash
+    assert abs(lv - lr_) == 0.0
+    assert float(np.linalg.norm(gr - gv) / np.linalg.norm(gv)) < 1e-3
+    eng.close()

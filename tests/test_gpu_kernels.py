@@ -245,13 +245,29 @@ def attn_ref(qkv, B, N, H, hd=64):
     return o.permute(0, 2, 1, 3).reshape(B * N, H * hd), torch.logsumexp(s, -1)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2], ids=["tcgen05", "mma_sync", "tcgen05_2pass"])
+@pytest.fixture(params=[0, 1, 2], ids=["tcgen05", "mma_sync", "tcgen05_2pass"])
+def impl(request):
+    """The process-global attention implementation switch, restored whatever the test
+    does (a failed assertion must not leave impl 1 / 2 active for later tests)."""
+    from paper_2306_09342_b200 import _capi
+    _capi.check(_capi.lib().rp_set_attention_impl(request.param), "set_attention_impl")
+    try:
+        yield request.param
+    finally:
+        _capi.lib().rp_set_attention_impl(0)
+
+
+def test_attention_impl_switch_validates():
+    from paper_2306_09342_b200 import _capi
+    assert _capi.lib().rp_set_attention_impl(3) == 3  # RP_ERR_CONFIG
+    assert _capi.lib().rp_set_attention_impl(-1) == 3
+    assert _capi.lib().rp_set_attention_impl(0) == 0
+
+
 @pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3), (2, 300, 2), (1, 480, 3), (3, 768, 1),
-                                   (3, 256, 2), (2, 129, 1), (3, 1, 2), (2, 2, 1), (1, 17, 1),
+                                   (3, 256, 2), (2, 129, 1), (3, 1, 2), (8, 2, 4), (1, 17, 1),
                                    (4, 257, 1)])
 def test_attention_fwd_bwd(K, B, N, H, impl):
-    from paper_2306_09342_b200 import _capi
-    _capi.lib().rp_set_attention_impl(impl)
     torch.manual_seed(7919 * B + 131 * N + H)  # inputs fixed per case (order-independent)
     qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
     out, lse = K.attention_fwd(qkv, B, N, H)
@@ -270,13 +286,15 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
             # of dP - D, bounded relative to the whole gradient
             assert (dqkv[:, sl].float() - g[:, sl]).abs().max() < 1e-3 * g.abs().max(), name
         else:
-            # N = 2: dS of a row is (+x, -x), x = P0 (dP0 - D) = P0 P1 (dP0 - dP1) evaluated as a
-            # cancellation against D = rowsum(dO * O) from the bf16-stored O (the flash-style
-            # backward), then rounded to bf16 for the tensor core; dq = x (k0 - k1) carries
-            # that error undamped (2.6 % seen on unseeded inputs), so two keys get 4 %
-            assert rel(dqkv[:, sl], g[:, sl]) < (4e-2 if N == 2 else 2e-2), name
+            # N = 2, q and k only: dS of a row is (+x, -x), x = P0 (dP0 - D) = P0 P1 (dP0 - dP1)
+            # evaluated as a cancellation against D = rowsum(dO * O) from the bf16-stored O
+            # (the flash-style backward), then rounded to bf16 for the tensor core; dq =
+            # x (k0 - k1) and dk carry that error undamped (2.6 % seen on unseeded inputs), so
+            # they get 4 %; dv = P^T dO does not involve D and keeps 2 %. The case runs 64
+            # query rows (B H N) so the max-relative metric is not decided by one row.
+            tol = 4e-2 if (N == 2 and name != "v") else 2e-2
+            assert rel(dqkv[:, sl], g[:, sl]) < tol, name
     assert torch.equal(dqkv, K.attention_bwd(qkv, out, lse, dout, B, N, H))
-    _capi.lib().rp_set_attention_impl(0)
 
 
 @pytest.mark.parametrize("bn", [256, 128, 512])

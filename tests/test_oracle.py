@@ -285,13 +285,34 @@ def test_sgd_descent_oracle():
 
 
 # ---------------------------------------------------------------- data parallel (gloo)
-def _dp_worker(rank, world, port, q):
+# (widths / hidden multiples of 64, head_dim a multiple of 8: the engine's constraints)
+DP_ISO = dict(depth=2, width=64, heads=2, hidden=128, seq_len=8, in_dim=16, num_classes=5)
+DP_HIER = dict(depth=4, width=64, heads=2, hidden=128, seq_len=32, in_dim=16, num_classes=5,
+               window=4, depths=(1, 2, 1), widths=(64, 128, 192), stage_heads=(2, 4, 6),
+               reduction=4, fusion="mlp")
+
+
+def _engine_cfg(kw):
+    from paper_2306_09342_b200.engine import ModelConfig
+    kw = dict(kw)
+    return ModelConfig(**kw)
+
+
+def _dp_worker(rank, world, port, kw, q):
+    try:
+        _dp_work(rank, world, port, kw, q)
+    except Exception as ex:  # report instead of leaving the parent waiting on the queue
+        q.put((rank, repr(ex), None, None))
+
+
+def _dp_work(rank, world, port, kw, q):
     import sys
     sys.path.insert(0, os.path.dirname(HERE))
     import torch
     import torch.distributed as dist
     from oracle import revprop_oracle as O2
-    mc = O2.ModelConfig(2, 16, 2, 32, 8, 16, 5)
+    from paper_2306_09342_b200.engine import bucket_plan
+    mc = O2.ModelConfig(**kw)
     p = O2.init_params(mc, 3)
     x, lab = O2.synthetic_batch(mc, 4, seed=8)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
@@ -299,18 +320,29 @@ def _dp_worker(rank, world, port, q):
     shard = slice(rank * x.shape[0] // world, (rank + 1) * x.shape[0] // world)
     r = O2.step(mc, p, x[shard], lab[shard])
     g = torch.from_numpy(r.grads.copy())
-    dist.all_reduce(g)  # the engine's per-block ncclAllReduce(sum) ...
-    g /= world  # ... with 1/world folded into the SGD step
-    q.put((rank, g.numpy()))
+    # the engine's own bucket plan (rp_model_bucket_plan, the function its step enqueues
+    # from): one all-reduce (sum) per bucket in the engine's issue order ...
+    plan = bucket_plan(_engine_cfg(kw))
+    for off, n, _ in plan:
+        sl = g[off:off + n]
+        dist.all_reduce(sl)
+        g[off:off + n] = sl
+    # ... then that bucket's SGD step with 1/world folded in (engine.cpp bucket_update)
+    lr = 0.5
+    p_new = p - (lr * (1.0 / world)) * g.numpy()
+    q.put((rank, g.numpy() / world, p_new, plan))
     dist.destroy_process_group()
 
 
-def test_data_parallel_decomposition_gloo():
-    """The N>1 path's math on world_size 2 (gloo, two processes): the mean over ranks of
-    per-shard gradients equals the full-batch gradient."""
+@pytest.mark.parametrize("kw", [DP_ISO, DP_HIER], ids=["isotropic", "hierarchical"])
+def test_data_parallel_buckets_gloo(kw):
+    """The N>1 path on world_size 2 (gloo, two processes) with the engine's bucket plan: the
+    buckets tile the parameter vector exactly once, the per-bucket all-reduced mean of the
+    per-shard gradients equals the full-batch gradient, and both ranks end with identical
+    parameters equal to full-batch SGD."""
     import multiprocessing as mp
     import socket
-    mc = O.ModelConfig(2, 16, 2, 32, 8, 16, 5)
+    mc = O.ModelConfig(**kw)
     p = O.init_params(mc, 3)
     x, lab = O.synthetic_batch(mc, 4, seed=8)
     full = O.step(mc, p, x, lab).grads
@@ -320,13 +352,25 @@ def test_data_parallel_decomposition_gloo():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_dp_worker, args=(r, 2, port, kw, q)) for r in range(2)]
     for pr in ps:
         pr.start()
-    out = dict(q.get(timeout=120) for _ in range(2))
+    out = {}
+    for _ in range(2):
+        rk, g, pn, plan = q.get(timeout=180)
+        assert plan is not None, g
+        out[rk] = (g, pn, plan)
     for pr in ps:
         pr.join(timeout=60)
-    assert rel(out[0], full) < 1e-12 and np.array_equal(out[0], out[1])
+    plan = out[0][2]
+    cover = np.zeros(p.size, np.int64)
+    for off, n, _ in plan:
+        cover[off:off + n] += 1
+    assert np.all(cover == 1)
+    assert [k for _, _, k in plan][0] == "head" and plan[-1][2] == "embed"
+    assert rel(out[0][0], full) < 1e-12 and np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert rel(out[0][1], p - 0.5 * full) < 1e-12
 
 
 # ---------------------------------------------------------------- hierarchical (Rev-Swin) path
