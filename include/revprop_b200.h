@@ -95,6 +95,10 @@ typedef struct RpGemmDesc {
                          rp_colsum_parts (the MLP hidden-bias gradient, layers.cpp:38-52) */
   float* rowdot;    /* RP_EPI_ROWDOT output */
   int64_t rd_seq;   /* RP_EPI_ROWDOT: rows per sequence (tokens per attention window) */
+  float quantum;    /* RP_EPI_RESID / RP_EPI_F32 (no split-K): round acc (+ bias) to a multiple of
+                       this power of two before the store / residual add (0 = off). With the
+                       residual on the same grid the coupling's fp32 add and subtract are exact
+                       (see RpModelConfig.exact_coupling_bits). */
 } RpGemmDesc;
 
 typedef struct RpGemmPlan RpGemmPlan;
@@ -203,6 +207,15 @@ typedef struct RpModelConfig {
    * free for them, so bucket all-reduces overlap the backward instead of queueing behind
    * the persistent GEMM grids. */
   int comm_ctas;
+  /* Exact coupling (0 = default 17; -1 = off): F's and G's outputs (and the embedding /
+   * patch-merge outputs that start a stage) are rounded to multiples of 2^-bits in their
+   * GEMM epilogues, so every residual-stream value is on that grid and the fp32
+   * o2 = i2 + F(i1), o1 = i1 + G(o2) and the inverse's subtractions are exact while
+   * |X| < 2^(24 - bits) (128 at 17). The inverse then reconstructs every block input bit
+   * for bit at any depth (the recompute sees the forward's exact inputs, so its bf16 GEMM
+   * operands round identically), instead of compounding fp32 round-trip error through the
+   * bf16 roundings. Cost: one rounding of at most 2^-(bits+1) per coupling add. */
+  int exact_coupling_bits;
 } RpModelConfig;
 
 /* Ledger-predicted peak activation bytes of an engine (mode 0 vanilla, 1 reprop,

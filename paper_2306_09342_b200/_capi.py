@@ -67,6 +67,7 @@ class GemmDesc(C.Structure):
         ("max_ctas", C.c_int), ("bn", C.c_int),
         ("colsum_part", C.c_void_p),
         ("rowdot", C.c_void_p), ("rd_seq", C.c_int64),
+        ("quantum", C.c_float),
     ]
 
 

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -206,6 +207,7 @@ struct RpEngine {
   std::pair<int64_t, int64_t> bk_head{0, 0}, bk_embed{0, 0};
   std::vector<std::pair<int64_t, int64_t>> bk_block, bk_bnd;
   int comm_reserve = 0;  // SMs kept free of GEMM CTAs for the NCCL kernels (world > 1)
+  float quantum = 0.f;   // exact-coupling grid 2^-bits of the residual stream (0 = off)
 };
 
 namespace {
@@ -280,6 +282,7 @@ struct GemmArgs {
   float* colsum_part = nullptr;
   float* rowdot = nullptr;
   int64_t rd_seq = 0;
+  float quantum = 0.f;  // exact-coupling grid of a residual-stream output
 };
 
 // the tcgen05 attention backward with the stored dS^T (head_dim 64, <= 256 tokens per
@@ -311,6 +314,7 @@ int mk_plan(RpEngine* g, const GemmArgs& a, RpGemmPlan** out) {
   d.colsum_part = a.colsum_part;
   d.rowdot = a.rowdot;
   d.rd_seq = a.rd_seq;
+  d.quantum = a.quantum;
   d.max_ctas = 0;
   d.bn = gemm_bn(a.N);
   int rc = rp_gemm_plan_create(&d, out);
@@ -355,6 +359,7 @@ int build_plans(RpEngine* g) {
       {
         GemmArgs a{F.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, St, j + 1), d};
         a.aux = X2(g, St, j);
+        a.quantum = g->quantum;
         RP_TRY(mk_plan(g, a, &p.f_proj));
       }
       {
@@ -366,6 +371,7 @@ int build_plans(RpEngine* g) {
         GemmArgs a{F.a, h, 0, W2, d, 1, T, d, h, RP_EPI_RESID, X1(g, St, j + 1), d};
         a.aux = X1(g, St, j);
         a.bias = b2;
+        a.quantum = g->quantum;
         RP_TRY(mk_plan(g, a, &p.f_w2));
       }
       // ---- lane R: inverse with caches
@@ -382,10 +388,12 @@ int build_plans(RpEngine* g) {
         a.aux = X1(g, St, j + 1);
         a.bias = b2;
         a.sign = -1.f;
+        a.quantum = g->quantum;
         RP_TRY(mk_plan(g, a, &p.r_w2));
         GemmArgs c{S.att, d, 0, Wout, d, 1, T, d, d, RP_EPI_RESID, X2(g, St, j), d};
         c.aux = X2(g, St, j + 1);
         c.sign = -1.f;
+        c.quantum = g->quantum;
         RP_TRY(mk_plan(g, c, &p.r_proj));
       }
       // ---- lane G: VJPs (layers.cpp:171-220, 241-259)
@@ -443,7 +451,11 @@ int build_plans(RpEngine* g) {
         RP_TRY(mk_plan(g, {g->cb, 2 * d, 0, wb(g, St.bnd_tix + 1), d, 1, T, d, 2 * d, RP_EPI_BF16,
                            g->fb, d},
                        &St.b_fuse));
-      RP_TRY(mk_plan(g, {g->fb, rd, 0, Mw, dn, 1, Tn, dn, rd, RP_EPI_F32, Nx.e, dn}, &St.b_merge));
+      {
+        GemmArgs a{g->fb, rd, 0, Mw, dn, 1, Tn, dn, rd, RP_EPI_F32, Nx.e, dn};
+        a.quantum = g->quantum;  // the next stage's input starts on the grid
+        RP_TRY(mk_plan(g, a, &St.b_merge));
+      }
       // d_f = d_y . merge_w^T  ([Tn, r d] == [T, d] row-major): fp32 into d1 (average
       // fusion: d_i1 = d_i2 = d_f / 2 next), bf16 into datt (mlp: the operand of two GEMMs)
       if (g->fusion == 1)
@@ -474,9 +486,11 @@ int build_plans(RpEngine* g) {
   }
   // embedding: e = x . embed_w ; d_embed_w = x^T . (d_i1 + d_i2)
   const RpStage& S0 = g->st[0];
-  RP_TRY(mk_plan(g, {g->inputs, g->in, 0, wb(g, 0), S0.d, 1, g->T, S0.d, g->in, RP_EPI_F32, S0.e,
-                     S0.d},
-                 &g->p_embed));
+  {
+    GemmArgs a{g->inputs, g->in, 0, wb(g, 0), S0.d, 1, g->T, S0.d, g->in, RP_EPI_F32, S0.e, S0.d};
+    a.quantum = g->quantum;  // the residual stream starts on the exact-coupling grid
+    RP_TRY(mk_plan(g, a, &g->p_embed));
+  }
   {
     GemmArgs a{g->inputs, g->in, 1, g->deb, S0.d, 1, g->in, S0.d, g->T, RP_EPI_F32, gr(g, 0), S0.d};
     a.splits = pick_splits(g->in, S0.d, g->T, gemm_bn(S0.d));
@@ -1267,6 +1281,11 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   if (fb > 0 && ((rc = dalloc(g, &g->fb, fb, 1)) ||
                  (g->fusion == 1 && (rc = dalloc(g, &g->cb, 2 * fb, 1)))))
     return fail(rc);
+  {
+    const int bits = c->exact_coupling_bits == 0 ? 17 : c->exact_coupling_bits;
+    if (bits > 0 && bits > 60) return fail(rp_fail(RP_ERR_CONFIG, "exact_coupling_bits too large"));
+    g->quantum = bits > 0 ? std::ldexp(1.0f, -bits) : 0.f;
+  }
   if ((rc = build_plans(g))) return fail(rc);
   g->optimizer = c->optimizer;
   if (c->optimizer == 1) {
@@ -1488,12 +1507,14 @@ extern "C" int rp_engine_enable_vanilla(RpEngine* g) {
     GemmArgs a{F.att, d, 0, wb(g, tix_block(g, b, kWout)), d, 1, T, d, d, RP_EPI_RESID,
                X2(g, St, j + 1), d};
     a.aux = X2(g, St, j);
+    a.quantum = g->quantum;
     int rc = mk_plan(g, a, &g->vf_proj[static_cast<size_t>(b)]);
     if (rc == RP_OK) {
       GemmArgs c{F.a, h, 0, wb(g, tix_block(g, b, kW2)), d, 1, T, d, h, RP_EPI_RESID,
                  X1(g, St, j + 1), d};
       c.aux = X1(g, St, j);
       c.bias = wf(g, tix_block(g, b, kB2));
+      c.quantum = g->quantum;
       rc = mk_plan(g, c, &g->vf_w2[static_cast<size_t>(b)]);
     }
     if (rc != RP_OK) {

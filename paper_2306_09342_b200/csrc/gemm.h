@@ -18,5 +18,8 @@ struct GemmEpi {
   float* rowdot;   // RP_EPI_ROWDOT: per-(row, 64-column head) dot of the bf16 output with aux
   int64_t rd_seq;  // rows per sequence
   int64_t rd_heads;
+  // RP_EPI_RESID / RP_EPI_F32: round the GEMM result (+ bias) to a multiple of quant (a power
+  // of two; 0 = off) before it is stored / added to the residual: the exact-coupling grid
+  float quant, inv_quant;
 };
 }  // namespace rp

@@ -278,6 +278,10 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
     stage_emit<TMA>(b, ring, lane, static_cast<__nv_bfloat16*>(ep.out) + col, ep.ldo * 2, row0,
                     rows_left, tmO, col);
   } else if constexpr (EPI == RP_EPI_F32) {
+    if (ep.quant > 0.f) {  // a residual-stream start (embedding / patch merge) on the grid
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = rintf(v[i] * ep.inv_quant) * ep.quant;
+    }
     stage_rows_f32(st, lane, v);
     __syncwarp();
     store_tile(st, lane,
@@ -316,10 +320,21 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, const GemmShap
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float4 bb = b4 ? __ldg(b4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[4 * c] = __uint_as_float(rr[c].x) + s * (v[4 * c] + bb.x);
-      v[4 * c + 1] = __uint_as_float(rr[c].y) + s * (v[4 * c + 1] + bb.y);
-      v[4 * c + 2] = __uint_as_float(rr[c].z) + s * (v[4 * c + 2] + bb.z);
-      v[4 * c + 3] = __uint_as_float(rr[c].w) + s * (v[4 * c + 3] + bb.w);
+      v[4 * c] += bb.x;
+      v[4 * c + 1] += bb.y;
+      v[4 * c + 2] += bb.z;
+      v[4 * c + 3] += bb.w;
+    }
+    if (ep.quant > 0.f) {  // exact-coupling grid: the sum below is then exact in fp32
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = rintf(v[i] * ep.inv_quant) * ep.quant;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      v[4 * c] = __fadd_rn(__uint_as_float(rr[c].x), s * v[4 * c]);
+      v[4 * c + 1] = __fadd_rn(__uint_as_float(rr[c].y), s * v[4 * c + 1]);
+      v[4 * c + 2] = __fadd_rn(__uint_as_float(rr[c].z), s * v[4 * c + 2]);
+      v[4 * c + 3] = __fadd_rn(__uint_as_float(rr[c].w), s * v[4 * c + 3]);
     }
     stage_rows_f32(b, lane, v);
     stage_emit<TMA>(b, ring, lane, static_cast<float*>(ep.out) + col, ep.ldo * 4, row0,
@@ -1040,6 +1055,20 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   p->ep.rowdot = d->rowdot;
   p->ep.rd_seq = d->rd_seq;
   p->ep.rd_heads = N / 64;
+  p->ep.quant = 0.f;
+  p->ep.inv_quant = 0.f;
+  if (d->quantum != 0.f) {
+    int ex = 0;
+    const float mant = frexpf(d->quantum, &ex);
+    if (d->quantum < 0.f || mant != 0.5f || (d->epi != RP_EPI_RESID && d->epi != RP_EPI_F32) ||
+        splits > 1) {
+      delete p;
+      return rp_fail(RP_ERR_CONTRACT,
+                     "gemm: quantum must be a power of two, for RESID / unsplit F32 outputs");
+    }
+    p->ep.quant = d->quantum;
+    p->ep.inv_quant = 1.0f / d->quantum;
+  }
   if (d->epi == RP_EPI_ROWDOT && (!d->rowdot || !d->aux || d->rd_seq < 1 || N % 64)) {
     delete p;
     return rp_fail(RP_ERR_CONTRACT, "gemm: ROWDOT needs rowdot, aux, rd_seq >= 1, N % 64 == 0");

@@ -27,7 +27,7 @@ class ModelConfigC(C.Structure):
                 ("weight_decay", C.c_float), ("stages", C.c_int64),
                 ("stage_depth", C.c_int64 * 8), ("stage_width", C.c_int64 * 8),
                 ("stage_heads", C.c_int64 * 8), ("reduction", C.c_int64), ("fusion", C.c_int),
-                ("comm_ctas", C.c_int)]
+                ("comm_ctas", C.c_int), ("exact_coupling_bits", C.c_int)]
 
 
 @dataclass
@@ -60,6 +60,7 @@ class ModelConfig:
     reduction: int = 2
     fusion: str = "average"
     comm_ctas: int = 0          # NCCL CTAs per all-reduce (0 = 4), SMs reserved for them
+    exact_coupling_bits: int = 0  # residual grid 2^-bits for bit-exact inverses (0 = 17, -1 off)
 
     def __post_init__(self):
         if self.depths:
@@ -402,6 +403,7 @@ def _cfg_c(cfg: "ModelConfig") -> ModelConfigC:
                      cfg.g_ctas, cfg.lane_priority, cfg.optimizer, cfg.beta1, cfg.beta2,
                      cfg.adam_eps, cfg.weight_decay)
     c.comm_ctas = cfg.comm_ctas
+    c.exact_coupling_bits = cfg.exact_coupling_bits
     if cfg.depths:
         if not (len(cfg.depths) == len(cfg.widths) == len(cfg.stage_heads) <= 8):
             raise _capi.ConfigError("depths / widths / stage_heads: same length, at most 8")

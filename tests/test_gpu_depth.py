@@ -13,24 +13,39 @@ pytestmark = pytest.mark.gpu
 import depth_parity as DP  # noqa: E402  (tests/ is on sys.path under pytest)
 
 
-@pytest.mark.parametrize("case", list(DP.CASES))
+@pytest.mark.parametrize("case", [c for c in DP.CASES if not c.endswith("-plain")])
 def test_depth_parity(case):
+    """Exact coupling (the default): the inverse chain reconstructs every block input bit
+    for bit at depth 12 / 24 / 48, so Reprop's gradients equal Vanilla's (stored inputs)
+    exactly, and both are within the stated tolerance of the f64 oracle."""
     r = DP.run_case(case)
     assert r["stats"]["blocks_processed"] == r["depth"]
     assert r["loss_rel"] < DP.TOL_LOSS, r["loss_rel"]
     bad = [(x["block"], x["rec"]) for x in r["blocks"] if x["rec"] > DP.TOL_REC]
     assert not bad, ("reconstruction", bad)
+    assert r["reprop_vs_vanilla_l2"] == 0.0
     bad = [(x["block"], x["fwd"]) for x in r["blocks"] if x["fwd"] > DP.TOL_FWD]
     assert not bad, ("forward", bad)
+    assert r["grad_worst_matrix"] < DP.TOL_GRAD_MATRIX, r["grad_worst_matrix"]
     assert r["grad_worst"] < DP.TOL_GRAD, (r["grad_worst_tensor"], r["grad_worst"])
     assert r["grad_l2"] < DP.TOL_L2, r["grad_l2"]
+
+
+@pytest.mark.parametrize("case", [c for c in DP.CASES if c.endswith("-plain")])
+def test_depth_parity_plain_fp32_coupling(case):
+    """With plain fp32 coupling adds the reconstruction is only approximate and its error
+    compounds with depth (documented in DESIGN.md §5); held to the looser bounds."""
+    r = DP.run_case(case)
+    assert r["rec_l2_max"] < DP.PLAIN_REC_L2, r["rec_l2_max"]
+    assert r["grad_l2"] < DP.PLAIN_GRAD_L2, r["grad_l2"]
+    assert r["loss_rel"] < DP.TOL_LOSS
 
 
 def test_forward_trace_is_the_vanilla_stash():
     """The forward trace the reconstruction is measured against is exactly what the Vanilla
     engine stores: Vanilla's stored block inputs equal the Reprop
-    forward's bit for bit, and Vanilla's gradients (stored X) match Reprop's (recomputed X)
-    within the stated tolerance."""
+    forward's bit for bit, Reprop's reconstruction equals them bit for bit (exact
+    coupling), and so do the two engines' gradients."""
     from paper_2306_09342_b200.engine import REPROP, VANILLA, Engine, ModelConfig, bf16_bits
     from oracle import revprop_oracle as O
     geo, batch = DP.CASES["b-d12-b2"]
@@ -55,7 +70,7 @@ def test_forward_trace_is_the_vanilla_stash():
     fr, rr, gr, lr_ = out[REPROP]
     np.testing.assert_array_equal(fv, fr)      # same forward kernels, same stored X
     np.testing.assert_array_equal(rv, fv)      # Vanilla's backward reads the stash itself
-    assert DP.maxrel(rr, fv) < DP.TOL_REC      # Reprop's reconstruction vs the stash
+    np.testing.assert_array_equal(rr, fv)      # Reprop's reconstruction == the stash
     assert abs(lv - lr_) == 0.0
-    assert float(np.linalg.norm(gr - gv) / np.linalg.norm(gv)) < 1e-3
+    np.testing.assert_array_equal(gr, gv)      # hence identical gradients
     eng.close()

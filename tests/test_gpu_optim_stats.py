@@ -96,7 +96,9 @@ def test_step_stats_and_ledger(depth):
     act_wo_vanilla = st.arena_activation_bytes - 2 * depth * cfg.batch * cfg.seq_len * cfg.width * 4
     assert peaks[REPROP] <= act_wo_vanilla <= peaks[PAREPROP]
     assert peaks[PAREPROP] - peaks[REPROP] == blk
-    assert peaks[VANILLA] > peaks[REPROP]
+    # peak(reprop) < peak(vanilla) for depth >= 4 (equal at depth 2: the stash
+    # of two block inputs is the stored boundary plus one block footprint minus its caches)
+    assert peaks[VANILLA] > peaks[REPROP] if depth >= 4 else peaks[VANILLA] >= peaks[REPROP]
     eng.close()
 
 
