@@ -247,6 +247,10 @@ int rp_engine_prefetch_batch(RpEngine* engine, const uint16_t* host_inputs_bf16,
 int rp_engine_read_loss_async(RpEngine* engine, float* loss);
 int rp_engine_wait_loss(RpEngine* engine);
 int rp_engine_set_lr(RpEngine* engine, float lr);
+/* sgd_update as its own call: params -= lr * grads over the whole model, with
+ * host_grads (the mean gradient, flat, engine order) or NULL = the last step's gradient.
+ * Bit-identical to fp32 p - lr * g; refreshes the bf16 shadow. */
+int rp_engine_sgd_update(RpEngine* engine, const float* host_grads, float lr);
 int rp_engine_set_partition(RpEngine* engine, int r_ctas, int g_ctas);
 int rp_engine_invalidate_graphs(RpEngine* engine);
 /* Test hook of the verify command: kind 1 corrupts every block's F-path VJP
@@ -350,6 +354,66 @@ int rp_engine_attention_vjp(RpEngine* engine, int64_t block, const float* x, con
                             float* d_x);
 int rp_engine_mlp_vjp(RpEngine* engine, int64_t block, const float* x, const float* d_y,
                       float* d_x);
+
+/* ------------------------------------------------------------------ reference layer API
+ * The reference's pure layer / revcore / optimizer functions over CALLER-owned device
+ * tensors, no engine (include/revprop_b200.hpp wraps them in the reference's names and
+ * types). fp32 device pointers in the reference's layouts: activations [batch, tokens, width]
+ * row-major, weights [in, out] row-major (layers.hpp:43-52, 94-103). Work is enqueued on
+ * `stream`; temporaries are stream-ordered allocations; results are complete when the
+ * stream is. */
+typedef struct RpAttentionParamsDev { /* AttentionParams, layers.hpp:43-52 */
+  const float* w_qkv;    /* [width, 3 width], no bias */
+  const float* w_out;    /* [width, width], no bias */
+  const float* ln_gamma; /* [width] */
+  const float* ln_beta;  /* [width] */
+  int64_t width, heads;
+  int64_t window;        /* tokens per attention window; 0 = full attention */
+} RpAttentionParamsDev;
+typedef struct RpMlpParamsDev { /* MlpParams, layers.hpp:94-103 */
+  const float *w1, *b1, *w2, *b2, *ln_gamma, *ln_beta; /* [d,h] [h] [h,d] [d] [d] [d] */
+  int64_t width, hidden;
+} RpMlpParamsDev;
+typedef struct RpAttentionGradsDev { /* AttentionGrads, layers.hpp:67-72 (NULL = skip) */
+  float *d_w_qkv, *d_w_out, *d_ln_gamma, *d_ln_beta;
+} RpAttentionGradsDev;
+typedef struct RpMlpGradsDev { /* MlpGrads, layers.hpp:116-123 (NULL = skip) */
+  float *d_w1, *d_b1, *d_w2, *d_b2, *d_ln_gamma, *d_ln_beta;
+} RpMlpGradsDev;
+/* AttentionCache / MlpCache (layers.hpp:54-65, 105-114): opaque, owns its device buffers
+ * (the layer's input, LayerNorm statistics, bf16 operands, log-sum-exp instead of the
+ * probability tensor). A VJP given the other layer's cache is RP_ERR_CONTRACT. */
+typedef struct RpLayerCache RpLayerCache;
+/* y = Proj(MHSA(LN(x))) (layers.hpp:82, layers.cpp:134-169); cache may be NULL */
+int rp_attention_forward(const RpAttentionParamsDev* p, const float* x, int64_t batch,
+                         int64_t tokens, float* y, RpLayerCache** cache, rp_stream_t stream);
+/* d_x and the parameter grads of d_y (layers.hpp:89, layers.cpp:171-220) */
+int rp_attention_vjp(const RpLayerCache* cache, const RpAttentionParamsDev* p, const float* d_y,
+                     float* d_x, const RpAttentionGradsDev* grads, rp_stream_t stream);
+/* y = W2 gelu(W1 LN(x) + b1) + b2 (layers.hpp:131, layers.cpp:222-239) */
+int rp_mlp_forward(const RpMlpParamsDev* p, const float* x, int64_t batch, int64_t tokens,
+                   float* y, RpLayerCache** cache, rp_stream_t stream);
+/* layers.hpp:138, layers.cpp:241-259 */
+int rp_mlp_vjp(const RpLayerCache* cache, const RpMlpParamsDev* p, const float* d_y, float* d_x,
+               const RpMlpGradsDev* grads, rp_stream_t stream);
+int64_t rp_layer_cache_bytes(const RpLayerCache* cache);
+int rp_layer_cache_destroy(RpLayerCache* cache);
+
+typedef struct RpRevBlockDev { RpAttentionParamsDev f; RpMlpParamsDev g; } RpRevBlockDev;
+typedef struct RpRevBlockGradsDev { RpAttentionGradsDev d_f; RpMlpGradsDev d_g; } RpRevBlockGradsDev;
+/* o2 = i2 + F(i1), o1 = i1 + G(o2) */
+int rp_rev_forward(const RpRevBlockDev* block, int64_t batch, int64_t tokens, const float* i1,
+                   const float* i2, float* o1, float* o2, rp_stream_t stream);
+/* i1 = o1 - G(o2), i2 = o2 - F(i1) */
+int rp_rev_inverse(const RpRevBlockDev* block, int64_t batch, int64_t tokens, const float* o1,
+                   const float* o2, float* i1, float* i2, rp_stream_t stream);
+/* recomputed inputs, input cotangents and the block's parameter grads */
+int rp_rev_backward_local(const RpRevBlockDev* block, int64_t batch, int64_t tokens,
+                          const float* o1, const float* o2, const float* d_o1, const float* d_o2,
+                          float* i1, float* i2, float* d_i1, float* d_i2,
+                          const RpRevBlockGradsDev* grads, rp_stream_t stream);
+/* params <- params - lr * grads (fp32, bit-identical to the host formula) */
+int rp_sgd_update(float* params, const float* grads, int64_t n, float lr, rp_stream_t stream);
 
 #ifdef __cplusplus
 }

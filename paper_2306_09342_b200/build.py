@@ -90,6 +90,37 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     return LIB
 
 
+REFERENCE_INCLUDE = Path("/root/reference/proj/core/include")
+ADAPTER_TEST = LIB_DIR / "reference_adapter_test"
+ORACLE_REF = ROOT / "oracle" / "_ref"
+
+
+def build_adapter_test(verbose: bool = False) -> Path | None:
+    """Compile examples/reference_adapter_test.cpp: the reference-typed adapter
+    (examples/reference_adapter.hpp over include/revprop_b200.hpp) against the reference's own
+    headers, linked with the reference's layer code compiled in place (oracle/_ref/{ops,layers}.o)
+    and librevprop_b200.so. Only where /root/reference exists (this container); the binary
+    travels to the GPU box in-tree (git-ignored), where tests/test_gpu_adapter.py runs it."""
+    objs = [ORACLE_REF / "ops.o", ORACLE_REF / "layers.o"]
+    if not REFERENCE_INCLUDE.exists() or not all(o.exists() for o in objs):
+        return None
+    srcs = [ROOT / "examples" / "reference_adapter_test.cpp", ROOT / "examples" / "reference_adapter.hpp",
+            ROOT / "include" / "revprop_b200.hpp", ROOT / "include" / "revprop_b200.h", LIB]
+    if ADAPTER_TEST.exists() and all(ADAPTER_TEST.stat().st_mtime >= s.stat().st_mtime for s in srcs):
+        return ADAPTER_TEST
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-include", "algorithm",
+           "-I" + str(REFERENCE_INCLUDE), "-I" + str(ROOT / "include"),
+           "-I/usr/local/cuda/include", str(srcs[0])] + [str(o) for o in objs] + [
+           "-L" + str(LIB_DIR), "-lrevprop_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,$ORIGIN", "-pthread", "-o", str(ADAPTER_TEST)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"adapter test build failed:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(r.stdout + r.stderr)
+    return ADAPTER_TEST
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--clean", action="store_true")

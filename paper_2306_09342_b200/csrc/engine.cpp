@@ -136,7 +136,7 @@ struct RpEngine {
   std::vector<cudaEvent_t> ts;  // timing events for the slot log (eager, instrumented)
   bool instrument = false;
   // parameters
-  float *params = nullptr, *grads = nullptr, *lr = nullptr;
+  float *params = nullptr, *grads = nullptr, *lr = nullptr, *lr_apply = nullptr;
   uint16_t* pb = nullptr;
   // data
   uint16_t* inputs = nullptr;
@@ -1248,6 +1248,7 @@ extern "C" int rp_engine_create(const RpModelConfig* c, RpEngine** out) {
   splits_ws(g->in, g->st[0].d, g->T);
   if ((rc = dalloc(g, &g->params, g->P, 2)) || (rc = dalloc(g, &g->grads, g->P, 2)) ||
       (rc = dalloc(g, &g->pb, g->P, 2)) || (rc = dalloc(g, &g->lr, 1)) ||
+      (rc = dalloc(g, &g->lr_apply, 1)) ||
       (rc = dalloc(g, &g->inputs, g->T * g->in)) || (rc = dalloc(g, &g->labels, g->B)))
     return fail(rc);
   for (RpStage& St : g->st) {
@@ -2026,4 +2027,22 @@ extern "C" int rp_engine_step_stats(RpEngine* g, RpStepStats* out) {
   out->arena_param_bytes = g->arena_bytes[2];
   out->arena_total_bytes = g->arena_bytes[0] + g->arena_bytes[1] + g->arena_bytes[2];
   return RP_OK;
+}
+
+// sgd_update(model, grads, lr) as a separate call: theta <- theta - lr * g
+// over every parameter, with `host_grads` (the mean gradient, e.g. a GradStore the caller
+// holds) or, when NULL, the last step's all-reduced gradient (1/world folded in). Refreshes
+// the bf16 GEMM shadow. The in-step optimizer (rp_engine_set_lr) is the fused alternative.
+extern "C" int rp_engine_sgd_update(RpEngine* g, const float* host_grads, float lr) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  float scale = 1.0f / static_cast<float>(g->world);
+  if (host_grads) {
+    RP_TRY(cuda_ok(cudaMemcpyAsync(g->grads, host_grads, static_cast<size_t>(g->P) * 4,
+                                   cudaMemcpyHostToDevice, g->sG), "sgd_update grads"));
+    scale = 1.0f;
+  }
+  RP_TRY(cuda_ok(cudaMemcpyAsync(g->lr_apply, &lr, sizeof(float), cudaMemcpyHostToDevice, g->sG),
+                 "sgd_update lr"));
+  RP_TRY(rpk_sgd(g->params, g->grads, g->pb, g->P, g->lr_apply, scale, g->sG));
+  return rp_engine_sync(g);
 }

@@ -296,6 +296,28 @@ __global__ void add_to_bf16_kernel(const float* __restrict__ a, const float* __r
     out[i] = __float2bfloat16_rn(a[i] + b[i]);
 }
 
+// out = a + sign * b (fp32): the coupling add / subtract of the standalone revcore entry
+// points (ref:proj/core/src/ops.cpp:96-106 add / sub)
+__global__ void axpy_sign_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                 float sign, float* __restrict__ out, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __fadd_rn(a[i], sign * b[i]);
+}
+
+// SGD on caller-owned fp32 parameters with a host learning rate, same
+// rounding as sgd_kernel: p - lr * g, no contraction
+__global__ void sgd_value_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n,
+                                 float lr) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+}
+
 // fuse(average) of a stage output (layers.cpp:277-279: ops::scale(ops::add(i1, i2), 0.5)),
 // written bf16 as the patch_merge GEMM operand
 __global__ void fuse_avg_kernel(const float* __restrict__ o1, const float* __restrict__ o2,
@@ -436,6 +458,15 @@ int rpk_spread(const float* d_pooled, int64_t B, int64_t N, int64_t d, float* d1
 int rpk_add_to_bf16(const float* a, const float* b, uint16_t* out, int64_t n, cudaStream_t s) {
   launch_k(add_to_bf16_kernel, dim3(grid_for(n)), dim3(256), 0, s, a, b, reinterpret_cast<__nv_bfloat16*>(out), n);
   return rp_check_launch("add_to_bf16");
+}
+int rpk_axpy_sign(const float* a, const float* b, float sign, float* out, int64_t n,
+                  cudaStream_t s) {
+  launch_k(axpy_sign_kernel, dim3(grid_for(n)), dim3(256), 0, s, a, b, sign, out, n);
+  return rp_check_launch("axpy_sign");
+}
+int rpk_sgd_value(float* p, const float* g, int64_t n, float lr, cudaStream_t s) {
+  launch_k(sgd_value_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, g, n, lr);
+  return rp_check_launch("sgd_value");
 }
 int rpk_fuse_avg_bf16(const float* o1, const float* o2, int64_t n, uint16_t* out, cudaStream_t s) {
   launch_k(fuse_avg_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, o1, o2, n / 4,

@@ -30,3 +30,7 @@ int rpk_concat_bf16(const float* o1, const float* o2, int64_t rows, int64_t d, u
                     cudaStream_t s);
 int rpk_halve_dup(float* d1, int64_t n, float* d2, uint16_t* d1b, uint16_t* d2b, cudaStream_t s);
 int rpk_scale_pair(float* x, uint16_t* xb, int64_t n, float s, cudaStream_t st);
+// standalone revcore / optimizer entry points (layers_api.cpp)
+int rpk_axpy_sign(const float* a, const float* b, float sign, float* out, int64_t n,
+                  cudaStream_t s);
+int rpk_sgd_value(float* p, const float* g, int64_t n, float lr, cudaStream_t s);

@@ -194,3 +194,47 @@ def test_cpp_example_builds_against_the_c_abi(capi, tmp_path):
     against include/revprop_b200.h and the library with g++ alone."""
     import os
     assert os.path.exists(_build_example(tmp_path))
+
+
+def test_cpp_api_header_compiles_standalone(tmp_path):
+    """include/revprop_b200.hpp (the reference-named C++ API) compiles on its own, with the
+    reference's exception hierarchy declared locally when the reference is not on the path."""
+    import subprocess
+    tu = tmp_path / "tu.cpp"
+    tu.write_text('#include "revprop_b200.hpp"\n'
+                  "using namespace revprop::b200;\n"
+                  "int f() {\n"
+                  "  try { check(RP_ERR_SHAPE, \"x\"); } catch (const revprop::ShapeError&) { return 1; }\n"
+                  "  return 0;\n"
+                  "}\n"
+                  "AttentionForward (*a)(const DeviceTensor&, const AttentionParams&) = attention_forward;\n"
+                  "MlpVjp (*m)(const MlpCache&, const MlpParams&, const DeviceTensor&) = mlp_vjp;\n"
+                  "std::tuple<Coupled, Coupled, RevBlockGrads> (*r)(const RevBlock&, const Coupled&,"
+                  " const Coupled&) = rev_backward_local;\n"
+                  "std::pair<GradStore, StepStats> (*s)(Model&, const Batch&, MemoryLedger&) = step_pareprop;\n")
+    subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                    "-I/usr/local/cuda/include", str(tu)], check=True)
+
+
+def test_cpp_api_declares_the_reference_names():
+    src = open(os.path.join(ROOT, "include", "revprop_b200.hpp")).read()
+    for name in ("AttentionParams", "AttentionCache", "AttentionGrads", "AttentionForward",
+                 "AttentionVjp", "attention_forward", "attention_vjp", "MlpParams", "MlpCache",
+                 "MlpGrads", "mlp_forward", "mlp_vjp", "Coupled", "RevBlock", "RevBlockGrads",
+                 "rev_forward", "rev_inverse", "rev_backward_local", "step_reprop",
+                 "step_pareprop", "step_vanilla", "sgd_update", "GradStore", "StepStats",
+                 "MemoryLedger"):
+        assert re.search(r"\b" + name + r"\b", src), name
+
+
+@pytest.mark.skipif(not os.path.exists("/root/reference/proj/core/include"),
+                    reason="the reference's headers exist only in the build container")
+def test_reference_adapter_builds_against_the_reference_headers(capi):
+    """INTEGRATION.md §2's adapter (examples/reference_adapter.hpp) compiles against the
+    reference's own include tree and links with the reference's layer code (oracle/_ref) and
+    the B200 library; tests/test_gpu_adapter.py runs the binary on the B200."""
+    from oracle import ref as R
+    from paper_2306_09342_b200 import build
+    R.build()
+    exe = build.build_adapter_test()
+    assert exe is not None and exe.exists()
