@@ -108,6 +108,10 @@ int rp_gemm_plan_set_max_ctas(RpGemmPlan* plan, int max_ctas);
 void rp_gemm_plan_destroy(RpGemmPlan* plan);
 int rp_gemm_plan_shape(const RpGemmPlan* plan, int64_t* M, int64_t* N, int64_t* K);
 int rp_gemm(const RpGemmDesc* desc, rp_stream_t stream);
+/* MMA issue form of the GEMM kernels (A/B switch, process-global, read at launch; captured
+ * graphs keep theirs): 1 (default) the issuing warp stays converged and issues predicated on
+ * one lane, 0 a single diverged lane issues. Same MMAs in the same order: bit-identical. */
+int rp_set_mma_issue(int mode);
 
 /* ------------------------------------------------------------------ LayerNorm / reductions
  * rp_layer_norm_fwd: ref:proj/core/src/ops.cpp:264-304 (y = x_hat*gamma + beta, two-pass
@@ -170,6 +174,12 @@ int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
  * Process-global; other values are RP_ERR_CONFIG. Captured engine graphs keep the kernels
  * they were captured with: call rp_engine_invalidate_graphs after changing it. */
 int rp_set_attention_impl(int impl);
+/* tcgen05 forward for N <= 256 (A/B switch, process-global like the above): 0 (default) two
+ * ping-pong groups of softmax warps on alternate query tiles; 1 the lockstep kernel (N <= 224) */
+int rp_set_attention_fwd_variant(int variant);
+/* Instrumentation: a device buffer of 64 x 12 uint64 receives clock64 stamps of the ping-pong
+ * forward's CTA 0 (per tile: S issue, PV issue, softmax phases); NULL turns it off. */
+int rp_set_attention_trace(void* device_buffer);
 
 /* ------------------------------------------------------------------ training engine
  * Isotropic reversible model and its engines:

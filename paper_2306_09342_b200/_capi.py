@@ -98,6 +98,9 @@ _SIGS = {
     "rp_attention_bwd_ex": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I, _P]),
     "rp_attention_bwd_workspace_floats": (_I64, [_I64, _I64, _I64]),
     "rp_set_attention_impl": (_I, [_I]),
+    "rp_set_attention_fwd_variant": (_I, [_I]),
+    "rp_set_mma_issue": (_I, [_I]),
+    "rp_set_attention_trace": (_I, [_P]),
 }
 
 

@@ -552,6 +552,24 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
 // backward that keeps no dS
 static int g_attn_impl = 0;
 
+// clock64 trace of the ping-pong forward's CTA 0 (tools/attn_fwd_trace.py): on when set
+static unsigned long long* g_attn_trace = nullptr;
+unsigned long long* rp_attn_trace_buffer() { return g_attn_trace; }
+extern "C" int rp_set_attention_trace(void* device_buffer) {
+  g_attn_trace = static_cast<unsigned long long*>(device_buffer);
+  return RP_OK;
+}
+
+// forward kernel variant for N <= 256 (A/B): 0 ping-pong softmax groups (attn_fwd_tc_pp),
+// 1 the lockstep persistent kernel (N <= 224)
+static int g_attn_fwd_variant = 0;
+int rp_attn_fwd_variant() { return g_attn_fwd_variant; }
+extern "C" int rp_set_attention_fwd_variant(int v) {
+  if (v < 0 || v > 1) return rp_fail(RP_ERR_CONFIG, "attention forward variant must be 0 or 1");
+  g_attn_fwd_variant = v;
+  return RP_OK;
+}
+
 // Process-global switch, read when a step is enqueued: engines must drop their captured
 // graphs (rp_engine_invalidate_graphs) after changing it, or the graphs keep the old kernels.
 extern "C" int rp_set_attention_impl(int impl) {

@@ -269,6 +269,316 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 16) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------- ping-pong forward (N <= 256)
+// The persistent kernel above runs its 16 softmax warps in lockstep on one tile: all of them
+// sit in the row-max pass, the max exchange or the O epilogue at the same time, so the MUFU
+// pipe (the exp2 floor: 16 / clock / SM, measured, tools/tmem_mufu_bench.cu) idles for most
+// of every tile. Here the softmax warps form TWO groups that own alternate tiles (group g:
+// tiles j = g, g + 2, ...), each warp a TMEM lane quarter q = w % 4 (its SM sub-partition)
+// and a key half; while one group exchanges maxima or drains O, the other group's exp2
+// stream keeps the MUFU busy. Per tile and warp:
+//   pass 1   row max over the warp's key half, read from S in TMEM (16-column loads)
+//   xchg     max with the partner warp of the same quarter and group (named barrier, 64)
+//   pass 2   S re-read, p = exp2(s scale log2e - m), bf16 P packed IN the warp's own S
+//            columns (half 0: chunk c -> column 8c; half 1: 16 cs + 8 (c - cs)), row sums
+//   PV       issued by the MMA warp once the group's 8 warps arrived; O accumulates at
+//            column ocol of the tile's own S buffer (free once P is packed)
+//   epilogue O / l (sums exchanged the same way) -> bf16 att, log2-domain LSE
+// S is double-buffered (buffer j % 2 at column 256 (j % 2)); S(j + 2) waits for
+// epilogue(j). Works for N <= 256 (the persistent kernel stops at 224).
+// Warp 16 issues the loads and S = Q K^T, warp 17 every P V (a PV then never waits behind
+// an S issue). (Splitting the PV issue per group over two warps measured slower.)
+constexpr int kPPThreads = kFwdThreads + 32;
+struct PPPlan {
+  int ntile, nitems;
+  int cs;    // 16-key chunks in key half 0 (the rest are half 1's)
+  int ocol;  // O accumulator column inside each S buffer
+  unsigned long long* trace;  // optional clock64 trace of CTA 0's first kTraceTiles tiles
+};
+constexpr int kTraceTiles = 64;
+#define PP_TRACE(j, slot)                                                                   \
+  do {                                                                                      \
+    if (pl.trace && blockIdx.x == 0 && (j) < kTraceTiles)                                  \
+      pl.trace[(j) * 12 + (slot)] = static_cast<unsigned long long>(clock64());            \
+  } while (0)
+
+__device__ __forceinline__ uint32_t pp_pcol(int c, int cs) {
+  return static_cast<uint32_t>(c < cs ? 8 * c : 16 * cs + 8 * (c - cs));
+}
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    attn_fwd_tc_pp(const __grid_constant__ CUtensorMap tm_q,
+                   const __grid_constant__ CUtensorMap tm_kv, __nv_bfloat16* __restrict__ out,
+                   float* __restrict__ lse, Geom g, PPPlan pl) {
+  pdl_trigger();
+
+  __shared__ float red_max[2][2][128];  // [group][key half][row]
+  __shared__ float red_sum[2][2][128];
+  __shared__ __align__(8) uint64_t bars[12];
+  __shared__ uint32_t tmem_slot;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bar_load = bars;      // [2] per smem buffer: TMA bytes landed
+  uint64_t* bar_free = bars + 2;  // [2] per smem buffer: every tile's epilogue done with it
+  uint64_t* bar_s = bars + 4;     // [2] per S buffer: S ready
+  uint64_t* bar_p = bars + 6;     // [2] per S buffer: P in TMEM (8 warps of the group)
+  uint64_t* bar_o = bars + 8;     // [2] per S buffer: O ready
+  uint64_t* bar_e = bars + 10;    // [2] per S buffer: O read out (8 warps)
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Nk = g.Nk, ntile = pl.ntile, nitems = pl.nitems, nch = g.Nk / 16, cs = pl.cs;
+  if (warp == 16) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_kv);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&bar_load[i], 1);
+        mbar_init(&bar_free[i], static_cast<uint32_t>(8 * pl.ntile));
+        mbar_init(&bar_s[i], 1);
+        mbar_init(&bar_p[i], 8);
+        mbar_init(&bar_o[i], 1);
+        mbar_init(&bar_e[i], 8);
+      }
+      fence_barrier_init();
+    }
+    tmem_alloc(&tmem_slot, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  const int d = g.H * 64;
+  const int K = nitems > static_cast<int>(blockIdx.x)
+                    ? (nitems - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                          static_cast<int>(gridDim.x)
+                    : 0;
+  const int J = K * ntile;
+  auto item_of = [&](int k) { return static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x); };
+  auto sbuf = [&](int j) { return tmem + static_cast<uint32_t>((j & 1) * 256); };
+
+  if (warp == 16) {
+    if (lane == 0) {
+      auto issue_load = [&](int k) {
+        const int item = item_of(k), buf = k & 1;
+        const int h = item % g.H, b = item / g.H;
+        const int row_seq = b * g.N;
+        uint8_t* base = smem + buf * kFwdBuf;
+        mbar_arrive_expect_tx(&bar_load[buf], (ntile * 128 + 2 * Nk) * 128);
+        for (int t = 0; t < ntile; ++t)
+          tma_load_2d(base + t * 16384, &tm_q, &bar_load[buf], h * 64, row_seq + t * 128);
+        tma_load_2d(base + 32768, &tm_kv, &bar_load[buf], d + h * 64, row_seq);
+        tma_load_2d(base + 65536, &tm_kv, &bar_load[buf], 2 * d + h * 64, row_seq);
+      };
+      auto ready = [](const uint64_t* bar, uint32_t parity) { return mbar_test(bar, parity); };
+      const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(Nk), false, false);
+      int jS = 0, kL = 0;
+      while (jS < J) {
+        if (kL < K && (kL < 2 || ready(&bar_free[kL & 1], ((kL - 2) >> 1) & 1))) {
+          issue_load(kL);
+          ++kL;
+        }
+        // S(jS): operands landed and the S buffer's previous tile (jS - 2) drained
+        {
+          const int k = jS / ntile, t = jS % ntile;
+          const bool buf_ok = jS < 2 || ready(&bar_e[jS & 1], ((jS - 2) >> 1) & 1);
+          if (k < kL && buf_ok && ready(&bar_load[k & 1], (k >> 1) & 1)) {
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + (k & 1) * kFwdBuf);
+            const uint32_t aq = base + static_cast<uint32_t>(t) * 16384u, bk = base + 32768u;
+            PP_TRACE(jS, 0);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(sbuf(jS), make_sdesc_sw128(aq + kk * 32, 16, 1024),
+                        make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            umma_commit(&bar_s[jS & 1]);
+            PP_TRACE(jS, 1);
+            ++jS;
+          }
+        }
+      }
+    }
+  } else if (warp == 17) {
+    // P V issuer (both groups' tiles in order), so a PV never waits behind an S issue
+    if (lane == 0) {
+      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      for (int jP = 0; jP < J; ++jP) {
+        mbar_wait(&bar_p[jP & 1], (jP >> 1) & 1);
+        tc_fence_after();
+        const int k = jP / ntile;
+        const uint32_t bv = smem_u32(smem + (k & 1) * kFwdBuf) + 65536u;
+        const uint32_t sb = sbuf(jP), od = sb + static_cast<uint32_t>(pl.ocol);
+        PP_TRACE(jP, 2);
+        for (int c = 0; c < nch; ++c)
+          umma_ts_bf16(od, sb + pp_pcol(c, cs), make_sdesc_sw128(bv + c * 2048, 8192, 1024),
+                       idesc_o, c > 0 ? 1u : 0u);
+        umma_commit(&bar_o[jP & 1]);
+        PP_TRACE(jP, 3);
+      }
+    }
+  } else {
+    const int q = static_cast<int>(warp & 3u), r = static_cast<int>(warp >> 2);
+    const int grp = r >> 1, half = r & 1;
+    const int ch0 = half ? cs : 0, ch1 = half ? nch : cs;
+    const uint32_t lq = (static_cast<uint32_t>(q) * 32u) << 16;
+    const int rloc = q * 32 + static_cast<int>(lane);
+    const int valid = g.N;
+    const int bar_id = 1 + grp * 4 + q;
+    for (int j = grp; j < J; j += 2) {
+      const int k = j / ntile, t = j % ntile;
+      const bool active = t * 128 + q * 32 < g.N;
+      const uint32_t sb = sbuf(j) + lq;
+      const bool tr = q == 0 && half == 0 && lane == 0;
+      if (tr) PP_TRACE(j, 4);
+      mbar_wait(&bar_s[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (tr) PP_TRACE(j, 5);
+      // ---- pass 1: row max over this warp's key half, two chunks per TMEM wait (four would
+      // need > 96 registers: with 18 warps, five share an SM sub-partition's 16 K registers)
+      float m0 = -INFINITY, m1 = -INFINITY;
+      if (active) {
+        for (int c = ch0; c < ch1; c += 2) {
+          const uint32_t a0 = sb + static_cast<uint32_t>(c * 16);
+          float va[16], vb[16];
+          if (c + 1 < ch1) {
+            tmem_ld16x2(a0, a0 + 16, va, vb);
+          } else {
+            tmem_ld16(a0, va);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vb[e] = -INFINITY;
+          }
+          if ((c + 2) * 16 <= valid) {
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              m0 = fmaxf(m0, fmaxf(va[e], va[e + 1]));
+              m1 = fmaxf(m1, fmaxf(vb[e], vb[e + 1]));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              if (c * 16 + e < valid) m0 = fmaxf(m0, va[e]);
+              if (c * 16 + 16 + e < valid && c + 1 < ch1) m1 = fmaxf(m1, vb[e]);
+            }
+          }
+        }
+      }
+      red_max[grp][half][rloc] = fmaxf(m0, m1);
+      if (tr) PP_TRACE(j, 6);
+      named_bar(bar_id, 64);
+      if (tr) PP_TRACE(j, 7);
+      const float ms = fmaxf(red_max[grp][0][rloc], red_max[grp][1][rloc]) * g.scale_log2;
+      // ---- pass 2: p = exp2(s * scale - m), packed bf16 P in this warp's own S columns
+      // (a chunk's P lands on columns already read)
+      float l0 = 0.f, l1 = 0.f;
+      auto expchunk = [&](const float* a, int cc) {
+        uint32_t pk[8];
+        if (cc * 16 + 16 <= valid) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float p0 = ex2(fmaf(a[2 * e], g.scale_log2, -ms));
+            const float p1 = ex2(fmaf(a[2 * e + 1], g.scale_log2, -ms));
+            l0 += p0;
+            l1 += p1;
+            pk[e] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int key = cc * 16 + 2 * e;
+            const float p0 = key < valid ? ex2(fmaf(a[2 * e], g.scale_log2, -ms)) : 0.f;
+            const float p1 = key + 1 < valid ? ex2(fmaf(a[2 * e + 1], g.scale_log2, -ms)) : 0.f;
+            l0 += p0;
+            l1 += p1;
+            pk[e] = pack_bf16x2(p0, p1);
+          }
+        }
+        tmem_st8(sb + pp_pcol(cc, cs), pk);
+      };
+      if (active) {
+        for (int c = ch0; c < ch1; c += 2) {
+          const uint32_t a0 = sb + static_cast<uint32_t>(c * 16);
+          if (c + 1 < ch1) {
+            float va[16], vb[16];
+            tmem_ld16x2(a0, a0 + 16, va, vb);
+            expchunk(va, c);
+            expchunk(vb, c + 1);
+          } else {
+            float va[16];
+            tmem_ld16(a0, va);
+            expchunk(va, c);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_p[j & 1]);
+      if (tr) PP_TRACE(j, 8);
+      red_sum[grp][half][rloc] = l0 + l1;
+      named_bar(bar_id, 64);
+      const float l = red_sum[grp][0][rloc] + red_sum[grp][1][rloc];
+      // ---- epilogue: O / l -> att (this warp's 32 of the 64 head columns), LSE; the
+      // reciprocal and log (MUFU) are taken before waiting for O
+      const int item = item_of(k);
+      const int h = item % g.H, b = item / g.H;
+      const int row = t * 128 + rloc;
+      const float inv = 1.0f / l;
+      const float lse_v = ms + log2f(l);
+      mbar_wait(&bar_o[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (tr) PP_TRACE(j, 9);
+      float o[32];
+      if (active)
+        tmem_ld16x2(sbuf(j) + lq + static_cast<uint32_t>(pl.ocol + half * 32),
+                    sbuf(j) + lq + static_cast<uint32_t>(pl.ocol + half * 32 + 16), o, o + 16);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_e[j & 1]);
+      // O / l staged through the tile's own Q slot in smem (dead since S(j); 128 rows x 128 B,
+      // 16-byte chunks XOR-swizzled by row so the row-per-lane writes are conflict free), then
+      // written back as whole 128-byte rows (8 lanes per row): coalesced, where a direct
+      // row-per-lane store scatters each warp instruction over 32 lines. The item's smem
+      // buffer is released (bar_free) by these warps once the staging is read back.
+      const uint32_t stg = smem_u32(smem + (k & 1) * kFwdBuf + t * 16384);
+      if (active) {
+        const uint32_t rbase = stg + static_cast<uint32_t>(rloc) * 128u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t ch = static_cast<uint32_t>((half * 4 + u) ^ (rloc & 7));
+          sts128_a(rbase + ch * 16u,
+                 make_uint4(pack_bf16x2(o[8 * u] * inv, o[8 * u + 1] * inv),
+                            pack_bf16x2(o[8 * u + 2] * inv, o[8 * u + 3] * inv),
+                            pack_bf16x2(o[8 * u + 4] * inv, o[8 * u + 5] * inv),
+                            pack_bf16x2(o[8 * u + 6] * inv, o[8 * u + 7] * inv)));
+        }
+      }
+      if (row < g.N && half == 0) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = lse_v;
+      named_bar(bar_id, 64);  // both halves of these 32 rows staged
+      if (active) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rl = q * 32 + half * 16 + it * 4 + static_cast<int>(lane >> 3);
+          const int ch = static_cast<int>(lane & 7);
+          const int grow = t * 128 + rl;
+          const uint4 x = lds128_a(stg + static_cast<uint32_t>(rl) * 128u +
+                                 static_cast<uint32_t>((ch ^ (rl & 7)) * 16));
+          if (grow < g.N)
+            *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(b) * g.N + grow) * g.ld_o +
+                                      h * 64 + ch * 8) = x;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_free[k & 1]);
+      if (tr) PP_TRACE(j, 10);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 16) tmem_dealloc(tmem, 512);
+}
+
 // ------------------------------------------------------------- long-sequence forward
 // 224 < N <= 512 (the Rev-RoBERTa shape): the key row no longer fits next to its O in one
 // TMEM buffer, so each 128-query tile makes two passes over 128-key blocks:
@@ -540,7 +850,8 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   g.scale_log2 = (1.0f / 8.0f) * 1.4426950408889634f;
   const int64_t T = S * N, cols = 3 * H * 64;
   CUtensorMap mq, mkv;
-  if (g.Nk > 224) {  // two-pass kernel with K / V resident per (sequence, head) group
+  if (g.Nk > 256 || (g.Nk > 224 && rp_attn_fwd_variant() != 0)) {
+    // two-pass kernel with K / V resident per (sequence, head) group
     if (make_map(&mq, qkv, T, cols, 128))
       return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
     const int smem = 1024 + kLongKV + 2 * 16384;
@@ -570,6 +881,33 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   if (make_map(&mq, qkv, T, cols, 128) || make_map(&mkv, qkv, T, cols, static_cast<uint32_t>(g.Nk)))
     return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
   const int smem = 1024 + 2 * kFwdBuf;
+  const int smem_pp = smem;
+  // ping-pong softmax groups by default (256 x 197 x 12: 113.4 vs 113.5 us; x 16 heads:
+  // 134.3 vs 144.7; 64 x 128: 19.0 vs 21.0), except 208 < Nk <= 224 where the lockstep
+  // kernel measured faster (128 x 224: 64.5 vs 70.1 us) (tools/attn_fwd_ab.py)
+  const bool pp = g.Nk > 224 || (rp_attn_fwd_variant() == 0 && g.Nk <= 208);
+  if (pp) {
+    static std::once_flag once_pp;
+    static int nsm_pp = 148;
+    std::call_once(once_pp, [smem_pp] {
+      cudaFuncSetAttribute(attn_fwd_tc_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm_pp, cudaDevAttrMultiProcessorCount, dev);
+    });
+    PPPlan pp;
+    pp.ntile = static_cast<int>((N + 127) / 128);
+    pp.nitems = static_cast<int>(S * H);
+    const int nch = g.Nk / 16;
+    pp.cs = (nch + 1) / 2;
+    pp.ocol = (8 * (nch + pp.cs) + 15) / 16 * 16;
+    pp.trace = rp_attn_trace_buffer();
+    const unsigned grid = static_cast<unsigned>(pp.nitems < nsm_pp ? pp.nitems : nsm_pp);
+    launch_k(attn_fwd_tc_pp, dim3(grid), dim3(kPPThreads), smem_pp, stream, mq, mkv,
+             reinterpret_cast<__nv_bfloat16*>(out), lse, g, pp);
+    return rp_check_launch("attention_fwd_tc_pp");
+  }
+  if (g.Nk > 224) return RP_ERR_CONFIG;  // the lockstep kernel's TMEM plan stops at 224
   static std::once_flag once;
   static int nsm = 148;
   std::call_once(once, [smem] {

@@ -45,6 +45,7 @@ struct GemmCfg {
 struct GemmShape {
   int64_t M, N, K;
   int32_t m_tiles, n_tiles, k_blocks, splits;
+  int32_t issue;  // MMA issue form: 1 warp-converged (predicated), 0 one diverged lane
 };
 
 // ---------------------------------------------------------------- epilogue
@@ -503,7 +504,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (sh.issue == 1) {
+      // ---------------- MMA issuer, warp-converged: all lanes walk the pipeline, lane 0's
+      // predicate issues (same instruction stream and order as below)
+      constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN, B_MN);
+      const uint32_t is0 = lane == 0 ? 1u : 0u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int split = u / tiles;
+        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
+        const int kb1 =
+            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            umma_bf16_pred(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u, is0);
+          }
+          umma_commit_pred(&empty[stage], is0);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pred(&tfull[acc], is0);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      __syncwarp();
+    } else if (lane == 0) {
       // ---------------- MMA issuer (single thread issues and commits)
       constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN, B_MN);
       int stage = 0;
@@ -714,7 +758,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader && sh.issue == 1) {
+      // ---------------- MMA issuer (leader CTA), warp-converged, lane 0's predicate issues
+      constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
+      const uint32_t is0 = lane == 0 ? 1u : 0u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cluster_id; u < units; u += nclusters) {
+        const int split = u / tiles;
+        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
+        const int kb1 =
+            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kHalfBytes);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kHalfBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            umma_bf16_2sm_pred(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u, is0);
+          }
+          umma_commit_2sm_mc_pred(&empty[stage], 0x3, is0);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm_mc_pred(&tfull[acc], 0x3, is0);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      __syncwarp();
+    } else if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA only)
       constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
       int stage = 0;
@@ -1146,11 +1232,22 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   return RP_OK;
 }
 
+// MMA issue form of the GEMM kernels (A/B switch, read at launch): 1 warp-converged
+// predicated issue, 0 a single diverged lane
+static int g_mma_issue = 1;
+extern "C" int rp_set_mma_issue(int mode) {
+  if (mode < 0 || mode > 1) return rp_fail(RP_ERR_CONFIG, "mma issue mode must be 0 or 1");
+  g_mma_issue = mode;
+  return RP_OK;
+}
+
 extern "C" int rp_gemm_plan_launch(const RpGemmPlan* p, rp_stream_t stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!p) return RP_ERR_CONTRACT;
+  GemmShape sh = p->sh;
+  sh.issue = g_mma_issue;
   launch_k(p->kern, dim3(p->grid), dim3(kThreads), p->smem, stream, p->tmA, p->tmB, p->tmO,
-           p->tmO2, p->sh, p->ep);
+           p->tmO2, sh, p->ep);
   if (cudaPeekAtLastError() != cudaSuccess) return rp_check_launch("gemm");
   if (p->sh.splits > 1) {
     const int64_t n4 = p->red_n / 4;

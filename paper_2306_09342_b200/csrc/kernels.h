@@ -10,3 +10,6 @@
 int rp_fail(int code, const char* msg);
 // cudaGetLastError() -> RP_OK or RP_ERR_CUDA with the CUDA error string.
 int rp_check_launch(const char* what);
+// attention forward kernel variant (attention.cu, rp_set_attention_fwd_variant)
+int rp_attn_fwd_variant();
+unsigned long long* rp_attn_trace_buffer();

@@ -40,7 +40,66 @@ __global__ void bench(int M, int N, int ts, int chains, int n, int variant, long
   const uint32_t tmem = slot;
   // variant bit 0: whole warp 0 runs the loop, one elected lane issues (warp-uniform
   // control flow); bit 1: 8 MMAs per iteration with compile-time-constant operand offsets
-  if (static_cast<int>(warp) < issuers && (threadIdx.x & 31) == 0) {
+  if ((variant & 4) && static_cast<int>(warp) < issuers) {
+    // warp-convergent issue: all 32 lanes run the loop, elect.sync picks the issuing lane
+    // (the CUTLASS / DeepGEMM pattern), descriptors precomputed outside the loop
+    uint64_t& bar = bars[warp];
+    const uint32_t idesc = make_idesc_bf16(static_cast<uint32_t>(M), static_cast<uint32_t>(N), false, false);
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    uint64_t ad[4], bd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ad[j] = make_sdesc_sw128(a + j * 32, 16, 1024);
+      bd[j] = make_sdesc_sw128(b + j * 32, 16, 1024);
+    }
+    for (int rep = 0; rep < 2; ++rep) {
+      __syncwarp();
+      const long long t0 = clock64();
+      for (int i = 0; i < n; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t d = tmem + static_cast<uint32_t>((j % chains) * N);
+          if (variant & 8) {  // converged warp, predicate from a precomputed leader flag
+            const uint32_t leader = (threadIdx.x & 31) == 0;
+            asm volatile(
+                "{\n\t.reg .pred e;\n\tsetp.ne.b32 e, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n\t}" ::"r"(d),
+                "l"(ad[j & 3]), "l"(bd[j & 3]), "r"(idesc), "r"(leader)
+                : "memory");
+          } else if (variant & 16) {  // elect once, 1 divergent lane issues the block
+            if (j == 0 && (threadIdx.x & 31) == 0) {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+                asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(
+                                 tmem + static_cast<uint32_t>((jj % chains) * N)),
+                             "l"(ad[jj & 3]), "l"(bd[jj & 3]), "r"(idesc)
+                             : "memory");
+            }
+          } else if (ts)
+            asm volatile(
+                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 1;\n\t}" ::"r"(d),
+                "r"(tmem + 256u + static_cast<uint32_t>((j & 3) * 8)), "l"(bd[j & 3]), "r"(idesc)
+                : "memory");
+          else
+            asm volatile(
+                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n\t}" ::"r"(d),
+                "l"(ad[j & 3]), "l"(bd[j & 3]), "r"(idesc)
+                : "memory");
+        }
+      }
+      if ((threadIdx.x & 31) == 0) umma_commit(&bar);
+      __syncwarp();
+      const long long t1 = clock64();
+      mbar_wait(&bar, rep & 1);
+      const long long t2 = clock64();
+      if (rep == 1 && (threadIdx.x & 31) == 0 && warp == 0) {
+        out[0] = t1 - t0;
+        out[1] = t2 - t0;
+      }
+    }
+  } else if (static_cast<int>(warp) < issuers && (threadIdx.x & 31) == 0) {
     uint64_t& bar = bars[warp];
     const uint32_t idesc = make_idesc_bf16(static_cast<uint32_t>(M), static_cast<uint32_t>(N), false, false);
     const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
@@ -96,20 +155,24 @@ int main() {
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-  printf("issuers  N  cyc/mma(per issuer)  total_cyc\n");
-  const int variant = 2;
-  for (int issuers : {1, 2, 4})
-    for (int N : {64, 256}) {
-      const int n = 64;
-      bench<<<1, 128, 65536 + 1024>>>(128, N, 0, 1, n, variant, d, issuers);
-      long long h[2];
-      cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) {
-        printf("error %s\n", cudaGetErrorString(e));
-        return 1;
-      }
-      printf("%7d %4d  %18.1f  %9lld\n", issuers, N, static_cast<double>(h[1]) / n, h[1]);
-    }
+  printf("variant issuers ts  N chains  cyc/mma  total_cyc\n");
+  for (int variant : {2, 4, 12, 20})
+    for (int ts : {0})
+      for (int N : {64, 256})
+        for (int chains : {1, 2}) {
+          if (chains * N > 256 && ts) continue;  // TS: A lives at TMEM column 256
+          if (chains * N > 512) continue;
+          const int n = 64;
+          bench<<<1, 128, 65536 + 1024>>>(128, N, ts, chains, n, variant, d, 1);
+          long long h[2];
+          cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+          cudaError_t e = cudaGetLastError();
+          if (e != cudaSuccess) {
+            printf("error %s\n", cudaGetErrorString(e));
+            return 1;
+          }
+          printf("%7d %7d %2d %3d %6d  %7.1f  %9lld\n", variant, 1, ts, N, chains,
+                 static_cast<double>(h[1]) / n, h[1]);
+        }
   return 0;
 }
