@@ -332,12 +332,14 @@ def main_ours(a, rank, world, local_rank):
     pk = peaks()
     gms, gflops, glaunch = eng.gemm_profile(REPROP)  # kernels serialised: clean durations
     ach = gflops / (gms / 1e3) / 1e12
-    traffic = None  # DRAM bytes per GEMM launch, from the committed ncu capture (profiles/)
+    # DRAM bytes per GEMM launch: the ncu capture of this build's step committed under
+    # profiles/ (tools/gemm_traffic.py; re-captured whenever the kernels change)
+    traffic, traffic_src = None, "profiles/round2_gemm_traffic.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "round1_gemm_traffic_v5.json")) as f:
+        with open(os.path.join(ROOT, traffic_src)) as f:
             traffic = json.load(f)["avg_dram_bytes_per_launch"]
     except Exception:
-        pass
+        traffic_src = "unavailable"
     mf, hf = model_flops_per_img(dict(p, in_dim=cfg.in_dim, num_classes=cfg.num_classes))
     per_gpu = img_p / world
     launches = eng.graph_kernels(PAREPROP)
@@ -403,8 +405,8 @@ def main_ours(a, rank, world, local_rank):
                          "frac": ach / pk["bf16_sustained"],
                          "peak_note": f"{pk['source']} sustained bf16 (kernel timed inside a step)",
                          "launches_per_step": glaunch, "traffic": traffic,
-                         "traffic_note": "avg dram__bytes_read+write per GEMM launch, ncu, "
-                                         "profiles/round1_gemm_traffic_v5.json"},
+                         "traffic_note": "avg dram__bytes_read+write per GEMM launch of one "
+                                         "step, ncu, " + traffic_src},
             "gpu_launches": launches * a.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
