@@ -344,37 +344,50 @@ def main_ours(a, rank, world, local_rank):
     per_gpu = img_p / world
     launches = eng.graph_kernels(PAREPROP)
 
-    # PaReprop vs Reprop at a small per-GPU batch, where a single stream leaves SMs idle
-    # (context for the headline gain; same kernels, same device-timed protocol)
-    small = None
+    # The overlap bound at this batch: PaReprop with its two lanes free-running (no
+    # rendezvous; results garbage, timing only, rp_engine_set_diag) -- no schedule of the
+    # two lanes can beat it (profiles/round2_pareprop_bound.md sweeps the batch)
+    bound = None
+    if world == 1 and not a.no_small_batch:
+        eng.set_diag(1)
+        for _ in range(3):
+            eng.step(PAREPROP)
+        ms_free = timed(PAREPROP, a.steps)
+        eng.set_diag(0)
+        bound = {"free_running_lanes_ms_per_step": ms_free / a.steps,
+                 "gain_bound_pct": 100.0 * (ms_r / ms_free - 1.0)}
+    # PaReprop vs Reprop at small per-GPU batches, where a single stream leaves SMs idle
+    # (same kernels, same device-timed protocol)
+    small = []
     if world == 1 and not a.no_small_batch:
         eng.close()
-        ps = dict(p, batch=32)
-        es = Engine(ModelConfig(device=local_rank, seed=1234 + rank, **ps))
-        es.set_lr(1e-3)
-        for mode in (REPROP, PAREPROP):
-            for _ in range(max(a.warmup, 3)):
-                es.step(mode)
-        es.sync()
-        streams = torch.cuda.ExternalStream(es.stream_ptr)
-
-        def timed_small(mode, K):
-            torch.cuda.synchronize()
-            s0 = torch.cuda.Event(enable_timing=True)
-            e0 = torch.cuda.Event(enable_timing=True)
-            s0.record(streams)
-            for _ in range(K):
-                es.step(mode)
-            e0.record(streams)
-            e0.synchronize()
-            return s0.elapsed_time(e0)
-        k_small = max(a.steps, 10)
-        r_ms, p_ms = timed_small(REPROP, k_small), timed_small(PAREPROP, k_small)
-        small = {"per_gpu_batch": 32, "reprop_img_s": 32 * k_small / (r_ms / 1e3),
-                 "pareprop_img_s": 32 * k_small / (p_ms / 1e3),
-                 "gain_pct": 100.0 * (r_ms / p_ms - 1.0)}
-        es.close()
         eng = None
+        for bs in (8, 32):
+            es = Engine(ModelConfig(device=local_rank, seed=1234 + rank, **dict(p, batch=bs)))
+            es.set_lr(1e-3)
+            for mode in (REPROP, PAREPROP):
+                for _ in range(max(a.warmup, 3)):
+                    es.step(mode)
+            es.sync()
+            streams = torch.cuda.ExternalStream(es.stream_ptr)
+
+            def timed_small(mode, K):
+                torch.cuda.synchronize()
+                s0 = torch.cuda.Event(enable_timing=True)
+                e0 = torch.cuda.Event(enable_timing=True)
+                s0.record(streams)
+                for _ in range(K):
+                    es.step(mode)
+                e0.record(streams)
+                e0.synchronize()
+                return s0.elapsed_time(e0)
+            k_small = max(a.steps, 20)
+            r_ms = min(timed_small(REPROP, k_small) for _ in range(2))
+            p_ms = min(timed_small(PAREPROP, k_small) for _ in range(2))
+            small.append({"per_gpu_batch": bs, "reprop_img_s": bs * k_small / (r_ms / 1e3),
+                          "pareprop_img_s": bs * k_small / (p_ms / 1e3),
+                          "gain_pct": 100.0 * (r_ms / p_ms - 1.0)})
+            es.close()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -394,6 +407,7 @@ def main_ours(a, rank, world, local_rank):
             "reprop": {"value": img_r, "ms_per_step": ms_r / a.steps},
             "pareprop_gain_pct": 100.0 * (img_p / img_r - 1.0),
             "pareprop_gain_small_batch": small,
+            "pareprop_overlap_bound": bound,
             "mfu": mf * per_gpu / (pk["bf16"] * 1e12),
             "hfu": hf * per_gpu / (pk["bf16"] * 1e12),
             "loss": loss,

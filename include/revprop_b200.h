@@ -321,6 +321,10 @@ int rp_engine_set_caller_stream(RpEngine* engine, rp_stream_t stream);
  * Buffers: rp_engine_trace_floats() floats each, device memory; block b at the sum over
  * earlier blocks of 2 T_s d_s. NULL turns it off. Traced steps never use the CUDA graph. */
 int64_t rp_engine_trace_floats(const RpEngine* engine);
+/* Timing experiments only -- a step's numbers are garbage while flags != 0: 1 runs PaReprop's
+ * lanes R and G free (no rendezvous events; the upper bound of the overlap gain), 2 skips
+ * lane G's kernels, 4 skips lane R's. 0 restores the real schedule. */
+int rp_engine_set_diag(RpEngine* engine, int flags);
 int rp_engine_set_trace(RpEngine* engine, float* fwd, float* rec);
 /* Data parallelism over NCCL: one fp32 all-reduce (sum) per gradient
  * bucket on the engine's comm stream as soon as lane G finishes the bucket's owner, the

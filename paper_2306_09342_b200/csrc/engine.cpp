@@ -208,6 +208,10 @@ struct RpEngine {
   std::vector<std::pair<int64_t, int64_t>> bk_block, bk_bnd;
   int comm_reserve = 0;  // SMs kept free of GEMM CTAs for the NCCL kernels (world > 1)
   float quantum = 0.f;   // exact-coupling grid 2^-bits of the residual stream (0 = off)
+  // diagnostic schedule flags (rp_engine_set_diag; timing experiments only, results are
+  // garbage): 1 lanes R and G free-running (no rendezvous events), 2 skip lane G's kernels,
+  // 4 skip lane R's kernels
+  int diag = 0;
 };
 
 namespace {
@@ -816,16 +820,18 @@ int enqueue_step_impl(RpEngine* g, int mode) {
       led_release_block(g, b + (mode == 2 ? 2 : 1));
       led_charge_block(g, b, g->vmode ? St.led_cache : St.led_block);
       ++g->blocks_processed;
+      const bool free_lanes = (g->diag & 1) != 0;
       if (mode == 2) {
-        if (b + 2 <= g->L - 1)
+        if (b + 2 <= g->L - 1 && !free_lanes)
           RP_TRY(cuda_ok(cudaStreamWaitEvent(sR, g->evG[static_cast<size_t>(b + 2)], 0), "wait"));
-        RP_TRY(lane_r(g, b, sR));
+        if (!(g->diag & 4)) RP_TRY(lane_r(g, b, sR));
         RP_TRY(cuda_ok(cudaEventRecord(g->evR[static_cast<size_t>(b)], sR), "record"));
-        RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
-      } else {
+        if (!free_lanes)
+          RP_TRY(cuda_ok(cudaStreamWaitEvent(sG, g->evR[static_cast<size_t>(b)], 0), "wait"));
+      } else if (!(g->diag & 4)) {
         RP_TRY(lane_r(g, b, sG));
       }
-      RP_TRY(lane_g(g, b, sG, top, next_b2));
+      if (!(g->diag & 2)) RP_TRY(lane_g(g, b, sG, top, next_b2));
       RP_TRY(cuda_ok(cudaEventRecord(g->evG[static_cast<size_t>(b)], sG), "record"));
       RP_TRY(cuda_ok(cudaStreamWaitEvent(sC, g->evG[static_cast<size_t>(b)], 0), "wait"));
       RP_TRY(bucket_update(g, g->bk_block[static_cast<size_t>(b)].first,
@@ -2045,4 +2051,14 @@ extern "C" int rp_engine_sgd_update(RpEngine* g, const float* host_grads, float 
                  "sgd_update lr"));
   RP_TRY(rpk_sgd(g->params, g->grads, g->pb, g->P, g->lr_apply, scale, g->sG));
   return rp_engine_sync(g);
+}
+
+// Timing experiments only (the step's results are garbage while set): flags 1 = lanes R and G
+// free-running in PaReprop (no rendezvous: the upper bound of what overlapping them can
+// gain), 2 = skip lane G, 4 = skip lane R. 0 restores the real schedule.
+extern "C" int rp_engine_set_diag(RpEngine* g, int flags) {
+  if (!g) return rp_fail(RP_ERR_CONTRACT, "null engine");
+  if (flags < 0 || flags > 7) return rp_fail(RP_ERR_CONFIG, "diag flags must be in [0, 7]");
+  g->diag = flags;
+  return rp_engine_invalidate_graphs(g);
 }

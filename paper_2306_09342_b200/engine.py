@@ -139,6 +139,7 @@ _API = {
     "rp_engine_trace_floats": (_I64, [_P]),
     "rp_engine_set_trace": (_I, [_P, _P, _P]),
     "rp_model_bucket_plan": (_I, [C.POINTER(ModelConfigC), _P, _P, _P, _I64]),
+    "rp_engine_set_diag": (_I, [_P, _I]),
 }
 
 
@@ -314,6 +315,11 @@ class Engine:
         """Recompute trace buffers (device pointers, trace_floats() floats each; 0 = off)."""
         check(api("rp_engine_set_trace")(self._h, C.c_void_p(fwd_ptr or None),
                                          C.c_void_p(rec_ptr or None)), "set_trace")
+
+    def set_diag(self, flags: int):
+        """Timing experiments only (results are garbage while set): 1 free-running PaReprop
+        lanes, 2 skip lane G, 4 skip lane R; 0 = the real schedule."""
+        check(api("rp_engine_set_diag")(self._h, flags), "set_diag")
 
     def sync(self):
         check(api("rp_engine_sync")(self._h), "sync")
