@@ -64,6 +64,7 @@ def test_forward_trace_is_the_vanilla_stash():
         tr = torch.zeros(nf, device="cuda")
         eng.set_trace(tf.data_ptr(), tr.data_ptr())
         eng.step(mode, graph=False)
+        eng.sync()  # the step runs on the engine's own streams; order the trace reads after it
         out[mode] = (tf.cpu().numpy(), tr.cpu().numpy(), eng.grads(), eng.loss())
         eng.set_trace(0, 0)
     fv, rv, gv, lv = out[VANILLA]
