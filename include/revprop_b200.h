@@ -168,9 +168,11 @@ int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, const float* l
 /* D = rowsum(dO * O) (S N H floats) and, for the tcgen05 backward, the bf16 dS^T of every
  * (sequence, head) ([S H][Nk][Nk], Nk = N rounded up to 16) */
 int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
-/* 0 (default): tcgen05 kernels where they apply, backward = one dK/dV pass that also writes
- * dS^T + a dQ = dS K pass over it; 1: warp-level mma.sync only; 2: tcgen05 with the
- * two-pass backward (dQ pass, dK/dV pass, each recomputing S and dP; no dS stored).
+/* 0 (default): tcgen05 kernels where they apply; backward for N <= 208 = one fused pass per
+ * (sequence, head, 128-key tile) with dS kept on chip, above that one dK/dV pass that also
+ * writes dS^T + a dQ = dS K pass over it; 1: warp-level mma.sync only; 2: tcgen05 with the
+ * two-pass backward (dQ pass, dK/dV pass, each recomputing S and dP; no dS stored);
+ * 3: tcgen05 with the dS^T round trip at every N <= 256 (the round-1 default).
  * Process-global; other values are RP_ERR_CONFIG. Captured engine graphs keep the kernels
  * they were captured with: call rp_engine_invalidate_graphs after changing it. */
 int rp_set_attention_impl(int impl);

@@ -546,10 +546,12 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
                         float* lse, cudaStream_t stream);
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready);
-// 0 = tcgen05 where it applies (head_dim 64), backward as one dK/dV pass + dQ from the
-// stored dS^T; 1 = mma.sync only; 2 = tcgen05 with the two-pass (dQ pass, dK/dV pass)
-// backward that keeps no dS
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready,
+                        int fused);
+// 0 = tcgen05 where it applies (head_dim 64): backward in one fused pass for N <= 208
+// (attention_bwd_fused.cu), above that one dK/dV pass + dQ from the stored dS^T;
+// 1 = mma.sync only; 2 = tcgen05 with the two-pass (dQ pass, dK/dV pass) backward that
+// keeps no dS; 3 = tcgen05 with the dS^T round trip at every N <= 256 (the previous default)
 static int g_attn_impl = 0;
 
 // clock64 trace of the ping-pong forward's CTA 0 (tools/attn_fwd_trace.py): on when set
@@ -573,7 +575,7 @@ extern "C" int rp_set_attention_fwd_variant(int v) {
 // Process-global switch, read when a step is enqueued: engines must drop their captured
 // graphs (rp_engine_invalidate_graphs) after changing it, or the graphs keep the old kernels.
 extern "C" int rp_set_attention_impl(int impl) {
-  if (impl < 0 || impl > 2) return rp_fail(RP_ERR_CONFIG, "attention impl must be 0, 1 or 2");
+  if (impl < 0 || impl > 3) return rp_fail(RP_ERR_CONFIG, "attention impl must be 0, 1, 2 or 3");
   g_attn_impl = impl;
   return RP_OK;
 }
@@ -682,10 +684,11 @@ extern "C" int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, con
   if (g_attn_impl != 1 && head_dim == 64) {  // tcgen05 path computes D itself
     // dS^T storage pays off while it is small next to the dQ pass it replaces (measured:
     // 495 -> 450 us at N = 197, a loss at N = 512)
-    uint16_t* dst = g_attn_impl == 0 && N <= kFusedBwdMaxN
+    uint16_t* dst = (g_attn_impl == 0 || g_attn_impl == 3) && N <= kFusedBwdMaxN
                         ? reinterpret_cast<uint16_t*>(workspace + attn_ds_offset(B, N, H))
                         : nullptr;
-    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst, d_ready);
+    rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst, d_ready,
+                             g_attn_impl == 0);
     if (rc != RP_ERR_CONFIG) return rc;
   }
   if (head_dim <= 32)

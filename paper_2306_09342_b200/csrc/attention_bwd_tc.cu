@@ -537,9 +537,14 @@ using namespace rp;
 //   dSt != nullptr: D first (attn_d_kernel), then ONE pass over (key tile, query chunk)
 //     computing dK / dV and writing dS^T (bf16, [S*H][Nk][Nk]) on the way, then dQ = dS K
 //     as a streamed MMA over dS^T (attn_dq_tc) -- S and dP are formed once instead of twice.
+int rp_attention_bwd_fused_tc(const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                              const float* Dg, float* scratch, int64_t S, int64_t N, int64_t H,
+                              uint16_t* dqkv, cudaStream_t stream);
+
 int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
-                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready) {
+                        uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready,
+                        int fused) {
   using namespace attn_tc;
   if (N > 1024 || N < 1) return RP_ERR_CONFIG;
   BwdGeom g;
@@ -573,6 +578,18 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
   pl.ntile = static_cast<int>((N + 127) / 128);
   pl.nitems = static_cast<int>(S * H) * pl.ntile;
   const unsigned grid = static_cast<unsigned>(pl.nitems < 2 * nsm ? pl.nitems : 2 * nsm);
+  if (dSt != nullptr && fused && N <= 208) {
+    // single pass (attention_bwd_fused.cu); the dS^T region is its dQ scratch
+    if (!d_ready) {
+      const int64_t n = T * H * 8;
+      launch_k(attn_d_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
+               reinterpret_cast<const __nv_bfloat16*>(out),
+               reinterpret_cast<const __nv_bfloat16*>(dout), Dg, T, g.N, g.H);
+    }
+    const int rc = rp_attention_bwd_fused_tc(qkv, dout, lse, Dg, reinterpret_cast<float*>(dSt), S, N,
+                                             H, dqkv, stream);
+    if (rc != RP_ERR_CONFIG) return rc;
+  }
   if (dSt != nullptr) {
     CUtensorMap ds;
     if (make_map(&ds, dSt, S * H * g.Nk, g.Nk, 64))

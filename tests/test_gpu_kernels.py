@@ -245,7 +245,7 @@ def attn_ref(qkv, B, N, H, hd=64):
     return o.permute(0, 2, 1, 3).reshape(B * N, H * hd), torch.logsumexp(s, -1)
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["tcgen05", "mma_sync", "tcgen05_2pass"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["tcgen05", "mma_sync", "tcgen05_2pass", "tcgen05_dst"])
 def impl(request):
     """The process-global attention implementation switch, restored whatever the test
     does (a failed assertion must not leave impl 1 / 2 active for later tests)."""
@@ -259,14 +259,15 @@ def impl(request):
 
 def test_attention_impl_switch_validates():
     from paper_2306_09342_b200 import _capi
-    assert _capi.lib().rp_set_attention_impl(3) == 3  # RP_ERR_CONFIG
+    assert _capi.lib().rp_set_attention_impl(4) == 3  # RP_ERR_CONFIG
     assert _capi.lib().rp_set_attention_impl(-1) == 3
     assert _capi.lib().rp_set_attention_impl(0) == 0
 
 
 @pytest.mark.parametrize("B,N,H", [(2, 197, 12), (3, 64, 2), (1, 5, 1), (2, 512, 4), (1, 130, 3), (2, 300, 2), (1, 480, 3), (3, 768, 1),
                                    (3, 256, 2), (2, 129, 1), (3, 1, 2), (8, 2, 4), (1, 17, 1),
-                                   (4, 257, 1)])
+                                   (4, 257, 1), (3, 208, 5), (2, 128, 3), (1, 144, 2), (2, 200, 7),
+                                   (300, 197, 1)])
 def test_attention_fwd_bwd(K, B, N, H, impl):
     torch.manual_seed(7919 * B + 131 * N + H)  # inputs fixed per case (order-independent)
     qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()

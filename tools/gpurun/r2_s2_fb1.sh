@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "attention_fwd_bwd or impl_switch" > gpurun_out/s2_fb1_tests.log 2>&1; echo tests rc=$?
+tail -15 gpurun_out/s2_fb1_tests.log
+timeout 300 python tools/attn_bwd_ab.py 3 0 2 > gpurun_out/s2_fb1_ab.log 2>&1; echo ab rc=$?
+cat gpurun_out/s2_fb1_ab.log | tail -8

@@ -213,15 +213,15 @@ int main() {
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-  printf("variant issuers ts  N chains  cyc/mma  total_cyc\n");
+  // cycles per MMA as a function of the number of MMAs n: a fixed start-up / completion
+  // cost shows up as cyc/mma falling with n; the slope between two n is the true rate
+  printf("variant issuers  N chains     n  issue_cyc  total_cyc  cyc/mma\n");
   for (int variant : {2, 12})
-    for (int ts : {0})
-      for (int N : {64, 256})
-        for (int chains : {1, 2}) {
-          if (chains * N > 256 && ts) continue;  // TS: A lives at TMEM column 256
-          if (chains * N > 512) continue;
-          const int n = 64;
-          bench<<<1, 128, 65536 + 1024>>>(128, N, ts, chains, n, variant, d, 1);
+    for (int N : {64, 128, 256})
+      for (int issuers : {1, 2, 4})
+        for (int n : {64, 256, 1024, 4096}) {
+          if (issuers * N > 512) continue;
+          bench<<<1, 128, 65536 + 1024>>>(128, N, 0, 1, n, variant, d, issuers);
           long long h[2];
           cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
           cudaError_t e = cudaGetLastError();
@@ -229,18 +229,8 @@ int main() {
             printf("error %s\n", cudaGetErrorString(e));
             return 1;
           }
-          printf("%7d %7d %2d %3d %6d  %7.1f  %9lld\n", variant, 1, ts, N, chains,
-                 static_cast<double>(h[1]) / n, h[1]);
+          printf("%7d %7d %3d %6d %5d  %9lld  %9lld  %7.1f\n", variant, issuers, N, 1, n, h[0], h[1],
+                 static_cast<double>(h[1]) / n);
         }
-  for (int nw : {1, 2, 4})
-    for (int N : {64, 256}) {
-      cudaFuncSetAttribute(bench_alt, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-      const int n = 64;
-      bench_alt<<<1, 128, 65536 + 1024>>>(N, n, nw, d);
-      long long h = 0;
-      cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-      printf("alternating issuers %d N %3d: %.1f cyc/mma  (%s)\n", nw, N, double(h) / n,
-             cudaGetErrorString(cudaGetLastError()));
-    }
   return 0;
 }
