@@ -11,22 +11,23 @@
 //   MMA1   S^T  = K_kt Q^T   -> [0, Nk)          N = Nk (all queries in one instruction per
 //          dP^T = V_kt dO^T  -> [256, 256 + Nk)  K-step; two issuing warps, one product each)
 //   EW     16 warps (TMEM lane quarter w%4, 16-query chunks c = w/4 mod 4) read S^T, dP^T:
-//            P^T  = exp2(S^T scale log2e - lse_q)          bf16, packed into the chunk's own
-//                                                          first 8 columns (A operand of dV)
+//            P^T  = exp2(S^T scale log2e - lse_q)          bf16, packed into [0, 128)
+//                                                          (p_col; A operand of dV)
 //            dS^T = P^T (dP^T - D_q) scale                 bf16, to shared memory, 8-key x
 //                                                          64-query SW128 atoms: the K-major
 //                                                          A of dK and the MN-major A of dQ
-//   MMA2   dV  = P^T dO        (A TMEM)          -> [256, 320)   warp 17
-//          dK  = dS^T Q        (A smem K-major)  -> [320, 384)   warp 18
-//          dQ0 = dS[q<128] K_kt (A smem MN-major)-> [384, 448)   warp 19
-//          dQ1 = dS[q>=128] K_kt                 -> [448, 512)   warp 16 (Nk > 128)
-//          (all four over the consumed dP^T columns: P^T, the A of dV, is spread over
-//          [0, Nk) and must not overlap an accumulator)
+//   MMA2   dV  = P^T dO        (A TMEM, p_col)   -> [128, 192)   warp 17
+//          dK  = dS^T Q        (A smem K-major)  -> [224, 288)   warp 18
+//          dQ0 = dS[q<128] K_kt (A smem MN-major)-> [288, 352)   warp 19
+//          dQ1 = dS[q>=128] K_kt                 -> [352, 416)   warp 16 (Nk > 128)
+//          (over consumed S^T / dP^T columns; P^T, the A of dV, stays in [0, 128))
 //          four issuing warps on four SM sub-partitions: every product has N = 64, and one
 //          thread issues at most one such MMA per ~120 cycles (tools/umma2sm_bench.cu)
-//   EPI    the same 16 warps drain dV, dK (bf16 -> d_qkv) and dQ: the first key tile's dQ
-//          partial goes to a per-CTA fp32 scratch slot (L2-resident), the last key tile adds
-//          it (fixed order partial_0 + partial_1: deterministic) and writes bf16.
+//   EPI    the same 16 warps drain dV, dK and dQ into bf16 SW128 staging tiles (the dS^T
+//          region, consumed by then) that warp 19 writes out with bulk tensor stores. The first
+//          key tile's dQ partials wait for the second: dQ0 parked in TMEM columns the pair's
+//          later MMAs never touch, dQ1 (fp32) in a per-CTA scratch slot (L2-resident); the
+//          last key tile adds them (fixed order partial_0 + partial_1: deterministic).
 // No dS leaves the SM (the previous path wrote dS^T, 2 N^2 bytes per head, and read it back
 // in a second kernel). Each output element is written by one thread of one CTA.
 #include "attn_common.cuh"
@@ -42,6 +43,28 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
           reinterpret_cast<uint64_t>(map)),
       "r"(c0), "r"(c1), "r"(c2), "r"(src)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+
+// fp32 [rows][64] scratch: boxes of 32 columns x 128 rows, SWIZZLE_128B
+inline int make_map_scratch(CUtensorMap* m, const float* base, int64_t rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return RP_ERR_CUDA;
+  cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? RP_OK
+             : RP_ERR_CUDA;
 }
 
 // bf16 [S][N][cols] view of a [S N][ld] row-major matrix: boxes of 64 columns x 128 rows,
@@ -63,6 +86,14 @@ inline int make_map_seq(CUtensorMap* m, const void* base, int64_t S, int64_t N, 
 }
 
 constexpr int kEwWarps = 16;
+
+// TMEM column of the packed bf16 P^T of 16-query chunk c (8 columns). Warp cg converts
+// chunks cg, cg + 4, cg + 8, cg + 12 in that order and packs them into the S^T columns of
+// its own first two chunks (cg and cg + 4), which it has already read: race-free, and P^T
+// occupies only [0, 128), leaving [128, 256) whole for accumulators.
+__device__ __forceinline__ uint32_t p_col(int c) {
+  return static_cast<uint32_t>(16 * (c & 3) + 64 * (c >> 3) + 8 * ((c >> 2) & 1));
+}
 constexpr int kFbThreads = (kEwWarps + 4) * 32;  // + TMA/dQ1, S^T/dV, dP^T/dK, dQ0
 constexpr int kMaxNk = 208;
 
@@ -90,13 +121,14 @@ __host__ __device__ inline int fb_smem(const FbGeom& g) { return fb_off_ds(g) + 
 __global__ void __launch_bounds__(kFbThreads, 1)
     attn_bwd_fused_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_do,
-                      const __grid_constant__ CUtensorMap tm_dqkv, const float* __restrict__ lse,
+                      const __grid_constant__ CUtensorMap tm_dqkv,
+                      const __grid_constant__ CUtensorMap tm_scr, const float* __restrict__ lse,
                       const float* __restrict__ Dg, float* __restrict__ dq_scratch, FbGeom g) {
   pdl_trigger();
 
   __shared__ __align__(16) float sL[2][kMaxNk];  // -lse (log2 domain) per query, -inf past N
   __shared__ __align__(16) float sD[2][kMaxNk];  // -D * scale per query, 0 past N (per pair)
-  __shared__ __align__(8) uint64_t bars[12];
+  __shared__ __align__(8) uint64_t bars[16];
   __shared__ uint32_t tmem_slot;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -108,6 +140,9 @@ __global__ void __launch_bounds__(kFbThreads, 1)
   uint64_t* bar_ew = bars + 6;   //     P^T in TMEM, dS^T in smem (16 warps)
   uint64_t* bar_m2 = bars + 7;   //     dV, dK, dQ accumulated (3 or 4 issuers)
   uint64_t* bar_epi = bars + 8;  //     accumulators drained, TMEM free (16 warps)
+  uint64_t* bar_stg = bars + 9;  //     outputs staged in the dS^T region (16 warps)
+  uint64_t* bar_scr = bars + 10;    //  a first key tile's dQ1 partial is in global memory
+  uint64_t* bar_sfree = bars + 11;  // [4] staging tile t (= dS^T 64-query chunk t) read out
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int Nk = g.Nk, nch = Nk / 16, ntile = g.ntile;
@@ -118,6 +153,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_dqkv);
+      tma_prefetch_desc(&tm_scr);
       for (int i = 0; i < 2; ++i) {
         mbar_init(&qd_full[i], 1);
         mbar_init(&k_full[i], 1);
@@ -127,6 +163,9 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       mbar_init(bar_ew, kEwWarps);
       mbar_init(bar_m2, two ? 4 : 3);
       mbar_init(bar_epi, kEwWarps);
+      mbar_init(bar_stg, kEwWarps);
+      for (int t = 0; t < 4; ++t) mbar_init(&bar_sfree[t], 1);
+      mbar_init(bar_scr, 1);
       fence_barrier_init();
     }
     tmem_alloc(&tmem_slot, 512);
@@ -196,7 +235,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
           const uint32_t kb = s_k + static_cast<uint32_t>((i & 1) * 16384);
           const int ns = dq_steps(kt);
           for (int ks = 0; ks < ns; ++ks)
-            umma_bf16_pred(tmem + 448u,
+            umma_bf16_pred(tmem + 352u,
                            make_sdesc_sw128(s_ds + 2u * 16384u + static_cast<uint32_t>(ks) * 2048u, 16384, 1024),
                            make_sdesc_sw128(kb + static_cast<uint32_t>(ks) * 2048u, 8192, 1024), idesc_q,
                            ks > 0 ? 1u : 0u, is0);
@@ -235,13 +274,13 @@ __global__ void __launch_bounds__(kFbThreads, 1)
         if (role == 1) {  // dV += P^T dO   (A = P^T from TMEM, chunk c packed at column 16c)
           const uint32_t bo = s_do(j);
           for (int c = 0; c < nch; ++c)
-            umma_ts_bf16_pred(tmem + 256u, tmem + static_cast<uint32_t>(16 * c),
+            umma_ts_bf16_pred(tmem + 128u, tmem + p_col(c),
                               make_sdesc_sw128(bo + static_cast<uint32_t>(c) * 2048u, 8192, 1024),
                               idesc_kv, c > 0 ? 1u : 0u, is0);
         } else {  // dK += dS^T Q   (A = dS^T from smem, K-major)
           const uint32_t bq = s_q(j);
           for (int c = 0; c < nch; ++c)
-            umma_bf16_pred(tmem + 320u,
+            umma_bf16_pred(tmem + 224u,
                            make_sdesc_sw128(s_ds + static_cast<uint32_t>(c >> 2) * 16384u +
                                                 static_cast<uint32_t>(c & 3) * 32u,
                                             16, 1024),
@@ -260,14 +299,53 @@ __global__ void __launch_bounds__(kFbThreads, 1)
         const uint32_t kb = s_k + static_cast<uint32_t>((i & 1) * 16384);
         const int ns = dq_steps(kt);
         for (int ks = 0; ks < ns; ++ks)
-          umma_bf16_pred(tmem + 384u,
+          umma_bf16_pred(tmem + 288u,
                          make_sdesc_sw128(s_ds + static_cast<uint32_t>(ks) * 2048u, 16384, 1024),
                          make_sdesc_sw128(kb + static_cast<uint32_t>(ks) * 2048u, 8192, 1024), idesc_q,
                          ks > 0 ? 1u : 0u, is0);
         umma_commit_pred(bar_m2, is0);
         FB_TRACE(i, 9);
         __syncwarp();
+        // the epilogue's bulk stores: bf16 dV, dK (and dQ on the last key tile) into d_qkv,
+        // rows past N clipped by the [S][N][cols] map; the first key tile's dQ1 partial (fp32,
+        // two 32-column halves) into this CTA's scratch slot
+        const int j = i / ntile, p = pair_of(j), b = p / g.H, h = p % g.H;
+        mbar_wait(bar_stg, static_cast<uint32_t>(i & 1));
+        if (lane == 0) {
+          // one bulk group per staging tile, released one by one: the next item's dS^T
+          // writes (64-query chunk t = staging tile t, in order) wait only for their tile
+          tma_store_3d(&tm_dqkv, s_ds, 2 * d + h * 64, kt * 128, b);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          tma_store_3d(&tm_dqkv, s_ds + 16384u, d + h * 64, kt * 128, b);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          if (kt == ntile - 1) {
+            tma_store_3d(&tm_dqkv, s_ds + 32768u, h * 64, 0, b);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (two) tma_store_3d(&tm_dqkv, s_ds + 49152u, h * 64, 128, b);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          } else {
+            tma_store_2d(&tm_scr, s_ds + 32768u, 0, cta * 128);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            tma_store_2d(&tm_scr, s_ds + 49152u, 32, cta * 128);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+          mbar_arrive(&bar_sfree[0]);
+          asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+          mbar_arrive(&bar_sfree[1]);
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive(&bar_sfree[2]);
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&bar_sfree[3]);
+          if (kt != ntile - 1) {  // the partial must be in global memory before it is read
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_arrive(bar_scr);
+          }
+        }
+        __syncwarp();
       }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   } else {
     // ------------------------------------------------ elementwise + epilogue warps
@@ -284,10 +362,14 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const uint32_t srow = s_ds + static_cast<uint32_t>(kl) * 128u;
     const uint32_t su0 = ((2u * static_cast<uint32_t>(cg)) ^ sw) << 4;
     const uint32_t su1 = ((2u * static_cast<uint32_t>(cg) + 1u) ^ sw) << 4;
-    // dQ partial of the first key tile: this CTA's fp32 slot, [64 / 4 column quads][Nk
-    // queries][4] so a warp's 16-byte accesses cover 512 contiguous bytes
-    float4* scratch = reinterpret_cast<float4*>(dq_scratch + static_cast<int64_t>(cta) * Nk * 64) +
-                      static_cast<int64_t>(4 * cg) * Nk;
+    // dQ partials of the first key tile: dQ0 parked in TMEM columns no later MMA of the pair
+    // writes ([208, 224) and [464, 512): S^T / dP^T use [0, Nk) and [256, 256 + Nk), Nk <=
+    // 208; the accumulators avoid them), this warp's 16 columns at `park`; dQ1 through the
+    // CTA's fp32 scratch slot
+    // [128 rows][64] (bulk store from staging, read back row-wise)
+    const uint32_t park = cg < 3 ? 464u + 16u * static_cast<uint32_t>(cg) : 208u;
+    const float4* scr_row = reinterpret_cast<const float4*>(dq_scratch + (static_cast<int64_t>(cta) * 128 + kl) * 64) +
+                            4 * cg;
     auto load_lse = [&](int j, int buf) {  // the pair's -lse and -D * scale, per query
       const int p = pair_of(j);
       const int64_t hb = (static_cast<int64_t>(p / g.H) * g.H + p % g.H) * g.N;
@@ -295,6 +377,16 @@ __global__ void __launch_bounds__(kFbThreads, 1)
         sL[buf][t] = t < g.N ? -lse[hb + t] : -INFINITY;
         sD[buf][t] = t < g.N ? -Dg[hb + t] * g.scale : 0.f;
       }
+    };
+    // fp32 staging of the dQ1 partial: two 128-row x 32-column SW128 tiles at 32 / 48 KB
+    auto stage16f = [&](const float* v) {
+      const uint32_t base = s_ds + 32768u + static_cast<uint32_t>(cg >> 1) * 16384u +
+                            static_cast<uint32_t>(kl) * 128u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        sts128_a(base + (((static_cast<uint32_t>((cg & 1) * 4 + u)) ^ sw) << 4),
+                 make_uint4(__float_as_uint(v[4 * u]), __float_as_uint(v[4 * u + 1]),
+                            __float_as_uint(v[4 * u + 2]), __float_as_uint(v[4 * u + 3])));
     };
     auto stage16 = [&](uint32_t tile, const float* v) {
       const uint32_t base = srow + tile * 16384u;
@@ -315,10 +407,6 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       mbar_wait(bar_s, static_cast<uint32_t>(i & 1));
       tc_fence_after();
       if (warp == 0) FB_TRACE(i, 3);
-      if (i > 0) {  // every warp's output stores of item i-1 have read the staging region
-        if (warp == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        named_bar(2, kEwWarps * 32);
-      }
       if (warp == 0) FB_TRACE(i, 20);
       for (int c = cg; c < nch; c += 4) {
         float s[16], dp[16];
@@ -343,8 +431,10 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             pd[2 * u + t] = pack_bf16x2(d0, d1);
           }
         }
-        tmem_st8(tmem + lq + static_cast<uint32_t>(16 * c), pp);  // over this chunk's own S^T
-        // dS^T (16 queries = two 16-byte units of the 64-query chunk c/4) into the atom row
+        tmem_st8(tmem + lq + p_col(c), pp);  // over S^T columns this warp has read
+        // dS^T (16 queries = two 16-byte units of the 64-query chunk c/4) into the atom row,
+        // once item i-1's output store has read that staging tile
+        if (i > 0) mbar_wait(&bar_sfree[c >> 2], static_cast<uint32_t>((i - 1) & 1));
         const uint32_t row = ds_row + static_cast<uint32_t>(c >> 2) * 16384u;
         const uint32_t u0 = static_cast<uint32_t>((c & 3) * 2);
         sts128_a(row + ((u0 ^ sw) << 4), make_uint4(pd[0], pd[1], pd[2], pd[3]));
@@ -359,16 +449,13 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       if (warp == 15) FB_TRACE(i, 5);
       // under MMA2: the next pair's -lse / -D, and the first key tile's dQ partial
       if (last && j + 1 < npc) load_lse(j + 1, (j + 1) & 1);
-      float4 part[2][4];
+      float4 part[4];  // the dQ1 partial of this pair's first key tile (rows 128 + kl)
       const bool add_part = ntile == 2 && kt == 1;
-      if (add_part) {
+      if (add_part) {  // written by the bulk store (async proxy): L1-bypassing loads
+        mbar_wait(bar_scr, static_cast<uint32_t>(j & 1));
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int qr = mt * 128 + kl;
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            part[mt][e] = qr < Nk ? scratch[e * Nk + qr] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int e = 0; e < 4; ++e)
+          part[e] = 128 + kl < Nk ? __ldcg(scr_row + e) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       // ---- epilogue: 16 columns of each accumulator per warp
       mbar_wait(bar_m2, static_cast<uint32_t>(i & 1));
@@ -376,62 +463,50 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       if (warp == 0) FB_TRACE(i, 11);
       {
         float v[16], k[16];
-        tmem_ld16x2(tmem + lq + 256u + static_cast<uint32_t>(16 * cg),
-                    tmem + lq + 320u + static_cast<uint32_t>(16 * cg), v, k);
+        tmem_ld16x2(tmem + lq + 128u + static_cast<uint32_t>(16 * cg),
+                    tmem + lq + 224u + static_cast<uint32_t>(16 * cg), v, k);
         stage16(0, v);
         stage16(1, k);
       }
       float q0[16], q1[16];
-      tmem_ld16x2(tmem + lq + 384u + static_cast<uint32_t>(16 * cg),
-                  tmem + lq + 448u + static_cast<uint32_t>(16 * cg), q0, q1);
+      tmem_ld16x2(tmem + lq + 288u + static_cast<uint32_t>(16 * cg),
+                  tmem + lq + 352u + static_cast<uint32_t>(16 * cg), q0, q1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_epi);
       if (warp == 0) FB_TRACE(i, 12);
       if (warp == 0) FB_TRACE(i, 16);
-      const bool store_q = last;
-      if (ntile == 2 && kt == 0) {  // first key tile: fp32 partial to this CTA's slot
+      if (ntile == 2 && kt == 0) {  // first key tile: park dQ0, stage the fp32 dQ1 partial
+        uint32_t pq[16];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int qr = mt * 128 + kl;
-          const float* o = mt == 0 ? q0 : q1;
-          if (qr < Nk) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              scratch[e * Nk + qr] = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
-          }
-        }
+        for (int e = 0; e < 16; ++e) pq[e] = __float_as_uint(q0[e]);
+        tmem_st16(tmem + lq + park, pq);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        stage16f(q1);
       } else {
-        if (add_part) {  // partial_0 + partial_1
+        if (add_part) {  // partial_0 + partial_1, in this order
+          float p0[16];
+          tmem_ld16(tmem + lq + park, p0);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) q0[e] = p0[e] + q0[e];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            q0[4 * e] = part[0][e].x + q0[4 * e];
-            q0[4 * e + 1] = part[0][e].y + q0[4 * e + 1];
-            q0[4 * e + 2] = part[0][e].z + q0[4 * e + 2];
-            q0[4 * e + 3] = part[0][e].w + q0[4 * e + 3];
-            q1[4 * e] = part[1][e].x + q1[4 * e];
-            q1[4 * e + 1] = part[1][e].y + q1[4 * e + 1];
-            q1[4 * e + 2] = part[1][e].z + q1[4 * e + 2];
-            q1[4 * e + 3] = part[1][e].w + q1[4 * e + 3];
+            q1[4 * e] = part[e].x + q1[4 * e];
+            q1[4 * e + 1] = part[e].y + q1[4 * e + 1];
+            q1[4 * e + 2] = part[e].z + q1[4 * e + 2];
+            q1[4 * e + 3] = part[e].w + q1[4 * e + 3];
           }
         }
         stage16(2, q0);
         stage16(3, q1);
       }
       if (warp == 0) FB_TRACE(i, 17);
-      fence_proxy_async_smem();
-      named_bar(3, kEwWarps * 32);  // all tiles staged
+      fence_proxy_async_smem();  // staged tiles are read by the bulk stores (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_stg);
       if (warp == 0) FB_TRACE(i, 18);
-      if (warp == 0 && lane == 0) {  // rows past N are clipped by the [S][N][cols] tensor map
-        tma_store_3d(&tm_dqkv, s_ds, 2 * d + h * 64, kt * 128, b);
-        tma_store_3d(&tm_dqkv, s_ds + 16384u, d + h * 64, kt * 128, b);
-        if (store_q) tma_store_3d(&tm_dqkv, s_ds + 32768u, h * 64, 0, b);
-        if (store_q && two) tma_store_3d(&tm_dqkv, s_ds + 49152u, h * 64, 128, b);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
       if (warp == 0) FB_TRACE(i, 13);
     }
-    if (warp == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -448,7 +523,7 @@ unsigned long long* rp_attn_trace_buffer();
 
 // Returns RP_ERR_CONFIG (nothing launched) when the shape is outside this kernel
 // (head_dim 64 is the caller's check; N <= 208 here). `Dg` holds D = rowsum(dO * O) per
-// (sequence, head, query); `scratch` >= min(S H, #SMs) * Nk * 64 floats when N > 128.
+// (sequence, head, query); `scratch` >= min(S H, #SMs) * 128 * 64 floats when N > 128.
 int rp_attention_bwd_fused_tc(const uint16_t* qkv, const uint16_t* dout, const float* lse,
                               const float* Dg, float* scratch, int64_t S, int64_t N, int64_t H,
                               uint16_t* dqkv, cudaStream_t stream) {
@@ -481,14 +556,15 @@ int rp_attention_bwd_fused_tc(const uint16_t* qkv, const uint16_t* dout, const f
   });
   if (smem > max_optin - 4096) return RP_ERR_CONFIG;
   const int64_t T = S * N;
-  CUtensorMap mq, mk, mdo, mdq;
+  const unsigned grid = static_cast<unsigned>(g.npairs < nsm ? g.npairs : nsm);
+  CUtensorMap mq, mk, mdo, mdq, msc;
   if (make_map(&mq, qkv, T, 3 * H * 64, static_cast<uint32_t>(g.Nk)) ||
       make_map(&mk, qkv, T, 3 * H * 64, 128) ||
       make_map(&mdo, dout, T, H * 64, static_cast<uint32_t>(g.Nk)) ||
-      make_map_seq(&mdq, dqkv, S, N, 3 * H * 64, 3 * H * 64))
+      make_map_seq(&mdq, dqkv, S, N, 3 * H * 64, 3 * H * 64) ||
+      make_map_scratch(&msc, scratch, static_cast<int64_t>(grid) * 128))
     return rp_fail(RP_ERR_CUDA, "attention_bwd_fused: tensor map encode failed");
-  const unsigned grid = static_cast<unsigned>(g.npairs < nsm ? g.npairs : nsm);
   launch_k(attn_bwd_fused_tc, dim3(grid), dim3(kFbThreads), static_cast<size_t>(smem), stream, mq, mk,
-           mdo, mdq, lse, Dg, scratch, g);
+           mdo, mdq, msc, lse, Dg, scratch, g);
   return rp_check_launch("attention_bwd_fused");
 }
