@@ -30,9 +30,15 @@ b1 = torch.randn(h, device=dev) * 0.1
 o1 = torch.empty(T, h, device=dev, dtype=torch.bfloat16)
 o2 = torch.empty_like(o1)
 res = {}
+x3 = torch.randn(T, h, device=dev).bfloat16()
+w2 = (torch.randn(h, d, device=dev) * 0.03).bfloat16()
+dy = torch.randn(T, d, device=dev).bfloat16()
+part = torch.empty((T + 31) // 32, h, device=dev)
 res["bias_gelu_slope"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BIAS_GELU_SLOPE,
-                                         out=o1, out2=o2, bias=b1))
-res["bias_gelu_u"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BIAS_GELU,
-                                     out=o1, out2=o2, bias=b1))
-res["bf16"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BF16, out=o1))
+                                         out=o1, out2=o2, bias=b1, bn=512))
+res["bias_gelu"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BIAS_GELU,
+                                   out=o1, bias=b1, bn=512))
+res["slope_mul"] = t(lambda: K.gemm(dy, w2, T, h, d, b_mn=False, epi=_capi.RP_EPI_MUL, out=o1, aux=o2,
+                                   colsum_part=part, bn=512))
+res["bf16"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BF16, out=o1, bn=512))
 print(" ".join(f"{k} {v:.1f}us" for k, v in res.items()))
