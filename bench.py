@@ -389,6 +389,52 @@ def main_ours(a, rank, world, local_rank):
                           "gain_pct": 100.0 * (r_ms / p_ms - 1.0)})
             es.close()
 
+    # RevViT-L (BASELINE's metric names RevViT-B/L; configs[2] is L data parallel at
+    # 1/2/4/8 GPUs): the same device-timed protocol on the L preset, per-GPU batch 256, at
+    # every world size (its own NCCL communicator for N > 1)
+    revvit_l = None
+    if not a.no_revvit_l:
+        if eng is not None:
+            eng.close()
+            eng = None
+        pl_ = dict(PRESETS["revvit-l"])
+        el = Engine(ModelConfig(device=local_rank, seed=1234, **pl_))
+        el.synthetic_batch(1234 + rank)
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            el.comm_init(obj[0], world, rank)
+        el.set_lr(1e-3)
+        sl_ = torch.cuda.ExternalStream(el.stream_ptr)
+        for mode in (REPROP, PAREPROP):
+            for _ in range(3):
+                el.step(mode)
+        el.sync()
+
+        def timed_l(mode, K):
+            barrier()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            e0 = torch.cuda.Event(enable_timing=True)
+            s0.record(sl_)
+            for _ in range(K):
+                el.step(mode)
+            e0.record(sl_)
+            e0.synchronize()
+            barrier()
+            return max_over_ranks(s0.elapsed_time(e0))
+        kl = 5
+        lr_ms, lp_ms = timed_l(REPROP, kl), timed_l(PAREPROP, kl)
+        bl = pl_["batch"]
+        mfl, _ = model_flops_per_img(dict(pl_, in_dim=el.cfg.in_dim, num_classes=el.cfg.num_classes))
+        img_lp = world * bl * kl / (lp_ms / 1e3)
+        revvit_l = {"config": f"RevViT-L (depth 24, dim 1024, 16 heads, 197 tokens), per-GPU batch {bl}, "
+                              f"dp{world}, device-timed over {kl} steps",
+                    "reprop_img_s": world * bl * kl / (lr_ms / 1e3), "pareprop_img_s": img_lp,
+                    "pareprop_gain_pct": 100.0 * (lr_ms / lp_ms - 1.0),
+                    "mfu": mfl * img_lp / world / (peaks()["bf16"] * 1e12)}
+        el.close()
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
@@ -408,6 +454,7 @@ def main_ours(a, rank, world, local_rank):
             "pareprop_gain_pct": 100.0 * (img_p / img_r - 1.0),
             "pareprop_gain_small_batch": small,
             "pareprop_overlap_bound": bound,
+            "revvit_l": revvit_l,
             "mfu": mf * per_gpu / (pk["bf16"] * 1e12),
             "hfu": hf * per_gpu / (pk["bf16"] * 1e12),
             "loss": loss,
@@ -442,6 +489,7 @@ def main(argv=None):
     ap.add_argument("--g-ctas", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small-batch", action="store_true")
+    ap.add_argument("--no-revvit-l", action="store_true")
     a = ap.parse_args(argv)
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `bench.py --gpus N` without a launcher: start the N ranks ourselves (one per GPU,
