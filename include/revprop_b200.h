@@ -112,6 +112,10 @@ int rp_gemm(const RpGemmDesc* desc, rp_stream_t stream);
  * graphs keep theirs): 1 (default) the issuing warp stays converged and issues predicated on
  * one lane, 0 a single diverged lane issues. Same MMAs in the same order: bit-identical. */
 int rp_set_mma_issue(int mode);
+/* Instrumentation (tools/gemm_trace.py): a device buffer of 64 x 8 uint64 receives clock64
+ * stamps of the CTA-pair GEMM's cluster 0 (per tile: accumulator wait / acquire / operand
+ * wait cycles / last MMA; epilogue start / end). NULL turns it off. */
+int rp_set_gemm_trace(void* device_buffer);
 
 /* ------------------------------------------------------------------ LayerNorm / reductions
  * rp_layer_norm_fwd: ref:proj/core/src/ops.cpp:264-304 (y = x_hat*gamma + beta, two-pass

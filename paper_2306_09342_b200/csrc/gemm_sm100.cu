@@ -28,6 +28,16 @@
 namespace rp {
 
 constexpr int kBM = 128;
+
+// Instrumentation (tools/gemm_trace.py): when set, the CTA-pair kernel's cluster 0 records
+// per tile (first 64 of its tiles, 8 uint64 each): MMA warp waits for the accumulator /
+// gets it / cycles spent waiting for operand stages / last MMA issued; epilogue warp 2 gets
+// the accumulator / releases it.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+#define GEMM_TRACE(t, slot, val)                                                        \
+  do {                                                                                  \
+    if (gtr && (t) < 64) gtr[(t) * 8 + (slot)] = static_cast<unsigned long long>(val);  \
+  } while (0)
 constexpr int kBK = 64;
 constexpr int kThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 
@@ -692,6 +702,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  unsigned long long* const gtr = blockIdx.x == 0 ? g_gemm_trace : nullptr;  // instrumentation
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -762,29 +773,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---------------- MMA issuer (leader CTA), warp-converged, lane 0's predicate issues
       constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
       const uint32_t is0 = lane == 0 ? 1u : 0u;
+      const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = B_MN ? make_sdesc_sw128(smem_u32(sB), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sB), 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cluster_id; u < units; u += nclusters) {
+      int ti = 0;
+      for (int u = cluster_id; u < units; u += nclusters, ++ti) {
         const int split = u / tiles;
         const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
         const int kb1 =
             static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        if (lane == 0) GEMM_TRACE(ti, 0, clock64());
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (lane == 0) GEMM_TRACE(ti, 1, clock64());
+        long long wfull = 0;
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = kb0; kb < kb1; ++kb) {
+          const long long w0 = clock64();
           mbar_wait(&full[stage], phase);
+          wfull += clock64() - w0;
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kHalfBytes);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kHalfBytes);
+          // descriptors = stage-0 descriptor + (byte offset >> 4) in the start-address field
+          // (no carry: shared addresses < 256 KB), so the issue loop is additions only
+          const uint64_t soff = static_cast<uint64_t>((stage * Cfg::kHalfBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            const uint64_t ad = adesc0 + soff + static_cast<uint64_t>(A_MN ? kk * 128 : kk * 2);
+            const uint64_t bd = bdesc0 + soff + static_cast<uint64_t>(B_MN ? kk * 128 : kk * 2);
             umma_bf16_2sm_pred(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u, is0);
           }
           umma_commit_2sm_mc_pred(&empty[stage], 0x3, is0);
@@ -794,6 +814,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit_2sm_mc_pred(&tfull[acc], 0x3, is0);
+        if (lane == 0) {
+          GEMM_TRACE(ti, 2, wfull);
+          GEMM_TRACE(ti, 3, clock64());
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -803,6 +827,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA only)
       constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
+      const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = B_MN ? make_sdesc_sw128(smem_u32(sB), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sB), 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -818,14 +846,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kHalfBytes);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kHalfBytes);
+          const uint64_t soff = static_cast<uint64_t>((stage * Cfg::kHalfBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            const uint64_t ad = adesc0 + soff + static_cast<uint64_t>(A_MN ? kk * 128 : kk * 2);
+            const uint64_t bd = bdesc0 + soff + static_cast<uint64_t>(B_MN ? kk * 128 : kk * 2);
             umma_bf16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           umma_commit_2sm_mc(&empty[stage], 0x3);
@@ -850,12 +875,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     StageRing ring{st, 0, Cfg::kTmaBufs};  // TMA-store staging buffers (kTmaStore)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cluster_id; u < units; u += nclusters) {
+    int ti = 0;
+    for (int u = cluster_id; u < units; u += nclusters, ++ti) {
       const int split = u / tiles, tile = u % tiles;
       const int64_t m0 = static_cast<int64_t>(tile / sh.n_tiles) * 256 + 128 * rank;
       const int64_t n0 = static_cast<int64_t>(tile % sh.n_tiles) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0) GEMM_TRACE(ti, 4, clock64());
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * BN);
       const int64_t row0 = m0 + q * 32;
       const int c_begin = half * (BN / 2), c_end = (half + 1) * (BN / 2);
@@ -881,6 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (warp == 2 && lane == 0) GEMM_TRACE(ti, 5, clock64());
       if (lane == 0) mbar_arrive_cluster(leader_tempty0 + static_cast<uint32_t>(acc * 8));
       if (++acc == 2) {
         acc = 0;
@@ -1230,6 +1258,12 @@ extern "C" int rp_gemm_plan_create(const RpGemmDesc* d, RpGemmPlan** out) {
   rp_gemm_plan_set_max_ctas(p, d->max_ctas);
   *out = p;
   return RP_OK;
+}
+
+extern "C" int rp_set_gemm_trace(void* device_buffer) {
+  unsigned long long* p = static_cast<unsigned long long*>(device_buffer);
+  return cudaMemcpyToSymbol(g_gemm_trace, &p, sizeof(p)) == cudaSuccess ? RP_OK
+                                                                          : rp_fail(RP_ERR_CUDA, "gemm trace");
 }
 
 // MMA issue form of the GEMM kernels (A/B switch, read at launch): 1 warp-converged
