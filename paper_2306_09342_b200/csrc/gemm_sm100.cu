@@ -58,6 +58,18 @@ struct GemmShape {
   int32_t issue;  // MMA issue form: 1 warp-converged (predicated), 0 one diverged lane
 };
 
+// Work unit u -> (split, tile, k-block range). splits == 1 (every non-wgrad GEMM) needs no
+// division: the per-tile index math sits between two tiles' MMA streams on the issuing warp.
+struct UnitRange {
+  int split, tile, kb0, kb1;
+};
+__device__ __forceinline__ UnitRange unit_range(const GemmShape& sh, int u, int tiles) {
+  if (sh.splits == 1) return {0, u, 0, sh.k_blocks};
+  const int split = u / tiles;
+  return {split, u - split * tiles, (split * sh.k_blocks) / sh.splits,
+          ((split + 1) * sh.k_blocks) / sh.splits};
+}
+
 // ---------------------------------------------------------------- epilogue
 // Each epilogue warp owns 32 accumulator rows (its TMEM lane quarter) and half of the BN
 // columns, processed in 32x32 chunks. tcgen05.ld gives one row per thread; the chunk is
@@ -482,11 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int split = u / tiles, tile = u % tiles;
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int tile = ur.tile, kb0 = ur.kb0, kb1 = ur.kb1;
         const int m0 = (tile / sh.n_tiles) * kBM, n0 = (tile % sh.n_tiles) * BN;
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * Cfg::kABytes;
@@ -524,10 +534,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int split = u / tiles;
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int kb0 = ur.kb0, kb1 = ur.kb1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -565,10 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int split = u / tiles;
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int kb0 = ur.kb0, kb1 = ur.kb1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -608,7 +614,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int split = u / tiles, tile = u % tiles;
+      const UnitRange ur = unit_range(sh, u, tiles);
+      const int split = ur.split, tile = ur.tile;
       const int64_t m0 = static_cast<int64_t>(tile / sh.n_tiles) * kBM;
       const int64_t n0 = static_cast<int64_t>(tile % sh.n_tiles) * BN;
       mbar_wait(&tfull[acc], acc_phase);
@@ -736,12 +743,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cluster_id; u < units; u += nclusters) {
-        const int split = u / tiles, tile = u % tiles;
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int tile = ur.tile, kb0 = ur.kb0, kb1 = ur.kb1;
         const int m0 = (tile / sh.n_tiles) * 256 + 128 * static_cast<int>(rank);
         const int n0 = (tile % sh.n_tiles) * BN + 128 * static_cast<int>(rank);
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
@@ -783,10 +788,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       int ti = 0;
       for (int u = cluster_id; u < units; u += nclusters, ++ti) {
-        const int split = u / tiles;
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int kb0 = ur.kb0, kb1 = ur.kb1;
         if (lane == 0) GEMM_TRACE(ti, 0, clock64());
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -836,10 +839,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = cluster_id; u < units; u += nclusters) {
-        const int split = u / tiles;
-        const int kb0 = static_cast<int>((static_cast<int64_t>(split) * sh.k_blocks) / sh.splits);
-        const int kb1 =
-            static_cast<int>((static_cast<int64_t>(split + 1) * sh.k_blocks) / sh.splits);
+        const UnitRange ur = unit_range(sh, u, tiles);
+        const int kb0 = ur.kb0, kb1 = ur.kb1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -877,7 +878,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int ti = 0;
     for (int u = cluster_id; u < units; u += nclusters, ++ti) {
-      const int split = u / tiles, tile = u % tiles;
+      const UnitRange ur = unit_range(sh, u, tiles);
+      const int split = ur.split, tile = ur.tile;
       const int64_t m0 = static_cast<int64_t>(tile / sh.n_tiles) * 256 + 128 * rank;
       const int64_t n0 = static_cast<int64_t>(tile % sh.n_tiles) * BN;
       mbar_wait(&tfull[acc], acc_phase);
