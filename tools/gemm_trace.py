@@ -27,7 +27,17 @@ o1 = torch.empty(T, h, device=dev, dtype=torch.bfloat16)
 o2 = torch.empty_like(o1)
 oq = torch.empty(T, 3 * d, device=dev, dtype=torch.bfloat16)
 od = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+res = torch.randn(T, d, device=dev)
+dyb = torch.randn(T, h, device=dev).bfloat16()
+ws = torch.empty(8 * d * h, device=dev)
+dW = torch.empty(d, h, device=dev)
 cases = {
+    "resid fp32 K=3072": lambda: K.gemm(x3, w2, T, d, h, b_mn=True, epi=_capi.RP_EPI_RESID, out=res,
+                                         aux=res, bn=512),
+    "resid fp32 K=768": lambda: K.gemm(x, wq[:, :d].contiguous(), T, d, d, b_mn=True,
+                                        epi=_capi.RP_EPI_RESID, out=res, aux=res, bn=512),
+    "wgrad split-K": lambda: K.gemm(x, dyb, d, h, T, a_mn=True, b_mn=True, epi=_capi.RP_EPI_F32,
+                                    out=dW, splits=4, workspace=ws, bn=512),
     "qkv_bf16 K=768": lambda: K.gemm(x, wq, T, 3 * d, d, b_mn=True, epi=_capi.RP_EPI_BF16, out=oq, bn=512),
     "gelu_slope K=768": lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BIAS_GELU_SLOPE,
                                        out=o1, out2=o2, bias=b1, bn=512),
