@@ -1,16 +1,22 @@
 """Same-process A/B of whole-step time: Reprop / PaReprop x PDL on / off (device-timed,
 CUDA graphs), so clock / power-cap drift between boxes does not enter the comparison.
 
-    python -m paper_2306_09342_b200.ab_step [--rounds 3]
+    python tools/ab_step.py [--rounds 3]
 """
 from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import argparse
 import json
 
-from . import _capi
-from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
-from .sweep_partition import time_steps
+from paper_2306_09342_b200 import _capi
+from paper_2306_09342_b200.engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from sweep_partition import time_steps
 
 
 def main(argv=None):

@@ -4,7 +4,7 @@ kernel kind; writes the GEMM traffic file bench.py reports as roofline.traffic.
 
     ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,\\
         gpu__time_duration.sum --clock-control none --csv --log-file traffic.csv \\
-        python -m paper_2306_09342_b200.profile_step --mode reprop
+        python tools/profile_step.py --mode reprop
     python tools/gemm_traffic.py traffic.csv profiles/round2_gemm_traffic
 """
 import csv

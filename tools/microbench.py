@@ -1,6 +1,6 @@
 """Per-kernel timing of the RevViT-B block shapes (T = 256*197 rows, d = 768, h = 3072).
 
-    python -m paper_2306_09342_b200.microbench [--json out.json]
+    python tools/microbench.py [--json out.json]
 
 Times every sm_100a kernel of one reversible block with CUDA events (warm-up, then the
 median of repeated launches on one stream) and reports TFLOP/s or GB/s against
@@ -9,14 +9,20 @@ as a library yardstick only; it is never on the product path.
 """
 from __future__ import annotations
 
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
 import argparse
 import json
 import os
 
 import torch
 
-from . import _capi, kernels as K
-from ._capi import RP_EPI_BF16, RP_EPI_BIAS_GELU, RP_EPI_F32, RP_EPI_GELU_BWD, RP_EPI_RESID
+from paper_2306_09342_b200 import _capi, kernels as K
+from paper_2306_09342_b200._capi import RP_EPI_BF16, RP_EPI_BIAS_GELU, RP_EPI_F32, RP_EPI_GELU_BWD, RP_EPI_RESID
 
 
 def _peaks():

@@ -1,13 +1,19 @@
 """Launch each hot kernel once at the RevViT-B block shapes (T = 256*197), for ncu:
 
-    ncu --set full -k regex:<kernel> -c 1 python -m paper_2306_09342_b200.ncu_targets
+    ncu --set full -k regex:<kernel> -c 1 python tools/ncu_targets.py
 """
 from __future__ import annotations
 
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
 import torch
 
-from . import _capi, kernels as K
-from ._capi import (RP_EPI_BF16, RP_EPI_BIAS_GELU, RP_EPI_BIAS_GELU_SLOPE, RP_EPI_F32, RP_EPI_MUL,
+from paper_2306_09342_b200 import _capi, kernels as K
+from paper_2306_09342_b200._capi import (RP_EPI_BF16, RP_EPI_BIAS_GELU, RP_EPI_BIAS_GELU_SLOPE, RP_EPI_F32, RP_EPI_MUL,
                     RP_EPI_RESID)
 
 

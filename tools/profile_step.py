@@ -1,15 +1,21 @@
 """One RevViT-B training step under cudaProfilerStart/Stop, for ncu:
 
     ncu --profile-from-start off --metrics gpu__time_duration.sum --csv \
-        python -m paper_2306_09342_b200.profile_step --mode reprop
+        python tools/profile_step.py --mode reprop
 """
 from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import argparse
 
 import torch
 
-from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from paper_2306_09342_b200.engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
 
 
 def main(argv=None):

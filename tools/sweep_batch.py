@@ -1,15 +1,21 @@
 """Reprop vs PaReprop step time across per-GPU batch sizes (§3.3: the gain comes
 from GPU under-utilisation, largest at small batch).
 
-    python -m paper_2306_09342_b200.sweep_batch [--batches 8,16,32,64,128,256]
+    python tools/sweep_batch.py [--batches 8,16,32,64,128,256]
 """
 from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import argparse
 import json
 
-from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
-from .sweep_partition import time_steps
+from paper_2306_09342_b200.engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from sweep_partition import time_steps
 
 
 def main(argv=None):

@@ -1,16 +1,22 @@
 """PaReprop SM-partition sweep: step time of Reprop and of PaReprop with the recompute
 lane's GEMMs capped at r CTAs and the gradient lane's at g CTAs (device-timed, CUDA graphs).
 
-    python -m paper_2306_09342_b200.sweep_partition [--steps 10]
+    python tools/sweep_partition.py [--steps 10]
 """
 from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import argparse
 import json
 
 import torch
 
-from .engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
+from paper_2306_09342_b200.engine import PAREPROP, PRESETS, REPROP, Engine, ModelConfig
 
 
 def time_steps(eng, mode, K):
