@@ -257,6 +257,27 @@ def impl(request):
         _capi.lib().rp_set_attention_impl(0)
 
 
+@pytest.mark.parametrize("B,N,H", [(64, 197, 12), (40, 208, 16), (96, 150, 8)])
+def test_fused_attention_bwd_matches_dst_path(K, B, N, H):
+    """The single-pass fused backward (impl 0, N <= 208) against the dS^T round-trip path
+    (impl 3) at shapes with several (sequence, head) pairs per CTA: the same products in a
+    different association, so they agree to bf16 rounding, and each is deterministic."""
+    from paper_2306_09342_b200 import _capi
+    qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
+    out, lse = K.attention_fwd(qkv, B, N, H)
+    dout = torch.randn(B * N, H * 64, device="cuda").bfloat16()
+    res = {}
+    try:
+        for impl in (0, 3):
+            _capi.check(_capi.lib().rp_set_attention_impl(impl), "set_attention_impl")
+            a = K.attention_bwd(qkv, out, lse, dout, B, N, H)
+            assert torch.equal(a, K.attention_bwd(qkv, out, lse, dout, B, N, H))
+            res[impl] = a.float()
+    finally:
+        _capi.lib().rp_set_attention_impl(0)
+    assert rel(res[0], res[3]) < 1e-2
+
+
 def test_attention_impl_switch_validates():
     from paper_2306_09342_b200 import _capi
     assert _capi.lib().rp_set_attention_impl(4) == 3  # RP_ERR_CONFIG
