@@ -531,6 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t is0 = lane == 0 ? 1u : 0u;
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = B_MN ? make_sdesc_sw128(smem_u32(sB), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sB), 16, 1024);
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -542,14 +546,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+          const uint64_t soa = static_cast<uint64_t>((stage * Cfg::kABytes) >> 4);
+          const uint64_t sob = static_cast<uint64_t>((stage * Cfg::kBBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            const uint64_t ad = adesc0 + soa + static_cast<uint64_t>(A_MN ? kk * 128 : kk * 2);
+            const uint64_t bd = bdesc0 + sob + static_cast<uint64_t>(B_MN ? kk * 128 : kk * 2);
             umma_bf16_pred(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u, is0);
           }
           umma_commit_pred(&empty[stage], is0);
@@ -570,6 +572,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = B_MN ? make_sdesc_sw128(smem_u32(sB), 8192, 1024)
+                                   : make_sdesc_sw128(smem_u32(sB), 16, 1024);
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -581,14 +587,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+          const uint64_t soa = static_cast<uint64_t>((stage * Cfg::kABytes) >> 4);
+          const uint64_t sob = static_cast<uint64_t>((stage * Cfg::kBBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            const uint64_t ad = adesc0 + soa + static_cast<uint64_t>(A_MN ? kk * 128 : kk * 2);
+            const uint64_t bd = bdesc0 + sob + static_cast<uint64_t>(B_MN ? kk * 128 : kk * 2);
             umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
