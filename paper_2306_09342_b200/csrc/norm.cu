@@ -378,48 +378,69 @@ __global__ void __launch_bounds__(kFinWarps * 32)
   }
 }
 
-// Column sums over many parts in two fixed-order stages: stage 1 (below) sums slices of
-// kSlice parts per CTA (8 warps x 32 columns, grid = column groups x slices) and writes the
-// slice sum IN PLACE over the slice's first part row (no other CTA reads that row); stage 2
-// is colsum_final_kernel over the slice rows (stride kSlice * ld). One CTA per 32 columns
-// walking all parts (the single-stage form) leaves most SMs idle when cols is small.
-constexpr int kSlice = 64;
-__global__ void __launch_bounds__(256)
-    colsum_slice_kernel(float* __restrict__ part, int64_t nparts, int cols, int64_t ld) {
+// Column sums over many parts in ONE launch: a cluster of kClu CTAs per 32 columns, CTA r of
+// the cluster summing the r-th contiguous slice of the parts (16 warps, each warp every 16th
+// part of the slice, 8 loads in flight), then the leader CTA adding the kClu slice sums from
+// the other CTAs' shared memory in rank order. The association order depends only on
+// (nparts, cols), so results are bit-reproducible. Replaces a slice-sum launch writing the
+// slice sums back to global + a finalising launch (two launches and a dependent global round
+// trip per reduction; 8.5 us -> see DESIGN.md section 9).
+constexpr int kClu = 8;
+constexpr int kCluWarps = 16;
+__global__ void __cluster_dims__(1, kClu, 1) __launch_bounds__(kCluWarps * 32)
+    colsum_cluster_kernel(const float* __restrict__ part, int64_t nparts, int cols, int64_t ld,
+                          float* __restrict__ out, int accumulate) {
   pdl_trigger();
   pdl_wait();
 
-  __shared__ float red[8][33];
+  __shared__ float red[kCluWarps][33];
+  __shared__ float slice_sum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  const int64_t p0 = static_cast<int64_t>(blockIdx.y) * kSlice;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t per = (nparts + kClu - 1) / kClu;
+  const int64_t p_end = min(nparts, (rank + 1) * per);
   float a0 = 0.f, a1 = 0.f;
   if (c < cols) {
+    int64_t p = rank * per + warp;
+    for (; p + 7 * kCluWarps < p_end; p += 8 * kCluWarps) {
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < kSlice / 8; i += 2) {
-      const int64_t p = p0 + warp + 8 * i, q = p + 8;
-      if (p < nparts) a0 += part[p * ld + c];
-      if (q < nparts) a1 += part[q * ld + c];
+      for (int i = 0; i < 8; ++i) v[i] = __ldcg(part + (p + i * kCluWarps) * ld + c);
+      a0 += (v[0] + v[2]) + (v[4] + v[6]);
+      a1 += (v[1] + v[3]) + (v[5] + v[7]);
     }
+    for (; p < p_end; p += kCluWarps) a0 += __ldcg(part + p * ld + c);
   }
   red[warp][lane] = a0 + a1;
   __syncthreads();
-  if (warp == 0 && c < cols) {
+  if (warp == 0) {
     float t = red[0][lane];
-    for (int w = 1; w < 8; ++w) t += red[w][lane];
-    part[p0 * ld + c] = t;
+#pragma unroll
+    for (int w = 1; w < kCluWarps; ++w) t += red[w][lane];
+    slice_sum[lane] = t;
   }
+  cluster_sync_all();
+  if (rank == 0 && warp == 0 && c < cols) {
+    const uint32_t local = smem_u32(&slice_sum[lane]);
+    float s = 0.f;
+#pragma unroll
+    for (uint32_t r = 0; r < kClu; ++r) {
+      float v;
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(mapa_shared(local, r)) : "memory");
+      s += v;
+    }
+    out[c] = accumulate ? out[c] + s : s;
+  }
+  cluster_sync_all();  // the leader's remote reads complete before any CTA exits
 }
 
 static void colsum_final(cudaStream_t s, float* part, int64_t nparts, int cols, int64_t ld,
                          float* out, int accumulate) {
   const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
-  if (nparts > 2 * kSlice) {
-    const int64_t split = (nparts + kSlice - 1) / kSlice;
-    launch_k(colsum_slice_kernel, dim3(gb, static_cast<unsigned>(split)), dim3(256), 0, s, part,
-             nparts, cols, ld);
-    launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, part, split, cols,
-             ld * kSlice, out, accumulate);
+  if (nparts > 2 * kClu * kCluWarps) {
+    launch_k(colsum_cluster_kernel, dim3(gb, kClu), dim3(kCluWarps * 32), 0, s,
+             static_cast<const float*>(part), nparts, cols, ld, out, accumulate);
     return;
   }
   launch_k(colsum_final_kernel, dim3(gb), dim3(kFinWarps * 32), 0, s, part, nparts, cols, ld, out,

@@ -206,6 +206,22 @@ def test_layer_norm_fwd_bwd(K, rows, cols):
     assert rel(dg4, dg) < 1e-5 and rel(db4, db) < 1e-5
 
 
+@pytest.mark.parametrize("nparts,cols", [(1576, 3072), (788, 1536), (257, 40), (300, 100),
+                                         (5000, 64), (129, 3072), (2, 8)])
+def test_colsum_parts(K, nparts, cols):
+    """Many-part column sums (one cluster launch above 256 parts, one CTA per 32 columns
+    below): fp64 reference, ragged part counts and column counts, accumulate, determinism."""
+    part = torch.randn(nparts, cols, device="cuda")
+    ref = part.double().sum(0)
+    out = K.colsum_parts(part)
+    assert (out.double() - ref).abs().max().item() < 1e-5 * nparts ** 0.5 * 4
+    assert torch.equal(out, K.colsum_parts(part))
+    base = torch.randn(cols, device="cuda")
+    acc = base.clone()
+    K.colsum_parts(part, out=acc, accumulate=True)
+    assert torch.allclose(acc.double(), base.double() + ref, atol=1e-4 * nparts ** 0.5)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_colsum(K, dtype):
     x = torch.randn(50432 // 8, 3072, device="cuda").to(dtype)
