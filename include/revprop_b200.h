@@ -181,7 +181,9 @@ int64_t rp_attention_bwd_workspace_floats(int64_t S, int64_t N, int64_t H);
  * they were captured with: call rp_engine_invalidate_graphs after changing it. */
 int rp_set_attention_impl(int impl);
 /* tcgen05 forward for N <= 256 (A/B switch, process-global like the above): 0 (default) two
- * ping-pong groups of softmax warps on alternate query tiles; 1 the lockstep kernel (N <= 224) */
+ * ping-pong groups of softmax warps on alternate query tiles, the P V product split by key half
+ * over two issuing warps where it fits TMEM (N <= 208); 1 the lockstep kernel (N <= 224);
+ * 2 the ping-pong kernel with one P V issuer */
 int rp_set_attention_fwd_variant(int variant);
 /* Instrumentation: a device buffer of 64 x 12 uint64 receives clock64 stamps of the ping-pong
  * forward's CTA 0 (per tile: S issue, PV issue, softmax phases); NULL turns it off. */

@@ -562,12 +562,14 @@ extern "C" int rp_set_attention_trace(void* device_buffer) {
   return RP_OK;
 }
 
-// forward kernel variant for N <= 256 (A/B): 0 ping-pong softmax groups (attn_fwd_tc_pp),
-// 1 the lockstep persistent kernel (N <= 224)
+// forward kernel variant for N <= 256 (A/B): 0 ping-pong softmax groups (attn_fwd_tc_pp)
+// with the P V product split over two issuers where the TMEM plan allows (Nk <= 208),
+// 1 the lockstep persistent kernel (N <= 224), 2 ping-pong with one P V issuer
 static int g_attn_fwd_variant = 0;
 int rp_attn_fwd_variant() { return g_attn_fwd_variant; }
 extern "C" int rp_set_attention_fwd_variant(int v) {
-  if (v < 0 || v > 1) return rp_fail(RP_ERR_CONFIG, "attention forward variant must be 0 or 1");
+  if (v < 0 || v > 2)
+    return rp_fail(RP_ERR_CONFIG, "attention forward variant must be 0, 1 or 2");
   g_attn_fwd_variant = v;
   return RP_OK;
 }

@@ -286,13 +286,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 //   epilogue O / l (sums exchanged the same way) -> bf16 att, log2-domain LSE
 // S is double-buffered (buffer j % 2 at column 256 (j % 2)); S(j + 2) waits for
 // epilogue(j). Works for N <= 256 (the persistent kernel stops at 224).
-// Warp 16 issues the loads and S = Q K^T, warp 17 every P V (a PV then never waits behind
-// an S issue). (Splitting the PV issue per group over two warps measured slower.)
-constexpr int kPPThreads = kFwdThreads + 32;
+// Warp 16 issues the loads and S = Q K^T, warps 17 and 18 the P V products (a PV then never
+// waits behind an S issue). One N = 64 MMA costs its issuing thread ~120 cycles whatever N
+// (tools/umma_bench.cu), so with Nk <= 208 ("split" plan) the P V product is split by key
+// half into two accumulators issued by the two warps in parallel (7 + 6 MMAs instead of 13
+// in a row) and summed in the epilogue: key half 1 packs its P into the free tail columns
+// [p1, 256) of the S buffer (never S columns, so no race with half 0's reads), which leaves
+// the whole middle of the buffer dead once both halves are packed: O_a and O_b at oa and
+// oa + 64. Otherwise (one accumulator at ocol) warp 17 issues every P V.
+// (Splitting the PV issue per GROUP over two warps measured slower.)
+constexpr int kPPThreads = kFwdThreads + 64;
 struct PPPlan {
   int ntile, nitems;
   int cs;    // 16-key chunks in key half 0 (the rest are half 1's)
-  int ocol;  // O accumulator column inside each S buffer
+  int ocol;  // O accumulator column inside each S buffer (O_a with split)
+  int split; // two P V accumulators (O_a at ocol, O_b at ocol + 64), half 1's P at p1
+  int p1;    // split: first TMEM column of key half 1's packed P
   unsigned long long* trace;  // optional clock64 trace of CTA 0's first kTraceTiles tiles
 };
 constexpr int kTraceTiles = 64;
@@ -302,8 +311,8 @@ constexpr int kTraceTiles = 64;
       pl.trace[(j) * 12 + (slot)] = static_cast<unsigned long long>(clock64());            \
   } while (0)
 
-__device__ __forceinline__ uint32_t pp_pcol(int c, int cs) {
-  return static_cast<uint32_t>(c < cs ? 8 * c : 16 * cs + 8 * (c - cs));
+__device__ __forceinline__ uint32_t pp_pcol(int c, int cs, int p1) {
+  return static_cast<uint32_t>(c < cs ? 8 * c : p1 + 8 * (c - cs));
 }
 
 __global__ void __launch_bounds__(kPPThreads, 1)
@@ -328,6 +337,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int Nk = g.Nk, ntile = pl.ntile, nitems = pl.nitems, nch = g.Nk / 16, cs = pl.cs;
+  const int p1 = pl.split ? pl.p1 : 16 * cs;  // half 1's P: tail columns, or its own S columns
   if (warp == 16) {
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         mbar_init(&bar_free[i], static_cast<uint32_t>(8 * pl.ntile));
         mbar_init(&bar_s[i], 1);
         mbar_init(&bar_p[i], 8);
-        mbar_init(&bar_o[i], 1);
+        mbar_init(&bar_o[i], pl.split ? 2 : 1);
         mbar_init(&bar_e[i], 8);
       }
       fence_barrier_init();
@@ -399,22 +409,26 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         }
       }
     }
-  } else if (warp == 17) {
-    // P V issuer (both groups' tiles in order), so a PV never waits behind an S issue
-    if (lane == 0) {
+  } else if (warp == 17 || warp == 18) {
+    // P V issuers (both groups' tiles in order), so a PV never waits behind an S issue:
+    // warp 17 key half 0 into O_a (all keys without the split), warp 18 key half 1 into O_b
+    const bool hb = warp == 18;
+    if (lane == 0 && (pl.split || !hb)) {
       const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      const int c0 = hb ? cs : 0, c1 = pl.split && !hb ? cs : nch;
+      const uint32_t ocol = static_cast<uint32_t>(pl.ocol + (hb ? 64 : 0));
       for (int jP = 0; jP < J; ++jP) {
         mbar_wait(&bar_p[jP & 1], (jP >> 1) & 1);
         tc_fence_after();
         const int k = jP / ntile;
         const uint32_t bv = smem_u32(smem + (k & 1) * kFwdBuf) + 65536u;
-        const uint32_t sb = sbuf(jP), od = sb + static_cast<uint32_t>(pl.ocol);
-        PP_TRACE(jP, 2);
-        for (int c = 0; c < nch; ++c)
-          umma_ts_bf16(od, sb + pp_pcol(c, cs), make_sdesc_sw128(bv + c * 2048, 8192, 1024),
-                       idesc_o, c > 0 ? 1u : 0u);
+        const uint32_t sb = sbuf(jP), od = sb + ocol;
+        if (!hb) PP_TRACE(jP, 2);
+        for (int c = c0; c < c1; ++c)
+          umma_ts_bf16(od, sb + pp_pcol(c, cs, p1), make_sdesc_sw128(bv + c * 2048, 8192, 1024),
+                       idesc_o, c > c0 ? 1u : 0u);
         umma_commit(&bar_o[jP & 1]);
-        PP_TRACE(jP, 3);
+        if (!hb) PP_TRACE(jP, 3);
       }
     }
   } else {
@@ -493,7 +507,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             pk[e] = pack_bf16x2(p0, p1);
           }
         }
-        tmem_st8(sb + pp_pcol(cc, cs), pk);
+        tmem_st8(sb + pp_pcol(cc, cs, p1), pk);
       };
       if (active) {
         for (int c = ch0; c < ch1; c += 2) {
@@ -529,9 +543,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       tc_fence_after();
       if (tr) PP_TRACE(j, 9);
       float o[32];
-      if (active)
-        tmem_ld16x2(sbuf(j) + lq + static_cast<uint32_t>(pl.ocol + half * 32),
-                    sbuf(j) + lq + static_cast<uint32_t>(pl.ocol + half * 32 + 16), o, o + 16);
+      if (active) {
+        const uint32_t oa = sbuf(j) + lq + static_cast<uint32_t>(pl.ocol + half * 32);
+        tmem_ld16x2(oa, oa + 16, o, o + 16);
+        if (pl.split) {  // + O_b, summed in a fixed order
+          float ob[32];
+          tmem_ld16x2(oa + 64, oa + 80, ob, ob + 16);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] += ob[e];
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_e[j & 1]);
@@ -885,7 +906,7 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   // ping-pong softmax groups by default (256 x 197 x 12: 113.4 vs 113.5 us; x 16 heads:
   // 134.3 vs 144.7; 64 x 128: 19.0 vs 21.0), except 208 < Nk <= 224 where the lockstep
   // kernel measured faster (128 x 224: 64.5 vs 70.1 us) (tools/attn_fwd_ab.py)
-  const bool pp = g.Nk > 224 || (rp_attn_fwd_variant() == 0 && g.Nk <= 208);
+  const bool pp = g.Nk > 224 || (rp_attn_fwd_variant() != 1 && g.Nk <= 208);
   if (pp) {
     static std::once_flag once_pp;
     static int nsm_pp = 148;
@@ -900,7 +921,12 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
     pp.nitems = static_cast<int>(S * H);
     const int nch = g.Nk / 16;
     pp.cs = (nch + 1) / 2;
-    pp.ocol = (8 * (nch + pp.cs) + 15) / 16 * 16;
+    pp.p1 = 256 - 8 * (nch - pp.cs);
+    const int oa = (8 * pp.cs + 31) / 32 * 32;
+    // split P V: half 1's P in the tail [p1, 256) beyond every S column, O_a | O_b in the
+    // columns dead once both halves are packed (Nk <= 208 at 256 columns per S buffer)
+    pp.split = rp_attn_fwd_variant() == 0 && nch >= 2 && pp.p1 >= g.Nk && oa + 128 <= pp.p1;
+    pp.ocol = pp.split ? oa : (8 * (nch + pp.cs) + 15) / 16 * 16;
     pp.trace = rp_attn_trace_buffer();
     const unsigned grid = static_cast<unsigned>(pp.nitems < nsm_pp ? pp.nitems : nsm_pp);
     launch_k(attn_fwd_tc_pp, dim3(grid), dim3(kPPThreads), smem_pp, stream, mq, mkv,

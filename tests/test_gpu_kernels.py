@@ -294,6 +294,32 @@ def test_fused_attention_bwd_matches_dst_path(K, B, N, H):
     assert rel(res[0], res[3]) < 1e-2
 
 
+@pytest.mark.parametrize("B,N,H", [(4, 197, 12), (3, 208, 2), (2, 192, 3), (2, 160, 2),
+                                   (3, 17, 2), (2, 33, 1), (1, 100, 3), (2, 224, 2)])
+def test_attention_fwd_split_pv(K, B, N, H):
+    """Forward variant 0 (P V split by key half over two issuers, N <= 208) against the
+    single-issuer ping-pong kernel (variant 2) and the fp32 reference: the same P, two
+    partial accumulators summed in the epilogue, so O agrees to fp32 rounding (bf16 output),
+    and the LSE is the same computation."""
+    from paper_2306_09342_b200 import _capi
+    torch.manual_seed(31 * N + B)
+    qkv = torch.randn(B * N, 3 * H * 64, device="cuda").bfloat16()
+    res = {}
+    try:
+        for v in (0, 2):
+            assert _capi.lib().rp_set_attention_fwd_variant(v) == 0
+            res[v] = K.attention_fwd(qkv, B, N, H)
+            assert all(torch.equal(a, b) for a, b in zip(res[v], K.attention_fwd(qkv, B, N, H)))
+    finally:
+        _capi.lib().rp_set_attention_fwd_variant(0)
+    assert _capi.lib().rp_set_attention_fwd_variant(3) == 3  # RP_ERR_CONFIG
+    o_ref, lse_ref = attn_ref(qkv.float(), B, N, H)
+    assert rel(res[0][0], o_ref) < 1e-2
+    assert (res[0][0].float() - res[2][0].float()).abs().max().item() <= 2 ** -7 * \
+        res[2][0].float().abs().max().item()
+    assert torch.equal(res[0][1], res[2][1])
+
+
 def test_attention_impl_switch_validates():
     from paper_2306_09342_b200 import _capi
     assert _capi.lib().rp_set_attention_impl(4) == 3  # RP_ERR_CONFIG

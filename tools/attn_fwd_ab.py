@@ -2,7 +2,8 @@
 interleaved per shape so both variants see the same clocks).
 
     python tools/attn_fwd_ab.py [reps]
-variant 0 = ping-pong softmax groups (default), 1 = lockstep persistent kernel.
+variant 0 = ping-pong softmax groups with the split P V (default), 2 = ping-pong with one
+P V issuer, 1 = lockstep persistent kernel.
 """
 import sys
 
@@ -37,7 +38,7 @@ for (B, N, H) in [(256, 197, 12), (256, 197, 16), (64, 128, 12), (128, 224, 12),
     ref = (torch.softmax(s, -1) @ v).permute(0, 2, 1, 3).reshape(B * N, H * 64)
     res = {}
     for _ in range(reps):
-        for var in (0, 1):
+        for var in (0, 2, 1):
             if var == 1 and N > 224:
                 continue
             L.rp_set_attention_fwd_variant(var)
