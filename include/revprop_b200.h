@@ -185,6 +185,11 @@ int rp_set_attention_impl(int impl);
  * over two issuing warps where it fits TMEM (N <= 208); 1 the lockstep kernel (N <= 224);
  * 2 the ping-pong kernel with one P V issuer */
 int rp_set_attention_fwd_variant(int variant);
+/* Windows of N <= 64 tokens (Swin), any head_dim (A/B switch, process-global like the above):
+ * 0 (default) single-tile persistent kernels -- the backward one fused pass per (window, head)
+ * with D = rowsum(P * dP) formed in the kernel; 1 the general mma.sync kernels (D pre-pass,
+ * separate dK/dV and dQ passes) */
+int rp_set_attention_window_variant(int variant);
 /* Instrumentation: a device buffer of 64 x 12 uint64 receives clock64 stamps of the ping-pong
  * forward's CTA 0 (per tile: S issue, PV issue, softmax phases); NULL turns it off. */
 int rp_set_attention_trace(void* device_buffer);

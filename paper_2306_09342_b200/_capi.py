@@ -99,6 +99,7 @@ _SIGS = {
     "rp_attention_bwd_workspace_floats": (_I64, [_I64, _I64, _I64]),
     "rp_set_attention_impl": (_I, [_I]),
     "rp_set_attention_fwd_variant": (_I, [_I]),
+    "rp_set_attention_window_variant": (_I, [_I]),
     "rp_set_mma_issue": (_I, [_I]),
     "rp_set_gemm_trace": (_I, [_P]),
     "rp_set_attention_trace": (_I, [_P]),

@@ -22,7 +22,12 @@
 #include "../../include/revprop_b200.h"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "attn_common.cuh"
 #include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "launch.h"
 
@@ -505,6 +510,416 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ------------------------------------------------------------ short windows (N <= 64)
+// Swin's 49-token windows: every (window, head) item is ONE 64-row tile, so the online
+// softmax (rescaling), the per-element exp2f range handling and the per-tile loop bounds of
+// the general kernels are pure instruction overhead -- the general kernels run
+// instruction-issue-bound here (ncu: 69 % issue slots busy, ~1000 instructions per warp and
+// item, profiles/round2_window_attention.md). These kernels are persistent (a CTA walks
+// items with the next item's tiles landing in the other half of a double buffer), stage
+// the tiles by TMA when head_dim is 32 or 64 (one thread issues 3-4 box loads per item; the
+// SW64 / SW128 smem swizzle is the one swz<> describes), else by cp.async, compute every
+// 16 x 64 tile over all 64 key columns (no per-tile bounds) and mask only the boundary
+// key tile, and use ex2.approx directly.
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2,
+                                        uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr),
+               "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void zero_smem(uint8_t* p, int bytes) {
+  for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(p + i) = make_uint4(0, 0, 0, 0);
+}
+// c = a . b with a zero accumulator (no register zeroing before the first k step)
+__device__ __forceinline__ void mma16816_z(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%10,%10,%10,%10};"
+      : "=f"(c[0]), "=f"(c[1]), "=f"(c[2]), "=f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
+}
+// S(16 x 64) = A(16 x HDP) . B^T over all 64 rows of the B tile
+template <int HDP>
+__device__ __forceinline__ void mm_abt64(const uint32_t (*a)[4], uint32_t bbase, float (*s)[4]) {
+#pragma unroll
+  for (int ks = 0; ks < HDP / 16; ++ks)
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      uint32_t b[4];
+      load_b_nk<HDP>(bbase, 16 * np, 2 * ks, b);
+      if (ks == 0) {
+        mma16816_z(s[2 * np], a[0], b[0], b[1]);
+        mma16816_z(s[2 * np + 1], a[0], b[2], b[3]);
+      } else {
+        mma16816(s[2 * np], a[ks], b[0], b[1]);
+        mma16816(s[2 * np + 1], a[ks], b[2], b[3]);
+      }
+    }
+}
+// acc(16 x HDP) = P(16 x 64, C-fragment layout) . B over all 64 rows of the B tile [k][n]
+template <int HDP>
+__device__ __forceinline__ void mm_pb64(const float (*p)[4], uint32_t bbase, float (*acc)[4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t a[4];
+    a[0] = pack_bf16x2(p[2 * ks][0], p[2 * ks][1]);
+    a[1] = pack_bf16x2(p[2 * ks][2], p[2 * ks][3]);
+    a[2] = pack_bf16x2(p[2 * ks + 1][0], p[2 * ks + 1][1]);
+    a[3] = pack_bf16x2(p[2 * ks + 1][2], p[2 * ks + 1][3]);
+#pragma unroll
+    for (int np = 0; np < HDP / 16; ++np) {
+      uint32_t b[4];
+      load_b_kn<HDP>(bbase, 16 * ks, 2 * np, b);
+      if (ks == 0) {
+        mma16816_z(acc[2 * np], a, b[0], b[1]);
+        mma16816_z(acc[2 * np + 1], a, b[2], b[3]);
+      } else {
+        mma16816(acc[2 * np], a, b[0], b[1]);
+        mma16816(acc[2 * np + 1], a, b[2], b[3]);
+      }
+    }
+  }
+}
+
+// cp.async staging (head_dim without a TMA box): rows [0, N) of q, k, v (qkv column blocks
+// m * H * hd, row pitch ldq) and, with NM = 4, dO (row pitch ldo). Chunks beyond hd and
+// rows beyond N are never written (zeroed once at kernel start). Slot j of a row = (matrix
+// j / (HDP/8), chunk j % (HDP/8)): compile-time divisions only.
+template <int HDP, int NM>
+__device__ __forceinline__ void win_load(uint8_t* buf, const __nv_bfloat16* qb, int64_t mstride,
+                                         int64_t ldq, const __nv_bfloat16* ob, int64_t ldo,
+                                         int N, int hd) {
+  constexpr int CH = HDP / 8, SL = NM * CH, kTileBytes = kTile * HDP * 2;
+  const uint32_t sb = smem_u32(buf);
+  const int chv = hd / 8;
+  for (int i = threadIdx.x; i < N * SL; i += blockDim.x) {
+    const int r = i / SL, j = i % SL, m = j / CH, c = j % CH;
+    if (c < chv) {
+      const __nv_bfloat16* src = (NM == 4 && m == 3) ? ob + r * ldo : qb + m * mstride + r * ldq;
+      cp_async16(sb + m * kTileBytes + swz<HDP>(r, c), src + c * 8, 16);
+    }
+  }
+}
+
+// Mask keys >= N of a score fragment (only n8 tiles reaching past N; uniform branches).
+__device__ __forceinline__ void mask_cols(float (*s)[4], int N, int tq, float fill) {
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    if (nt * 8 + 8 > N) {
+      const int c0 = nt * 8 + 2 * tq;
+      if (c0 >= N) s[nt][0] = s[nt][2] = fill;
+      if (c0 + 1 >= N) s[nt][1] = s[nt][3] = fill;
+    }
+  }
+}
+
+// TMA maps of one window item: q | k | v boxes of {hd, N} out of qkv [T][3 H hd], dO boxes
+// out of dout [T][H hd], the LSE row as a 1-D box of N rounded up to 4 floats
+struct WinMaps {
+  CUtensorMap qkv, dout, lse;
+};
+
+// grid = min(items, SMs x resident CTAs); block 128 (4 warps x 16 query rows)
+template <int HDP, bool TMA>
+__global__ void __launch_bounds__(128)
+    attn_fwd_win_kernel(const __grid_constant__ WinMaps maps,
+                        const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
+                        float* __restrict__ lse, AttnGeom g) {
+  constexpr int kT = kTile * HDP * 2, kBuf = 3 * kT;
+  pdl_trigger();
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t bar[2];
+  zero_smem(sm, 2 * kBuf);
+  if (TMA && threadIdx.x == 0) {
+    tma_prefetch_desc(&maps.qkv);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();  // the zero fill is visible to the TMA writes around it
+  __syncthreads();
+  pdl_wait();
+  const int total = g.B * g.H, hd = g.hd, N = g.N;
+  auto prefetch = [&](int item, int slot) {
+    const int h = item % g.H, b = item / g.H;
+    uint8_t* buf = sm + slot * kBuf;
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar[slot], static_cast<uint32_t>(3 * N * hd * 2));
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+          tma_load_2d(buf + m * kT, &maps.qkv, &bar[slot], (m * g.H + h) * hd, b * N);
+      }
+    } else {
+      const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * N * g.ld_qkv + h * hd;
+      win_load<HDP, 3>(buf, base, g.H * hd, g.ld_qkv, nullptr, 0, N, hd);
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  int item = blockIdx.x;
+  if (item < total) prefetch(item, 0);
+  if (!TMA) asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int k = 0; item < total; ++k, item += gridDim.x) {
+    const int next = item + gridDim.x;
+    if (next < total) prefetch(next, (k + 1) & 1);
+    if constexpr (TMA) {
+      mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    } else {
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+    }
+    if (warp * 16 < N) {
+      const uint32_t bQ = smem_u32(sm + (k & 1) * kBuf), bK = bQ + kT, bV = bQ + 2 * kT;
+      uint32_t qa[HDP / 16][4];
+#pragma unroll
+      for (int ks = 0; ks < HDP / 16; ++ks) load_a<HDP>(bQ, warp * 16, 2 * ks, qa[ks]);
+      float s[8][4];
+      mm_abt64<HDP>(qa, bK, s);
+      mask_cols(s, N, tq, -INFINITY);
+      float mx[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float m = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) m = fmaxf(m, fmaxf(s[nt][2 * r], s[nt][2 * r + 1]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        mx[r] = m * g.scale_log2;
+      }
+      float l[2] = {0.f, 0.f};
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p = ex2a(fmaf(s[nt][e], g.scale_log2, -mx[e >> 1]));
+          s[nt][e] = p;
+          l[e >> 1] += p;
+        }
+      float o[HDP / 8][4];
+      mm_pb64<HDP>(s, bV, o);
+      const int h = item % g.H, b = item / g.H;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+        l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+        const int row = warp * 16 + gq + 8 * r;
+        if (row < N) {
+          const float inv = __fdividef(1.0f, l[r]);
+          __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * N + row) * g.ld_o + h * hd;
+#pragma unroll
+          for (int nt = 0; nt < HDP / 8; ++nt)
+            store_pair(orow, nt * 8 + 2 * tq, hd, o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
+          if (tq == 0) lse[(static_cast<int64_t>(b) * g.H + h) * N + row] = mx[r] + __log2f(l[r]);
+        }
+      }
+    }
+    __syncthreads();  // this buffer is refilled by the prefetch two items ahead
+  }
+  if (!TMA) asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Fused backward of one (window, head) item per pass, no D pre-pass and no O read:
+//   phase A (warp w = queries 16w..): S = Q K^T, dP = dO V^T, P = exp2(S scale - lse),
+//     D = rowsum(P * dP) (the softmax VJP's sum as ref:proj/core/src/ops.cpp:219-220 forms
+//     it from the cached probabilities), dS = P (dP - D) scale, dQ = dS K; P and dS -> smem
+//     (bf16, stmatrix)
+//   phase B (warp w = keys 16w..): dV = P^T dO, dK = dS^T Q (ldmatrix.trans of P / dS)
+// Every output element is written by one warp: no atomics, bit-reproducible.
+template <int HDP, bool TMA>
+__global__ void __launch_bounds__(128)
+    attn_bwd_win_kernel(const __grid_constant__ WinMaps maps,
+                        const __nv_bfloat16* __restrict__ qkv,
+                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
+                        __nv_bfloat16* __restrict__ dqkv, AttnGeom g) {
+  constexpr int kT = kTile * HDP * 2, kBuf = 4 * kT + kTile * 4;  // Q K V dO | lse
+  constexpr int kPS = kTile * 64 * 2;                              // P or dS, bf16 [64][64]
+  pdl_trigger();
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t bar[2];
+  zero_smem(sm, 2 * kBuf + 2 * kPS);
+  if (TMA && threadIdx.x == 0) {
+    tma_prefetch_desc(&maps.qkv);
+    tma_prefetch_desc(&maps.dout);
+    tma_prefetch_desc(&maps.lse);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  pdl_wait();
+  const int total = g.B * g.H, hd = g.hd, N = g.N;
+  const int nl = (N + 3) & ~3;  // LSE box (16-byte multiple)
+  auto prefetch = [&](int item, int slot) {
+    const int h = item % g.H, b = item / g.H;
+    uint8_t* buf = sm + slot * kBuf;
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar[slot], static_cast<uint32_t>(4 * N * hd * 2 + nl * 4));
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+          tma_load_2d(buf + m * kT, &maps.qkv, &bar[slot], (m * g.H + h) * hd, b * N);
+        tma_load_2d(buf + 3 * kT, &maps.dout, &bar[slot], h * hd, b * N);
+        asm volatile(
+            "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3}], [%2];" ::"r"(smem_u32(buf + 4 * kT)),
+            "l"(reinterpret_cast<uint64_t>(&maps.lse)), "r"(smem_u32(&bar[slot])), "r"(item * N)
+            : "memory");
+      }
+    } else {
+      const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * N * g.ld_qkv + h * hd;
+      win_load<HDP, 4>(buf, base, g.H * hd, g.ld_qkv,
+                       dout + static_cast<int64_t>(b) * N * g.ld_o + h * hd, g.ld_o, N, hd);
+      const float* lrow = lse + static_cast<int64_t>(item) * N;  // [B][H][N]: item = b H + h
+      const uint32_t sl = smem_u32(buf + 4 * kT);
+      for (int i = threadIdx.x; i < N; i += blockDim.x) cp_async4(sl + 4 * i, lrow + i);
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  const uint32_t bP = smem_u32(sm + 2 * kBuf), bS = bP + kPS;
+  int item = blockIdx.x;
+  if (item < total) prefetch(item, 0);
+  if (!TMA) asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int k = 0; item < total; ++k, item += gridDim.x) {
+    const int next = item + gridDim.x;
+    if (next < total) prefetch(next, (k + 1) & 1);
+    if constexpr (TMA) {
+      mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    } else {
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+    }
+    uint8_t* buf = sm + (k & 1) * kBuf;
+    const uint32_t bQ = smem_u32(buf), bK = bQ + kT, bV = bQ + 2 * kT, bO = bQ + 3 * kT;
+    const float* sL = reinterpret_cast<const float*>(buf + 4 * kT);
+    const int h = item % g.H, b = item / g.H;
+    const int64_t row0 = static_cast<int64_t>(b) * N;
+    // ---- phase A: warp w owns queries [16w, 16w + 16)
+    if (warp * 16 < N) {
+      float s[8][4], dp[8][4];
+      {
+        uint32_t qa[HDP / 16][4], oa[HDP / 16][4];
+#pragma unroll
+        for (int ks = 0; ks < HDP / 16; ++ks) {
+          load_a<HDP>(bQ, warp * 16, 2 * ks, qa[ks]);
+          load_a<HDP>(bO, warp * 16, 2 * ks, oa[ks]);
+        }
+        mm_abt64<HDP>(qa, bK, s);
+        mm_abt64<HDP>(oa, bV, dp);
+      }
+      mask_cols(s, N, tq, -INFINITY);
+      float lr[2], dsum[2] = {0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int row = warp * 16 + gq + 8 * r;
+        lr[r] = row < N ? sL[row] : INFINITY;  // padded query rows: P = 0
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p = ex2a(fmaf(s[nt][e], g.scale_log2, -lr[e >> 1]));
+          s[nt][e] = p;
+          dsum[e >> 1] = fmaf(p, dp[nt][e], dsum[e >> 1]);
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        dsum[r] += __shfl_xor_sync(0xffffffffu, dsum[r], 1);
+        dsum[r] += __shfl_xor_sync(0xffffffffu, dsum[r], 2);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dp[nt][e] = s[nt][e] * (dp[nt][e] - dsum[e >> 1]) * g.scale;
+      // P and dS (bf16) to smem as [query][key] 64 x 64 tiles, one stmatrix per 16 x 16 block
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        const uint32_t off =
+            swz<64>(warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, 2 * np + (lane >> 4));
+        stsm_x4(bP + off, pack_bf16x2(s[2 * np][0], s[2 * np][1]),
+                pack_bf16x2(s[2 * np][2], s[2 * np][3]),
+                pack_bf16x2(s[2 * np + 1][0], s[2 * np + 1][1]),
+                pack_bf16x2(s[2 * np + 1][2], s[2 * np + 1][3]));
+        stsm_x4(bS + off, pack_bf16x2(dp[2 * np][0], dp[2 * np][1]),
+                pack_bf16x2(dp[2 * np][2], dp[2 * np][3]),
+                pack_bf16x2(dp[2 * np + 1][0], dp[2 * np + 1][1]),
+                pack_bf16x2(dp[2 * np + 1][2], dp[2 * np + 1][3]));
+      }
+      float dq[HDP / 8][4];
+      mm_pb64<HDP>(dp, bK, dq);  // dQ = dS K
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int row = warp * 16 + gq + 8 * r;
+        if (row < N) {
+          __nv_bfloat16* drow = dqkv + (row0 + row) * g.ld_qkv + h * hd;
+#pragma unroll
+          for (int nt = 0; nt < HDP / 8; ++nt)
+            store_pair(drow, nt * 8 + 2 * tq, hd, dq[nt][2 * r], dq[nt][2 * r + 1]);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase B: warp w owns keys [16w, 16w + 16): dV = P^T dO, dK = dS^T Q
+    if (warp * 16 < N) {
+      float dk[HDP / 8][4], dv[HDP / 8][4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        // A = P^T (16 keys x 16 queries): transposed 8 x 8 blocks of P rows 16 ks..
+        const uint32_t off =
+            swz<64>(16 * ks + (lane & 7) + ((lane >> 4) << 3), 2 * warp + ((lane >> 3) & 1));
+        uint32_t pa[4], sa[4];
+        ldsm_x4_t(bP + off, pa);
+        ldsm_x4_t(bS + off, sa);
+#pragma unroll
+        for (int np = 0; np < HDP / 16; ++np) {
+          uint32_t bo[4], bq[4];
+          load_b_kn<HDP>(bO, 16 * ks, 2 * np, bo);
+          load_b_kn<HDP>(bQ, 16 * ks, 2 * np, bq);
+          if (ks == 0) {
+            mma16816_z(dv[2 * np], pa, bo[0], bo[1]);
+            mma16816_z(dv[2 * np + 1], pa, bo[2], bo[3]);
+            mma16816_z(dk[2 * np], sa, bq[0], bq[1]);
+            mma16816_z(dk[2 * np + 1], sa, bq[2], bq[3]);
+          } else {
+            mma16816(dv[2 * np], pa, bo[0], bo[1]);
+            mma16816(dv[2 * np + 1], pa, bo[2], bo[3]);
+            mma16816(dk[2 * np], sa, bq[0], bq[1]);
+            mma16816(dk[2 * np + 1], sa, bq[2], bq[3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int row = warp * 16 + gq + 8 * r;
+        if (row < N) {
+          __nv_bfloat16* drow_k = dqkv + (row0 + row) * g.ld_qkv + g.H * hd + h * hd;
+          __nv_bfloat16* drow_v = drow_k + g.H * hd;
+#pragma unroll
+          for (int nt = 0; nt < HDP / 8; ++nt) {
+            store_pair(drow_k, nt * 8 + 2 * tq, hd, dk[nt][2 * r], dk[nt][2 * r + 1]);
+            store_pair(drow_v, nt * 8 + 2 * tq, hd, dv[nt][2 * r], dv[nt][2 * r + 1]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // P / dS and this buffer are rewritten by the next items
+  }
+  if (!TMA) asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 static AttnGeom make_geom(int64_t B, int64_t N, int64_t H, int64_t hd) {
   AttnGeom g;
   g.B = static_cast<int>(B);
@@ -582,10 +997,89 @@ extern "C" int rp_set_attention_impl(int impl) {
   return RP_OK;
 }
 
+// window kernels for N <= 64 (A/B switch): 0 the single-tile fused kernels
+// (attn_fwd_win_kernel / attn_bwd_win_kernel), 1 the general mma.sync kernels
+static int g_attn_win_variant = 0;
+extern "C" int rp_set_attention_window_variant(int v) {
+  if (v < 0 || v > 1) return rp_fail(RP_ERR_CONFIG, "attention window variant must be 0 or 1");
+  g_attn_win_variant = v;
+  return RP_OK;
+}
+
+// TMA staging for the window kernels: head_dim 32 (64-byte rows, SW64) or 64 (SW128)
+static bool win_tma(int64_t hd) { return hd == 32 || hd == 64; }
+static int win_maps(WinMaps* m, const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                    int64_t B, int64_t N, int64_t H, int64_t hd) {
+  attn_tc::EncodeFn fn = attn_tc::encode_fn();
+  if (!fn) return RP_ERR_CUDA;
+  std::memset(m, 0, sizeof(*m));
+  const CUtensorMapSwizzle sw = hd == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(hd), static_cast<cuuint32_t>(N)};
+  const cuuint32_t es[2] = {1, 1};
+  auto map2d = [&](CUtensorMap* t, const void* base, int64_t cols) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(B * N)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    return fn(t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+              es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!map2d(&m->qkv, qkv, 3 * H * hd)) return RP_ERR_CUDA;
+  if (dout && !map2d(&m->dout, dout, H * hd)) return RP_ERR_CUDA;
+  if (lse) {
+    const cuuint64_t dims[1] = {static_cast<cuuint64_t>(B * H * N)};
+    const cuuint32_t lbox[1] = {static_cast<cuuint32_t>((N + 3) & ~3)};
+    if (fn(&m->lse, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(lse), dims, nullptr,
+           lbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return RP_ERR_CUDA;
+  }
+  return RP_OK;
+}
+
+// persistent grid: items capped at SMs x resident CTAs of `fn` (cached per kernel)
+static int64_t persistent_grid(const void* fn, int smem, int64_t items) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+      if (e.first == fn) occ = e.second;
+    if (!occ) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem);
+      if (occ < 1) occ = 1;
+      cache.emplace_back(fn, occ);
+    }
+  }
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return std::min<int64_t>(items, static_cast<int64_t>(nsm) * occ);
+}
+
 template <int HDP>
 static int attn_fwd_mma(const uint16_t* qkv, int64_t B, int64_t N, int64_t H, int64_t hd,
                         uint16_t* out, float* lse, cudaStream_t stream) {
   const AttnGeom g = make_geom(B, N, H, hd);
+  if (N <= kTile && g_attn_win_variant == 0) {
+    const int smem = 1024 + 2 * 3 * kTile * HDP * 2;
+    WinMaps maps;
+    const bool tma = win_tma(hd) && !win_maps(&maps, qkv, nullptr, nullptr, B, N, H, hd);
+    int rc;
+    const void* fn = tma ? reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, true>)
+                         : reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, false>);
+    if ((rc = set_smem_attr(fn, smem))) return rc;
+    const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
+    if (tma)
+      launch_k(attn_fwd_win_kernel<HDP, true>, dim3(grid), dim3(128), smem, stream, maps,
+               reinterpret_cast<const __nv_bfloat16*>(qkv),
+               reinterpret_cast<__nv_bfloat16*>(out), lse, g);
+    else
+      launch_k(attn_fwd_win_kernel<HDP, false>, dim3(grid), dim3(128), smem, stream, maps,
+               reinterpret_cast<const __nv_bfloat16*>(qkv),
+               reinterpret_cast<__nv_bfloat16*>(out), lse, g);
+    return rp_check_launch("attention_fwd_window");
+  }
   if (N <= kTile && B * H >= 4 * 148) {  // many short windows: persistent, double-buffered
     const int smem = 2 * 3 * kTile * HDP * 2;
     int rc;
@@ -649,6 +1143,27 @@ static int attn_bwd_mma(const uint16_t* qkv, const uint16_t* out, const float* l
                         const uint16_t* dout, int64_t B, int64_t N, int64_t H, int64_t hd,
                         uint16_t* dqkv, float* workspace, cudaStream_t s) {
   const AttnGeom g = make_geom(B, N, H, hd);
+  if (N <= kTile && g_attn_win_variant == 0) {
+    const int smem = 1024 + 2 * (4 * kTile * HDP * 2 + kTile * 4) + 2 * kTile * 64 * 2;
+    WinMaps maps;
+    const bool tma = win_tma(hd) && !win_maps(&maps, qkv, dout, lse, B, N, H, hd);
+    int rc;
+    const void* fn = tma ? reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, true>)
+                         : reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, false>);
+    if ((rc = set_smem_attr(fn, smem))) return rc;
+    const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
+    if (tma)
+      launch_k(attn_bwd_win_kernel<HDP, true>, dim3(grid), dim3(128), smem, s, maps,
+               reinterpret_cast<const __nv_bfloat16*>(qkv),
+               reinterpret_cast<const __nv_bfloat16*>(dout), lse,
+               reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+    else
+      launch_k(attn_bwd_win_kernel<HDP, false>, dim3(grid), dim3(128), smem, s, maps,
+               reinterpret_cast<const __nv_bfloat16*>(qkv),
+               reinterpret_cast<const __nv_bfloat16*>(dout), lse,
+               reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+    return rp_check_launch("attention_bwd_window");
+  }
   const int64_t total = B * N * H;
   int blocks = static_cast<int>((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
