@@ -24,6 +24,7 @@
 #include "ptx.cuh"
 #include "attn_common.cuh"
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <utility>
@@ -532,9 +533,6 @@ __device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1,
                "r"(r0), "r"(r1), "r"(r2), "r"(r3)
                : "memory");
 }
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
 __device__ __forceinline__ void zero_smem(uint8_t* p, int bytes) {
   for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
     *reinterpret_cast<uint4*>(p + i) = make_uint4(0, 0, 0, 0);
@@ -623,9 +621,9 @@ __device__ __forceinline__ void mask_cols(float (*s)[4], int N, int tq, float fi
 }
 
 // TMA maps of one window item: q | k | v boxes of {hd, N} out of qkv [T][3 H hd], dO boxes
-// out of dout [T][H hd], the LSE row as a 1-D box of N rounded up to 4 floats
+// out of dout [T][H hd]
 struct WinMaps {
-  CUtensorMap qkv, dout, lse;
+  CUtensorMap qkv, dout;
 };
 
 // grid = min(items, SMs x resident CTAs); block 128 (4 warps x 16 query rows)
@@ -742,7 +740,9 @@ __global__ void __launch_bounds__(128)
                         const __nv_bfloat16* __restrict__ qkv,
                         const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                         __nv_bfloat16* __restrict__ dqkv, AttnGeom g) {
-  constexpr int kT = kTile * HDP * 2, kBuf = 4 * kT + kTile * 4;  // Q K V dO | lse
+  // Q K V dO (every tile 1024-byte aligned, as the TMA swizzle requires); the LSE of the
+  // next item is loaded into registers one item ahead
+  constexpr int kT = kTile * HDP * 2, kBuf = 4 * kT;
   constexpr int kPS = kTile * 64 * 2;                              // P or dS, bf16 [64][64]
   pdl_trigger();
   extern __shared__ uint8_t sm_raw[];
@@ -753,7 +753,6 @@ __global__ void __launch_bounds__(128)
   if (TMA && threadIdx.x == 0) {
     tma_prefetch_desc(&maps.qkv);
     tma_prefetch_desc(&maps.dout);
-    tma_prefetch_desc(&maps.lse);
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_barrier_init();
@@ -762,35 +761,36 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   pdl_wait();
   const int total = g.B * g.H, hd = g.hd, N = g.N;
-  const int nl = (N + 3) & ~3;  // LSE box (16-byte multiple)
   auto prefetch = [&](int item, int slot) {
     const int h = item % g.H, b = item / g.H;
     uint8_t* buf = sm + slot * kBuf;
     if constexpr (TMA) {
       if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&bar[slot], static_cast<uint32_t>(4 * N * hd * 2 + nl * 4));
+        mbar_arrive_expect_tx(&bar[slot], static_cast<uint32_t>(4 * N * hd * 2));
 #pragma unroll
         for (int m = 0; m < 3; ++m)
           tma_load_2d(buf + m * kT, &maps.qkv, &bar[slot], (m * g.H + h) * hd, b * N);
         tma_load_2d(buf + 3 * kT, &maps.dout, &bar[slot], h * hd, b * N);
-        asm volatile(
-            "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%3}], [%2];" ::"r"(smem_u32(buf + 4 * kT)),
-            "l"(reinterpret_cast<uint64_t>(&maps.lse)), "r"(smem_u32(&bar[slot])), "r"(item * N)
-            : "memory");
       }
     } else {
       const __nv_bfloat16* base = qkv + static_cast<int64_t>(b) * N * g.ld_qkv + h * hd;
       win_load<HDP, 4>(buf, base, g.H * hd, g.ld_qkv,
                        dout + static_cast<int64_t>(b) * N * g.ld_o + h * hd, g.ld_o, N, hd);
-      const float* lrow = lse + static_cast<int64_t>(item) * N;  // [B][H][N]: item = b H + h
-      const uint32_t sl = smem_u32(buf + 4 * kT);
-      for (int i = threadIdx.x; i < N; i += blockDim.x) cp_async4(sl + 4 * i, lrow + i);
     }
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
   const uint32_t bP = smem_u32(sm + 2 * kBuf), bS = bP + kPS;
+  // this thread's two query rows' LSE ([B][H][N]: item = b H + h); padded rows: P = 0
+  auto load_lse = [&](int it, float* v) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = warp * 16 + gq + 8 * r;
+      v[r] = it < total && row < N ? __ldg(lse + static_cast<int64_t>(it) * N + row) : INFINITY;
+    }
+  };
   int item = blockIdx.x;
+  float lse_next[2];
+  load_lse(item, lse_next);
   if (item < total) prefetch(item, 0);
   if (!TMA) asm volatile("cp.async.commit_group;" ::: "memory");
   for (int k = 0; item < total; ++k, item += gridDim.x) {
@@ -804,7 +804,8 @@ __global__ void __launch_bounds__(128)
     }
     uint8_t* buf = sm + (k & 1) * kBuf;
     const uint32_t bQ = smem_u32(buf), bK = bQ + kT, bV = bQ + 2 * kT, bO = bQ + 3 * kT;
-    const float* sL = reinterpret_cast<const float*>(buf + 4 * kT);
+    const float lr[2] = {lse_next[0], lse_next[1]};
+    load_lse(next, lse_next);
     const int h = item % g.H, b = item / g.H;
     const int64_t row0 = static_cast<int64_t>(b) * N;
     // ---- phase A: warp w owns queries [16w, 16w + 16)
@@ -821,12 +822,7 @@ __global__ void __launch_bounds__(128)
         mm_abt64<HDP>(oa, bV, dp);
       }
       mask_cols(s, N, tq, -INFINITY);
-      float lr[2], dsum[2] = {0.f, 0.f};
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int row = warp * 16 + gq + 8 * r;
-        lr[r] = row < N ? sL[row] : INFINITY;  // padded query rows: P = 0
-      }
+      float dsum[2] = {0.f, 0.f};
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
@@ -1008,8 +1004,8 @@ extern "C" int rp_set_attention_window_variant(int v) {
 
 // TMA staging for the window kernels: head_dim 32 (64-byte rows, SW64) or 64 (SW128)
 static bool win_tma(int64_t hd) { return hd == 32 || hd == 64; }
-static int win_maps(WinMaps* m, const uint16_t* qkv, const uint16_t* dout, const float* lse,
-                    int64_t B, int64_t N, int64_t H, int64_t hd) {
+static int win_maps(WinMaps* m, const uint16_t* qkv, const uint16_t* dout, int64_t B, int64_t N,
+                    int64_t H, int64_t hd) {
   attn_tc::EncodeFn fn = attn_tc::encode_fn();
   if (!fn) return RP_ERR_CUDA;
   std::memset(m, 0, sizeof(*m));
@@ -1019,19 +1015,20 @@ static int win_maps(WinMaps* m, const uint16_t* qkv, const uint16_t* dout, const
   auto map2d = [&](CUtensorMap* t, const void* base, int64_t cols) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(B * N)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-    return fn(t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-              es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return static_cast<int>(fn(t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   };
-  if (!map2d(&m->qkv, qkv, 3 * H * hd)) return RP_ERR_CUDA;
-  if (dout && !map2d(&m->dout, dout, H * hd)) return RP_ERR_CUDA;
-  if (lse) {
-    const cuuint64_t dims[1] = {static_cast<cuuint64_t>(B * H * N)};
-    const cuuint32_t lbox[1] = {static_cast<cuuint32_t>((N + 3) & ~3)};
-    if (fn(&m->lse, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(lse), dims, nullptr,
-           lbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return RP_ERR_CUDA;
+  char msg[96];
+  int e;
+  if ((e = map2d(&m->qkv, qkv, 3 * H * hd))) {
+    std::snprintf(msg, sizeof(msg), "attention window: qkv tensor map (CUresult %d)", e);
+    return rp_fail(RP_ERR_CUDA, msg);
+  }
+  if (dout && (e = map2d(&m->dout, dout, H * hd))) {
+    std::snprintf(msg, sizeof(msg), "attention window: dout tensor map (CUresult %d)", e);
+    return rp_fail(RP_ERR_CUDA, msg);
   }
   return RP_OK;
 }
@@ -1064,8 +1061,10 @@ static int attn_fwd_mma(const uint16_t* qkv, int64_t B, int64_t N, int64_t H, in
   if (N <= kTile && g_attn_win_variant == 0) {
     const int smem = 1024 + 2 * 3 * kTile * HDP * 2;
     WinMaps maps;
-    const bool tma = win_tma(hd) && !win_maps(&maps, qkv, nullptr, nullptr, B, N, H, hd);
+    std::memset(&maps, 0, sizeof(maps));
+    const bool tma = win_tma(hd);
     int rc;
+    if (tma && (rc = win_maps(&maps, qkv, nullptr, B, N, H, hd))) return rc;
     const void* fn = tma ? reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, true>)
                          : reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, false>);
     if ((rc = set_smem_attr(fn, smem))) return rc;
@@ -1144,10 +1143,12 @@ static int attn_bwd_mma(const uint16_t* qkv, const uint16_t* out, const float* l
                         uint16_t* dqkv, float* workspace, cudaStream_t s) {
   const AttnGeom g = make_geom(B, N, H, hd);
   if (N <= kTile && g_attn_win_variant == 0) {
-    const int smem = 1024 + 2 * (4 * kTile * HDP * 2 + kTile * 4) + 2 * kTile * 64 * 2;
+    const int smem = 1024 + 2 * 4 * kTile * HDP * 2 + 2 * kTile * 64 * 2;
     WinMaps maps;
-    const bool tma = win_tma(hd) && !win_maps(&maps, qkv, dout, lse, B, N, H, hd);
+    std::memset(&maps, 0, sizeof(maps));
+    const bool tma = win_tma(hd);
     int rc;
+    if (tma && (rc = win_maps(&maps, qkv, dout, B, N, H, hd))) return rc;
     const void* fn = tma ? reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, true>)
                          : reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, false>);
     if ((rc = set_smem_attr(fn, smem))) return rc;
