@@ -207,7 +207,8 @@ def test_layer_norm_fwd_bwd(K, rows, cols):
 
 
 @pytest.mark.parametrize("nparts,cols", [(1576, 3072), (788, 1536), (257, 40), (300, 100),
-                                         (5000, 64), (129, 3072), (2, 8)])
+                                         (5000, 64), (129, 3072), (2, 8), (12544, 512),
+                                         (2049, 200), (70000, 32)])
 def test_colsum_parts(K, nparts, cols):
     """Many-part column sums (one cluster launch above 256 parts, one CTA per 32 columns
     below): fp64 reference, ragged part counts and column counts, accumulate, determinism."""

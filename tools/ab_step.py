@@ -1,5 +1,6 @@
-"""Same-process A/B of whole-step time: Reprop / PaReprop x PDL on / off (device-timed,
-CUDA graphs), so clock / power-cap drift between boxes does not enter the comparison.
+"""Same-process A/B of whole-step time: Reprop / PaReprop x PDL on / off, or x window-attention
+kernels 0 / 1 with --window (device-timed, CUDA graphs), so clock / power-cap drift between
+boxes does not enter the comparison.
 
     python tools/ab_step.py [--rounds 3]
 """
@@ -25,6 +26,8 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--window", action="store_true",
+                    help="A/B the window-attention kernels (variant 0 vs 1) instead of PDL")
     a = ap.parse_args(argv)
     p = dict(PRESETS[a.preset])
     if a.batch:
@@ -33,13 +36,19 @@ def main(argv=None):
     eng.set_lr(1e-4)
     res = {}
     for r in range(a.rounds):
-        for pdl in (1, 0):
-            _capi.lib().rp_set_pdl(pdl)
+        for v in (1, 0):
+            if a.window:
+                _capi.lib().rp_set_attention_window_variant(v)
+                tag = f"win{v}"
+            else:
+                _capi.lib().rp_set_pdl(v)
+                tag = f"pdl{v}"
             eng.invalidate_graphs()
             for mode, name in ((REPROP, "reprop"), (PAREPROP, "pareprop")):
                 ms = time_steps(eng, mode, a.steps)
-                res.setdefault(f"{name}_pdl{pdl}", []).append(ms)
-    _capi.lib().rp_set_pdl(1)
+                res.setdefault(f"{name}_{tag}", []).append(ms)
+    _capi.lib().rp_set_pdl(0)
+    _capi.lib().rp_set_attention_window_variant(0)
     B = p["batch"]
     out = {k: {"ms": min(v), "img_s": B * 1e3 / min(v)} for k, v in res.items()}
     print(json.dumps(out))

@@ -1,6 +1,6 @@
 """Device-timed column-sum reductions at the engine's shapes (RevViT-B, batch 256):
 the d_u GEMM's per-32-row partials -> db1 (1576 x 3072) and the LayerNorm backward's
-per-64-row dgamma|dbeta partials (788 x 1536). Prints one JSON line of us per call.
+per-64-row dgamma|dbeta partials (788 x 1536); Rev-Swin-B (batch 128) stage shapes after. Prints one JSON line of us per call.
 
     RP_LIB=... python tools/colsum_ab.py
 """
@@ -28,7 +28,7 @@ def t(fn, iters=200):
 
 
 res = {}
-for n, c in ((1576, 3072), (788, 1536)):
+for n, c in ((1576, 3072), (788, 1536), (12544, 512), (3136, 1024), (6272, 256), (784, 2048)):
     part = torch.randn(n, c, device="cuda")
     out = torch.zeros(c, device="cuda")
     res[f"{n}x{c}"] = round(t(lambda: K.colsum_parts(part, out=out)), 2)
