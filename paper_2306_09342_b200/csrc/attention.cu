@@ -627,7 +627,9 @@ struct WinMaps {
 };
 
 // grid = min(items, SMs x resident CTAs); block 128 (4 warps x 16 query rows)
-template <int HDP, bool TMA>
+// NW > 0: the window length as a compile-time constant (Swin's 7 x 7 = 49): masks, loop
+// bounds and row offsets fold; NW = 0 reads it from g.N. With TMA the head dim is HDP.
+template <int HDP, bool TMA, int NW>
 __global__ void __launch_bounds__(128)
     attn_fwd_win_kernel(const __grid_constant__ WinMaps maps,
                         const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(128)
   fence_proxy_async_smem();  // the zero fill is visible to the TMA writes around it
   __syncthreads();
   pdl_wait();
-  const int total = g.B * g.H, hd = g.hd, N = g.N;
+  const int total = g.B * g.H, hd = TMA ? HDP : g.hd, N = NW ? NW : g.N;
   auto prefetch = [&](int item, int slot) {
     const int h = item % g.H, b = item / g.H;
     uint8_t* buf = sm + slot * kBuf;
@@ -730,11 +732,12 @@ __global__ void __launch_bounds__(128)
 // Fused backward of one (window, head) item per pass, no D pre-pass and no O read:
 //   phase A (warp w = queries 16w..): S = Q K^T, dP = dO V^T, P = exp2(S scale - lse),
 //     D = rowsum(P * dP) (the softmax VJP's sum as ref:proj/core/src/ops.cpp:219-220 forms
-//     it from the cached probabilities), dS = P (dP - D) scale, dQ = dS K; P and dS -> smem
-//     (bf16, stmatrix)
-//   phase B (warp w = keys 16w..): dV = P^T dO, dK = dS^T Q (ldmatrix.trans of P / dS)
+//     it from the cached probabilities), dS' = P (dP - D), dQ = scale (dS' K); P and dS'
+//     -> smem (bf16, stmatrix)
+//   phase B (warp w = keys 16w..): dV = P^T dO, dK = scale (dS'^T Q) (ldmatrix.trans)
+// (the softmax scale is applied once per output element instead of per score)
 // Every output element is written by one warp: no atomics, bit-reproducible.
-template <int HDP, bool TMA>
+template <int HDP, bool TMA, int NW>
 __global__ void __launch_bounds__(128)
     attn_bwd_win_kernel(const __grid_constant__ WinMaps maps,
                         const __nv_bfloat16* __restrict__ qkv,
@@ -760,7 +763,7 @@ __global__ void __launch_bounds__(128)
   fence_proxy_async_smem();
   __syncthreads();
   pdl_wait();
-  const int total = g.B * g.H, hd = g.hd, N = g.N;
+  const int total = g.B * g.H, hd = TMA ? HDP : g.hd, N = NW ? NW : g.N;
   auto prefetch = [&](int item, int slot) {
     const int h = item % g.H, b = item / g.H;
     uint8_t* buf = sm + slot * kBuf;
@@ -839,7 +842,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) dp[nt][e] = s[nt][e] * (dp[nt][e] - dsum[e >> 1]) * g.scale;
+        for (int e = 0; e < 4; ++e) dp[nt][e] = s[nt][e] * (dp[nt][e] - dsum[e >> 1]);
       // P and dS (bf16) to smem as [query][key] 64 x 64 tiles, one stmatrix per 16 x 16 block
 #pragma unroll
       for (int np = 0; np < 4; ++np) {
@@ -855,7 +858,7 @@ __global__ void __launch_bounds__(128)
                 pack_bf16x2(dp[2 * np + 1][2], dp[2 * np + 1][3]));
       }
       float dq[HDP / 8][4];
-      mm_pb64<HDP>(dp, bK, dq);  // dQ = dS K
+      mm_pb64<HDP>(dp, bK, dq);  // dQ = scale (dS' K)
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int row = warp * 16 + gq + 8 * r;
@@ -863,7 +866,8 @@ __global__ void __launch_bounds__(128)
           __nv_bfloat16* drow = dqkv + (row0 + row) * g.ld_qkv + h * hd;
 #pragma unroll
           for (int nt = 0; nt < HDP / 8; ++nt)
-            store_pair(drow, nt * 8 + 2 * tq, hd, dq[nt][2 * r], dq[nt][2 * r + 1]);
+            store_pair(drow, nt * 8 + 2 * tq, hd, dq[nt][2 * r] * g.scale,
+                       dq[nt][2 * r + 1] * g.scale);
         }
       }
     }
@@ -905,7 +909,8 @@ __global__ void __launch_bounds__(128)
           __nv_bfloat16* drow_v = drow_k + g.H * hd;
 #pragma unroll
           for (int nt = 0; nt < HDP / 8; ++nt) {
-            store_pair(drow_k, nt * 8 + 2 * tq, hd, dk[nt][2 * r], dk[nt][2 * r + 1]);
+            store_pair(drow_k, nt * 8 + 2 * tq, hd, dk[nt][2 * r] * g.scale,
+                       dk[nt][2 * r + 1] * g.scale);
             store_pair(drow_v, nt * 8 + 2 * tq, hd, dv[nt][2 * r], dv[nt][2 * r + 1]);
           }
         }
@@ -1065,18 +1070,20 @@ static int attn_fwd_mma(const uint16_t* qkv, int64_t B, int64_t N, int64_t H, in
     const bool tma = win_tma(hd);
     int rc;
     if (tma && (rc = win_maps(&maps, qkv, nullptr, B, N, H, hd))) return rc;
-    const void* fn = tma ? reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, true>)
-                         : reinterpret_cast<const void*>(attn_fwd_win_kernel<HDP, false>);
-    if ((rc = set_smem_attr(fn, smem))) return rc;
-    const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
-    if (tma)
-      launch_k(attn_fwd_win_kernel<HDP, true>, dim3(grid), dim3(128), smem, stream, maps,
+    auto go = [&](auto kernel) {
+      const void* fn = reinterpret_cast<const void*>(kernel);
+      int e = set_smem_attr(fn, smem);
+      if (e) return e;
+      const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
+      launch_k(kernel, dim3(grid), dim3(128), smem, stream, maps,
                reinterpret_cast<const __nv_bfloat16*>(qkv),
                reinterpret_cast<__nv_bfloat16*>(out), lse, g);
-    else
-      launch_k(attn_fwd_win_kernel<HDP, false>, dim3(grid), dim3(128), smem, stream, maps,
-               reinterpret_cast<const __nv_bfloat16*>(qkv),
-               reinterpret_cast<__nv_bfloat16*>(out), lse, g);
+      return 0;
+    };
+    if ((rc = !tma ? go(attn_fwd_win_kernel<HDP, false, 0>)
+              : N == 49 ? go(attn_fwd_win_kernel<HDP, true, 49>)
+                        : go(attn_fwd_win_kernel<HDP, true, 0>)))
+      return rc;
     return rp_check_launch("attention_fwd_window");
   }
   if (N <= kTile && B * H >= 4 * 148) {  // many short windows: persistent, double-buffered
@@ -1149,20 +1156,21 @@ static int attn_bwd_mma(const uint16_t* qkv, const uint16_t* out, const float* l
     const bool tma = win_tma(hd);
     int rc;
     if (tma && (rc = win_maps(&maps, qkv, dout, B, N, H, hd))) return rc;
-    const void* fn = tma ? reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, true>)
-                         : reinterpret_cast<const void*>(attn_bwd_win_kernel<HDP, false>);
-    if ((rc = set_smem_attr(fn, smem))) return rc;
-    const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
-    if (tma)
-      launch_k(attn_bwd_win_kernel<HDP, true>, dim3(grid), dim3(128), smem, s, maps,
+    auto go = [&](auto kernel) {
+      const void* fn = reinterpret_cast<const void*>(kernel);
+      int e = set_smem_attr(fn, smem);
+      if (e) return e;
+      const unsigned grid = static_cast<unsigned>(persistent_grid(fn, smem, B * H));
+      launch_k(kernel, dim3(grid), dim3(128), smem, s, maps,
                reinterpret_cast<const __nv_bfloat16*>(qkv),
                reinterpret_cast<const __nv_bfloat16*>(dout), lse,
                reinterpret_cast<__nv_bfloat16*>(dqkv), g);
-    else
-      launch_k(attn_bwd_win_kernel<HDP, false>, dim3(grid), dim3(128), smem, s, maps,
-               reinterpret_cast<const __nv_bfloat16*>(qkv),
-               reinterpret_cast<const __nv_bfloat16*>(dout), lse,
-               reinterpret_cast<__nv_bfloat16*>(dqkv), g);
+      return 0;
+    };
+    if ((rc = !tma ? go(attn_bwd_win_kernel<HDP, false, 0>)
+              : N == 49 ? go(attn_bwd_win_kernel<HDP, true, 49>)
+                        : go(attn_bwd_win_kernel<HDP, true, 0>)))
+      return rc;
     return rp_check_launch("attention_bwd_window");
   }
   const int64_t total = B * N * H;
