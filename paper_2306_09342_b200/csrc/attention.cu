@@ -964,6 +964,9 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
                         uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready,
                         int fused);
+int rp_attention_bwd_tc_wide(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
+                             const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
+                             int64_t hd, uint16_t* dqkv, cudaStream_t stream);
 // 0 = tcgen05 where it applies (head_dim 64): backward in one fused pass for N <= 208
 // (attention_bwd_fused.cu), above that one dK/dV pass + dQ from the stored dS^T;
 // 1 = mma.sync only; 2 = tcgen05 with the two-pass (dQ pass, dK/dV pass) backward that
@@ -1215,6 +1218,11 @@ extern "C" int rp_attention_bwd_ex(const uint16_t* qkv, const uint16_t* out, con
                         : nullptr;
     rc = rp_attention_bwd_tc(qkv, out, dout, lse, workspace, B, N, H, dqkv, s, dst, d_ready,
                              g_attn_impl == 0);
+    if (rc != RP_ERR_CONFIG) return rc;
+  }
+  // head dims 72..128 (G48's 104) above the window range: two-pass tcgen05, D in-kernel
+  if (g_attn_impl != 1 && head_dim > 64 && N > kTile) {
+    rc = rp_attention_bwd_tc_wide(qkv, out, dout, lse, workspace, B, N, H, head_dim, dqkv, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
   if (head_dim <= 32)

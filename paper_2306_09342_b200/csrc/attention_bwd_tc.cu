@@ -22,14 +22,17 @@
 #include "attn_common.cuh"
 #include "launch.h"
 
+#include <cstring>
+
 namespace rp {
 namespace attn_tc {
 
 
 struct BwdGeom {
   int B, N, H, Nk;    // sequences, tokens, heads, N rounded up to 16
-  int64_t ld_o;       // row pitch of O / dO (H * 64)
-  int64_t ld_qkv;     // row pitch of qkv / dqkv (3 H * 64)
+  int hd;             // head dim (64, or 72..128 on the wide variant)
+  int64_t ld_o;       // row pitch of O / dO (H * hd)
+  int64_t ld_qkv;     // row pitch of qkv / dqkv (3 H * hd)
   float scale, scale_log2;
 };
 
@@ -63,28 +66,50 @@ __device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* dst, const float
 
 // ------------------------------------------------------------------ the kernel (two passes)
 // 288 threads: warps 0-7 elementwise (TMEM lane quarter w%4, column half w/4 of a 64-wide
-// chunk), warp 8 TMA + MMA issue (one thread). 256 TMEM columns: S [0, 64), dP [64, 128),
-// accumulators [128, 256). ~100 KB of smem, so two CTAs share an SM and one's elementwise
-// phase overlaps the other's MMAs. Operands:
+// chunk), warp 8 TMA + MMA issue (one thread). TMEM: S [0, 64), dP [64, 128), accumulators
+// from 128 (HP = 64: two 64-column ones in 256 columns, ~100 KB of smem, so two CTAs share an
+// SM and one's elementwise phase overlaps the other's MMAs; HP = 128: head dims 72..128, two
+// round16(hd)-column accumulators at 128 and 256 of 512 columns, ~193 KB, one CTA per SM).
+// Operands (bf16, K-major SW128 atoms of 64 columns; HP = 128 stores each operand as two
+// atom planes [atom][rows][128 B], the second loaded by a box of hd - 64 columns whose
+// untouched tail stays zero -- tools/probe/tma_narrow_box.cu shows the narrow box landing in
+// the same swizzled 128-byte rows):
 //   tile  A | B   128 rows of the item (DQ: Q | dO, DKDV: K | V), double-buffered per item
 //                 so the next item's tile streams in during the current one
 //   chunk C | D   64 rows of the streamed side (DQ: K | V, DKDV: Q | dO), a 2-slot ring
 //                 that runs ahead across item boundaries; any N up to 1024
-// MMA1: S = A C_c^T, dP = B D_c^T (N = chunk width); MMA2: DQ dQ += dS C_c; DKDV
-// dV += P^T D_c, dK += dS^T C_c (A operands re-packed to bf16 in TMEM).
+// MMA1: S = A C_c^T, dP = B D_c^T (N = chunk width, K = hd in 16-column steps); MMA2: DQ
+// dQ += dS C_c; DKDV dV += P^T D_c, dK += dS^T C_c (A operands re-packed to bf16 in TMEM;
+// B operands MN-major over the chunk's atom planes, plane stride 64 rows x 128 B = LBO).
 constexpr int kBwdWarps = 9;
 constexpr int kBwdThreads = kBwdWarps * 32;
-constexpr int kTileBytes = 2 * 128 * 128;   // A | B
-constexpr int kChunkBytes = 2 * 64 * 128;   // C_c | D_c
-constexpr int kBwdSmem = 2 * kTileBytes + 2 * kChunkBytes;
+template <int HP>
+struct BwdCfg {
+  static constexpr int kAtoms = HP / 64;
+  static constexpr int kTileBytes = 2 * 128 * 128 * kAtoms;  // A | B
+  static constexpr int kChunkBytes = 2 * 64 * 128 * kAtoms;  // C_c | D_c
+  static constexpr int kSmem = 2 * kTileBytes + 2 * kChunkBytes;
+  static constexpr int kTmemCols = HP == 64 ? 256 : 512;
+  static constexpr int kAcc1 = HP == 64 ? 192 : 256;  // second accumulator (DKDV dK)
+};
+constexpr int kBwdSmem = BwdCfg<64>::kSmem;
 
-template <bool DQ>
-__global__ void __launch_bounds__(kBwdThreads, 2)
-    attn_bwd_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
+// TMA maps of one operand: box {64, rows} over the first 64 head columns and, for head dims
+// above 64, box {hd - 64, rows} over the rest
+struct OpMaps {
+  CUtensorMap lo, hi;
+};
+
+template <bool DQ, int HP>
+__global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
+    attn_bwd_tc(const __grid_constant__ OpMaps tm_a, const __grid_constant__ OpMaps tm_b,
+                const __grid_constant__ OpMaps tm_c, const __grid_constant__ OpMaps tm_d,
                 const __nv_bfloat16* __restrict__ O, const float* __restrict__ lse,
                 float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv, BwdGeom g, BwdPlan pl,
                 __nv_bfloat16* __restrict__ dSt) {
+  using Cfg = BwdCfg<HP>;
+  constexpr int kTileBytes = Cfg::kTileBytes, kChunkBytes = Cfg::kChunkBytes;
+  constexpr uint32_t kTilePlane = 128 * 128, kChunkPlane = 64 * 128;  // one atom plane
   pdl_trigger();
 
   __shared__ float red[2][128];                // DQ: D partials [column half][row]
@@ -107,12 +132,19 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   uint64_t* bar_e = bars + 11;      // accumulators read out (8 warps)
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  const int hd = HP == 64 ? 64 : g.hd;
+  if constexpr (HP > 64) {
+    // the second atom plane's columns past hd are never written by the TMA: zero them once
+    for (int i = static_cast<int>(threadIdx.x) * 16; i < Cfg::kSmem; i += kBwdThreads * 16)
+      *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   if (warp == 8) {
     if (lane == 0) {
-      tma_prefetch_desc(&tm_a);
-      tma_prefetch_desc(&tm_b);
-      tma_prefetch_desc(&tm_c);
-      tma_prefetch_desc(&tm_d);
+      tma_prefetch_desc(&tm_a.lo);
+      tma_prefetch_desc(&tm_b.lo);
+      tma_prefetch_desc(&tm_c.lo);
+      tma_prefetch_desc(&tm_d.lo);
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tile_full[i], 1);
         mbar_init(&tile_free[i], 1);
@@ -125,14 +157,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       mbar_init(bar_e, 8);
       fence_barrier_init();
     }
-    tmem_alloc(&tmem_slot, 256);
+    tmem_alloc(&tmem_slot, Cfg::kTmemCols);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   pdl_wait();
-  const int Nk = g.Nk, d = g.H * 64;
+  const int Nk = g.Nk, d = g.H * hd;
   const int nch = (Nk + 63) / 64;
   const int K = pl.nitems > static_cast<int>(blockIdx.x)
                     ? (pl.nitems - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
@@ -145,15 +177,21 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 
   if (warp == 8) {
     if (lane == 0) {
+      // one operand block of `plane`-byte atom planes: box {64} then, above 64, {hd - 64}
+      auto load_op = [&](uint8_t* dst, const OpMaps& m, uint64_t* bar, int col, int row,
+                         uint32_t plane) {
+        tma_load_2d(dst, &m.lo, bar, col, row);
+        if constexpr (HP > 64) tma_load_2d(dst + plane, &m.hi, bar, col + 64, row);
+      };
       auto load_tile = [&](int k) {
         int tile, h, b;
         item_coords(item_of(k), pl.ntile, g.H, tile, h, b);
         const int row = b * g.N + tile * 128;
         uint8_t* dst = tiles + (k & 1) * kTileBytes;
         uint64_t* bar = &tile_full[k & 1];
-        mbar_arrive_expect_tx(bar, kTileBytes);
-        tma_load_2d(dst, &tm_a, bar, ca + h * 64, row);
-        tma_load_2d(dst + 16384, &tm_b, bar, cb + h * 64, row);
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 128 * hd * 2));
+        load_op(dst, tm_a, bar, ca + h * hd, row, kTilePlane);
+        load_op(dst + kTileBytes / 2, tm_b, bar, cb + h * hd, row, kTilePlane);
       };
       auto load_chunk = [&](int idx) {  // flat chunk index over (item, chunk)
         const int k = idx / nch, c = idx % nch;
@@ -162,11 +200,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const int row = b * g.N + 64 * c;
         uint8_t* dst = ring + (idx & 1) * kChunkBytes;
         uint64_t* bar = &ring_full[idx & 1];
-        mbar_arrive_expect_tx(bar, kChunkBytes);
-        tma_load_2d(dst, &tm_c, bar, cc + h * 64, row);
-        tma_load_2d(dst + 8192, &tm_d, bar, cd + h * 64, row);
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 64 * hd * 2));
+        load_op(dst, tm_c, bar, cc + h * hd, row, kChunkPlane);
+        load_op(dst + kChunkBytes / 2, tm_d, bar, cd + h * hd, row, kChunkPlane);
       };
-      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      const int nacc = (hd + 15) / 16 * 16, nks = nacc / 16;
+      const uint32_t idesc_o = make_idesc_bf16(128, static_cast<uint32_t>(nacc), false, true);
       const int total = K * nch;
       if (K > 0) {
         load_tile(0);
@@ -179,19 +218,20 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           load_tile(k + 1);
         }
         mbar_wait(&tile_full[k & 1], (k >> 1) & 1);
-        const uint32_t ta = smem_u32(tiles + (k & 1) * kTileBytes), tb = ta + 16384u;
+        const uint32_t ta = smem_u32(tiles + (k & 1) * kTileBytes), tb = ta + kTileBytes / 2;
         for (int c = 0; c < nch; ++c, ++u) {
           const int w = min(64, Nk - 64 * c);
           mbar_wait(&ring_full[u & 1], (u >> 1) & 1);
           tc_fence_after();
-          const uint32_t rc = smem_u32(ring + (u & 1) * kChunkBytes), rd = rc + 8192u;
+          const uint32_t rc = smem_u32(ring + (u & 1) * kChunkBytes), rd = rc + kChunkBytes / 2;
           const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(w), false, false);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            umma_bf16(tmem, make_sdesc_sw128(ta + kk * 32, 16, 1024),
-                      make_sdesc_sw128(rc + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-            umma_bf16(tmem + 64, make_sdesc_sw128(tb + kk * 32, 16, 1024),
-                      make_sdesc_sw128(rd + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < nks; ++kk) {
+            const uint32_t ka = static_cast<uint32_t>(kk >> 2) * kTilePlane + (kk & 3) * 32;
+            const uint32_t kc = static_cast<uint32_t>(kk >> 2) * kChunkPlane + (kk & 3) * 32;
+            umma_bf16(tmem, make_sdesc_sw128(ta + ka, 16, 1024),
+                      make_sdesc_sw128(rc + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            umma_bf16(tmem + 64, make_sdesc_sw128(tb + ka, 16, 1024),
+                      make_sdesc_sw128(rd + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
           }
           umma_commit(bar_s);
           if (u + 1 < total) {  // next chunk into the other ring slot once its MMAs retired
@@ -206,12 +246,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
             const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
             if constexpr (DQ) {
               umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
-                           make_sdesc_sw128(rc + row16, 8192, 1024), idesc_o, acc);  // dQ += dS K_c
+                           make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dQ += dS K_c
             } else {
               umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
-                           make_sdesc_sw128(rd + row16, 8192, 1024), idesc_o, acc);  // dV += P^T dO_c
-              umma_ts_bf16(tmem + 192, tmem + 64 + chunk_acol(ks),
-                           make_sdesc_sw128(rc + row16, 8192, 1024), idesc_o, acc);  // dK += dS^T Q_c
+                           make_sdesc_sw128(rd + row16, kChunkPlane, 1024), idesc_o, acc);  // dV += P^T dO_c
+              umma_ts_bf16(tmem + Cfg::kAcc1, tmem + 64 + chunk_acol(ks),
+                           make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dK += dS^T Q_c
             }
           }
           umma_commit(&ring_free[u & 1]);
@@ -240,24 +280,30 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               : nullptr;
       float lr = 0.f, nds = 0.f;
       if constexpr (DQ) {
-        // ---- D = rowsum(dO * O) for this lane's query (dO from the smem tile, O global)
+        // ---- D = rowsum(dO * O) for this lane's query (dO from the smem tile, O global):
+        // warp half kh covers head columns [32 kh, 32 kh + 32) of each 64-column atom plane
         lr = row < g.N ? lse[hb + row] : 0.f;
         mbar_wait(&tile_full[k & 1], (k >> 1) & 1);
         float dpart = 0.f;
         if (row < g.N) {
-          const uint4* o4 = reinterpret_cast<const uint4*>(O + grow * g.ld_o + h * 64 + kh * 32);
-          const uint8_t* drow = tiles + (k & 1) * kTileBytes + 16384 + rloc * 128;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 ov = __ldg(o4 + c);
-            const int ch = kh * 4 + c;
-            const uint4 dv = *reinterpret_cast<const uint4*>(drow + ((ch ^ (rloc & 7)) << 4));
-            const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
+          for (int a = 0; a < HP / 64; ++a) {
+            const uint8_t* drow =
+                tiles + (k & 1) * kTileBytes + kTileBytes / 2 + a * kTilePlane + rloc * 128;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 a = unpack_bf16x2(ow[e]), bb = unpack_bf16x2(dw[e]);
-              dpart = fmaf(a.x, bb.x, dpart);
-              dpart = fmaf(a.y, bb.y, dpart);
+            for (int c = 0; c < 4; ++c) {
+              const int col = 64 * a + 32 * kh + 8 * c;  // head column of this 16-byte chunk
+              if (col >= hd) break;
+              const uint4 ov = __ldg(reinterpret_cast<const uint4*>(O + grow * g.ld_o + h * hd + col));
+              const int ch = kh * 4 + c;
+              const uint4 dv = *reinterpret_cast<const uint4*>(drow + ((ch ^ (rloc & 7)) << 4));
+              const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x = unpack_bf16x2(ow[e]), y = unpack_bf16x2(dw[e]);
+                dpart = fmaf(x.x, y.x, dpart);
+                dpart = fmaf(x.y, y.y, dpart);
+              }
             }
           }
         }
@@ -334,32 +380,50 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p);
       }
-      // ---- epilogue
+      // ---- epilogue: warp half kh stores head columns [kh HP / 2, (kh + 1) HP / 2) < hd
       mbar_wait(bar_o, k & 1);
       tc_fence_after();
-      float o[32];
-      __nv_bfloat16* dst = dqkv + grow * g.ld_qkv + h * 64 + kh * 32;
+      constexpr int kHalf = HP / 2;
+      float o[kHalf];
+      const int c0 = kh * kHalf;
+      __nv_bfloat16* dst = dqkv + grow * g.ld_qkv + h * hd + c0;
+      auto ld_acc = [&](uint32_t col) {
+        if (active)
+#pragma unroll
+          for (int j = 0; j < kHalf / 32; ++j)
+            tmem_ld32(tmem + lq + col + static_cast<uint32_t>(c0 + 32 * j), o + 32 * j);
+      };
+      auto st_acc = [&](__nv_bfloat16* p) {
+        if (row < g.N)
+#pragma unroll
+          for (int j = 0; j < kHalf / 8; ++j)
+            if (c0 + 8 * j < hd)
+              reinterpret_cast<uint4*>(p)[j] =
+                  make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                             pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                             pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+      };
       if constexpr (DQ) {
-        if (active) tmem_ld32(tmem + lq + 128 + static_cast<uint32_t>(32 * kh), o);
+        ld_acc(128);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_e);
-        if (row < g.N) store_row32_bf16(dst, o);
+        st_acc(dst);
       } else {
-        if (active) tmem_ld32(tmem + lq + 128 + static_cast<uint32_t>(32 * kh), o);
-        if (row < g.N) store_row32_bf16(dst + 2 * d, o);  // dV
-        if (active) tmem_ld32(tmem + lq + 192 + static_cast<uint32_t>(32 * kh), o);
+        ld_acc(128);
+        st_acc(dst + 2 * d);  // dV
+        ld_acc(Cfg::kAcc1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_e);
-        if (row < g.N) store_row32_bf16(dst + d, o);  // dK
+        st_acc(dst + d);  // dK
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, 256);
+  if (warp == 8) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
 // ------------------------------------------------------------------ D and dQ for the fused path
@@ -552,23 +616,30 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
   g.N = static_cast<int>(N);
   g.H = static_cast<int>(H);
   g.Nk = static_cast<int>((N + 15) / 16 * 16);
+  g.hd = 64;
   g.ld_o = H * 64;
   g.ld_qkv = 3 * H * 64;
   g.scale = 1.0f / 8.0f;
   g.scale_log2 = g.scale * 1.4426950408889634f;
   const int64_t T = S * N;
-  CUtensorMap q128, do128, k128, q64, do64, k64;
-  if (make_map(&q128, qkv, T, 3 * H * 64, 128) || make_map(&do128, dout, T, H * 64, 128) ||
-      make_map(&k128, qkv, T, 3 * H * 64, 128) || make_map(&q64, qkv, T, 3 * H * 64, 64) ||
-      make_map(&do64, dout, T, H * 64, 64) || make_map(&k64, qkv, T, 3 * H * 64, 64))
+  OpMaps q128, do128, k128, q64, do64, k64;
+  std::memset(&q128, 0, sizeof(OpMaps));
+  std::memset(&do128, 0, sizeof(OpMaps));
+  std::memset(&k128, 0, sizeof(OpMaps));
+  std::memset(&q64, 0, sizeof(OpMaps));
+  std::memset(&do64, 0, sizeof(OpMaps));
+  std::memset(&k64, 0, sizeof(OpMaps));
+  if (make_map(&q128.lo, qkv, T, 3 * H * 64, 128) || make_map(&do128.lo, dout, T, H * 64, 128) ||
+      make_map(&k128.lo, qkv, T, 3 * H * 64, 128) || make_map(&q64.lo, qkv, T, 3 * H * 64, 64) ||
+      make_map(&do64.lo, dout, T, H * 64, 64) || make_map(&k64.lo, qkv, T, 3 * H * 64, 64))
     return rp_fail(RP_ERR_CUDA, "attention_bwd_tc: tensor map encode failed");
   const int smem = 1024 + kBwdSmem;
   const int smem_dq = 1024 + kDqStages * kDqStage;
   static std::once_flag once;
   static int nsm = 148;
   std::call_once(once, [smem, smem_dq] {
-    cudaFuncSetAttribute(attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_tc<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_tc<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -600,20 +671,71 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
                reinterpret_cast<const __nv_bfloat16*>(out),
                reinterpret_cast<const __nv_bfloat16*>(dout), Dg, T, g.N, g.H);
     }
-    launch_k(attn_bwd_tc<false>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64,
+    launch_k(attn_bwd_tc<false, 64>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64,
              do64, reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
              reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, reinterpret_cast<__nv_bfloat16*>(dSt));
-    launch_k(attn_dq_tc, dim3(grid), dim3(192), smem_dq, stream, ds, k64,
+    launch_k(attn_dq_tc, dim3(grid), dim3(192), smem_dq, stream, ds, k64.lo,
              reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl);
     return rp_check_launch("attention_bwd_tc");
   }
   // dQ (+ D): tiles Q | dO, chunks K | V (qkv maps; the dO map for the dO tile)
-  launch_k(attn_bwd_tc<true>, dim3(grid), dim3(kBwdThreads), smem, stream, q128, do128, k64, k64,
+  launch_k(attn_bwd_tc<true, 64>, dim3(grid), dim3(kBwdThreads), smem, stream, q128, do128, k64, k64,
            reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
            reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
   // dK, dV: tiles K | V, chunks Q | dO
-  launch_k(attn_bwd_tc<false>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64, do64,
+  launch_k(attn_bwd_tc<false, 64>, dim3(grid), dim3(kBwdThreads), smem, stream, k128, k128, q64, do64,
            reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
            reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
   return rp_check_launch("attention_bwd_tc");
+}
+
+// Two-pass tcgen05 backward for head dims 72..128 (multiples of 8; e.g. the G48 config's
+// 104): dQ (+ D) then dK / dV, operands as two 64-column atom planes. RP_ERR_CONFIG without
+// launching outside that range.
+int rp_attention_bwd_tc_wide(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
+                             const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
+                             int64_t hd, uint16_t* dqkv, cudaStream_t stream) {
+  using namespace attn_tc;
+  if (N > 1024 || N < 1 || hd <= 64 || hd > 128 || hd % 8) return RP_ERR_CONFIG;
+  BwdGeom g;
+  g.B = static_cast<int>(S);
+  g.N = static_cast<int>(N);
+  g.H = static_cast<int>(H);
+  g.Nk = static_cast<int>((N + 15) / 16 * 16);
+  g.hd = static_cast<int>(hd);
+  g.ld_o = H * hd;
+  g.ld_qkv = 3 * H * hd;
+  g.scale = 1.0f / sqrtf(static_cast<float>(hd));
+  g.scale_log2 = g.scale * 1.4426950408889634f;
+  const int64_t T = S * N;
+  const uint32_t hi = static_cast<uint32_t>(hd - 64);
+  OpMaps qkv128, do128, qkv64, do64;
+  if (make_map(&qkv128.lo, qkv, T, 3 * H * hd, 128) || make_map(&qkv128.hi, qkv, T, 3 * H * hd, 128, hi) ||
+      make_map(&do128.lo, dout, T, H * hd, 128) || make_map(&do128.hi, dout, T, H * hd, 128, hi) ||
+      make_map(&qkv64.lo, qkv, T, 3 * H * hd, 64) || make_map(&qkv64.hi, qkv, T, 3 * H * hd, 64, hi) ||
+      make_map(&do64.lo, dout, T, H * hd, 64) || make_map(&do64.hi, dout, T, H * hd, 64, hi))
+    return rp_fail(RP_ERR_CUDA, "attention_bwd_tc_wide: tensor map encode failed");
+  const int smem = 1024 + BwdCfg<128>::kSmem;
+  static std::once_flag once;
+  static int nsm = 148;
+  std::call_once(once, [smem] {
+    cudaFuncSetAttribute(attn_bwd_tc<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_tc<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  });
+  BwdPlan pl;
+  pl.ntile = static_cast<int>((N + 127) / 128);
+  pl.nitems = static_cast<int>(S * H) * pl.ntile;
+  const unsigned grid = static_cast<unsigned>(pl.nitems < nsm ? pl.nitems : nsm);
+  // dQ (+ D): tiles Q | dO, chunks K | V
+  launch_k(attn_bwd_tc<true, 128>, dim3(grid), dim3(kBwdThreads), smem, stream, qkv128, do128,
+           qkv64, qkv64, reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
+           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
+  // dK, dV: tiles K | V, chunks Q | dO
+  launch_k(attn_bwd_tc<false, 128>, dim3(grid), dim3(kBwdThreads), smem, stream, qkv128, qkv128,
+           qkv64, do64, reinterpret_cast<const __nv_bfloat16*>(out), lse, Dg,
+           reinterpret_cast<__nv_bfloat16*>(dqkv), g, pl, static_cast<__nv_bfloat16*>(nullptr));
+  return rp_check_launch("attention_bwd_tc_wide");
 }

@@ -234,7 +234,9 @@ def test_colsum(K, dtype):
 @pytest.mark.parametrize("B,N,H,hd", [(2, 197, 2, 104), (3, 64, 3, 32), (1, 130, 2, 128),
                                       (2, 50, 4, 96), (1, 300, 1, 104), (64, 49, 4, 32),
                                       (5, 49, 2, 16), (2, 100, 3, 24), (1, 700, 1, 32),
-                                      (512, 49, 2, 32), (1000, 49, 1, 16), (300, 64, 2, 104)])
+                                      (512, 49, 2, 32), (1000, 49, 1, 16), (300, 64, 2, 104),
+                                      (3, 197, 3, 72), (2, 256, 2, 120), (1, 384, 1, 104),
+                                      (4, 65, 2, 104), (1, 208, 16, 104)])
 def test_attention_general_head_dim(K, B, N, H, hd):
     """head_dim != 64 (e.g. the G48 config's 104, Swin's 32 over 49-token windows) runs on
     the mma.sync kernels with the head padded to 32 / 64 / 128 columns in smem."""

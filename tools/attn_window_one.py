@@ -1,6 +1,6 @@
 """Window attention at a Rev-Swin-B shape (default stage 3 at batch 128: 512 windows of 49
 tokens, 16 heads of 32): `python tools/attn_window_one.py [S N H hd] [--time]`.
---variant=1: the general mma.sync kernels. Without --time: two forward + backward calls (for ncu -k). With --time: CUDA-event
+--variant=1: the general mma.sync kernels; --impl=1: mma.sync only. Without --time: two forward + backward calls (for ncu -k). With --time: CUDA-event
 microseconds per forward and per backward, and the HBM floors of both (Q, K, V read +
 O written; Q, K, V, dO read + dQ, dK, dV written)."""
 import json
@@ -14,6 +14,8 @@ from paper_2306_09342_b200 import _capi, kernels as K  # noqa: E402
 for a in sys.argv[1:]:
     if a.startswith("--variant="):  # window kernels: 0 single-tile (default), 1 general
         _capi.lib().rp_set_attention_window_variant(int(a.split("=")[1]))
+    if a.startswith("--impl="):  # rp_set_attention_impl: 0 tcgen05 where it applies, 1 mma.sync
+        _capi.lib().rp_set_attention_impl(int(a.split("=")[1]))
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 S, N, H, hd = (int(x) for x in args) if args else (512, 49, 16, 32)
