@@ -964,6 +964,8 @@ int rp_attention_bwd_tc(const uint16_t* qkv, const uint16_t* out, const uint16_t
                         const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
                         uint16_t* dqkv, cudaStream_t stream, uint16_t* dSt, int d_ready,
                         int fused);
+int rp_attention_fwd_tc_wide(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64_t hd,
+                             uint16_t* out, float* lse, cudaStream_t stream);
 int rp_attention_bwd_tc_wide(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                              const float* lse, float* Dg, int64_t S, int64_t N, int64_t H,
                              int64_t hd, uint16_t* dqkv, cudaStream_t stream);
@@ -1130,6 +1132,10 @@ extern "C" int rp_attention_fwd(const uint16_t* qkv, int64_t B, int64_t N, int64
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (g_attn_impl != 1 && head_dim == 64 && N <= 512) {
     rc = rp_attention_fwd_tc(qkv, B, N, H, out, lse, s);
+    if (rc != RP_ERR_CONFIG) return rc;
+  }
+  if (g_attn_impl != 1 && head_dim > 64 && N > kTile) {  // G48's 104: tcgen05 at N <= 256
+    rc = rp_attention_fwd_tc_wide(qkv, B, N, H, head_dim, out, lse, s);
     if (rc != RP_ERR_CONFIG) return rc;
   }
   if (head_dim <= 32) return attn_fwd_mma<32>(qkv, B, N, H, head_dim, out, lse, s);

@@ -10,6 +10,8 @@
 #include "attn_common.cuh"
 #include "launch.h"
 
+#include <cstring>
+
 namespace rp {
 namespace attn_tc {
 
@@ -611,19 +613,36 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 // elementwise warps (TMEM lane quarter w%4, 32-key column quarter w/4 of a block) and one
 // TMA + MMA warp; S is double-buffered in TMEM so the next block's S is computed while the
 // current one is processed.
-constexpr int kLongKV = 2 * 512 * 128;  // K | V, up to 512 rows each
+// HP = 128 (head dims 72..128, N <= 256): every operand is two 64-column atom planes, the
+// second loaded by a TMA box of hd - 64 columns whose untouched tail stays zero (as in the
+// wide backward), S = Q K^T takes round16(hd) / 16 K steps and O has round16(hd) columns.
+constexpr int kLongKV = 2 * 512 * 128;  // K | V, up to 512 rows each (HP = 64)
+template <int HP>
+struct LongCfg {
+  static constexpr int kAtoms = HP / 64;
+  static constexpr int kMaxRows = HP == 64 ? 512 : 256;        // resident keys
+  static constexpr int kPlaneKV = kMaxRows * 128;               // one atom plane of K or V
+  static constexpr int kKV = 2 * kAtoms * kPlaneKV;             // K | V
+  static constexpr int kQTile = 128 * 128 * kAtoms;             // one Q tile
+  static constexpr int kSmem = kKV + 2 * kQTile;
+};
 
 struct LongPlan {
   int nitems, ntile, ngroup;  // items = S * H * ngroup; ntile query tiles per sequence
   int group;                  // query tiles per item (K, V loaded once per item)
   int nkb;                    // 128-key blocks
+  int hd;                     // head dim (64 on HP = 64)
 };
 
+struct LongMaps {
+  CUtensorMap lo, hi;  // qkv boxes of {64, 128} and (HP = 128) {hd - 64, 128}
+};
+
+template <int HP>
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    attn_fwd_tc_long(const __grid_constant__ CUtensorMap tm_q,
-                     const __grid_constant__ CUtensorMap tm_kv,
-                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse, Geom g,
-                     LongPlan pl) {
+    attn_fwd_tc_long(const __grid_constant__ LongMaps tm, __nv_bfloat16* __restrict__ out,
+                     float* __restrict__ lse, Geom g, LongPlan pl) {
+  using Cfg = LongCfg<HP>;
   pdl_trigger();
 
   __shared__ float red_max[4][128];
@@ -633,9 +652,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sK = smem;                       // Nk rows
-  uint8_t* sV = smem + 512 * 128;           // Nk rows
-  uint8_t* sQ = smem + kLongKV;             // [2][128 rows]
+  uint8_t* sK = smem;                                 // [atom][kMaxRows rows]
+  uint8_t* sV = smem + Cfg::kAtoms * Cfg::kPlaneKV;   // [atom][kMaxRows rows]
+  uint8_t* sQ = smem + Cfg::kKV;                      // [2][atom][128 rows]
   uint64_t* kv_full = bars;                 // K, V of the item landed
   uint64_t* kv_free = bars + 1;             // the item's last MMA retired
   uint64_t* q_full = bars + 2;              // [2]
@@ -647,10 +666,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int Nk = g.Nk, nkb = pl.nkb;
+  const int hd = HP == 64 ? 64 : pl.hd;
+  if constexpr (HP > 64) {
+    // the second atom plane's columns past hd are never written by the TMA: zero them once
+    for (int i = static_cast<int>(threadIdx.x) * 16; i < Cfg::kSmem; i += kFwdThreads * 16)
+      *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   if (warp == 16) {
     if (lane == 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_kv);
+      tma_prefetch_desc(&tm.lo);
       mbar_init(kv_full, 1);
       mbar_init(kv_free, 1);
       for (int i = 0; i < 2; ++i) {
@@ -670,7 +695,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   pdl_wait();
-  const int d = g.H * 64;
+  const int d = g.H * hd;
   const int K = pl.nitems > static_cast<int>(blockIdx.x)
                     ? (pl.nitems - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
                           static_cast<int>(gridDim.x)
@@ -687,22 +712,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   if (warp == 16) {
     if (lane == 0) {
-      const uint32_t idesc_o = make_idesc_bf16(128, 64, false, true);
+      const int nacc = (hd + 15) / 16 * 16, nks = nacc / 16;
+      const uint32_t idesc_o = make_idesc_bf16(128, static_cast<uint32_t>(nacc), false, true);
       // flat unit sequence: per item, per tile, pass 1 blocks then pass 2 blocks
       int u = 0, tt = 0;  // unit and global tile counters
+      // 128 rows of one operand at head column col: atom planes `plane` bytes apart
+      auto load_rows = [&](uint8_t* dst, uint64_t* bar, int col, int row, int plane) {
+        tma_load_2d(dst, &tm.lo, bar, col, row);
+        if constexpr (HP > 64) tma_load_2d(dst + plane, &tm.hi, bar, col + 64, row);
+      };
       auto load_q = [&](int k, int t, int slot) {
         int b, h, t0, nt;
         coords(k, b, h, t0, nt);
-        mbar_arrive_expect_tx(&q_full[slot], 128 * 128);
-        tma_load_2d(sQ + slot * 16384, &tm_q, &q_full[slot], h * 64, b * g.N + (t0 + t) * 128);
+        mbar_arrive_expect_tx(&q_full[slot], static_cast<uint32_t>(128 * hd * 2));
+        load_rows(sQ + slot * Cfg::kQTile, &q_full[slot], h * hd, b * g.N + (t0 + t) * 128, 16384);
       };
       auto load_kv = [&](int k) {
         int b, h, t0, nt;
         coords(k, b, h, t0, nt);
-        mbar_arrive_expect_tx(kv_full, 2 * nkb * 128 * 128);
+        mbar_arrive_expect_tx(kv_full, static_cast<uint32_t>(2 * nkb * 128 * hd * 2));
         for (int j = 0; j < nkb; ++j) {  // 128-row boxes (a TMA box is at most 256 rows)
-          tma_load_2d(sK + j * 16384, &tm_kv, kv_full, d + h * 64, b * g.N + 128 * j);
-          tma_load_2d(sV + j * 16384, &tm_kv, kv_full, 2 * d + h * 64, b * g.N + 128 * j);
+          load_rows(sK + j * 16384, kv_full, d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
+          load_rows(sV + j * 16384, kv_full, 2 * d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
         }
       };
       if (K > 0) {
@@ -728,7 +759,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
           }
           mbar_wait(&q_full[tt & 1], (tt >> 1) & 1);
-          const uint32_t aq = smem_u32(sQ + (tt & 1) * 16384);
+          const uint32_t aq = smem_u32(sQ + (tt & 1) * Cfg::kQTile);
           for (int ps = 0; ps < 2; ++ps) {
             for (int j = 0; j < nkb; ++j, ++u) {
               const int w = min(128, Nk - 128 * j);
@@ -737,10 +768,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const uint32_t sb = tmem + static_cast<uint32_t>((u & 1) * 128);
               const uint32_t bk = smem_u32(sK) + static_cast<uint32_t>(128 * j * 128);
               const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(w), false, false);
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_bf16(sb, make_sdesc_sw128(aq + kk * 32, 16, 1024),
-                          make_sdesc_sw128(bk + kk * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < nks; ++kk)
+                umma_bf16(sb, make_sdesc_sw128(aq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                          make_sdesc_sw128(bk + (kk >> 2) * Cfg::kPlaneKV + (kk & 3) * 32, 16, 1024),
+                          idesc_s, kk > 0 ? 1u : 0u);
               umma_commit(&bar_s[u & 1]);
               if (ps == 1 && j == nkb - 1) umma_commit(&q_free[tt & 1]);
               if (ps == 1) {
@@ -750,8 +781,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 const uint32_t bv = smem_u32(sV) + static_cast<uint32_t>(128 * j * 128);
                 for (int ks = 0; ks < w / 16; ++ks)
                   umma_ts_bf16(ocol, sb + static_cast<uint32_t>((ks >> 1) * 32 + (ks & 1) * 8),
-                               make_sdesc_sw128(bv + ks * 2048, 8192, 1024), idesc_o,
-                               (j > 0 || ks > 0) ? 1u : 0u);
+                               make_sdesc_sw128(bv + ks * 2048, HP == 64 ? 8192 : Cfg::kPlaneKV, 1024),
+                               idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
                 if (j == nkb - 1) umma_commit(bar_o);
               }
             }
@@ -821,11 +852,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         red_sum[cq][rloc] = l;
         named_bar(1 + q, 128);
         const float lt = (red_sum[0][rloc] + red_sum[1][rloc]) + (red_sum[2][rloc] + red_sum[3][rloc]);
-        // ---- epilogue: O / l (16 of the 64 head columns per warp), LSE
+        // ---- epilogue: O / l (HP / 4 of the head columns per warp, those < hd stored), LSE
         mbar_wait(bar_o, tt & 1);
         tc_fence_after();
-        float o[16];
-        if (active) tmem_ld16(ocol + lq + static_cast<uint32_t>(cq * 16), o);
+        constexpr int kQ = HP / 4;
+        float o[kQ];
+        if (active) {
+          if constexpr (kQ == 16)
+            tmem_ld16(ocol + lq + static_cast<uint32_t>(cq * kQ), o);
+          else
+            tmem_ld32(ocol + lq + static_cast<uint32_t>(cq * kQ), o);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_e);
@@ -833,13 +870,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (row < g.N) {
           const float inv = 1.0f / lt;
           uint4* dst = reinterpret_cast<uint4*>(
-              out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * 64 + cq * 16);
-          dst[0] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
-                              pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
-          dst[1] = make_uint4(pack_bf16x2(o[8] * inv, o[9] * inv),
-                              pack_bf16x2(o[10] * inv, o[11] * inv),
-                              pack_bf16x2(o[12] * inv, o[13] * inv),
-                              pack_bf16x2(o[14] * inv, o[15] * inv));
+              out + (static_cast<int64_t>(b) * g.N + row) * g.ld_o + h * hd + cq * kQ);
+#pragma unroll
+          for (int j = 0; j < kQ / 8; ++j)
+            if (cq * kQ + 8 * j < hd)
+              dst[j] = make_uint4(pack_bf16x2(o[8 * j] * inv, o[8 * j + 1] * inv),
+                                  pack_bf16x2(o[8 * j + 2] * inv, o[8 * j + 3] * inv),
+                                  pack_bf16x2(o[8 * j + 4] * inv, o[8 * j + 5] * inv),
+                                  pack_bf16x2(o[8 * j + 6] * inv, o[8 * j + 7] * inv));
           if (cq == 0) lse[(static_cast<int64_t>(b) * g.H + h) * g.N + row] = ms + log2f(lt);
         }
       }
@@ -873,13 +911,15 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   CUtensorMap mq, mkv;
   if (g.Nk > 256 || (g.Nk > 224 && rp_attn_fwd_variant() != 0)) {
     // two-pass kernel with K / V resident per (sequence, head) group
-    if (make_map(&mq, qkv, T, cols, 128))
+    LongMaps lm;
+    std::memset(&lm, 0, sizeof(lm));
+    if (make_map(&lm.lo, qkv, T, cols, 128))
       return rp_fail(RP_ERR_CUDA, "attention_tc: tensor map encode failed");
-    const int smem = 1024 + kLongKV + 2 * 16384;
+    const int smem = 1024 + LongCfg<64>::kSmem;
     static std::once_flag once_l;
     static int nsm_l = 148;
     std::call_once(once_l, [smem] {
-      cudaFuncSetAttribute(attn_fwd_tc_long, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(attn_fwd_tc_long<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm_l, cudaDevAttrMultiProcessorCount, dev);
@@ -894,8 +934,9 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
     pl.ngroup = (pl.ntile + pl.group - 1) / pl.group;
     pl.nitems = static_cast<int>(S * H) * pl.ngroup;
     pl.nkb = static_cast<int>((N + 127) / 128);
+    pl.hd = 64;
     const unsigned grid = static_cast<unsigned>(pl.nitems < nsm_l ? pl.nitems : nsm_l);
-    launch_k(attn_fwd_tc_long, dim3(grid), dim3(kFwdThreads), smem, stream, mq, mq,
+    launch_k(attn_fwd_tc_long<64>, dim3(grid), dim3(kFwdThreads), smem, stream, lm,
              reinterpret_cast<__nv_bfloat16*>(out), lse, g, pl);
     return rp_check_launch("attention_fwd_tc_long");
   }
@@ -953,5 +994,46 @@ int rp_attention_fwd_tc(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, ui
   launch_k(attn_fwd_tc_persistent, dim3(grid), dim3(kFwdThreads), smem, stream, mq, mkv,
            reinterpret_cast<__nv_bfloat16*>(out), lse, g, pl);
   return rp_check_launch("attention_fwd_tc");
+}
+
+// tcgen05 forward for head dims 72..128 (multiples of 8; G48's 104) at N <= 256: the
+// two-pass kernel with K / V resident per item, operands as two 64-column atom planes.
+// RP_ERR_CONFIG without launching outside that range.
+int rp_attention_fwd_tc_wide(const uint16_t* qkv, int64_t S, int64_t N, int64_t H, int64_t hd,
+                             uint16_t* out, float* lse, cudaStream_t stream) {
+  using namespace attn_tc;
+  if (N > 256 || N < 1 || hd <= 64 || hd > 128 || hd % 8) return RP_ERR_CONFIG;
+  Geom g;
+  g.B = static_cast<int>(S);
+  g.N = static_cast<int>(N);
+  g.H = static_cast<int>(H);
+  g.Nk = static_cast<int>((N + 15) / 16 * 16);
+  g.ld_o = H * hd;
+  g.scale_log2 = (1.0f / sqrtf(static_cast<float>(hd))) * 1.4426950408889634f;
+  const int64_t T = S * N, cols = 3 * H * hd;
+  LongMaps lm;
+  if (make_map(&lm.lo, qkv, T, cols, 128) ||
+      make_map(&lm.hi, qkv, T, cols, 128, static_cast<uint32_t>(hd - 64)))
+    return rp_fail(RP_ERR_CUDA, "attention_tc_wide: tensor map encode failed");
+  const int smem = 1024 + LongCfg<128>::kSmem;
+  static std::once_flag once;
+  static int nsm = 148;
+  std::call_once(once, [smem] {
+    cudaFuncSetAttribute(attn_fwd_tc_long<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  });
+  LongPlan pl;
+  pl.ntile = static_cast<int>((N + 127) / 128);
+  pl.group = pl.ntile;
+  pl.ngroup = 1;
+  pl.nitems = static_cast<int>(S * H);
+  pl.nkb = static_cast<int>((N + 127) / 128);
+  pl.hd = static_cast<int>(hd);
+  const unsigned grid = static_cast<unsigned>(pl.nitems < nsm ? pl.nitems : nsm);
+  launch_k(attn_fwd_tc_long<128>, dim3(grid), dim3(kFwdThreads), smem, stream, lm,
+           reinterpret_cast<__nv_bfloat16*>(out), lse, g, pl);
+  return rp_check_launch("attention_fwd_tc_wide");
 }
 
