@@ -760,33 +760,45 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
           mbar_wait(&q_full[tt & 1], (tt >> 1) & 1);
           const uint32_t aq = smem_u32(sQ + (tt & 1) * Cfg::kQTile);
-          for (int ps = 0; ps < 2; ++ps) {
-            for (int j = 0; j < nkb; ++j, ++u) {
+          // the tile's units: nkb pass-1 blocks then nkb pass-2 blocks. S of unit i + 1 is
+          // issued before the P V of unit i, so the elementwise warps' next block overlaps
+          // the P V products (S is double-buffered; the P V of unit i - 1, which reads the
+          // buffer S(i + 1) overwrites, was issued earlier and MMAs retire in order)
+          const int U = 2 * nkb, ubase = u;
+          auto issue_s = [&](int i) {
+            const int gu = ubase + i, j = i % nkb;
+            const int w = min(128, Nk - 128 * j);
+            if (gu >= 2) mbar_wait(&bar_p[gu & 1], ((gu - 2) >> 1) & 1);  // buffer consumed
+            tc_fence_after();
+            const uint32_t sb = tmem + static_cast<uint32_t>((gu & 1) * 128);
+            const uint32_t bk = smem_u32(sK) + static_cast<uint32_t>(128 * j * 128);
+            const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(w), false, false);
+            for (int kk = 0; kk < nks; ++kk)
+              umma_bf16(sb, make_sdesc_sw128(aq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                        make_sdesc_sw128(bk + (kk >> 2) * Cfg::kPlaneKV + (kk & 3) * 32, 16, 1024),
+                        idesc_s, kk > 0 ? 1u : 0u);
+            umma_commit(&bar_s[gu & 1]);
+            if (i == U - 1) umma_commit(&q_free[tt & 1]);
+          };
+          issue_s(0);
+          for (int i = 0; i < U; ++i) {
+            if (i + 1 < U) issue_s(i + 1);
+            if (i >= nkb) {  // pass 2: O += P V_j
+              const int gu = ubase + i, j = i - nkb;
               const int w = min(128, Nk - 128 * j);
-              if (u >= 2) mbar_wait(&bar_p[u & 1], ((u - 2) >> 1) & 1);  // buffer consumed
+              if (j == 0 && tt > 0) mbar_wait(bar_e, (tt - 1) & 1);  // previous O read out
+              mbar_wait(&bar_p[gu & 1], (gu >> 1) & 1);
               tc_fence_after();
-              const uint32_t sb = tmem + static_cast<uint32_t>((u & 1) * 128);
-              const uint32_t bk = smem_u32(sK) + static_cast<uint32_t>(128 * j * 128);
-              const uint32_t idesc_s = make_idesc_bf16(128, static_cast<uint32_t>(w), false, false);
-              for (int kk = 0; kk < nks; ++kk)
-                umma_bf16(sb, make_sdesc_sw128(aq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                          make_sdesc_sw128(bk + (kk >> 2) * Cfg::kPlaneKV + (kk & 3) * 32, 16, 1024),
-                          idesc_s, kk > 0 ? 1u : 0u);
-              umma_commit(&bar_s[u & 1]);
-              if (ps == 1 && j == nkb - 1) umma_commit(&q_free[tt & 1]);
-              if (ps == 1) {
-                if (j == 0 && tt > 0) mbar_wait(bar_e, (tt - 1) & 1);  // previous O read out
-                mbar_wait(&bar_p[u & 1], (u >> 1) & 1);
-                tc_fence_after();
-                const uint32_t bv = smem_u32(sV) + static_cast<uint32_t>(128 * j * 128);
-                for (int ks = 0; ks < w / 16; ++ks)
-                  umma_ts_bf16(ocol, sb + static_cast<uint32_t>((ks >> 1) * 32 + (ks & 1) * 8),
-                               make_sdesc_sw128(bv + ks * 2048, HP == 64 ? 8192 : Cfg::kPlaneKV, 1024),
-                               idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
-                if (j == nkb - 1) umma_commit(bar_o);
-              }
+              const uint32_t sb = tmem + static_cast<uint32_t>((gu & 1) * 128);
+              const uint32_t bv = smem_u32(sV) + static_cast<uint32_t>(128 * j * 128);
+              for (int ks = 0; ks < w / 16; ++ks)
+                umma_ts_bf16(ocol, sb + static_cast<uint32_t>((ks >> 1) * 32 + (ks & 1) * 8),
+                             make_sdesc_sw128(bv + ks * 2048, HP == 64 ? 8192 : Cfg::kPlaneKV, 1024),
+                             idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+              if (j == nkb - 1) umma_commit(bar_o);
             }
           }
+          u += U;
         }
         umma_commit(kv_free);
       }
