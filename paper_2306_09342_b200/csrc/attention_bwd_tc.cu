@@ -81,7 +81,12 @@ __device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* dst, const float
 // MMA1: S = A C_c^T, dP = B D_c^T (N = chunk width, K = hd in 16-column steps); MMA2: DQ
 // dQ += dS C_c; DKDV dV += P^T D_c, dK += dS^T C_c (A operands re-packed to bf16 in TMEM;
 // B operands MN-major over the chunk's atom planes, plane stride 64 rows x 128 B = LBO).
-constexpr int kBwdWarps = 9;
+// Two MMA issuers (one thread each; an MMA costs its issuing thread ~120 cycles, so one issuer
+// serialised the chunk's 12-22 MMAs): warp 8 issues S and the accumulation that reads the S
+// columns (DQ dQ += dS K_c, DKDV dV += P^T dO_c) and the TMA loads; warp 9 issues dP and the
+// one that reads the dP columns (DKDV dK += dS^T Q_c). Each owns its TMEM columns, so the
+// in-order retirement of one thread's MMAs is the only ordering either needs.
+constexpr int kBwdWarps = 10;
 constexpr int kBwdThreads = kBwdWarps * 32;
 template <int HP>
 struct BwdCfg {
@@ -147,13 +152,13 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
       tma_prefetch_desc(&tm_d.lo);
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tile_full[i], 1);
-        mbar_init(&tile_free[i], 1);
+        mbar_init(&tile_free[i], 2);
         mbar_init(&ring_full[i], 1);
-        mbar_init(&ring_free[i], 1);
+        mbar_init(&ring_free[i], 2);
       }
-      mbar_init(bar_s, 1);
+      mbar_init(bar_s, 2);
       mbar_init(bar_p, 8);
-      mbar_init(bar_o, 1);
+      mbar_init(bar_o, 2);
       mbar_init(bar_e, 8);
       fence_barrier_init();
     }
@@ -175,8 +180,9 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
   // DKDV: A=K, B=V, C=Q, D=dO)
   const int ca = DQ ? 0 : d, cb = DQ ? 0 : 2 * d, cc = DQ ? d : 0, cd = DQ ? 2 * d : 0;
 
-  if (warp == 8) {
+  if (warp >= 8) {
     if (lane == 0) {
+      const bool ia = warp == 8;  // issuer A (S, its accumulation, TMA) or B (dP, dK)
       // one operand block of `plane`-byte atom planes: box {64} then, above 64, {hd - 64}
       auto load_op = [&](uint8_t* dst, const OpMaps& m, uint64_t* bar, int col, int row,
                          uint32_t plane) {
@@ -207,13 +213,13 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
       const int nacc = (hd + 15) / 16 * 16, nks = nacc / 16;
       const uint32_t idesc_o = make_idesc_bf16(128, static_cast<uint32_t>(nacc), false, true);
       const int total = K * nch;
-      if (K > 0) {
+      if (ia && K > 0) {
         load_tile(0);
         load_chunk(0);
       }
       int u = 0;
       for (int k = 0; k < K; ++k) {
-        if (k + 1 < K) {  // the next item's tile streams in during this one
+        if (ia && k + 1 < K) {  // the next item's tile streams in during this one
           if (k >= 1) mbar_wait(&tile_free[(k + 1) & 1], ((k - 1) >> 1) & 1);
           load_tile(k + 1);
         }
@@ -228,13 +234,15 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
           for (int kk = 0; kk < nks; ++kk) {
             const uint32_t ka = static_cast<uint32_t>(kk >> 2) * kTilePlane + (kk & 3) * 32;
             const uint32_t kc = static_cast<uint32_t>(kk >> 2) * kChunkPlane + (kk & 3) * 32;
-            umma_bf16(tmem, make_sdesc_sw128(ta + ka, 16, 1024),
-                      make_sdesc_sw128(rc + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-            umma_bf16(tmem + 64, make_sdesc_sw128(tb + ka, 16, 1024),
-                      make_sdesc_sw128(rd + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            if (ia)  // S = A C_c^T
+              umma_bf16(tmem, make_sdesc_sw128(ta + ka, 16, 1024),
+                        make_sdesc_sw128(rc + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            else     // dP = B D_c^T
+              umma_bf16(tmem + 64, make_sdesc_sw128(tb + ka, 16, 1024),
+                        make_sdesc_sw128(rd + kc, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
           }
           umma_commit(bar_s);
-          if (u + 1 < total) {  // next chunk into the other ring slot once its MMAs retired
+          if (ia && u + 1 < total) {  // next chunk into the other ring slot once its MMAs retired
             if (u >= 1) mbar_wait(&ring_free[(u + 1) & 1], ((u - 1) >> 1) & 1);
             load_chunk(u + 1);
           }
@@ -245,13 +253,16 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
             const uint32_t row16 = static_cast<uint32_t>(16 * ks * 128);
             const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
             if constexpr (DQ) {
-              umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
-                           make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dQ += dS K_c
+              if (ia)
+                umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
+                             make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dQ += dS K_c
             } else {
-              umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
-                           make_sdesc_sw128(rd + row16, kChunkPlane, 1024), idesc_o, acc);  // dV += P^T dO_c
-              umma_ts_bf16(tmem + Cfg::kAcc1, tmem + 64 + chunk_acol(ks),
-                           make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dK += dS^T Q_c
+              if (ia)
+                umma_ts_bf16(tmem + 128, tmem + chunk_acol(ks),
+                             make_sdesc_sw128(rd + row16, kChunkPlane, 1024), idesc_o, acc);  // dV += P^T dO_c
+              else
+                umma_ts_bf16(tmem + Cfg::kAcc1, tmem + 64 + chunk_acol(ks),
+                             make_sdesc_sw128(rc + row16, kChunkPlane, 1024), idesc_o, acc);  // dK += dS^T Q_c
             }
           }
           umma_commit(&ring_free[u & 1]);
@@ -423,7 +434,7 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, Cfg::kTmemCols);
+  if (warp == 8) tmem_dealloc(tmem, Cfg::kTmemCols);  // (warp 9 idles at the barrier)
 }
 
 // ------------------------------------------------------------------ D and dQ for the fused path
