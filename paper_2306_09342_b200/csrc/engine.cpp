@@ -66,21 +66,31 @@ constexpr int kGemmBn = 512;
 // CTA-pair tile; they run on single-CTA 128 x 128 tiles instead.
 int gemm_bn(int64_t N) { return (N % 256 != 0 && N < 512) ? 128 : kGemmBn; }
 
+// Split-K count for a weight-gradient GEMM: minimise (waves of work units) x (k-blocks per
+// split) x (time per k-block per tile) + the extra HBM traffic splitting costs (s fp32
+// partial tiles written instead of one, then read back and reduced: 2 s M N 4 bytes).
+// Counting only wave efficiency picked 10 splits for G48's QKV wgrad (1664 x 4992, K =
+// 12608): ~300 MB of partials + a 55 us reduction to save 4 % of a 165 us GEMM.
 int pick_splits(int64_t M, int64_t N, int64_t K, int bn) {
   const bool pair = bn == 512;
   const int tm = pair ? 256 : 128, tn = pair ? 256 : bn;
   const int slots = pair ? kSms / 2 : kSms;
   const int64_t tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
   const int64_t kb = (K + 63) / 64;
+  // ~0.42 us per 64-deep k-block of a 128 x 256 tile per SM (or 256 x 256 per CTA pair) at
+  // ~10 TFLOP/s per SM; ~6 TB/s of HBM for the partials
+  const double t_kb = 0.42e-6 * (pair ? 1.0 : static_cast<double>(tn) / 256.0);
+  const double t_byte = 1.0 / 6.0e12;
   int best = 1;
-  double best_eff = 0.0;
+  double best_t = 0.0;
   for (int s = 1; s <= 64; ++s) {
-    if (kb / s < 8) break;  // keep >= 8 k-blocks per split
+    if (s > 1 && kb / s < 8) break;  // keep >= 8 k-blocks per split
     const int64_t units = tiles * s;
     const double waves = static_cast<double>((units + slots - 1) / slots);
-    const double eff = static_cast<double>(units) / (waves * slots) - 0.004 * s;
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
+    const double t = waves * static_cast<double>((kb + s - 1) / s) * t_kb +
+                     (s > 1 ? 2.0 * s * static_cast<double>(M) * static_cast<double>(N) * 4.0 * t_byte : 0.0);
+    if (s == 1 || t < best_t * (1.0 - 1e-6)) {
+      best_t = t;
       best = s;
     }
   }
