@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int Nk = g.Nk, nch = Nk / 16, ntile = g.ntile;
+  const int ngrp = (nch + 3) / 4;  // 64-query dS^T chunks = staging tiles released per item
   const bool two = Nk > 128;
   if (warp == 16) {
     if (lane == 0) {
@@ -329,14 +330,16 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             tma_store_2d(&tm_scr, s_ds + 49152u, 32, cta * 128);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+          // (only the tiles some 64-query chunk of dS^T will rewrite are released: every
+          // arrival has a waiter)
           asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
           mbar_arrive(&bar_sfree[0]);
           asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
-          mbar_arrive(&bar_sfree[1]);
+          if (ngrp > 1) mbar_arrive(&bar_sfree[1]);
           asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          mbar_arrive(&bar_sfree[2]);
+          if (ngrp > 2) mbar_arrive(&bar_sfree[2]);
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          mbar_arrive(&bar_sfree[3]);
+          if (ngrp > 3) mbar_arrive(&bar_sfree[3]);
           if (kt != ntile - 1) {  // the partial must be in global memory before it is read
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -507,6 +510,10 @@ __global__ void __launch_bounds__(kFbThreads, 1)
       if (warp == 0) FB_TRACE(i, 18);
       if (warp == 0) FB_TRACE(i, 13);
     }
+    // observe the last item's staging releases too (every arrival gets a wait; the stores
+    // have read their tiles before the CTA's shared memory goes away)
+    if (nI > 0)
+      for (int t = 0; t < ngrp; ++t) mbar_wait(&bar_sfree[t], static_cast<uint32_t>((nI - 1) & 1));
   }
   tc_fence_before();
   __syncthreads();

@@ -318,12 +318,16 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
             }
           }
         }
+        if (k > 0) named_bar(1, 256);  // previous item's red[] read (as sL / sD below)
         red[kh][rloc] = dpart;
         named_bar(1, 256);
         const float D = red[0][rloc] + red[1][rloc];
         if (kh == 0 && row < g.N) Dg[hb + row] = D;
         nds = -D * g.scale;
       } else {
+        // (ordered after every warp's reads of the previous item's sL / sD by the bar_p ->
+        // MMA -> bar_o chain already; the barrier states it where racecheck can see it)
+        if (k > 0) named_bar(1, 256);
         for (int i = static_cast<int>(threadIdx.x); i < Nk; i += 256) {
           sL[i] = i < g.N ? -lse[hb + i] : -INFINITY;
           sD[i] = i < g.N ? -Dg[hb + i] * g.scale : 0.f;

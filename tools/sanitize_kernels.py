@@ -1,7 +1,7 @@
 """Small-shape driver of every kernel family for compute-sanitizer (memcheck / racecheck /
 synccheck): GEMM epilogue kinds (1-CTA and CTA-pair), LayerNorm forward / backward, column
 sums, attention forward / backward on all paths (tcgen05 fused and two-pass, mma.sync at
-head_dim 32 / 64 / 104 incl. the short-window kernel).
+head_dim 32 / 64 / 104 incl. the window kernels and the head_dim-104 tcgen05 kernels).
 
     compute-sanitizer --tool racecheck python tools/sanitize_kernels.py
 """
@@ -48,11 +48,20 @@ for cols in (64, 192, 768):
     K.layer_norm_bwd(x, mean, rstd, g, y, dres=torch.randn_like(x), dx=torch.empty_like(x),
                      dx_bf16=torch.empty_like(y))
     K.colsum(y)
+# many-part column sums (one cluster launch, DSMEM finalize)
+K.colsum_parts(torch.randn(1000, 96, device=dev))
 for impl in (0, 1, 2):
     _capi.lib().rp_set_attention_impl(impl)
-    for (B, Nn, H, hd) in [(2, 197, 2, 64), (1, 300, 1, 64), (700, 49, 1, 32), (2, 70, 2, 104)]:
+    # windows: TMA hd 32 / 64 (compile-time 49 and runtime N), cp.async hd 24; wide tcgen05
+    # hd 104 (fwd N <= 256, bwd); split P V forward at N = 197
+    for (B, Nn, H, hd) in [(2, 197, 2, 64), (1, 300, 1, 64), (700, 49, 1, 32), (2, 70, 2, 104),
+                           (300, 49, 2, 64), (200, 33, 1, 32), (100, 49, 2, 24), (2, 197, 2, 104)]:
         qkv = torch.randn(B * Nn, 3 * H * hd, device=dev).to(bf)
-        out, lse = K.attention_fwd(qkv, B, Nn, H, head_dim=hd)
+        try:
+            out, lse = K.attention_fwd(qkv, B, Nn, H, head_dim=hd)
+        except _capi.ShapeError as e:  # synccheck's own shared memory can push the largest
+            print("skipped", (impl, B, Nn, H, hd), e)  # mma.sync tiles past the limit
+            continue
         K.attention_bwd(qkv, out, lse, torch.randn(B * Nn, H * hd, device=dev).to(bf), B, Nn, H,
                         head_dim=hd)
 _capi.lib().rp_set_attention_impl(0)
