@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   __shared__ float red_max[4][128];
   __shared__ float red_sum[4][128];
-  __shared__ __align__(8) uint64_t bars[14];
+  __shared__ __align__(8) uint64_t bars[16];
   __shared__ uint32_t tmem_slot;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* sK = smem;                                 // [atom][kMaxRows rows]
   uint8_t* sV = smem + Cfg::kAtoms * Cfg::kPlaneKV;   // [atom][kMaxRows rows]
   uint8_t* sQ = smem + Cfg::kKV;                      // [2][atom][128 rows]
-  uint64_t* kv_full = bars;                 // K, V of the item landed
+  uint64_t* kv_full = bars + 12;            // [4] K, V rows of 128-key block j of the item landed
   uint64_t* kv_free = bars + 1;             // the item's last MMA retired
   uint64_t* q_full = bars + 2;              // [2]
   uint64_t* q_free = bars + 4;              // [2] the tile's last S MMA retired
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 16) {
     if (lane == 0) {
       tma_prefetch_desc(&tm.lo);
-      mbar_init(kv_full, 1);
+      for (int j = 0; j < 4; ++j) mbar_init(&kv_full[j], 1);
       mbar_init(kv_free, 1);
       for (int i = 0; i < 2; ++i) {
         mbar_init(&q_full[i], 1);
@@ -730,10 +730,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto load_kv = [&](int k) {
         int b, h, t0, nt;
         coords(k, b, h, t0, nt);
-        mbar_arrive_expect_tx(kv_full, static_cast<uint32_t>(2 * nkb * 128 * hd * 2));
+        // per 128-key block, so the item's first S waits for its first block only (the rest
+        // of K and V lands under it)
         for (int j = 0; j < nkb; ++j) {  // 128-row boxes (a TMA box is at most 256 rows)
-          load_rows(sK + j * 16384, kv_full, d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
-          load_rows(sV + j * 16384, kv_full, 2 * d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
+          mbar_arrive_expect_tx(&kv_full[j], static_cast<uint32_t>(2 * 128 * hd * 2));
+          load_rows(sK + j * 16384, &kv_full[j], d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
+          load_rows(sV + j * 16384, &kv_full[j], 2 * d + h * hd, b * g.N + 128 * j, Cfg::kPlaneKV);
         }
       };
       if (K > 0) {
@@ -747,7 +749,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_wait(kv_free, (k - 1) & 1);  // every MMA of item k-1 retired
           load_kv(k);
         }
-        mbar_wait(kv_full, k & 1);
         for (int t = 0; t < nt; ++t, ++tt) {
           // next tile's Q (this item's next tile or the next item's first one)
           {
@@ -768,6 +769,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           auto issue_s = [&](int i) {
             const int gu = ubase + i, j = i % nkb;
             const int w = min(128, Nk - 128 * j);
+            if (t == 0 && i < nkb) mbar_wait(&kv_full[j], k & 1);  // the item's K, V block j
             if (gu >= 2) mbar_wait(&bar_p[gu & 1], ((gu - 2) >> 1) & 1);  // buffer consumed
             tc_fence_after();
             const uint32_t sb = tmem + static_cast<uint32_t>((gu & 1) * 128);
