@@ -21,7 +21,23 @@
 namespace rp {
 
 constexpr int kLnWarps = 8;        // rows per CTA in the forward
-constexpr int kLnBwdRows = 64;     // rows per dgamma/dbeta partial
+// Rows per dgamma / dbeta partial: 64, except for wide rows, where the single-pass
+// backward's per-CTA shared memory (8 warps x 3 x cols floats) leaves only one or two CTAs
+// per SM: there the partials make exactly one wave on 148 SMs (a fixed 64 left G48, 12.6k
+// rows x 1664 columns at 160 KB per CTA, with 197 partials = 1.33 waves: 132 -> 100 us;
+// RevViT-L 181 -> 171 us). With three or more CTAs per SM the short CTAs of the fixed size
+// balance better (RevViT-B: 133 us fixed vs 149 us one-wave). Multiples of the 8 row warps;
+// set by (rows, cols) alone, so results do not depend on the device.
+static int64_t ln_bwd_rows_per_part(int64_t rows, int64_t cols) {
+  const int64_t smem = static_cast<int64_t>(kLnWarps) * 3 * cols * 4;
+  int64_t per_sm = (227 * 1024) / (smem > 0 ? smem : 1);
+  if (per_sm > 2) return 64;
+  per_sm = per_sm < 1 ? 1 : per_sm;
+  const int64_t slots = 148 * per_sm;
+  int64_t rpp = (rows + slots - 1) / slots;
+  rpp = (rpp + kLnWarps - 1) / kLnWarps * kLnWarps;
+  return rpp < kLnWarps ? kLnWarps : rpp;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -158,12 +174,14 @@ __global__ void __launch_bounds__(kLnWarps * 32)
 // rows (read-modify-write, the warp's rows in order), and the CTA combines its 8 warps in
 // warp order -> part[blk][NACC][cols]. Fixed association order, no atomics, one read of x,
 // dy and dres.
-template <int V, int NACC>
+// RPP: rows per partial when fixed at compile time (64: the row loop unrolls, which narrow
+// rows need for loads in flight), 0 = the runtime `rpp`
+template <int V, int NACC, int RPP = 64>
 __global__ void __launch_bounds__(kLnWarps * 32)
     ln_bwd_1pass_kernel(const float* __restrict__ x, const float* __restrict__ mean_in,
                         const float* __restrict__ rstd_in, const float* __restrict__ gamma,
                         const __nv_bfloat16* __restrict__ dy, const float* dres, int64_t rows,
-                        int cols, float* dx, __nv_bfloat16* __restrict__ dx_bf16,
+                        int cols, int rpp, float* dx, __nv_bfloat16* __restrict__ dx_bf16,
                         float* __restrict__ part) {
   pdl_trigger();
   pdl_wait();
@@ -175,8 +193,9 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   __syncwarp();  // when cols/4 is not a multiple of 32, another lane zeroed this lane's slots
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
   const float inv_n = 1.0f / static_cast<float>(cols);
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kLnBwdRows;
-  for (int rr = warp; rr < kLnBwdRows; rr += kLnWarps) {
+  if (RPP) rpp = RPP;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpp;
+  for (int rr = warp; rr < rpp; rr += kLnWarps) {
     const int64_t row = r0 + rr;
     if (row >= rows) break;
     const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
@@ -461,25 +480,25 @@ static void launch_ln_bwd_1pass(const float* x, const float* mean, const float* 
                                 const float* gamma, const __nv_bfloat16* dy, const float* dres,
                                 int64_t rows, int cols, float* dx, __nv_bfloat16* dxb,
                                 float* part, int nacc, cudaStream_t s) {
-  const int64_t blocks = (rows + kLnBwdRows - 1) / kLnBwdRows;
+  const int64_t rpp = ln_bwd_rows_per_part(rows, cols);
+  const int64_t blocks = (rows + rpp - 1) / rpp;
   const int smem = kLnWarps * nacc * cols * static_cast<int>(sizeof(float));
-  if (nacc == 3) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kLnWarps * 3 * 2048 * 4);
-    });
-    launch_k(ln_bwd_1pass_kernel<V, 3>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32),
-             smem, s, x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
-  } else {
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kLnWarps * 2 * 2048 * 4);
-    });
-    launch_k(ln_bwd_1pass_kernel<V, 2>, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32),
-             smem, s, x, mean, rstd, gamma, dy, dres, rows, cols, dx, dxb, part);
-  }
+  static std::once_flag once;  // (the four instantiations share one function-pointer type)
+  std::call_once(once, [] {
+    constexpr int a3 = kLnWarps * 3 * 2048 * 4, a2 = kLnWarps * 2 * 2048 * 4;
+    cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, a3);
+    cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, a3);
+    cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, a2);
+    cudaFuncSetAttribute(ln_bwd_1pass_kernel<V, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, a2);
+  });
+  auto go = [&](auto kernel, int) {
+    launch_k(kernel, dim3(static_cast<unsigned>(blocks)), dim3(kLnWarps * 32), smem, s, x, mean,
+             rstd, gamma, dy, dres, rows, cols, static_cast<int>(rpp), dx, dxb, part);
+  };
+  if (nacc == 3)
+    rpp == 64 ? go(ln_bwd_1pass_kernel<V, 3, 64>, 3) : go(ln_bwd_1pass_kernel<V, 3, 0>, 3);
+  else
+    rpp == 64 ? go(ln_bwd_1pass_kernel<V, 2, 64>, 2) : go(ln_bwd_1pass_kernel<V, 2, 0>, 2);
 }
 
 template <int V>
@@ -495,7 +514,10 @@ static void launch_ln_bwd(const float* x, const float* mean, const float* rstd,
 
 using namespace rp;
 
-int64_t rp_ln_bwd_num_parts(int64_t rows) { return (rows + kLnBwdRows - 1) / kLnBwdRows; }
+int64_t rp_ln_bwd_num_parts(int64_t rows, int64_t cols) {
+  const int64_t rpp = ln_bwd_rows_per_part(rows, cols);
+  return (rows + rpp - 1) / rpp;
+}
 
 #define RP_LN_DISPATCH(FN, ...)                      \
   do {                                               \
@@ -542,7 +564,7 @@ extern "C" int rp_layer_norm_bwd_ex(const float* x, const float* mean, const flo
   if (rows <= 0 || cols <= 0 || cols % 4) return rp_fail(RP_ERR_SHAPE, "layer_norm_vjp: cols % 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* dyb = reinterpret_cast<const __nv_bfloat16*>(dy);
-  const int64_t nparts = rp_ln_bwd_num_parts(rows);
+  const int64_t nparts = rp_ln_bwd_num_parts(rows, cols);
   const unsigned gb = static_cast<unsigned>((cols + 31) / 32);
   if ((dgamma || dbeta || dx_colsum) && (g_ln_bwd_impl == 1 || dx_colsum) && cols <= 2048) {
     const int nacc = dx_colsum ? 3 : 2;
@@ -565,7 +587,7 @@ extern "C" int rp_layer_norm_bwd_ex(const float* x, const float* mean, const flo
   if (dgamma || dbeta) {  // column partials first (reads x, dy before dx may alias dres)
     dim3 grid(static_cast<unsigned>(nparts), static_cast<unsigned>((cols / 4 + 255) / 256));
     launch_k(ln_bwd_dgb_partial_kernel, grid, dim3(256), 0, s, x, mean, rstd, dyb, rows,
-             static_cast<int>(cols), kLnBwdRows, workspace);
+             static_cast<int>(cols), static_cast<int>(ln_bwd_rows_per_part(rows, cols)), workspace);
     if (dgamma && dbeta == dgamma + cols) {  // adjacent in the flat grad buffer: one launch
       colsum_final(s, workspace, nparts, static_cast<int>(2 * cols), 2 * cols, dgamma, accumulate);
     } else {
@@ -591,7 +613,7 @@ extern "C" int rp_layer_norm_bwd(const float* x, const float* mean, const float*
 }
 
 extern "C" int64_t rp_layer_norm_bwd_workspace_floats(int64_t rows, int64_t cols) {
-  return rp_ln_bwd_num_parts(rows) * 3 * cols;
+  return rp_ln_bwd_num_parts(rows, cols) * 3 * cols;
 }
 
 extern "C" int rp_colsum_parts(float* part, int64_t nparts, int64_t cols, float* out,
