@@ -276,6 +276,40 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
     const uint32_t lq = (static_cast<uint32_t>(q) * 32u) << 16;
     const int rloc = q * 32 + static_cast<int>(lane);
     const uint32_t ts = tmem + lq + static_cast<uint32_t>(32 * kh);
+    // per-item global inputs of the NEXT item, loaded into registers under the current
+    // item's last chunk and epilogue (their latency was exposed at every item start):
+    // DQ: this lane's query row of O (its head-column part) and its LSE; DKDV: this thread's
+    // slots of the item's -lse / -D scale rows (published to sL / sD at the item start)
+    constexpr int kOq = (HP / 64) * 4;
+    uint4 o_nx[kOq];
+    float lr_nx = 0.f, sl_nx[4], sd_nx[4];
+    auto prefetch = [&](int kn) {
+      int tile_n, h_n, b_n;
+      item_coords(item_of(kn), pl.ntile, g.H, tile_n, h_n, b_n);
+      const int64_t hb_n = (static_cast<int64_t>(b_n) * g.H + h_n) * g.N;
+      if constexpr (DQ) {
+        const int row_n = tile_n * 128 + rloc;
+        const int64_t grow_n = static_cast<int64_t>(b_n) * g.N + row_n;
+        lr_nx = row_n < g.N ? __ldg(lse + hb_n + row_n) : 0.f;
+#pragma unroll
+        for (int a = 0; a < HP / 64; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int col = 64 * a + 32 * kh + 8 * c;
+            o_nx[4 * a + c] = row_n < g.N && col < hd
+                                  ? __ldg(reinterpret_cast<const uint4*>(O + grow_n * g.ld_o + h_n * hd + col))
+                                  : make_uint4(0, 0, 0, 0);
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = static_cast<int>(threadIdx.x) + 256 * j;
+          sl_nx[j] = i < g.N ? -__ldg(lse + hb_n + i) : -INFINITY;
+          sd_nx[j] = i < g.N ? -__ldg(Dg + hb_n + i) * g.scale : 0.f;
+        }
+      }
+    };
+    if (K > 0) prefetch(0);
     int u = 0;
     for (int k = 0; k < K; ++k) {
       int tile, h, b;
@@ -293,7 +327,7 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
       if constexpr (DQ) {
         // ---- D = rowsum(dO * O) for this lane's query (dO from the smem tile, O global):
         // warp half kh covers head columns [32 kh, 32 kh + 32) of each 64-column atom plane
-        lr = row < g.N ? lse[hb + row] : 0.f;
+        lr = lr_nx;
         mbar_wait(&tile_full[k & 1], (k >> 1) & 1);
         float dpart = 0.f;
         if (row < g.N) {
@@ -305,7 +339,7 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
             for (int c = 0; c < 4; ++c) {
               const int col = 64 * a + 32 * kh + 8 * c;  // head column of this 16-byte chunk
               if (col >= hd) break;
-              const uint4 ov = __ldg(reinterpret_cast<const uint4*>(O + grow * g.ld_o + h * hd + col));
+              const uint4 ov = o_nx[4 * a + c];
               const int ch = kh * 4 + c;
               const uint4 dv = *reinterpret_cast<const uint4*>(drow + ((ch ^ (rloc & 7)) << 4));
               const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
@@ -328,9 +362,13 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
         // (ordered after every warp's reads of the previous item's sL / sD by the bar_p ->
         // MMA -> bar_o chain already; the barrier states it where racecheck can see it)
         if (k > 0) named_bar(1, 256);
-        for (int i = static_cast<int>(threadIdx.x); i < Nk; i += 256) {
-          sL[i] = i < g.N ? -lse[hb + i] : -INFINITY;
-          sD[i] = i < g.N ? -Dg[hb + i] * g.scale : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = static_cast<int>(threadIdx.x) + 256 * j;
+          if (i < Nk) {
+            sL[i] = sl_nx[j];
+            sD[i] = sd_nx[j];
+          }
         }
         named_bar(1, 256);
       }
@@ -395,6 +433,7 @@ __global__ void __launch_bounds__(kBwdThreads, HP == 64 ? 2 : 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p);
       }
+      if (k + 1 < K) prefetch(k + 1);
       // ---- epilogue: warp half kh stores head columns [kh HP / 2, (kh + 1) HP / 2) < hd
       mbar_wait(bar_o, k & 1);
       tc_fence_after();
