@@ -750,7 +750,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const UnitRange ur = unit_range(sh, u, tiles);
         const int tile = ur.tile, kb0 = ur.kb0, kb1 = ur.kb1;
         const int m0 = (tile / sh.n_tiles) * 256 + 128 * static_cast<int>(rank);
-        const int n0 = (tile % sh.n_tiles) * BN + 128 * static_cast<int>(rank);
+        // a last tile column of <= 128 valid columns runs as an N = 128 product: each CTA of
+        // the pair then supplies 64 columns of B (its first atom / 64 rows)
+        const int nt = tile % sh.n_tiles;
+        const bool narrow = nt == sh.n_tiles - 1 && sh.N - nt * BN <= 128;
+        const int n0 = nt * BN + (narrow ? 64 : 128) * static_cast<int>(rank);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
@@ -780,7 +784,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader && sh.issue == 1) {
       // ---------------- MMA issuer (leader CTA), warp-converged, lane 0's predicate issues
-      constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(256, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_narrow = make_idesc_bf16(256, 128, A_MN, B_MN);
       const uint32_t is0 = lane == 0 ? 1u : 0u;
       const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
                                    : make_sdesc_sw128(smem_u32(sA), 16, 1024);
@@ -794,6 +799,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int u = cluster_id; u < units; u += nclusters, ++ti) {
         const UnitRange ur = unit_range(sh, u, tiles);
         const int kb0 = ur.kb0, kb1 = ur.kb1;
+        const int nt = ur.tile % sh.n_tiles;
+        const uint32_t idesc =
+            nt == sh.n_tiles - 1 && sh.N - nt * BN <= 128 ? idesc_narrow : idesc_full;
         if (lane == 0) GEMM_TRACE(ti, 0, clock64());
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -833,7 +841,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
     } else if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA only)
-      constexpr uint32_t idesc = make_idesc_bf16(256, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(256, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_narrow = make_idesc_bf16(256, 128, A_MN, B_MN);
       const uint64_t adesc0 = A_MN ? make_sdesc_sw128(smem_u32(sA), 8192, 1024)
                                    : make_sdesc_sw128(smem_u32(sA), 16, 1024);
       const uint64_t bdesc0 = B_MN ? make_sdesc_sw128(smem_u32(sB), 8192, 1024)
@@ -845,6 +854,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int u = cluster_id; u < units; u += nclusters) {
         const UnitRange ur = unit_range(sh, u, tiles);
         const int kb0 = ur.kb0, kb1 = ur.kb1;
+        const int nt = ur.tile % sh.n_tiles;
+        const uint32_t idesc =
+            nt == sh.n_tiles - 1 && sh.N - nt * BN <= 128 ? idesc_narrow : idesc_full;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);

@@ -31,7 +31,9 @@ def gelu_slope_ref(u):
     return 0.5 * (1 + t) + 0.5 * u * (1 - t * t) * c * (1 + 3 * a * u * u)
 
 
-SHAPES = [(296, 512, 200), (128, 256, 64), (1000, 768, 768), (264, 2304, 136)]
+# (M, N, K); N = 1664 / 384 end in a 128-column tile (the CTA pair's narrow N = 128 product)
+SHAPES = [(296, 512, 200), (128, 256, 64), (1000, 768, 768), (264, 2304, 136), (304, 1664, 192),
+          (200, 384, 128)]
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
@@ -72,9 +74,10 @@ def test_gemm_persistent_grid_independent(K):
 
 @pytest.mark.parametrize("bn", [256, 512])
 @pytest.mark.parametrize("splits", [1, 3, 8])
-def test_gemm_wgrad_splitk(K, splits, bn):
+@pytest.mark.parametrize("N", [768, 1664])
+def test_gemm_wgrad_splitk(K, splits, bn, N):
     from paper_2306_09342_b200._capi import RP_EPI_F32
-    T, M, N = 5000, 384, 768
+    T, M = 5000, 384
     X = torch.randn(T, M, device="cuda").bfloat16()
     dY = torch.randn(T, N, device="cuda").bfloat16()
     o = torch.empty(M, N, device="cuda")
