@@ -103,6 +103,30 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
   }
 }
 
+// The same update on 4 consecutive parameters per thread and iteration (16-byte p / g
+// accesses, one 8-byte bf16 store): the scalar loop's 4- and 2-byte accesses reached 78 % of
+// HBM bandwidth at G48's 33 M parameters per block. p, g 16-byte and pb 8-byte aligned;
+// n4 = n / 4 (the tail, n % 4, runs in the scalar kernel).
+__global__ void sgd4_kernel(float4* __restrict__ p, const float4* __restrict__ g,
+                            uint2* __restrict__ pb, int64_t n4, const float* __restrict__ lr,
+                            float scale) {
+  pdl_trigger();
+  pdl_wait();
+  const float step = __fmul_rn(lr[0], scale);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 pv = p[i], gv = g[i];
+    float4 v;
+    v.x = __fsub_rn(pv.x, __fmul_rn(step, gv.x));
+    v.y = __fsub_rn(pv.y, __fmul_rn(step, gv.y));
+    v.z = __fsub_rn(pv.z, __fmul_rn(step, gv.z));
+    v.w = __fsub_rn(pv.w, __fmul_rn(step, gv.w));
+    p[i] = v;
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    pb[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+  }
+}
+
 // AdamW (decoupled weight decay), bias-corrected with the device step counter t.
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
                              __nv_bfloat16* __restrict__ pb, float* __restrict__ m,
@@ -414,8 +438,15 @@ int rpk_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t s) {
 }
 int rpk_sgd(float* p, const float* g, uint16_t* pb, int64_t n, const float* lr, float scale,
             cudaStream_t s) {
-  launch_k(sgd_kernel, dim3(grid_for(n)), dim3(256), 0, s, p, g, reinterpret_cast<__nv_bfloat16*>(pb), n, lr,
-                                         scale);
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(pb) & 7) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  if (n4 > 0)
+    launch_k(sgd4_kernel, dim3(grid_for(n4)), dim3(256), 0, s, reinterpret_cast<float4*>(p),
+             reinterpret_cast<const float4*>(g), reinterpret_cast<uint2*>(pb), n4, lr, scale);
+  if (n - 4 * n4 > 0)
+    launch_k(sgd_kernel, dim3(grid_for(n - 4 * n4)), dim3(256), 0, s, p + 4 * n4, g + 4 * n4,
+             reinterpret_cast<__nv_bfloat16*>(pb) + 4 * n4, n - 4 * n4, lr, scale);
   return rp_check_launch("sgd");
 }
 int rpk_adamw(float* p, const float* g, uint16_t* pb, float* m, float* v, int64_t n,
