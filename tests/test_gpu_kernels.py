@@ -89,9 +89,10 @@ def test_gemm_wgrad_splitk(K, splits, bn, N):
 
 
 @pytest.mark.parametrize("bn", [256, 512])
-def test_gemm_bias_gelu(K, bn):
+@pytest.mark.parametrize("N", [1024, 1664])
+def test_gemm_bias_gelu(K, bn, N):
     from paper_2306_09342_b200._capi import RP_EPI_BIAS_GELU
-    M, N, Kd = 515, 1024, 192
+    M, Kd = 515, 192
     A = torch.randn(M, Kd, device="cuda").bfloat16()
     W = (0.1 * torch.randn(Kd, N, device="cuda")).bfloat16()
     bias = torch.randn(N, device="cuda")
@@ -105,7 +106,7 @@ def test_gemm_bias_gelu(K, bn):
 
 @pytest.mark.parametrize("bn", [256, 512])
 @pytest.mark.parametrize("sign", [1.0, -1.0])
-@pytest.mark.parametrize("Kd,N", [(3072, 768), (768, 768), (512, 320)])
+@pytest.mark.parametrize("Kd,N", [(3072, 768), (768, 768), (512, 320), (1664, 1664)])
 def test_gemm_residual(K, sign, bn, Kd, N):
     """Residual epilogue; CTA-pair tiles with K <= 1024 store through TMA (ragged N too)."""
     from paper_2306_09342_b200._capi import RP_EPI_RESID
@@ -127,10 +128,12 @@ def test_gemm_residual(K, sign, bn, Kd, N):
 
 
 @pytest.mark.parametrize("bn", [256, 512])
-def test_gemm_gelu_slope_then_mul(K, bn):
-    """Recompute epilogue keeps gelu'(u); the MLP dgrad multiplies by it."""
+@pytest.mark.parametrize("N", [1024, 1664])
+def test_gemm_gelu_slope_then_mul(K, bn, N):
+    """Recompute epilogue keeps gelu'(u); the MLP dgrad multiplies by it (N = 1664: the CTA
+    pair's last tile column is an N = 128 product; its column sums must stop at N)."""
     from paper_2306_09342_b200._capi import RP_EPI_BIAS_GELU_SLOPE, RP_EPI_MUL
-    M, N, Kd = 600, 1024, 256
+    M, Kd = 600, 256
     A = torch.randn(M, Kd, device="cuda").bfloat16()
     W = (0.1 * torch.randn(Kd, N, device="cuda")).bfloat16()
     bias = torch.randn(N, device="cuda")
@@ -407,11 +410,13 @@ def test_attention_fwd_bwd(K, B, N, H, impl):
 
 
 @pytest.mark.parametrize("bn", [256, 128, 512])
-def test_gemm_rowdot(K, bn):
+@pytest.mark.parametrize("H", [4, 26])
+def test_gemm_rowdot(K, bn, H):
     """RP_EPI_ROWDOT: bf16 output plus, per (row, 64-column head), the dot of the bf16 output
-    with aux -- the attention backward's D = rowsum(dO * O) laid out [(seq, head), token]."""
+    with aux -- the attention backward's D = rowsum(dO * O) laid out [(seq, head), token]
+    (H = 26: N = 1664 ends in a 128-column tile)."""
     from paper_2306_09342_b200._capi import RP_EPI_ROWDOT
-    S_, Ntok, H, Kd = 5, 197, 4, 768
+    S_, Ntok, Kd = 5, 197, 768
     M, N = S_ * Ntok, H * 64
     A = torch.randn(M, Kd, device="cuda").bfloat16()
     W = (0.05 * torch.randn(N, Kd, device="cuda")).bfloat16()
