@@ -31,8 +31,8 @@ constexpr int kLnWarps = 8;        // rows per CTA in the forward
 static int64_t ln_bwd_rows_per_part(int64_t rows, int64_t cols) {
   const int64_t smem = static_cast<int64_t>(kLnWarps) * 3 * cols * 4;
   int64_t per_sm = (227 * 1024) / (smem > 0 ? smem : 1);
-  if (per_sm > 2) return 64;
-  per_sm = per_sm < 1 ? 1 : per_sm;
+  if (per_sm > 2 && per_sm < 8) return 64;
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
   const int64_t slots = 148 * per_sm;
   int64_t rpp = (rows + slots - 1) / slots;
   rpp = (rpp + kLnWarps - 1) / kLnWarps * kLnWarps;

@@ -28,7 +28,8 @@ def t(fn, iters=30):
 
 
 res = {}
-for rows, cols in ((50432, 768), (12608, 1664), (50432, 1024), (401408, 128), (25088, 512)):
+for rows, cols in ((50432, 768), (12608, 1664), (50432, 1024), (401408, 128), (100352, 256),
+                   (25088, 512)):
     x = torch.randn(rows, cols, device="cuda")
     g = torch.rand(cols, device="cuda") + 0.5
     y = torch.empty(rows, cols, device="cuda", dtype=torch.bfloat16)
