@@ -21,13 +21,14 @@
 namespace rp {
 
 constexpr int kLnWarps = 8;        // rows per CTA in the forward
-// Rows per dgamma / dbeta partial: 64, except for wide rows, where the single-pass
-// backward's per-CTA shared memory (8 warps x 3 x cols floats) leaves only one or two CTAs
-// per SM: there the partials make exactly one wave on 148 SMs (a fixed 64 left G48, 12.6k
-// rows x 1664 columns at 160 KB per CTA, with 197 partials = 1.33 waves: 132 -> 100 us;
-// RevViT-L 181 -> 171 us). With three or more CTAs per SM the short CTAs of the fixed size
-// balance better (RevViT-B: 133 us fixed vs 149 us one-wave). Multiples of the 8 row warps;
-// set by (rows, cols) alone, so results do not depend on the device.
+// Rows per dgamma / dbeta partial. Wide rows (the single-pass backward's per-CTA shared
+// memory, 8 warps x 3 x cols floats, leaves one or two CTAs per SM) and narrow rows (eight
+// CTAs per SM): the partials make exactly one wave on 148 SMs (a fixed 64 left G48, 12.6k rows
+// x 1664 columns at 160 KB per CTA, with 197 partials = 1.33 waves: 132 -> 100 us; RevViT-L
+// 181 -> 171 us; Rev-Swin-B stage 1, 401k x 128: 182 -> 172 us). In between (three to seven
+// CTAs per SM) the short CTAs of a fixed 64 rows balance better (RevViT-B: 133 us vs 149 us
+// one-wave). Multiples of the 8 row warps; set by (rows, cols) alone, so results do not
+// depend on the device.
 static int64_t ln_bwd_rows_per_part(int64_t rows, int64_t cols) {
   const int64_t smem = static_cast<int64_t>(kLnWarps) * 3 * cols * 4;
   int64_t per_sm = (227 * 1024) / (smem > 0 ? smem : 1);
