@@ -1,0 +1,2 @@
+RP_LIB=ab/new.so timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -k "gemm_gelu_slope" 2>&1 | tail -2
+tools/ab_multi.sh "tools/ab_step.py --rounds 1 --steps 8" 3 ab/base.so ab/new.so
