@@ -41,4 +41,10 @@ res["bias_gelu"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_
 res["slope_mul"] = t(lambda: K.gemm(dy, w2, T, h, d, b_mn=False, epi=_capi.RP_EPI_MUL, out=o1, aux=o2,
                                    colsum_part=part, bn=512))
 res["bf16"] = t(lambda: K.gemm(x, w1, T, h, d, b_mn=True, epi=_capi.RP_EPI_BF16, out=o1, bn=512))
+wo = (torch.randn(d, d, device=dev) * 0.03).bfloat16()
+xr = torch.randn(T, d, device=dev)
+res["resid_proj"] = t(lambda: K.gemm(x, wo, T, d, d, b_mn=True, epi=_capi.RP_EPI_RESID, out=xr,
+                                    aux=xr, bn=512))
+res["resid_w2"] = t(lambda: K.gemm(x3, w2, T, d, h, b_mn=True, epi=_capi.RP_EPI_RESID, out=xr,
+                                  aux=xr, bn=512))
 print(" ".join(f"{k} {v:.1f}us" for k, v in res.items()))
